@@ -1,0 +1,181 @@
+// capi.cu -- the extern "C" boundary declared in include/lcc_b200.h.
+// Exceptions never cross it: each call returns an lcc_status and leaves a
+// one-line message in a thread-local buffer (lcc_last_error()).
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+lcc_status guard(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return LCC_OK;
+    } catch (const lcc::Invalid& e) {
+        g_err = e.what();
+        return LCC_ERR_INVALID;
+    } catch (const lcc::OutOfMemory& e) {
+        g_err = e.what();
+        return LCC_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LCC_ERR_CUDA;
+    }
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void check_graph(const lcc_graph* g) {
+    LCC_REQUIRE(g != nullptr, "graph is NULL");
+    LCC_REQUIRE(g->n >= 0, "negative vertex count");
+    LCC_REQUIRE(g->nnz >= 0, "negative entry count");
+    LCC_REQUIRE(g->n == 0 || g->indptr != nullptr, "indptr is NULL");
+    LCC_REQUIRE(g->nnz == 0 || g->indices != nullptr, "indices is NULL");
+    LCC_REQUIRE(g->weights == nullptr || g->wtype == LCC_W_F32 || g->wtype == LCC_W_F64, "unknown weight dtype");
+}
+
+void check_params(const lcc_params* p) {
+    LCC_REQUIRE(p != nullptr, "params is NULL");
+    LCC_REQUIRE(p->lambda >= 0.0 && p->lambda < 1.0, "lambda must lie in [0, 1)");
+}
+
+lcc::Options to_opts(const lcc_options* o) {
+    lcc::Options r;
+    if (o) {
+        LCC_REQUIRE(o->schedule == LCC_SYNC || o->schedule == LCC_ASYNC, "unknown schedule");
+        LCC_REQUIRE(o->frontier_policy >= 0 && o->frontier_policy <= 2, "unknown frontier policy");
+        LCC_REQUIRE(o->num_iter >= 1, "num_iter must be >= 1");
+        r.schedule = o->schedule;
+        r.policy = o->frontier_policy;
+        r.refine = o->refine;
+        r.num_iter = o->num_iter;
+        r.deg_threshold = o->degree_threshold;
+        r.async_chunks = o->async_chunks > 0 ? o->async_chunks : 1;
+    }
+    return r;
+}
+}  // namespace
+
+extern "C" {
+
+int lcc_abi_version(void) { return LCC_ABI_VERSION; }
+const char* lcc_last_error(void) { return g_err.c_str(); }
+
+lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p, int32_t* C, double* K,
+                                const int32_t* frontier, int64_t n_frontier, int32_t schedule,
+                                int32_t degree_threshold, int32_t async_chunks, int32_t* D, uint8_t* moved,
+                                int64_t* moved_count, void* stream) {
+    return guard([&] {
+        check_graph(g);
+        check_params(p);
+        LCC_REQUIRE(C && K && moved, "C, K and moved are required");
+        LCC_REQUIRE(n_frontier >= 0 && n_frontier <= g->n, "frontier size out of range");
+        const int64_t cnt = lcc::best_moves_round(*g, p->k, p->lambda, C, K, frontier, n_frontier, schedule,
+                                                  degree_threshold, async_chunks > 0 ? async_chunks : 1, D, moved,
+                                                  nullptr, S(stream));
+        if (moved_count) *moved_count = cnt;
+    });
+}
+
+lcc_status lcc_apply_moves(int64_t n, const int32_t* labels_in, int64_t label_range, const double* k, int32_t* C,
+                           double* K, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0 && label_range >= n, "label_range must be >= n");
+        LCC_REQUIRE(n == 0 || (labels_in && C && K), "NULL buffer");
+        lcc::apply_moves(n, labels_in, label_range, k, C, K, S(stream));
+    });
+}
+
+lcc_status lcc_compute_frontier(const lcc_graph* g, int32_t policy, const uint8_t* moved, const int32_t* C_old,
+                                const int32_t* C_new, int32_t* frontier, int64_t* n_frontier, void* stream) {
+    return guard([&] {
+        check_graph(g);
+        LCC_REQUIRE(moved && frontier, "NULL buffer");
+        LCC_REQUIRE(policy != LCC_FRONTIER_CLUSTER_NBRS || (C_old && C_new), "cluster-neighbours needs both labelings");
+        const int64_t nf = lcc::compute_frontier(*g, policy, moved, C_old, C_new, frontier, S(stream));
+        if (n_frontier) *n_frontier = nf;
+    });
+}
+
+lcc_status lcc_par_best_moves(const lcc_graph* g, const lcc_params* p, const lcc_options* opts, int32_t* C,
+                              double* K, int32_t* any_moved, lcc_stats* stats, void* stream) {
+    return guard([&] {
+        check_graph(g);
+        check_params(p);
+        LCC_REQUIRE(g->n == 0 || (C && K), "NULL buffer");
+        const bool a = lcc::par_best_moves(*g, p->k, p->lambda, to_opts(opts), C, K, stats, S(stream));
+        if (any_moved) *any_moved = a ? 1 : 0;
+    });
+}
+
+lcc_status lcc_par_compress(const lcc_graph* g, const lcc_params* p, const int32_t* C, const double* K,
+                            int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cweights,
+                            int64_t* cn, int64_t* cnnz, double* internal_offset, double* ctotal_weight,
+                            void* stream) {
+    return guard([&] {
+        check_graph(g);
+        check_params(p);
+        LCC_REQUIRE(g->n == 0 || (C && K && mapping && ck && cindptr), "NULL buffer");
+        LCC_REQUIRE(g->nnz == 0 || (cindices && cweights), "NULL buffer");
+        const lcc::Coarse r = lcc::compress(*g, p->k, p->lambda, C, K, mapping, ck, cindptr, cindices, cweights,
+                                            S(stream));
+        if (cn) *cn = r.cn;
+        if (cnnz) *cnnz = r.cnnz;
+        if (internal_offset) *internal_offset = r.internal_offset;
+        if (ctotal_weight) *ctotal_weight = r.total_weight;
+    });
+}
+
+lcc_status lcc_par_flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C,
+                           double* K, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0, "negative vertex count");
+        LCC_REQUIRE(n == 0 || (mapping && Cc && C && K), "NULL buffer");
+        lcc::flatten(n, mapping, Cc, k, C, K, S(stream));
+    });
+}
+
+lcc_status lcc_cc_objective(const lcc_graph* g, const lcc_params* p, const int32_t* C, double* objective,
+                            void* stream) {
+    return guard([&] {
+        check_graph(g);
+        check_params(p);
+        LCC_REQUIRE(objective, "objective is NULL");
+        LCC_REQUIRE(g->n == 0 || C, "C is NULL");
+        *objective = lcc::cc_objective(*g, p->k, p->lambda, C, S(stream));
+    });
+}
+
+lcc_status lcc_parallel_cc(const lcc_graph* g, const lcc_params* p, const lcc_options* opts, int32_t* C_out,
+                           lcc_stats* stats, void* stream) {
+    return guard([&] {
+        check_graph(g);
+        check_params(p);
+        LCC_REQUIRE(g->n == 0 || C_out, "C_out is NULL");
+        lcc::parallel_cc(*g, p->k, p->lambda, to_opts(opts), C_out, stats, S(stream));
+    });
+}
+
+lcc_status lcc_gen_rmat(int32_t scale, int64_t samples, double a, double b, double c, uint64_t seed, int64_t* indptr,
+                        int32_t* indices, int64_t* nnz, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(indptr && (samples == 0 || indices), "NULL buffer");
+        const int64_t r = lcc::gen_rmat(scale, samples, a, b, c, seed, indptr, indices, S(stream));
+        if (nnz) *nnz = r;
+    });
+}
+
+lcc_status lcc_build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u, const int32_t* v, int64_t* indptr,
+                                    int32_t* indices, int64_t* nnz, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(indptr && (n_pairs == 0 || (u && v && indices)), "NULL buffer");
+        const int64_t r = lcc::build_csr_from_pairs(n, n_pairs, u, v, indptr, indices, S(stream));
+        if (nnz) *nnz = r;
+    });
+}
+
+}  // extern "C"

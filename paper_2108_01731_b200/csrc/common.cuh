@@ -1,0 +1,137 @@
+// common.cuh -- shared helpers for the LambdaCC sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/lcc_b200.h"
+
+namespace lcc {
+
+// ---------------------------------------------------------------------------
+// errors: thrown inside the library, converted to lcc_status at the C ABI.
+// ---------------------------------------------------------------------------
+struct Invalid : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct OutOfMemory : std::runtime_error { using std::runtime_error::runtime_error; };
+
+#define LCC_CUDA(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            if (_e == cudaErrorMemoryAllocation)                                         \
+                throw ::lcc::OutOfMemory(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+            throw ::lcc::CudaError(std::string(__FILE__) + ":" + std::to_string(__LINE__) + \
+                                   " " #expr ": " + cudaGetErrorString(_e));            \
+        }                                                                               \
+    } while (0)
+
+#define LCC_LAUNCH_CHECK() LCC_CUDA(cudaGetLastError())
+
+#define LCC_REQUIRE(cond, msg)                                                          \
+    do { if (!(cond)) throw ::lcc::Invalid(msg); } while (0)
+
+// ---------------------------------------------------------------------------
+// stream-ordered scratch buffer (cudaMallocAsync pool; freed on scope exit)
+// ---------------------------------------------------------------------------
+template <class T>
+struct Buf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    Buf() = default;
+    Buf(size_t count, cudaStream_t st) { alloc(count, st); }
+    void alloc(size_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        if (count) LCC_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * count, st));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    ~Buf() { release(); }
+    Buf(const Buf&) = delete;
+    Buf& operator=(const Buf&) = delete;
+    Buf(Buf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    Buf& operator=(Buf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    T* get() const { return p; }
+    operator T*() const { return p; }
+};
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+inline unsigned grid_for(int64_t items, int block, int per_sm_cap = 8) {
+    int64_t g = (items + block - 1) / block;
+    int64_t cap = (int64_t)num_sms() * per_sm_cap;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+// Exact IEEE fp64 ops: the gain must be bit-identical to the oracle
+// (gcc -ffp-contract=off), so no FMA contraction anywhere in the formula.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// Weight loads: WNone means every edge weighs 1.
+struct WNone { };
+template <class W> struct WLoad;
+template <> struct WLoad<WNone> {
+    static constexpr bool weighted = false;
+    __device__ __forceinline__ static double at(const void*, int64_t) { return 1.0; }
+};
+template <> struct WLoad<float> {
+    static constexpr bool weighted = true;
+    __device__ __forceinline__ static double at(const void* w, int64_t e) {
+        return (double)__ldg(static_cast<const float*>(w) + e);
+    }
+};
+template <> struct WLoad<double> {
+    static constexpr bool weighted = true;
+    __device__ __forceinline__ static double at(const void* w, int64_t e) {
+        return __ldg(static_cast<const double*>(w) + e);
+    }
+};
+
+__device__ __forceinline__ double kval(const double* k, int64_t v) {
+    return k ? __ldg(k + v) : 1.0;
+}
+
+// "a beats b": higher gain, ties to the lower cluster id.
+__device__ __forceinline__ bool better(double ga, int32_t xa, double gb, int32_t xb) {
+    return ga > gb || (ga == gb && (uint32_t)xa < (uint32_t)xb);
+}
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+constexpr int32_t EMPTY_KEY = -1;
+constexpr int32_t NO_CAND = 0x7fffffff;
+
+}  // namespace lcc

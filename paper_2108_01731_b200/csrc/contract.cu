@@ -1,0 +1,224 @@
+// contract.cu -- par_compress / par_flatten.
+//
+// Coarse ids: clusters are renumbered densely by ascending smallest-member
+// id.  Labels are canonical (label == smallest member), so the root of every
+// cluster is the vertex with C[x] == x and the coarse id is an exclusive scan
+// of that flag.  Every directed CSR entry (v,u) is keyed (C'(v) << b | C'(u));
+// intra-cluster entries get an all-ones sentinel (sorted last) and are summed
+// into internal_offset.  A stable LSD radix sort over the 2b live key bits
+// followed by a run-length reduce gives the coarse rows already sorted by
+// neighbour id -- the same sort + segmented-sum contract as the reference's
+// build_graph_arrays (graph.py:126-164).
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+#include "prims.cuh"
+
+namespace lcc {
+namespace {
+
+struct IsRoot {
+    const int32_t* C;
+    int64_t n;
+    __device__ __forceinline__ int32_t operator()(int32_t x) const { return (x < n && C[x] == x) ? 1 : 0; }
+};
+
+__global__ void k_map(const int32_t* __restrict__ C, const int32_t* __restrict__ rank,
+                      const double* __restrict__ K, int64_t n, int32_t* mapping, double* ck) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = C[v];
+        mapping[v] = rank[c];
+        if (c == (int32_t)v) ck[rank[v]] = K[v];
+    }
+}
+
+template <class WT>
+__global__ void k_edge_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const void* __restrict__ w, const int32_t* __restrict__ mapping, int64_t n,
+                            int bits, uint64_t* keys, double* vals, unsigned long long* intra_cnt,
+                            double* intra_w) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
+    unsigned long long cnt = 0;
+    double acc = 0.0;
+    for (int64_t v = gw; v < n; v += nw) {
+        const uint64_t a = (uint32_t)mapping[v];
+        const int64_t e1 = indptr[v + 1];
+        for (int64_t e = indptr[v] + lane; e < e1; e += 32) {
+            const uint64_t b = (uint32_t)mapping[indices[e]];
+            const double wv = WLoad<WT>::at(w, e);
+            if (a == b) {
+                keys[e] = sentinel;
+                ++cnt;
+                acc += wv;
+            } else {
+                keys[e] = (a << bits) | b;
+            }
+            if (vals) vals[e] = wv;
+        }
+    }
+    for (int d = 16; d; d >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    }
+    if (lane == 0 && cnt) {
+        atomicAdd(intra_cnt, cnt);
+        atomicAdd(intra_w, acc);
+    }
+}
+
+__global__ void k_emit_rows(const uint64_t* __restrict__ ukeys, int64_t R, int bits, int64_t cn,
+                            int64_t* cindptr, int32_t* cindices) {
+    const uint64_t mask = (1ULL << bits) - 1ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= R; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i < R ? (int64_t)(ukeys[i] >> bits) : cn;
+        const int64_t prev = i > 0 ? (int64_t)(ukeys[i - 1] >> bits) : -1;
+        for (int64_t r = prev + 1; r <= row; ++r) cindptr[r] = i;
+        if (i < R) cindices[i] = (int32_t)(ukeys[i] & mask);
+    }
+}
+
+__global__ void k_counts_to_w(const int32_t* __restrict__ cnt, int64_t R, double* cw) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x)
+        cw[i] = (double)cnt[i];
+}
+
+struct Sq {
+    __device__ __forceinline__ double operator()(double x) const { return x * x; }
+};
+struct KSq {
+    const double* k;
+    __device__ __forceinline__ double operator()(int64_t v) const { const double x = k ? k[v] : 1.0; return x * x; }
+};
+
+template <class WT>
+Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
+                     int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cw,
+                     cudaStream_t s) {
+    const int64_t n = g.n, nnz = g.nnz;
+    Coarse out;
+    // 1. dense renumbering by smallest member
+    Buf<int32_t> rank(n + 1, s);
+    cub::TransformInputIterator<int32_t, IsRoot, cub::CountingInputIterator<int32_t>> roots(
+        cub::CountingInputIterator<int32_t>(0), IsRoot{C, n});
+    exclusive_sum(roots, rank.get(), n + 1, s);
+    int32_t hcn = 0;
+    LCC_CUDA(cudaMemcpyAsync(&hcn, rank.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    k_map<<<grid_for(n, 256), 256, 0, s>>>(C, rank.get(), K, n, mapping, ck);
+    LCC_LAUNCH_CHECK();
+    LCC_CUDA(cudaStreamSynchronize(s));
+    const int64_t cn = hcn;
+    out.cn = cn;
+    const int bits = std::max(1, bit_width((uint64_t)cn));
+    LCC_REQUIRE(2 * bits <= 64, "coarse graph too large");
+
+    // 2. keys for every directed entry
+    Buf<double> dacc(2, s);  // [intra_w, scratch]
+    Buf<unsigned long long> dintra(1, s);
+    LCC_CUDA(cudaMemsetAsync(dacc.get(), 0, 2 * sizeof(double), s));
+    LCC_CUDA(cudaMemsetAsync(dintra.get(), 0, sizeof(unsigned long long), s));
+    int64_t R = 0;
+    double intra_w = 0.0;
+    if (nnz > 0) {
+        Buf<uint64_t> keys(nnz, s), keys2(nnz, s);
+        Buf<double> vals, vals2;
+        if (WLoad<WT>::weighted) { vals.alloc(nnz, s); vals2.alloc(nnz, s); }
+        k_edge_keys<WT><<<grid_for(n * 32, 256, 16), 256, 0, s>>>(g.indptr, g.indices, g.weights, mapping, n, bits,
+                                                                  keys.get(), vals.get(), dintra.get(), dacc.get());
+        LCC_LAUNCH_CHECK();
+        // 3. stable radix sort on the 2*bits live bits
+        if (WLoad<WT>::weighted) sort_pairs(keys.get(), keys2.get(), vals.get(), vals2.get(), nnz, 2 * bits, s);
+        else sort_keys(keys.get(), keys2.get(), nnz, 2 * bits, s);
+        // 4. run-length reduce (keys reuse `keys` as unique output)
+        Buf<int64_t> druns(1, s);
+        if (WLoad<WT>::weighted) {
+            size_t bytes = 0;
+            LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, keys2.get(), keys.get(), vals2.get(), vals.get(),
+                                                    druns.get(), cub::Sum(), nnz, s));
+            Buf<unsigned char> tmp(bytes, s);
+            LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, keys2.get(), keys.get(), vals2.get(), vals.get(),
+                                                    druns.get(), cub::Sum(), nnz, s));
+        } else {
+            Buf<int32_t> counts(nnz, s);
+            size_t bytes = 0;
+            LCC_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, keys2.get(), keys.get(), counts.get(),
+                                                        druns.get(), nnz, s));
+            Buf<unsigned char> tmp(bytes, s);
+            LCC_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), bytes, keys2.get(), keys.get(), counts.get(),
+                                                        druns.get(), nnz, s));
+            int64_t runs = 0;
+            LCC_CUDA(cudaMemcpyAsync(&runs, druns.get(), sizeof(runs), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+            if (runs > 0) {
+                k_counts_to_w<<<grid_for(runs, 256), 256, 0, s>>>(counts.get(), runs, cw);
+                LCC_LAUNCH_CHECK();
+            }
+        }
+        int64_t runs = 0;
+        unsigned long long hintra = 0;
+        LCC_CUDA(cudaMemcpyAsync(&runs, druns.get(), sizeof(runs), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaMemcpyAsync(&hintra, dintra.get(), sizeof(hintra), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaMemcpyAsync(&intra_w, dacc.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaStreamSynchronize(s));
+        R = runs - (hintra > 0 ? 1 : 0);
+        if (WLoad<WT>::weighted && R > 0)
+            LCC_CUDA(cudaMemcpyAsync(cw, vals.get(), sizeof(double) * R, cudaMemcpyDeviceToDevice, s));
+        if (!WLoad<WT>::weighted) intra_w = (double)hintra;
+        k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(keys.get(), R, bits, cn, cindptr, cindices);
+        LCC_LAUNCH_CHECK();
+    } else {
+        LCC_CUDA(cudaMemsetAsync(cindptr, 0, sizeof(int64_t) * (cn + 1), s));
+    }
+    out.cnnz = R;
+    // 5. scalars: total weight, internal offset
+    Buf<double> sums(3, s);
+    LCC_CUDA(cudaMemsetAsync(sums.get(), 0, 3 * sizeof(double), s));
+    if (R > 0) device_sum(cw, sums.get() + 0, R, s);
+    if (cn > 0) {
+        cub::TransformInputIterator<double, Sq, const double*> sq(ck, Sq{});
+        device_sum(sq, sums.get() + 1, cn, s);
+    }
+    {
+        cub::TransformInputIterator<double, KSq, cub::CountingInputIterator<int64_t>> ksq(
+            cub::CountingInputIterator<int64_t>(0), KSq{k});
+        device_sum(ksq, sums.get() + 2, n, s);
+    }
+    double hs[3];
+    LCC_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    out.total_weight = hs[0] * 0.5;
+    out.internal_offset = intra_w * 0.5 - lam * (hs[1] - hs[2]) * 0.5;
+    return out;
+}
+
+__global__ void k_compose(const int32_t* __restrict__ mapping, const int32_t* __restrict__ Cc, int64_t n, int32_t* D) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        D[v] = Cc[mapping[v]];
+}
+
+}  // namespace
+
+Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
+                int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cw,
+                cudaStream_t s) {
+    LCC_REQUIRE(g.n >= 0 && g.n < (1LL << 31) - 1, "vertex count out of range");
+    switch (g.weights ? g.wtype : LCC_W_NONE) {
+        case LCC_W_NONE: return compress_impl<WNone>(g, k, lam, C, K, mapping, ck, cindptr, cindices, cw, s);
+        case LCC_W_F32: return compress_impl<float>(g, k, lam, C, K, mapping, ck, cindptr, cindices, cw, s);
+        case LCC_W_F64: return compress_impl<double>(g, k, lam, C, K, mapping, ck, cindptr, cindices, cw, s);
+        default: throw Invalid("unknown weight dtype");
+    }
+}
+
+void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C, double* K,
+             cudaStream_t s) {
+    if (n <= 0) return;
+    Buf<int32_t> D(n, s);
+    k_compose<<<grid_for(n, 256), 256, 0, s>>>(mapping, Cc, n, D.get());
+    LCC_LAUNCH_CHECK();
+    apply_moves(n, D.get(), n, k, C, K, s);
+}
+
+}  // namespace lcc

@@ -1,0 +1,169 @@
+// driver.cu -- par_best_moves and the multi-level parallel_cc driver
+// (Alg. 1, lines 1-19).
+//
+// Native host orchestration: one best-move iteration = bin partition +
+// best-move kernels + (sync) apply / (async) reconcile + frontier, with one
+// host read of the mover count per iteration for the early exit (Alg. 1
+// line 9).  Levels are kept on an explicit stack so refinement can revisit
+// them while unwinding.
+#include <memory>
+#include <utility>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace lcc {
+
+namespace {
+struct EventTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    explicit EventTimer(cudaStream_t st) : s(st) {
+        LCC_CUDA(cudaEventCreate(&a));
+        LCC_CUDA(cudaEventCreate(&b));
+        LCC_CUDA(cudaEventRecord(a, s));
+    }
+    float stop() {
+        LCC_CUDA(cudaEventRecord(b, s));
+        LCC_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        LCC_CUDA(cudaEventElapsedTime(&ms, a, b));
+        return ms;
+    }
+    ~EventTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+}  // namespace
+
+bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C, double* K,
+                    lcc_stats* st, cudaStream_t s) {
+    LCC_REQUIRE(o.num_iter >= 1, "num_iter must be >= 1");
+    const int64_t n = g.n;
+    if (n == 0) return false;
+    const bool as = o.schedule == LCC_ASYNC;
+    Buf<int32_t> D(n, s), Cnext(n, s), F(n, s);
+    Buf<uint8_t> moved(n, s);
+    Buf<double> K2;
+    if (as) K2.alloc(2 * n, s);
+    int32_t* cur = C;
+    int32_t* nxt = Cnext.get();
+    const int32_t* frontier = nullptr;  // V' <- V
+    int64_t nF = n;
+    bool any = false;
+    for (int it = 0; it < o.num_iter; ++it) {
+        if (frontier && nF == 0) break;
+        RoundStats rs;
+        int64_t cnt;
+        EventTimer tm(s);
+        if (!as) {
+            cnt = best_moves_round(g, k, lam, cur, K, frontier, nF, LCC_SYNC, o.deg_threshold, 1, D.get(),
+                                   moved.get(), &rs, s);
+        } else {
+            LCC_CUDA(cudaMemcpyAsync(D.get(), cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+            LCC_CUDA(cudaMemcpyAsync(K2.get(), K, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+            LCC_CUDA(cudaMemsetAsync(K2.get() + n, 0, sizeof(double) * n, s));
+            cnt = best_moves_round(g, k, lam, D.get(), K2.get(), frontier, nF, LCC_ASYNC, o.deg_threshold,
+                                   o.async_chunks, nullptr, moved.get(), &rs, s);
+        }
+        const float ms = tm.stop();
+        if (st) {
+            st->rounds += 1;
+            st->vertices += rs.vertices;
+            st->edges_scanned += rs.edges;
+            st->moves += rs.moved;
+            st->ms_best_moves += ms;
+        }
+        if (cnt == 0) break;  // Alg. 1 line 9
+        any = true;
+        apply_moves(n, D.get(), 2 * n, k, nxt, K, s);  // sync apply / async reconcile
+        nF = compute_frontier(g, o.policy, moved.get(), cur, nxt, F.get(), s);
+        frontier = F.get();
+        std::swap(cur, nxt);
+    }
+    if (cur != C) LCC_CUDA(cudaMemcpyAsync(C, cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    return any;
+}
+
+namespace {
+struct OwnedGraph {
+    Buf<int64_t> indptr;
+    Buf<int32_t> indices;
+    Buf<double> w;
+    Buf<double> k;
+    lcc_graph g{};
+};
+struct Frame {
+    lcc_graph g;
+    const double* k;
+    Buf<int32_t> mapping;
+};
+}  // namespace
+
+void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Options& o, int32_t* C_out,
+                 lcc_stats* st, cudaStream_t s) {
+    EventTimer total(s);
+    std::vector<std::unique_ptr<OwnedGraph>> owned;
+    std::vector<Frame> stack;
+    lcc_graph g = g0;
+    const double* k = k0;
+    Buf<int32_t> C;
+    Buf<double> K;
+    while (true) {
+        const int64_t n = g.n;
+        C.alloc(std::max<int64_t>(n, 1), s);
+        K.alloc(std::max<int64_t>(n, 1), s);
+        fill_iota(C.get(), n, s);  // singletons
+        fill_k(K.get(), k, n, s);
+        if (st) st->levels += 1;
+        const bool moved = par_best_moves(g, k, lam, o, C.get(), K.get(), st, s);
+        if (!moved) break;  // Alg. 1 line 13
+        // contraction into upper-bound buffers, then shrink to exact size
+        Buf<int32_t> mapping(n, s), cind(std::max<int64_t>(g.nnz, 1), s);
+        Buf<double> ck(n, s), cw(std::max<int64_t>(g.nnz, 1), s);
+        Buf<int64_t> cptr(n + 1, s);
+        const Coarse cs = compress(g, k, lam, C.get(), K.get(), mapping.get(), ck.get(), cptr.get(), cind.get(),
+                                   cw.get(), s);
+        if (cs.cn == n) break;  // no size reduction
+        auto og = std::make_unique<OwnedGraph>();
+        og->indptr.alloc(cs.cn + 1, s);
+        og->indices.alloc(std::max<int64_t>(cs.cnnz, 1), s);
+        og->w.alloc(std::max<int64_t>(cs.cnnz, 1), s);
+        og->k.alloc(std::max<int64_t>(cs.cn, 1), s);
+        LCC_CUDA(cudaMemcpyAsync(og->indptr.get(), cptr.get(), sizeof(int64_t) * (cs.cn + 1), cudaMemcpyDeviceToDevice, s));
+        if (cs.cnnz) {
+            LCC_CUDA(cudaMemcpyAsync(og->indices.get(), cind.get(), sizeof(int32_t) * cs.cnnz, cudaMemcpyDeviceToDevice, s));
+            LCC_CUDA(cudaMemcpyAsync(og->w.get(), cw.get(), sizeof(double) * cs.cnnz, cudaMemcpyDeviceToDevice, s));
+        }
+        LCC_CUDA(cudaMemcpyAsync(og->k.get(), ck.get(), sizeof(double) * cs.cn, cudaMemcpyDeviceToDevice, s));
+        og->g.n = cs.cn;
+        og->g.nnz = cs.cnnz;
+        og->g.indptr = og->indptr.get();
+        og->g.indices = og->indices.get();
+        og->g.weights = og->w.get();
+        og->g.wtype = LCC_W_F64;
+        og->g.total_weight = cs.total_weight;
+        stack.push_back(Frame{g, k, std::move(mapping)});
+        g = og->g;
+        k = og->k.get();
+        owned.push_back(std::move(og));
+    }
+    // unwind: flatten (+ refine) level by level (Alg. 1 lines 17-18)
+    Buf<int32_t> Cres = std::move(C);
+    for (auto it = stack.rbegin(); it != stack.rend(); ++it) {
+        const int64_t n = it->g.n;
+        Buf<int32_t> Cf(std::max<int64_t>(n, 1), s);
+        Buf<double> Kf(std::max<int64_t>(n, 1), s);
+        flatten(n, it->mapping.get(), Cres.get(), it->k, Cf.get(), Kf.get(), s);
+        if (o.refine) par_best_moves(it->g, it->k, lam, o, Cf.get(), Kf.get(), st, s);
+        Cres = std::move(Cf);
+    }
+    if (g0.n > 0)
+        LCC_CUDA(cudaMemcpyAsync(C_out, Cres.get(), sizeof(int32_t) * g0.n, cudaMemcpyDeviceToDevice, s));
+    const float ms = total.stop();
+    if (st) st->ms_total += ms;
+}
+
+}  // namespace lcc

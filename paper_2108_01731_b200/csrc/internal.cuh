@@ -1,0 +1,63 @@
+// internal.cuh -- C++ entry points shared between the translation units.
+#pragma once
+#include "common.cuh"
+
+namespace lcc {
+
+struct RoundStats {
+    int64_t vertices = 0;
+    int64_t edges = 0;
+    int64_t moved = 0;
+    int64_t n_small = 0, n_medium = 0, n_large = 0;
+};
+
+// best_moves.cu: one best-move iteration over `frontier` (nullptr = all).
+//   sync : D <- C, D[v] <- target for movers, moved[] set; C/K untouched.
+//   async: C and K (2n entries) updated live; D unused.
+// Returns the number of movers (synchronises the stream once).
+int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
+                         const int32_t* frontier, int64_t nF, int schedule, int deg_threshold,
+                         int async_chunks, int32_t* D, uint8_t* moved, RoundStats* st,
+                         cudaStream_t s);
+
+// apply.cu
+void apply_moves(int64_t n, const int32_t* labels_in, int64_t label_range, const double* k,
+                 int32_t* C, double* K, cudaStream_t s);
+int64_t compute_frontier(const lcc_graph& g, int policy, const uint8_t* moved,
+                         const int32_t* C_old, const int32_t* C_new, int32_t* frontier,
+                         cudaStream_t s);
+void fill_iota(int32_t* p, int64_t n, cudaStream_t s);
+void fill_k(double* K, const double* k, int64_t n, cudaStream_t s);
+
+// contract.cu
+struct Coarse {
+    int64_t cn = 0, cnnz = 0;
+    double internal_offset = 0.0, total_weight = 0.0;
+};
+Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
+                int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cw,
+                cudaStream_t s);
+void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C,
+             double* K, cudaStream_t s);
+
+// objective.cu
+double cc_objective(const lcc_graph& g, const double* k, double lam, const int32_t* C,
+                    cudaStream_t s);
+
+// gen.cu
+int64_t build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u, const int32_t* v,
+                             int64_t* indptr, int32_t* indices, cudaStream_t s);
+int64_t gen_rmat(int scale, int64_t samples, double a, double b, double c, uint64_t seed,
+                 int64_t* indptr, int32_t* indices, cudaStream_t s);
+
+// driver.cu
+struct Options {
+    int schedule = LCC_ASYNC, policy = LCC_FRONTIER_VERTEX_NBRS, refine = 1, num_iter = 10;
+    int deg_threshold = 1000, async_chunks = 16;
+};
+bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C,
+                    double* K, lcc_stats* st, cudaStream_t s);
+void parallel_cc(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C_out,
+                 lcc_stats* st, cudaStream_t s);
+
+}  // namespace lcc

@@ -1,0 +1,96 @@
+// objective.cu -- cc_objective, closed form over unordered pairs:
+//   CC = sum_{intra undirected edges} w - lambda * sum_c (K_c^2 - sum_{v in c} k_v^2) / 2
+// evaluated as  intra_dir*0.5 - lam*(sum K^2 - sum k^2)*0.5  (same order as the
+// oracle).  Unweighted graphs count intra entries in uint64, so the edge term
+// is exact and order independent; K sums are integer valued for every config
+// (k = 1 or k = degree) and therefore exact in fp64 below 2^53.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+#include "prims.cuh"
+
+namespace lcc {
+namespace {
+
+template <class WT>
+__global__ void k_intra(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                        const void* __restrict__ w, const int32_t* __restrict__ C, int64_t n,
+                        unsigned long long* cnt_out, double* w_out) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned long long cnt = 0;
+    double acc = 0.0;
+    for (int64_t v = gw; v < n; v += nw) {
+        const int32_t c = C[v];
+        const int64_t e1 = indptr[v + 1];
+        for (int64_t e = indptr[v] + lane; e < e1; e += 32) {
+            if (C[indices[e]] == c) {
+                ++cnt;
+                if (WLoad<WT>::weighted) acc += WLoad<WT>::at(w, e);
+            }
+        }
+    }
+    for (int d = 16; d; d >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    }
+    if (lane == 0 && cnt) {
+        atomicAdd(cnt_out, cnt);
+        if (WLoad<WT>::weighted) atomicAdd(w_out, acc);
+    }
+}
+
+__global__ void k_mass(const int32_t* __restrict__ C, const double* __restrict__ k, int64_t n, double* K) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(K + C[v], k ? k[v] : 1.0);
+}
+
+struct Sq {
+    __device__ __forceinline__ double operator()(double x) const { return x * x; }
+};
+struct KSq {
+    const double* k;
+    __device__ __forceinline__ double operator()(int64_t v) const { const double x = k ? k[v] : 1.0; return x * x; }
+};
+
+template <class WT>
+double objective_impl(const lcc_graph& g, const double* k, double lam, const int32_t* C, cudaStream_t s) {
+    const int64_t n = g.n;
+    if (n == 0) return 0.0;
+    Buf<unsigned long long> dcnt(1, s);
+    Buf<double> dd(3, s);
+    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long), s));
+    LCC_CUDA(cudaMemsetAsync(dd.get(), 0, 3 * sizeof(double), s));
+    k_intra<WT><<<grid_for(n * 32, 256, 16), 256, 0, s>>>(g.indptr, g.indices, g.weights, C, n, dcnt.get(), dd.get());
+    LCC_LAUNCH_CHECK();
+    Buf<double> K(n, s);
+    LCC_CUDA(cudaMemsetAsync(K.get(), 0, sizeof(double) * n, s));
+    k_mass<<<grid_for(n, 256), 256, 0, s>>>(C, k, n, K.get());
+    LCC_LAUNCH_CHECK();
+    cub::TransformInputIterator<double, Sq, const double*> sq(K.get(), Sq{});
+    device_sum(sq, dd.get() + 1, n, s);
+    cub::TransformInputIterator<double, KSq, cub::CountingInputIterator<int64_t>> ksq(
+        cub::CountingInputIterator<int64_t>(0), KSq{k});
+    device_sum(ksq, dd.get() + 2, n, s);
+    unsigned long long hc = 0;
+    double hd[3];
+    LCC_CUDA(cudaMemcpyAsync(&hc, dcnt.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaMemcpyAsync(hd, dd.get(), sizeof(hd), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    const double intra = WLoad<WT>::weighted ? hd[0] : (double)hc;
+    return intra * 0.5 - lam * (hd[1] - hd[2]) * 0.5;
+}
+
+}  // namespace
+
+double cc_objective(const lcc_graph& g, const double* k, double lam, const int32_t* C, cudaStream_t s) {
+    switch (g.weights ? g.wtype : LCC_W_NONE) {
+        case LCC_W_NONE: return objective_impl<WNone>(g, k, lam, C, s);
+        case LCC_W_F32: return objective_impl<float>(g, k, lam, C, s);
+        case LCC_W_F64: return objective_impl<double>(g, k, lam, C, s);
+        default: throw Invalid("unknown weight dtype");
+    }
+}
+
+}  // namespace lcc

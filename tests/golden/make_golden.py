@@ -1,0 +1,122 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE.
+
+Run in the build container (where /root/reference exists):
+    python tests/golden/make_golden.py
+The fixtures are committed; nothing at test time reads /root/reference.
+
+What comes from the reference (``/root/reference/pkg/src/lambdacc/graph.py``):
+* ``build_graph`` / ``build_graph_arrays`` (graph.py:79-164): the CSR of
+  every fixture graph, and the contraction edge-merge -- SURVEY.md §8c:
+  ``build_graph_arrays(mapping[src], mapping[dst], w, n=n')`` over all 2m
+  directed entries is exactly the coarse graph of ``compress``.
+* ``frontier_from_members`` (graph.py:205-215): vertex-neighbour frontiers.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from lambdacc.graph import build_graph, build_graph_arrays, frontier_from_members  # noqa: E402
+
+from paper_2108_01731_b200.gen import rmat_pairs_host, sbm  # noqa: E402
+
+
+def random_graph(rng, n, p, weighted, messy=True):
+    """Edge list with duplicates / both orientations / self loops, as the
+    reference builder accepts."""
+    u, v = np.nonzero(np.triu(rng.random((n, n)) < p, 1))
+    w = rng.uniform(-1.0, 2.0, u.size) if weighted else np.ones(u.size)
+    if messy and u.size:
+        # permuted orientation (average is exact when both orientations agree)
+        flip = rng.random(u.size) < 0.5
+        u, v = np.where(flip, v, u), np.where(flip, u, v)
+        # self loops are dropped by the builder
+        s = rng.integers(0, n, 3)
+        u = np.concatenate([u, s]); v = np.concatenate([v, s]); w = np.concatenate([w, np.ones(3)])
+    return build_graph_arrays(u, v, w, n=n)
+
+
+def canonical(labels):
+    n = labels.size
+    minm = np.full(labels.max() + 1, n, np.int64)
+    np.minimum.at(minm, labels, np.arange(n))
+    return minm[labels].astype(np.int32)
+
+
+def contraction_cases(rng):
+    out = {}
+    cases = []
+    for t in range(40):
+        n = int(rng.integers(2, 48))
+        g = random_graph(rng, n, float(rng.uniform(0.05, 0.5)), weighted=(t % 2 == 1))
+        nclus = int(rng.integers(1, n + 1))
+        C = canonical(rng.integers(0, nclus, n))
+        roots = np.flatnonzero(C == np.arange(n))
+        rank = np.full(n, -1, np.int64)
+        rank[roots] = np.arange(roots.size)
+        mapping = rank[C]
+        src = np.repeat(np.arange(n), np.diff(g.indptr))
+        cg = build_graph_arrays(mapping[src], mapping[g.indices], g.weights, n=int(roots.size))
+        pre = f"c{t}_"
+        out[pre + "indptr"] = g.indptr
+        out[pre + "indices"] = g.indices
+        out[pre + "weights"] = g.weights
+        out[pre + "C"] = C
+        out[pre + "mapping"] = mapping.astype(np.int32)
+        out[pre + "cindptr"] = cg.indptr
+        out[pre + "cindices"] = cg.indices
+        out[pre + "cweights"] = cg.weights
+        out[pre + "ctotal"] = np.array([cg.total_weight])
+        cases.append(t)
+    out["cases"] = np.array(cases)
+    return out
+
+
+def frontier_cases(rng):
+    out = {}
+    for t in range(30):
+        n = int(rng.integers(5, 80))
+        g = random_graph(rng, n, float(rng.uniform(0.02, 0.3)), weighted=False)
+        moved = np.flatnonzero(rng.random(n) < rng.uniform(0.0, 0.5))
+        nb = [g.neighbors(int(v))[0] for v in moved]
+        ids = np.concatenate(nb) if nb else np.empty(0, np.int64)
+        fr = frontier_from_members(ids, n, g)
+        pre = f"f{t}_"
+        out[pre + "indptr"] = g.indptr
+        out[pre + "indices"] = g.indices
+        out[pre + "moved"] = moved
+        out[pre + "frontier"] = fr.members()
+    out["cases"] = np.arange(30)
+    return out
+
+
+def main():
+    rng = np.random.default_rng(2108_01731)
+    np.savez_compressed(os.path.join(HERE, "contraction.npz"), **contraction_cases(rng))
+    np.savez_compressed(os.path.join(HERE, "frontier.npz"), **frontier_cases(rng))
+    # config-1 SBM through the reference builder
+    g, comm = sbm(seed=1)
+    src = np.repeat(np.arange(g.n), np.diff(g.indptr))
+    keep = src < g.indices
+    rg = build_graph_arrays(src[keep], g.indices[keep], np.ones(int(keep.sum())), n=g.n)
+    np.savez_compressed(os.path.join(HERE, "sbm_cfg1.npz"), indptr=rg.indptr, indices=rg.indices,
+                        weights=rg.weights, m=np.array([rg.m]), community=comm.astype(np.int32))
+    # R-MAT scale 10 sample stream through the reference builder
+    u, v = rmat_pairs_host(10, 16 << 10, 0.57, 0.19, 0.19, 24)
+    rg = build_graph([(int(a), int(b), 1.0) for a, b in zip(u, v)], n=1 << 10)
+    # unweighted duplicates merge by sum/average in the reference (erratum 3);
+    # the structural CSR is what the generator must reproduce
+    np.savez_compressed(os.path.join(HERE, "rmat_s10.npz"), indptr=rg.indptr, indices=rg.indices,
+                        m=np.array([rg.m]))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,384 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+* unweighted: sync labels, frontiers, contracted CSR and objective bit-exact;
+* weighted: labels equal except at gain ties within 1e-9 relative; weights
+  and objective within 1e-6 relative (tested tighter where exact);
+* async: final objective no worse than the oracle's by more than 0.5%.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2108_01731_b200 as L
+from oracle import oracle as O
+from paper_2108_01731_b200.gen import csr_from_pairs, lfr_like, rmat_pairs_host, sbm, rmat_device
+
+pytestmark = pytest.mark.gpu
+
+REL_W = 1e-6     # weighted contracted weights / objective (north_star)
+REL_TIE = 1e-9   # weighted label ties (north_star)
+
+
+def og(hg):
+    return O.as_graph(hg)
+
+
+def dg(hg):
+    return L.DeviceGraph.from_graph(hg)
+
+
+def rand_pairs(rng, n, p):
+    m = int(rng.binomial(n * (n - 1) // 2, p))
+    return rng.integers(0, n, m), rng.integers(0, n, m)
+
+
+def rand_weighted(rng, n, p, fp32=True, lo=0.0, hi=1.0):
+    u, v = rand_pairs(rng, n, p)
+    g = csr_from_pairs(n, u, v)
+    src = np.repeat(np.arange(n), np.diff(g.indptr))
+    lo_, hi_ = np.minimum(src, g.indices), np.maximum(src, g.indices)
+    # symmetric weight per unordered pair (hash of the pair)
+    w = np.sin(lo_ * 12.9898 + hi_ * 78.233) * 43758.5453
+    w = lo + (hi - lo) * (w - np.floor(w))
+    if fp32:
+        w = w.astype(np.float32).astype(np.float64)
+    g.weights = w
+    g.total_weight = float(w.sum() / 2)
+    return g
+
+
+def hub_graph(rng, n, hubs, hub_deg, base_p=0.002):
+    """Random graph plus a few high-degree hubs (exercises medium/large bins)."""
+    u, v = rand_pairs(rng, n, base_p)
+    us, vs = [u], [v]
+    for h, d in zip(hubs, hub_deg):
+        nb = rng.choice(n, size=d, replace=False)
+        us.append(np.full(d, h)); vs.append(nb)
+    return csr_from_pairs(n, np.concatenate(us), np.concatenate(vs))
+
+
+def clustered_state(rng, n, nclus, k=None):
+    lab = rng.integers(0, nclus, n).astype(np.int32)
+    return O.canonicalize(n, lab, n, k)
+
+
+def gpu_sync_round(g_host, k, lam, C, K, F=None, thr=1000):
+    d = dg(g_host)
+    p = L.ClusteringParams(lam, None if k is None else k)
+    c = L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda())
+    mb = L.best_moves_round(d, p, c, frontier=F, schedule=L.Schedule.Synchronous, degree_threshold=thr)
+    return mb.desired.cpu().numpy(), mb.moved.cpu().numpy(), mb.moved_count
+
+
+def oracle_gain(g, k, lam, C, K, v, x):
+    """Gain of moving v to cluster x, in the kernels' order."""
+    s, e = g.indptr[v], g.indptr[v + 1]
+    nb = g.indices[s:e]
+    w = np.ones(e - s) if g.weights is None else g.weights[s:e]
+    kv = 1.0 if k is None else k[v]
+    t = lam * kv
+    c = C[v]
+    Sc = w[C[nb] == c].sum()
+    b = (Sc - t * K[c]) + t * kv
+    if x >= g.n:
+        return 0.0 - b
+    if x == c:
+        return 0.0
+    Sx = w[C[nb] == x].sum()
+    return (Sx - t * K[x]) - b
+
+
+# --------------------------------------------------------------- rounds ----
+
+def test_sync_round_sbm_cfg1_exact():
+    hg, _ = sbm(seed=1)
+    g = og(hg)
+    C, K = O.singletons(g.n, None)
+    for it in range(4):
+        D0, m0, c0 = O.sync_round(g, None, 0.85, C, K)
+        D1, m1, c1 = gpu_sync_round(hg, None, 0.85, C, K)
+        assert np.array_equal(D0, D1), f"round {it}"
+        assert np.array_equal(m0, m1) and c0 == c1
+        C, K = O.canonicalize(g.n, D0, 2 * g.n, None)
+
+
+@pytest.mark.parametrize("thr", [1000, 40, 0])
+def test_sync_round_hubs_all_bins_exact(thr):
+    rng = np.random.default_rng(11)
+    hg = hub_graph(rng, 30_000, hubs=[5, 77, 900, 1234], hub_deg=[50, 700, 12_000, 25_000], base_p=0.0003)
+    g = og(hg)
+    for nclus in (30_000, 3000, 40):
+        C, K = clustered_state(rng, g.n, nclus)
+        for lam in (0.0, 0.3, 0.85):
+            D0, m0, c0 = O.sync_round(g, None, lam, C, K)
+            D1, m1, c1 = gpu_sync_round(hg, None, lam, C, K, thr=thr)
+            assert np.array_equal(D0, D1)
+            assert c0 == c1
+
+
+def test_sync_round_with_frontier_and_k_exact():
+    rng = np.random.default_rng(12)
+    hg, _ = lfr_like(n=50_000, seed=4)
+    g = og(hg)
+    k = np.diff(g.indptr).astype(np.float64)   # modularity weights
+    lam = 1.0 / (2 * g.m)
+    C, K = clustered_state(rng, g.n, 5000, k)
+    F = np.sort(rng.choice(g.n, size=7000, replace=False)).astype(np.int32)
+    D0, m0, c0 = O.sync_round(g, k, lam, C, K, F=F)
+    D1, m1, c1 = gpu_sync_round(hg, k, lam, C, K, F=F)
+    assert np.array_equal(D0, D1) and c0 == c1
+    assert np.all(m1[np.setdiff1d(np.arange(g.n), F)] == 0)
+
+
+@pytest.mark.parametrize("fp32", [True, False])
+def test_sync_round_weighted_ties(fp32):
+    rng = np.random.default_rng(13)
+    hg = rand_weighted(rng, 3000, 0.01, fp32=fp32)
+    g = og(hg)
+    for lam in (0.01, 0.1, 0.5):
+        C, K = clustered_state(rng, g.n, 600)
+        D0, _, _ = O.sync_round(g, None, lam, C, K)
+        D1, _, _ = gpu_sync_round(hg, None, lam, C, K)
+        diff = np.flatnonzero(D0 != D1)
+        for v in diff:
+            g0 = oracle_gain(g, None, lam, C, K, v, D0[v])
+            g1 = oracle_gain(g, None, lam, C, K, v, D1[v])
+            assert abs(g0 - g1) <= REL_TIE * max(1.0, abs(g0)), (v, D0[v], D1[v], g0, g1)
+        # degree <= 32 vertices sum in CSR order on both sides: exact
+        small = np.diff(g.indptr) <= 32
+        assert np.array_equal(D0[small], D1[small])
+
+
+def test_round_edge_cases():
+    # empty graph with isolated vertices; a vertex inside a bigger cluster leaves
+    hg = csr_from_pairs(5, np.array([0]), np.array([1]))
+    g = og(hg)
+    C = np.array([0, 0, 0, 3, 4], np.int32)
+    K = np.array([3.0, 0, 0, 1, 1])
+    D0, _, c0 = O.sync_round(g, None, 0.3, C, K)
+    D1, _, c1 = gpu_sync_round(hg, None, 0.3, C, K)
+    assert np.array_equal(D0, D1) and c0 == c1 and D1[2] == 5 + 2
+
+
+# ------------------------------------------------------ apply / frontier ----
+
+def test_apply_and_frontier_exact():
+    rng = np.random.default_rng(14)
+    hg = hub_graph(rng, 20_000, [1, 2], [3000, 15_000], base_p=0.0004)
+    g = og(hg)
+    C, K = clustered_state(rng, g.n, 2000)
+    D0, m0, _ = O.sync_round(g, None, 0.6, C, K)
+    Cn0, Kn0 = O.canonicalize(g.n, D0, 2 * g.n, None)
+    cl = L.apply_moves(torch.as_tensor(D0).cuda(), 2 * g.n, L.ClusteringParams(0.6))
+    assert np.array_equal(cl.assignment.cpu().numpy(), Cn0)
+    assert np.array_equal(cl.cluster_mass.cpu().numpy(), Kn0)
+    for pol in (O.ALL, O.VERTEX_NBRS, O.CLUSTER_NBRS):
+        F0 = O.frontier(g, pol, m0, C, Cn0)
+        F1 = L.compute_frontier(int(pol), torch.as_tensor(m0).cuda(), dg(hg),
+                                torch.as_tensor(C).cuda(), torch.as_tensor(Cn0).cuda())
+        assert np.array_equal(F0, F1.ids.cpu().numpy()), pol
+    # SPEC.md:273-275 KATs through the GPU API
+    p = csr_from_pairs(5, np.array([0, 1, 3]), np.array([1, 2, 4]))
+    assert L.compute_frontier("vertex-nbrs", [], p).size == 0
+    assert list(L.compute_frontier("vertex-nbrs", [1], p).members()) == [0, 2]
+    f = L.compute_frontier("cluster-nbrs", [1], p, np.array([0, 1, 2, 1, 4]), np.array([0, 0, 2, 3, 4]))
+    assert list(f.members()) == [0, 1, 2, 4]
+
+
+# ------------------------------------------------------------ contraction --
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_compress_matches_oracle(weighted):
+    rng = np.random.default_rng(15)
+    hg = rand_weighted(rng, 4000, 0.004) if weighted else hub_graph(rng, 40_000, [7], [9000], base_p=0.0002)
+    g = og(hg)
+    for nclus in (g.n, 900, 1):
+        C, K = clustered_state(rng, g.n, nclus)
+        lvl0 = O.compress(g, None, 0.4, C, K)
+        p = L.ClusteringParams(0.4)
+        c = L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda())
+        lvl1 = L.par_compress(dg(hg), p, c)
+        assert lvl1.graph.n == lvl0.graph.n
+        assert np.array_equal(lvl1.mapping.cpu().numpy(), lvl0.mapping)
+        assert np.array_equal(lvl1.graph.indptr.cpu().numpy(), lvl0.graph.indptr)
+        assert np.array_equal(lvl1.graph.indices.cpu().numpy(), lvl0.graph.indices)
+        assert np.array_equal(lvl1.weights.cpu().numpy(), lvl0.k)
+        w1 = lvl1.graph.weights.cpu().numpy()
+        if weighted:
+            np.testing.assert_allclose(w1, lvl0.graph.weights, rtol=1e-12)
+            assert lvl1.internal_offset == pytest.approx(lvl0.internal_offset, rel=1e-12, abs=1e-9)
+        else:
+            assert np.array_equal(w1, lvl0.graph.weights)
+            assert lvl1.internal_offset == lvl0.internal_offset
+            assert lvl1.graph.total_weight == lvl0.graph.total_weight
+
+
+def test_compress_against_reference_golden(golden):
+    z = golden("contraction.npz")
+    for t in z["cases"]:
+        p = f"c{t}_"
+        w = z[p + "weights"]
+        n = z[p + "indptr"].size - 1
+
+        class G:
+            pass
+        hg = G()
+        hg.n, hg.indptr, hg.indices, hg.weights = n, z[p + "indptr"], z[p + "indices"], w
+        hg.total_weight = float(w.sum() / 2)
+        C = z[p + "C"]
+        lvl = L.par_compress(dg(hg), L.ClusteringParams(0.3), C)
+        assert np.array_equal(lvl.mapping.cpu().numpy(), z[p + "mapping"])
+        assert np.array_equal(lvl.graph.indptr.cpu().numpy(), z[p + "cindptr"])
+        assert np.array_equal(lvl.graph.indices.cpu().numpy(), z[p + "cindices"])
+        np.testing.assert_allclose(lvl.graph.weights.cpu().numpy(), z[p + "cweights"], rtol=1e-12, atol=1e-12)
+
+
+def test_flatten_and_objective():
+    rng = np.random.default_rng(16)
+    hg, _ = sbm(seed=1)
+    g = og(hg)
+    C, K = clustered_state(rng, g.n, 700)
+    lvl = O.compress(g, None, 0.85, C, K)
+    Cc = rng.integers(0, lvl.graph.n, lvl.graph.n).astype(np.int32)
+    F0, _ = O.flatten(g.n, lvl.mapping, Cc, None)
+    F1 = L.par_flatten(L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda()), Cc, lvl.mapping)
+    assert np.array_equal(F1.assignment.cpu().numpy(), F0)
+    for lab in (C, F0, np.zeros(g.n, np.int32), np.arange(g.n, dtype=np.int32)):
+        assert L.cc_objective(hg, L.ClusteringParams(0.85), lab) == O.objective(g, None, 0.85, lab)
+    hw = rand_weighted(rng, 2000, 0.01)
+    gw = og(hw)
+    Cw, _ = clustered_state(rng, gw.n, 300)
+    assert L.cc_objective(hw, L.ClusteringParams(0.1), Cw) == pytest.approx(O.objective(gw, None, 0.1, Cw), rel=1e-12)
+
+
+# ------------------------------------------------------- full clustering ---
+
+def test_par_best_moves_sync_cfg1_exact():
+    hg, _ = sbm(seed=1)
+    g = og(hg)
+    C0, K0 = O.singletons(g.n, None)
+    trace0 = []
+    C0, K0, any0, _ = O.best_moves(g, None, 0.85, C0, K0, O.Opts(schedule=O.SYNC), trace0)
+    c1, any1 = L.par_best_moves(hg, L.ClusteringParams(0.85), None, L.ParOptions(schedule="sync"))
+    assert any0 == any1
+    assert np.array_equal(c1.labels(), C0)
+    assert np.array_equal(c1.cluster_mass.cpu().numpy()[:g.n], K0)
+    st = c1.meta["stats"]
+    assert st.rounds == len(trace0)
+    assert st.vertices == sum(t["F"] for t in trace0)
+    assert st.moves == sum(t["moved"] for t in trace0)
+
+
+@pytest.mark.parametrize("refine", [False, True])
+@pytest.mark.parametrize("policy", [O.ALL, O.VERTEX_NBRS, O.CLUSTER_NBRS])
+def test_parallel_cc_sync_exact(refine, policy):
+    """Config 1 semantics: unweighted sync -> bit-exact final labels."""
+    hg, _ = sbm(seed=1)
+    g = og(hg)
+    C0 = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC, frontier=policy, refine=refine))
+    cl = L.parallel_cc(hg, L.ClusteringParams(0.85),
+                       L.ParOptions(schedule="sync", frontier_policy=int(policy), refine=refine))
+    assert np.array_equal(cl.labels(), C0)
+    assert L.cc_objective(hg, L.ClusteringParams(0.85), cl) == O.objective(g, None, 0.85, C0)
+
+
+def test_parallel_cc_sync_rmat_exact():
+    u, v = rmat_pairs_host(14, 16 << 14, 0.57, 0.19, 0.19, 3)
+    hg = csr_from_pairs(1 << 14, u, v)
+    g = og(hg)
+    C0 = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC))
+    cl = L.parallel_cc(hg, L.ClusteringParams(0.85), L.ParOptions(schedule="sync"))
+    assert np.array_equal(cl.labels(), C0)
+
+
+def test_parallel_cc_weighted_sync_objective():
+    rng = np.random.default_rng(17)
+    hg = rand_weighted(rng, 3000, 0.006)
+    g = og(hg)
+    for lam in (0.01, 0.1, 0.5):
+        C0 = O.parallel_cc(g, None, lam, O.Opts(schedule=O.SYNC))
+        cl = L.parallel_cc(hg, L.ClusteringParams(lam), L.ParOptions(schedule="sync"))
+        o0 = O.objective(g, None, lam, C0)
+        o1 = L.cc_objective(hg, L.ClusteringParams(lam), cl)
+        assert o1 == pytest.approx(o0, rel=REL_W, abs=1e-9)
+
+
+def _async_check(hg, k, lam, chunks=16):
+    g = og(hg)
+    C0 = O.parallel_cc(g, k, lam, O.Opts(schedule=O.ASYNC))
+    o0 = O.objective(g, k, lam, C0)
+    p = L.ClusteringParams(lam, k)
+    cl = L.parallel_cc(hg, p, L.ParOptions(schedule="async", async_chunks=chunks))
+    o1 = L.cc_objective(hg, p, cl)
+    lab = cl.labels()
+    assert lab.min() >= 0 and lab.max() < g.n
+    assert np.all(lab[lab] == lab)               # canonical: every label is its own member
+    return o0, o1
+
+
+def test_parallel_cc_async_cfg1_objective():
+    hg, _ = sbm(seed=1)
+    o0, o1 = _async_check(hg, None, 0.85)
+    assert o1 >= o0 - 0.005 * abs(o0), (o0, o1)
+
+
+def test_parallel_cc_async_rmat_objective():
+    u, v = rmat_pairs_host(14, 16 << 14, 0.57, 0.19, 0.19, 4)
+    hg = csr_from_pairs(1 << 14, u, v)
+    o0, o1 = _async_check(hg, None, 0.85)
+    assert o1 >= o0 - 0.005 * abs(o0), (o0, o1)
+
+
+def test_parallel_cc_async_modularity_lfr():
+    hg, _ = lfr_like(n=60_000, seed=5)
+    g = og(hg)
+    k, lam = O.modularity_params(g, 1.0)
+    o0, o1 = _async_check(hg, k, lam)
+    assert o1 >= o0 - 0.005 * abs(o0), (o0, o1)
+
+
+def test_spec_kats_through_gpu_api():
+    # Figure 1 pathology (acceptance #4), two cliques
+    class G:
+        pass
+    f = G()
+    f.n, f.indptr = 3, np.array([0, 2, 4, 6])
+    f.indices = np.array([1, 2, 0, 2, 0, 1], np.int32)
+    f.weights = np.array([1.0, 1.0, 1.0, -3.0, 1.0, -3.0])
+    f.total_weight = -1.0
+    p0 = L.ClusteringParams(0.0)
+    c = L.singletons(3, p0)
+    mb = L.best_moves_round(f, p0, c, frontier=[1, 2])
+    assert list(mb.desired.cpu().numpy()) == [0, 0, 0]
+    assert L.cc_objective(f, p0, np.zeros(3, np.int32)) == -1.0
+    edges = [(b + i, b + j) for b in (0, 4) for i in range(4) for j in range(i + 1, 4)] + [(3, 4)]
+    hg = csr_from_pairs(8, np.array([e[0] for e in edges]), np.array([e[1] for e in edges]))
+    for sched in ("sync", "async"):
+        cl = L.parallel_cc(hg, L.ClusteringParams(0.4), L.ParOptions(schedule=sched))
+        assert list(cl.labels()) == [0] * 4 + [4] * 4
+        assert L.cc_objective(hg, L.ClusteringParams(0.4), cl) == pytest.approx(7.2)
+    # empty-edge graph -> singletons
+    e = csr_from_pairs(6, np.array([], np.int64), np.array([], np.int64))
+    cl = L.parallel_cc(e, L.ClusteringParams(0.5))
+    assert list(cl.labels()) == list(range(6))
+
+
+def test_errors():
+    hg, _ = sbm(seed=1)
+    with pytest.raises(L.GraphError):
+        L.ClusteringParams(1.5)
+    with pytest.raises(L.GraphError):
+        L.cc_objective(hg, L.ClusteringParams(0.5), np.zeros(5, np.int32))
+    with pytest.raises(L.GraphError):
+        L.ParOptions(num_iter=0)
+    with pytest.raises(L.GraphError):
+        L.parallel_cc(hg, L.ClusteringParams(0.5, np.ones(3)))
+
+
+def test_device_rmat_matches_host_stream():
+    d = rmat_device(scale=12, edge_factor=16, seed=7)
+    u, v = rmat_pairs_host(12, 16 << 12, 0.57, 0.19, 0.19, 7)
+    hg = csr_from_pairs(1 << 12, u, v)
+    assert np.array_equal(d.indptr.cpu().numpy(), hg.indptr)
+    assert np.array_equal(d.indices.cpu().numpy(), hg.indices)

@@ -85,12 +85,17 @@ typedef struct {
     int64_t vertices;      /* sum of |V'| over rounds                    */
     int64_t edges_scanned; /* sum of deg(v), v in V', over rounds        */
     int64_t moves;         /* sum of moved vertices over rounds          */
-    double ms_best_moves;  /* device time in best-move kernels (if timed)*/
+    double ms_best_moves;  /* device time of the best-move iterations     */
     double ms_total;       /* device time of the whole call              */
+    double ms_kernels;     /* device time of the best-move kernels alone */
+    int64_t kernel_launches; /* best-move kernel launches                */
 } lcc_stats;
 
 int lcc_abi_version(void);
 const char* lcc_last_error(void);
+/* Number of this library's own kernel launches so far in this process
+ * (diagnostics; CUB helper kernels are not counted).                       */
+int64_t lcc_kernel_launches(void);
 
 /* ---- one best-move iteration -------------------------------------------
  * Alg. 1 lines 6-8, per_vertex_best_target for every v in

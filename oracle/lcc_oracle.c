@@ -84,13 +84,16 @@ static int32_t best_target(int64_t n, const int64_t* indptr, const int32_t* indi
 
 /* Synchronous round.  D[v] = C[v] for all v, then D[v] = target for v in F.
  * moved[v] = 1 iff D[v] != C[v].  Returns number of moved vertices.
- * F == NULL means all vertices.  Labels in C must be < n (canonical).       */
+ * F == NULL means all vertices.  Labels in C must be < label_range (>= n;
+ * canonical labels are < n).                                                 */
 int64_t orc_sync_round(int64_t n, const int64_t* indptr, const int32_t* indices,
                        const double* w, const double* k, double lam,
                        const int32_t* C, const double* K,
                        const int32_t* F, int64_t nF,
-                       int32_t* D, uint8_t* moved, double* gains, int threads)
+                       int32_t* D, uint8_t* moved, double* gains, int threads,
+                       int64_t label_range)
 {
+    if (label_range < n) label_range = n;
     if (threads > 0) omp_set_num_threads(threads);
     memcpy(D, C, sizeof(int32_t) * (size_t)n);
     memset(moved, 0, (size_t)n);
@@ -103,7 +106,7 @@ int64_t orc_sync_round(int64_t n, const int64_t* indptr, const int32_t* indices,
     }
 #pragma omp parallel reduction(+ : nmoved)
     {
-        double* S = (double*)calloc((size_t)(n + 1), sizeof(double));   /* labels < n */
+        double* S = (double*)calloc((size_t)(label_range + 1), sizeof(double));
         int32_t* touched = (int32_t*)malloc(sizeof(int32_t) * (size_t)(maxdeg + 1));
 #pragma omp for schedule(dynamic, 256)
         for (int64_t i = 0; i < cnt; ++i) {

@@ -19,7 +19,7 @@ FRONTIER_ALL, FRONTIER_VERTEX_NBRS, FRONTIER_CLUSTER_NBRS = 0, 1, 2
 
 # Every symbol include/lcc_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
-    "lcc_abi_version", "lcc_last_error", "lcc_best_moves_round", "lcc_apply_moves",
+    "lcc_abi_version", "lcc_last_error", "lcc_kernel_launches", "lcc_best_moves_round", "lcc_apply_moves",
     "lcc_compute_frontier", "lcc_par_best_moves", "lcc_par_compress", "lcc_par_flatten",
     "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_build_csr_from_pairs",
 )
@@ -48,7 +48,8 @@ class LccOptions(ctypes.Structure):
 class LccStats(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("levels", ctypes.c_int64), ("vertices", ctypes.c_int64),
                 ("edges_scanned", ctypes.c_int64), ("moves", ctypes.c_int64),
-                ("ms_best_moves", ctypes.c_double), ("ms_total", ctypes.c_double)]
+                ("ms_best_moves", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("ms_kernels", ctypes.c_double), ("kernel_launches", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -77,6 +78,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "lcc_abi_version": (ctypes.c_int, []),
         "lcc_last_error": (ctypes.c_char_p, []),
+        "lcc_kernel_launches": (ctypes.c_int64, []),
         "lcc_best_moves_round": (ctypes.c_int, [G, PR, P, P, P, I64, I32, I32, I32, P, P, pI64, P]),
         "lcc_apply_moves": (ctypes.c_int, [I64, P, I64, P, P, P, P]),
         "lcc_compute_frontier": (ctypes.c_int, [G, I32, P, P, P, P, pI64, P]),

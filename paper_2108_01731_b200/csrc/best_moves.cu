@@ -486,6 +486,11 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved.get(), (int32_t)n};
     set_smem_attr<WT, ASYNC>();
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    LCC_CUDA(cudaEventCreate(&ev0));
+    LCC_CUDA(cudaEventCreate(&ev1));
+    const long long launches0 = launch_counter();
+    float kms = 0.f, kms_large = 0.f;
 
     // large bin: one pass over all large vertices (first sub-round)
     Buf<int64_t> lbuf;
@@ -510,12 +515,17 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         LCC_CUDA(cudaMemsetAsync(lkeys.get(), 0xff, sizeof(int32_t) * tot[0], s));
         LCC_CUDA(cudaMemsetAsync(lvals.get(), 0, sizeof(ValT<WT>) * tot[0], s));
         LargeLayout L{large, nL, cap_off, item_off, lkeys.get(), lvals.get()};
+        LCC_CUDA(cudaEventRecord(ev0, s));
         k_large_insert<WT, ASYNC><<<grid_for(tot[1] * LARGE_THREADS, LARGE_THREADS, 16), LARGE_THREADS, 0, s>>>(a, L, tot[1]);
         LCC_LAUNCH_CHECK();
         k_large_score<WT, ASYNC><<<grid_for(nL * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L);
         LCC_LAUNCH_CHECK();
+        LCC_CUDA(cudaEventRecord(ev1, s));
+        LCC_CUDA(cudaEventSynchronize(ev1));
+        LCC_CUDA(cudaEventElapsedTime(&kms_large, ev0, ev1));
     }
     const int P = ASYNC ? std::max(1, chunks) : 1;
+    LCC_CUDA(cudaEventRecord(ev0, s));
     for (int j = 0; j < P; ++j) {
         const int64_t s0 = nS * j / P, s1 = nS * (j + 1) / P;
         const int64_t m0 = nM * j / P, m1 = nM * (j + 1) / P;
@@ -529,9 +539,13 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             LCC_LAUNCH_CHECK();
         }
     }
+    LCC_CUDA(cudaEventRecord(ev1, s));
     unsigned long long hm = 0;
     LCC_CUDA(cudaMemcpyAsync(&hm, dmoved.get(), sizeof(hm), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
+    LCC_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (st) {
         st->vertices += nF;
         st->edges += hc[3];
@@ -539,6 +553,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         st->n_small += nS;
         st->n_medium += nM;
         st->n_large += nL;
+        st->ms_kernels += (double)kms + (double)kms_large;
+        st->launches += launch_counter() - launches0;
     }
     return (int64_t)hm;
 }

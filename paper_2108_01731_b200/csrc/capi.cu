@@ -6,6 +6,13 @@
 
 #include "internal.cuh"
 
+namespace lcc {
+long long& launch_counter() {
+    static long long c = 0;  // diagnostics only (bench.py "gpu_launches")
+    return c;
+}
+}  // namespace lcc
+
 namespace {
 thread_local std::string g_err;
 
@@ -63,6 +70,7 @@ lcc::Options to_opts(const lcc_options* o) {
 extern "C" {
 
 int lcc_abi_version(void) { return LCC_ABI_VERSION; }
+int64_t lcc_kernel_launches(void) { return lcc::launch_counter(); }
 const char* lcc_last_error(void) { return g_err.c_str(); }
 
 lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p, int32_t* C, double* K,

@@ -27,7 +27,14 @@ struct OutOfMemory : std::runtime_error { using std::runtime_error::runtime_erro
         }                                                                               \
     } while (0)
 
-#define LCC_LAUNCH_CHECK() LCC_CUDA(cudaGetLastError())
+// Every launch of one of this library's kernels is followed by
+// LCC_LAUNCH_CHECK(), which also counts it (lcc_kernel_launches()).
+long long& launch_counter();
+#define LCC_LAUNCH_CHECK()                     \
+    do {                                       \
+        ++::lcc::launch_counter();             \
+        LCC_CUDA(cudaGetLastError());          \
+    } while (0)
 
 #define LCC_REQUIRE(cond, msg)                                                          \
     do { if (!(cond)) throw ::lcc::Invalid(msg); } while (0)

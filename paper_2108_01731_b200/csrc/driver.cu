@@ -74,6 +74,8 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
             st->edges_scanned += rs.edges;
             st->moves += rs.moved;
             st->ms_best_moves += ms;
+            st->ms_kernels += rs.ms_kernels;
+            st->kernel_launches += rs.launches;
         }
         if (cnt == 0) break;  // Alg. 1 line 9
         any = true;

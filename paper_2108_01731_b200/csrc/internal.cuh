@@ -9,6 +9,8 @@ struct RoundStats {
     int64_t edges = 0;
     int64_t moved = 0;
     int64_t n_small = 0, n_medium = 0, n_large = 0;
+    double ms_kernels = 0.0;   // CUDA-event time of the best-move kernels
+    int64_t launches = 0;      // best-move kernel launches
 };
 
 // best_moves.cu: one best-move iteration over `frontier` (nullptr = all).

@@ -125,6 +125,8 @@ class RunStats:
     moves: int = 0
     ms_best_moves: float = 0.0
     ms_total: float = 0.0
+    ms_kernels: float = 0.0
+    kernel_launches: int = 0
     extra: dict = field(default_factory=dict)
 
 

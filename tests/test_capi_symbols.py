@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     hdr = open(os.path.join(ROOT, "include", "lcc_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:lcc_status|int|const char\*)\s+(lcc_\w+)\s*\(", hdr, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:lcc_status|int|int64_t|const char\*)\s+(lcc_\w+)\s*\(", hdr, re.M)))
 
 
 def test_header_matches_binding_list():

@@ -5,10 +5,13 @@
 //   id (segmented min by 32-bit atomicMin), then K is rebuilt from scratch
 //   with fp64 RED (exact for integer-valued k, which covers every config).
 // compute_frontier: AllVertices / VertexNeighbors / ClusterNeighbors
-//    as a byte mask scattered by warps
-//   over the neighbour lists, then stream-compacted into sorted ids.
+//    as a byte mask scattered over the
+//   contributing vertices' neighbour lists by the edge-balanced map
+//   (edgemap.cuh: hubs cost the same per edge as leaves), then
+//   stream-compacted into sorted ids.
 #include <cub/cub.cuh>
 
+#include "edgemap.cuh"
 #include "internal.cuh"
 #include "prims.cuh"
 
@@ -43,17 +46,33 @@ __global__ void k_relabel_mass(const int32_t* __restrict__ L, const int32_t* __r
     }
 }
 
-// one warp per listed vertex: mark all neighbours
-__global__ void k_mark_nbrs_of_moved(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                                     const uint8_t* __restrict__ moved, int64_t n, uint8_t* mark) {
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    for (int64_t v = gw; v < n; v += nw) {
-        if (!moved[v]) continue;
-        for (int64_t e = indptr[v] + lane; e < indptr[v + 1]; e += 32) mark[indices[e]] = 1;
+// degree of v if v contributes its neighbours to the frontier, else 0
+struct MovedDeg {
+    const int64_t* indptr;
+    const uint8_t* moved;
+    int64_t n;
+    __device__ __forceinline__ int64_t operator()(int64_t v) const {
+        return (v < n && moved[v]) ? indptr[v + 1] - indptr[v] : 0;
     }
-}
+};
+struct ClusterDeg {
+    const int64_t* indptr;
+    const int32_t* Cold;
+    const int32_t* Cnew;
+    const uint8_t* src;
+    const uint8_t* dst;
+    int64_t n;
+    __device__ __forceinline__ int64_t operator()(int64_t u) const {
+        return (u < n && (src[Cold[u]] || dst[Cnew[u]])) ? indptr[u + 1] - indptr[u] : 0;
+    }
+};
+// edge functor: mark the neighbour
+struct MarkNbr {
+    const int32_t* indices;
+    uint8_t* mark;
+    __device__ __forceinline__ void operator()(int64_t, int64_t e) const { mark[__ldg(indices + e)] = 1; }
+    __device__ __forceinline__ void flush() const {}
+};
 
 __global__ void k_cluster_flags(const uint8_t* __restrict__ moved, const int32_t* __restrict__ Cold,
                                 const int32_t* __restrict__ Cnew, int64_t n, uint8_t* src, uint8_t* dst) {
@@ -61,20 +80,10 @@ __global__ void k_cluster_flags(const uint8_t* __restrict__ moved, const int32_t
         if (moved[v]) { src[Cold[v]] = 1; dst[Cnew[v]] = 1; }
 }
 
-__global__ void k_mark_cluster_nbrs(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                                    const int32_t* __restrict__ Cold, const int32_t* __restrict__ Cnew,
-                                    const uint8_t* __restrict__ src, const uint8_t* __restrict__ dst,
-                                    int64_t n, uint8_t* mark) {
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    for (int64_t u = gw; u < n; u += nw) {
-        const bool d = dst[Cnew[u]];
-        const bool sflag = src[Cold[u]];
-        if (d && lane == 0) mark[u] = 1;
-        if (!(d || sflag)) continue;
-        for (int64_t e = indptr[u] + lane; e < indptr[u + 1]; e += 32) mark[indices[e]] = 1;
-    }
+__global__ void k_mark_dst_members(const int32_t* __restrict__ Cnew, const uint8_t* __restrict__ dst, int64_t n,
+                                   uint8_t* mark) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        if (dst[Cnew[u]]) mark[u] = 1;
 }
 
 }  // namespace
@@ -124,18 +133,27 @@ int64_t compute_frontier(const lcc_graph& g, int policy, const uint8_t* moved, c
     }
     Buf<uint8_t> mark(n, s);
     LCC_CUDA(cudaMemsetAsync(mark.get(), 0, n, s));
+    Buf<int64_t> off(n + 1, s);
+    Buf<uint8_t> flags;
     if (policy == LCC_FRONTIER_VERTEX_NBRS) {
-        k_mark_nbrs_of_moved<<<grid_for(n * 32, 256, 16), 256, 0, s>>>(g.indptr, g.indices, moved, n, mark.get());
-        LCC_LAUNCH_CHECK();
+        cub::TransformInputIterator<int64_t, MovedDeg, cub::CountingInputIterator<int64_t>> degs(
+            cub::CountingInputIterator<int64_t>(0), MovedDeg{g.indptr, moved, n});
+        exclusive_sum(degs, off.get(), n + 1, s);  // entry n contributes 0 -> off[n] = total
     } else {
-        Buf<uint8_t> flags(2 * n, s);
+        flags.alloc(2 * n, s);
         LCC_CUDA(cudaMemsetAsync(flags.get(), 0, 2 * n, s));
         k_cluster_flags<<<grid_for(n, 256), 256, 0, s>>>(moved, C_old, C_new, n, flags.get(), flags.get() + n);
         LCC_LAUNCH_CHECK();
-        k_mark_cluster_nbrs<<<grid_for(n * 32, 256, 16), 256, 0, s>>>(g.indptr, g.indices, C_old, C_new,
-                                                                     flags.get(), flags.get() + n, n, mark.get());
+        k_mark_dst_members<<<grid_for(n, 256), 256, 0, s>>>(C_new, flags.get() + n, n, mark.get());
         LCC_LAUNCH_CHECK();
+        cub::TransformInputIterator<int64_t, ClusterDeg, cub::CountingInputIterator<int64_t>> degs(
+            cub::CountingInputIterator<int64_t>(0), ClusterDeg{g.indptr, C_old, C_new, flags.get(), flags.get() + n, n});
+        exclusive_sum(degs, off.get(), n + 1, s);
     }
+    int64_t total = 0;
+    LCC_CUDA(cudaMemcpyAsync(&total, off.get() + n, sizeof(total), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    edge_balanced(g.indptr, nullptr, off.get(), n, total, MarkNbr{g.indices, mark.get()}, s);
     select_flagged(cub::CountingInputIterator<int32_t>(0), mark.get(), frontier, dcnt.get(), n, s);
     int64_t h = 0;
     LCC_CUDA(cudaMemcpyAsync(&h, dcnt.get(), sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -7,18 +7,22 @@
 // plus the fresh-singleton option (gain -b, temporary id n+v, loses ties),
 // and pick the argmax with the lowest-id tie rule; move iff gain > 0.
 //
-// Degree bins (all grid-stride, grids sized to the SM count):
-//   small  deg <= 32   : one warp handles 32 consecutive frontier vertices,
-//                        packed into 32-edge windows; labels grouped with
-//                        __match_any_sync on (vertex, label); segmented
-//                        argmax by warp shuffles.  Sums run in CSR order, so
-//                        weighted sums are bit-identical to the oracle.
-//   medium deg <= M    : one CTA per vertex, open-addressing hash table in
-//                        shared memory (M set by the 227 KB/SM budget).
-//   large  deg >  M    : edges split into CHUNK-edge work items spread over
-//                        all SMs, inserting into a per-vertex hash table in
-//                        global memory (L2-resident), then one CTA per
-//                        vertex scores the table.
+// The frontier is split by degree into bins, each with a kernel whose
+// thread count matches the work (grids sized to SM count x occupancy):
+//   0  deg <= 32          : k_small, one warp packs 32 vertices into 32-edge
+//                           windows; labels grouped by __match_any_sync on
+//                           (vertex, label); segmented argmax by shuffles.
+//                           Sums run in CSR order (bit-identical to the oracle
+//                           even for weighted graphs).
+//   1-3 33 .. threshold-1 : k_group, one WARP per vertex with a 256/1024/4096
+//                           slot shared-memory hash table (the paper's
+//                           "sequential" per-vertex accumulation)
+//   4-5 threshold .. 10240: k_group, 4 or 16 warps per vertex with a 4K/16K
+//                           slot shared-memory table ("parallel hash table")
+//   6   > 10240           : hubs; edges cut into 8192-edge work items spread
+//                           over all SMs inserting into per-vertex global
+//                           tables, batched so every batch's tables stay
+//                           L2-resident (48 MB), then CTA-per-vertex scoring.
 // sync  : targets written to D (apply happens in apply.cu);
 // async : C stored and K updated with relaxed device atomics right away
 //         (the CUDA analogue of _atomics.py:37-43), the
@@ -26,6 +30,7 @@
 #include <cub/cub.cuh>
 #include <math.h>
 #include <type_traits>
+#include <vector>
 
 #include "internal.cuh"
 #include "prims.cuh"
@@ -36,8 +41,6 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_MAX = 32;
 constexpr int SMALL_THREADS = 256;
-constexpr int MED_THREADS = 512;
-constexpr int MED_SMEM = 110 * 1024;  // two CTAs per SM
 constexpr int LARGE_CHUNK = 8192;
 constexpr int LARGE_THREADS = 256;
 constexpr int SCORE_THREADS = 512;
@@ -236,7 +239,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 }
 
 // ===========================================================================
-// shared hash-table helpers (medium bin: smem, large bin: global)
+// hash-table helpers (group bins: shared memory; large bin: global memory)
 // ===========================================================================
 __device__ __forceinline__ uint32_t slot_of(int32_t x, uint32_t cap) {
     return (uint32_t)(((uint64_t)hash32((uint32_t)x) * cap) >> 32);
@@ -259,16 +262,136 @@ __device__ __forceinline__ void table_insert(int32_t* keys, VT* vals, uint32_t c
     else atomicAdd(vals + h, (VT)1);
 }
 
-template <class VT>
-__device__ __forceinline__ double table_lookup(const int32_t* keys, const VT* vals, uint32_t cap, int32_t x) {
-    uint32_t h = slot_of(x, cap);
-    for (uint32_t probes = 0; probes < cap; ++probes) {
-        const int32_t kq = keys[h];
-        if (kq == x) return (double)vals[h];
-        if (kq == EMPTY_KEY) return 0.0;
-        h = (h + 1 == cap) ? 0 : h + 1;
+template <class WT>
+using ValT = typename std::conditional<WLoad<WT>::weighted, double, int32_t>::type;
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ===========================================================================
+// group bins: GW warps per vertex, CAP-slot shared-memory table per group
+// ===========================================================================
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
+__global__ void __launch_bounds__(GW * 32 * GROUPS)
+k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
+    using VT = ValT<WT>;
+    constexpr int GT = GW * 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_g[GROUPS * GW];
+    __shared__ int32_t s_x[GROUPS * GW];
+    const int gid = threadIdx.x / GT;
+    const int gt = threadIdx.x % GT;
+    const int wig = gt >> 5;
+    const int lane = threadIdx.x & 31;
+    VT* vals = reinterpret_cast<VT*>(smem) + (size_t)gid * CAP;
+    int32_t* keys = reinterpret_cast<int32_t*>(reinterpret_cast<VT*>(smem) + (size_t)GROUPS * CAP) + (size_t)gid * CAP;
+    auto gsync = [&]() {
+        if constexpr (GW == 1) __syncwarp();
+        else named_sync(1 + gid, GT);
+    };
+    unsigned long long my_moves = 0;
+    for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += (int64_t)gridDim.x * GROUPS) {
+        const int32_t v = __ldg(list + i);
+        const int64_t s = __ldg(a.indptr + v);
+        const int64_t deg = __ldg(a.indptr + v + 1) - s;
+        const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
+        for (uint32_t q = gt; q < cap; q += GT) { keys[q] = EMPTY_KEY; vals[q] = (VT)0; }
+        const int32_t c = ldC<ASYNC>(a.C, v);
+        const double kv = kval(a.k, v);
+        const double Kc = ldK<ASYNC>(a.K, c);
+        const double t = dmul(a.lam, kv);
+        gsync();
+        double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
+        for (int64_t e = s + gt; e < s + deg; e += GT) {
+            const int32_t x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
+            const double wv = WLoad<WT>::at(a.w, e);
+            if (x == c) sc += wv;
+            else table_insert<VT>(keys, vals, cap, x, wv);
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
+        if constexpr (GW > 1) {
+            if (lane == 0) s_g[gid * GW + wig] = sc;
+        }
+        gsync();
+        if constexpr (GW > 1) {
+            sc = 0.0;
+#pragma unroll
+            for (int w = 0; w < GW; ++w) sc += s_g[gid * GW + w];
+        }
+        const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
+        double bg = -INFINITY;
+        int32_t bx = NO_CAND;
+        for (uint32_t q = gt; q < cap; q += GT) {
+            const int32_t x = keys[q];
+            if (x != EMPTY_KEY) {
+                const double gq = dsub(dsub((double)vals[q], dmul(t, ldK<ASYNC>(a.K, x))), b);
+                if (better(gq, x, bg, bx)) { bg = gq; bx = x; }
+            }
+        }
+        warp_argmax(bg, bx);
+        if constexpr (GW > 1) {
+            gsync();  // everyone has read s_g (S_c) before it is reused
+            if (lane == 0) { s_g[gid * GW + wig] = bg; s_x[gid * GW + wig] = bx; }
+            gsync();
+#pragma unroll
+            for (int w = 0; w < GW; ++w) {
+                const double og = s_g[gid * GW + w];
+                const int32_t ox = s_x[gid * GW + w];
+                if (better(og, ox, bg, bx)) { bg = og; bx = ox; }
+            }
+        }
+        if (gt == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
+        gsync();  // table and s_g free for the next vertex
     }
-    return 0.0;
+    flush_moves(a, my_moves);
+}
+
+// ===========================================================================
+// large bin: vertices batched so that their global tables fit in L2; each
+// batch = multi-CTA insertion over CHUNK-edge work items + CTA-per-vertex
+// scoring.
+// ===========================================================================
+struct LargeBatch {
+    const int32_t* list;      // batch vertices
+    int64_t nL;
+    const int64_t* cap_off;   // [nL+1]
+    const int64_t* item_off;  // [nL+1]
+    int32_t* keys;
+    void* vals;
+    double* sc;               // [nL] S_c per vertex (own-cluster weight)
+};
+
+template <class WT, bool ASYNC>
+__global__ void __launch_bounds__(LARGE_THREADS)
+k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
+    using VT = ValT<WT>;
+    for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
+        int64_t lo = 0, hi = L.nL;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (L.item_off[mid] <= it) lo = mid; else hi = mid;
+        }
+        const int32_t v = L.list[lo];
+        const int64_t s = a.indptr[v], e_end = a.indptr[v + 1];
+        const int64_t e0 = s + (it - L.item_off[lo]) * LARGE_CHUNK;
+        const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
+        const uint32_t cap = (uint32_t)(L.cap_off[lo + 1] - L.cap_off[lo]);
+        int32_t* keys = L.keys + L.cap_off[lo];
+        VT* vals = static_cast<VT*>(L.vals) + L.cap_off[lo];
+        const int32_t c = ldC<ASYNC>(a.C, v);
+        double sc = 0.0;
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += LARGE_THREADS) {
+            const int32_t x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
+            const double wv = WLoad<WT>::at(a.w, e);
+            if (x == c) sc += wv;
+            else table_insert<VT>(keys, vals, cap, x, wv);
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
+        if ((threadIdx.x & 31) == 0 && sc != 0.0) atomicAdd(L.sc + lo, sc);
+    }
 }
 
 template <int THREADS>
@@ -284,120 +407,12 @@ __device__ __forceinline__ void block_argmax(double& g, int32_t& x, double* s_g,
     }
 }
 
-template <class WT>
-using ValT = typename std::conditional<WLoad<WT>::weighted, double, int32_t>::type;
-
-template <class WT>
-constexpr int med_capacity() {
-    return (MED_SMEM - 64) / (int)(sizeof(int32_t) + sizeof(ValT<WT>));
-}
-
-// ===========================================================================
-// medium bin: one CTA per vertex, shared-memory hash table
-// ===========================================================================
-template <class WT, bool ASYNC>
-__global__ void __launch_bounds__(MED_THREADS, 2)
-k_medium(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
-    using VT = ValT<WT>;
-    constexpr int CAP = med_capacity<WT>();
-    extern __shared__ __align__(16) unsigned char smem[];
-    VT* vals = reinterpret_cast<VT*>(smem);
-    int32_t* keys = reinterpret_cast<int32_t*>(vals + CAP);
-    __shared__ double s_g[MED_THREADS / 32];
-    __shared__ int32_t s_x[MED_THREADS / 32];
-    __shared__ double s_sc;
-    unsigned long long my_moves = 0;
-
-    for (int64_t i = lo + blockIdx.x; i < hi; i += gridDim.x) {
-        const int32_t v = __ldg(list + i);
-        const int64_t s = __ldg(a.indptr + v);
-        const int64_t deg = __ldg(a.indptr + v + 1) - s;
-        const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
-        for (uint32_t q = threadIdx.x; q < cap; q += MED_THREADS) { keys[q] = EMPTY_KEY; vals[q] = (VT)0; }
-        const int32_t c = ldC<ASYNC>(a.C, v);
-        const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC>(a.K, c);
-        const double t = dmul(a.lam, kv);
-        __syncthreads();
-        for (int64_t e = s + threadIdx.x; e < s + deg; e += MED_THREADS) {
-            const int32_t x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
-            table_insert<VT>(keys, vals, cap, x, WLoad<WT>::at(a.w, e));
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_sc = table_lookup<VT>(keys, vals, cap, c);
-        __syncthreads();
-        const double b = dadd(dsub(s_sc, dmul(t, Kc)), dmul(t, kv));
-        double bg = -INFINITY;
-        int32_t bx = NO_CAND;
-        for (uint32_t q = threadIdx.x; q < cap; q += MED_THREADS) {
-            const int32_t x = keys[q];
-            if (x != EMPTY_KEY && x != c) {
-                const double gq = dsub(dsub((double)vals[q], dmul(t, ldK<ASYNC>(a.K, x))), b);
-                if (better(gq, x, bg, bx)) { bg = gq; bx = x; }
-            }
-        }
-        block_argmax<MED_THREADS>(bg, bx, s_g, s_x);
-        if (threadIdx.x == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
-        __syncthreads();
-    }
-    if (threadIdx.x < 32) flush_moves(a, my_moves);
-}
-
-// ===========================================================================
-// large bin: multi-CTA insertion into global hash tables, CTA-per-vertex scoring
-// ===========================================================================
-struct LargeLayout {
-    const int32_t* list;     // large-bin vertices
-    int64_t nL;
-    const int64_t* cap_off;  // [nL+1] table offsets
-    const int64_t* item_off; // [nL+1] work-item offsets
-    int32_t* keys;
-    void* vals;
-};
-
-__global__ void k_large_sizes(const int64_t* __restrict__ indptr, const int32_t* __restrict__ list,
-                              int64_t nL, int64_t* caps, int64_t* items) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nL; i += (int64_t)gridDim.x * blockDim.x) {
-        if (i == nL) { caps[i] = 0; items[i] = 0; continue; }
-        const int32_t v = list[i];
-        const int64_t deg = indptr[v + 1] - indptr[v];
-        caps[i] = (2 * deg + 31) & ~31LL;
-        items[i] = (deg + LARGE_CHUNK - 1) / LARGE_CHUNK;
-    }
-}
-
-template <class WT, bool ASYNC>
-__global__ void __launch_bounds__(LARGE_THREADS)
-k_large_insert(BMArgs a, LargeLayout L, int64_t total_items) {
-    using VT = ValT<WT>;
-    for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
-        // owner: last li with item_off[li] <= it
-        int64_t lo = 0, hi = L.nL;  // item_off[0] = 0 <= it < item_off[nL]
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (L.item_off[mid] <= it) lo = mid; else hi = mid;
-        }
-        const int32_t v = L.list[lo];
-        const int64_t s = a.indptr[v], e_end = a.indptr[v + 1];
-        const int64_t e0 = s + (it - L.item_off[lo]) * LARGE_CHUNK;
-        const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
-        const uint32_t cap = (uint32_t)(L.cap_off[lo + 1] - L.cap_off[lo]);
-        int32_t* keys = L.keys + L.cap_off[lo];
-        VT* vals = static_cast<VT*>(L.vals) + L.cap_off[lo];
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += LARGE_THREADS) {
-            const int32_t x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
-            table_insert<VT>(keys, vals, cap, x, WLoad<WT>::at(a.w, e));
-        }
-    }
-}
-
 template <class WT, bool ASYNC>
 __global__ void __launch_bounds__(SCORE_THREADS)
-k_large_score(BMArgs a, LargeLayout L) {
+k_large_score(BMArgs a, LargeBatch L) {
     using VT = ValT<WT>;
     __shared__ double s_g[SCORE_THREADS / 32];
     __shared__ int32_t s_x[SCORE_THREADS / 32];
-    __shared__ double s_sc;
     unsigned long long my_moves = 0;
     for (int64_t li = blockIdx.x; li < L.nL; li += gridDim.x) {
         const int32_t v = L.list[li];
@@ -408,14 +423,12 @@ k_large_score(BMArgs a, LargeLayout L) {
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC>(a.K, c);
         const double t = dmul(a.lam, kv);
-        if (threadIdx.x == 0) s_sc = table_lookup<VT>(keys, vals, cap, c);
-        __syncthreads();
-        const double b = dadd(dsub(s_sc, dmul(t, Kc)), dmul(t, kv));
+        const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
         for (uint32_t q = threadIdx.x; q < cap; q += SCORE_THREADS) {
             const int32_t x = keys[q];
-            if (x != EMPTY_KEY && x != c) {
+            if (x != EMPTY_KEY) {
                 const double gq = dsub(dsub((double)vals[q], dmul(t, ldK<ASYNC>(a.K, x))), b);
                 if (better(gq, x, bg, bx)) { bg = gq; bx = x; }
             }
@@ -427,36 +440,139 @@ k_large_score(BMArgs a, LargeLayout L) {
     if (threadIdx.x < 32) flush_moves(a, my_moves);
 }
 
-// ---- degree predicates for the bin partition -----------------------------
-struct DegBetween {
-    const int64_t* indptr;
-    int64_t lo, hi;  // lo < deg <= hi
-    __device__ __forceinline__ bool operator()(int32_t v) const {
-        const int64_t d = indptr[v + 1] - indptr[v];
-        return d > lo && d <= hi;
-    }
-};
-struct DegOf {
-    const int64_t* indptr;
-    __device__ __forceinline__ int64_t operator()(int32_t v) const { return indptr[v + 1] - indptr[v]; }
+// ===========================================================================
+// degree-bin partition (one pass, block-aggregated reservations)
+// ===========================================================================
+constexpr int NBINS = 7;
+struct BinEdges {
+    int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
 
-template <class It>
-void partition_bins(It in, int64_t nF, const int64_t* indptr, int64_t med_max, int32_t* small,
-                    int32_t* med, int32_t* large, int64_t* d_counts, cudaStream_t s) {
-    select_if(in, small, d_counts + 0, nF, DegBetween{indptr, -1, SMALL_MAX}, s);
-    select_if(in, med, d_counts + 1, nF, DegBetween{indptr, SMALL_MAX, med_max}, s);
-    select_if(in, large, d_counts + 2, nF, DegBetween{indptr, med_max, INT64_MAX}, s);
-    cub::TransformInputIterator<int64_t, DegOf, It> degs(in, DegOf{indptr});
-    device_sum(degs, d_counts + 3, nF, s);
+__global__ void k_bin(const int64_t* __restrict__ indptr, const int32_t* __restrict__ frontier, int64_t nF,
+                      BinEdges be, int32_t* __restrict__ out, int64_t stride, unsigned long long* counts) {
+    __shared__ unsigned s_cnt[NBINS];
+    __shared__ unsigned long long s_base[NBINS];
+    __shared__ unsigned long long s_edges;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nF; base += (int64_t)gridDim.x * blockDim.x) {
+        if (threadIdx.x < NBINS) s_cnt[threadIdx.x] = 0;
+        if (threadIdx.x == 0) s_edges = 0;
+        __syncthreads();
+        const int64_t i = base + threadIdx.x;
+        int bin = -1;
+        unsigned slot = 0;
+        int32_t v = 0;
+        if (i < nF) {
+            v = frontier ? frontier[i] : (int32_t)i;
+            const int64_t d = indptr[v + 1] - indptr[v];
+            bin = 0;
+#pragma unroll
+            for (int b = 0; b < NBINS - 1; ++b) bin += d > be.hi[b] ? 1 : 0;
+            slot = atomicAdd(&s_cnt[bin], 1u);
+            atomicAdd(&s_edges, (unsigned long long)d);
+        }
+        __syncthreads();
+        if (threadIdx.x < NBINS) s_base[threadIdx.x] = atomicAdd(counts + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
+        if (threadIdx.x == NBINS) atomicAdd(counts + NBINS, s_edges);
+        __syncthreads();
+        if (bin >= 0) out[bin * stride + s_base[bin] + slot] = v;
+        __syncthreads();
+    }
+}
+
+__global__ void k_degrees_of(const int64_t* __restrict__ indptr, const int32_t* __restrict__ list, int64_t n,
+                             int64_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = list[i];
+        out[i] = indptr[v + 1] - indptr[v];
+    }
+}
+
+template <class K>
+void set_smem(K kernel, int bytes) {
+    LCC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
+void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
+    if (hi <= lo) return;
+    constexpr int THREADS = GW * 32 * GROUPS;
+    constexpr int SMEM = GROUPS * CAP * (int)(sizeof(int32_t) + sizeof(ValT<WT>));
+    static bool attr = false;
+    if (!attr) { set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS>, SMEM); attr = true; }
+    int occ = 0;
+    LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS>, THREADS, SMEM));
+    occ = std::max(occ, 1);
+    const int64_t blocks_needed = (hi - lo + GROUPS - 1) / GROUPS;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * occ));
+    k_group<WT, ASYNC, GW, CAP, GROUPS><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
+    LCC_LAUNCH_CHECK();
+}
+
+constexpr int B5_CAP = 16384;
+constexpr int64_t MED_MAX = (B5_CAP * 5) / 8;  // 10240: load factor <= 0.625
+constexpr int64_t LARGE_TABLE_BYTES = 48ll << 20;  // per batch: stays L2-resident
+
+template <class WT, bool ASYNC>
+void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
+    switch (bin) {
+        case 1: launch_group<WT, ASYNC, 1, 256, 8>(a, list, lo, hi, s); break;
+        case 2: launch_group<WT, ASYNC, 1, 1024, 8>(a, list, lo, hi, s); break;
+        case 3: launch_group<WT, ASYNC, 1, 4096, 4>(a, list, lo, hi, s); break;
+        case 4: launch_group<WT, ASYNC, 4, 4096, 2>(a, list, lo, hi, s); break;
+        case 5: launch_group<WT, ASYNC, 16, B5_CAP, 1>(a, list, lo, hi, s); break;
+        default: break;
+    }
 }
 
 template <class WT, bool ASYNC>
-void set_smem_attr() {
-    static bool done = false;
-    if (!done) {
-        LCC_CUDA(cudaFuncSetAttribute(k_medium<WT, ASYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, MED_SMEM));
-        done = true;
+void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_t nL, cudaStream_t s) {
+    using VT = ValT<WT>;
+    // degrees to the host, plan L2-sized batches
+    Buf<int64_t> ddeg(nL, s);
+    k_degrees_of<<<grid_for(nL, 256), 256, 0, s>>>(g.indptr, large, nL, ddeg.get());
+    LCC_LAUNCH_CHECK();
+    std::vector<int64_t> deg(nL);
+    LCC_CUDA(cudaMemcpyAsync(deg.data(), ddeg.get(), sizeof(int64_t) * nL, cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    const int64_t slot_bytes = sizeof(int32_t) + sizeof(VT);
+    const int64_t budget = LARGE_TABLE_BYTES / slot_bytes;
+    int64_t maxcap = 0;
+    for (int64_t d : deg) maxcap = std::max<int64_t>(maxcap, (2 * d + 31) & ~31LL);
+    const int64_t table_slots = std::max<int64_t>(budget, maxcap);
+    Buf<int32_t> keys(table_slots, s);
+    Buf<unsigned char> vals(table_slots * sizeof(VT), s);
+    Buf<int64_t> offs(2 * (nL + 1), s);
+    Buf<double> sc(nL, s);
+    std::vector<int64_t> h_cap(nL + 1), h_item(nL + 1);
+    int64_t b0 = 0;
+    while (b0 < nL) {
+        // greedy batch [b0, b1) with sum(cap) <= table_slots
+        int64_t b1 = b0, slots = 0, items = 0;
+        while (b1 < nL) {
+            const int64_t cap = (2 * deg[b1] + 31) & ~31LL;
+            if (b1 > b0 && slots + cap > table_slots) break;
+            h_cap[b1 - b0] = slots;
+            h_item[b1 - b0] = items;
+            slots += cap;
+            items += (deg[b1] + LARGE_CHUNK - 1) / LARGE_CHUNK;
+            ++b1;
+        }
+        const int64_t nb = b1 - b0;
+        h_cap[nb] = slots;
+        h_item[nb] = items;
+        LCC_CUDA(cudaMemcpyAsync(offs.get(), h_cap.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
+        LCC_CUDA(cudaMemcpyAsync(offs.get() + (nL + 1), h_item.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
+        LCC_CUDA(cudaMemsetAsync(keys.get(), 0xff, sizeof(int32_t) * slots, s));
+        LCC_CUDA(cudaMemsetAsync(vals.get(), 0, sizeof(VT) * slots, s));
+        LCC_CUDA(cudaMemsetAsync(sc.get(), 0, sizeof(double) * nb, s));
+        LargeBatch L{large + b0, nb, offs.get(), offs.get() + (nL + 1), keys.get(), vals.get(), sc.get()};
+        k_large_insert<WT, ASYNC><<<grid_for(items * LARGE_THREADS, LARGE_THREADS, 16), LARGE_THREADS, 0, s>>>(a, L, items);
+        LCC_LAUNCH_CHECK();
+        k_large_score<WT, ASYNC><<<grid_for(nb * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L);
+        LCC_LAUNCH_CHECK();
+        // the host-side offset vectors are rewritten next batch: keep ordering
+        LCC_CUDA(cudaStreamSynchronize(s));
+        b0 = b1;
     }
 }
 
@@ -465,61 +581,45 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
                   const int32_t* frontier, int64_t nF, int deg_threshold, int chunks, int32_t* D,
                   uint8_t* moved, RoundStats* st, cudaStream_t s) {
     const int64_t n = g.n;
-    constexpr int64_t CAP = med_capacity<WT>();
-    const int64_t med_max = std::max<int64_t>((int64_t)deg_threshold, (CAP * 2) / 3);
     if (!ASYNC) LCC_CUDA(cudaMemcpyAsync(D, C, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
     LCC_CUDA(cudaMemsetAsync(moved, 0, n, s));
 
-    Buf<int32_t> lists(3 * (size_t)std::max<int64_t>(nF, 1), s);
-    int32_t* small = lists.get();
-    int32_t* med = small + nF;
-    int32_t* large = med + nF;
-    Buf<int64_t> dcnt(4, s);
-    Buf<unsigned long long> dmoved(1, s);
-    LCC_CUDA(cudaMemsetAsync(dmoved.get(), 0, sizeof(unsigned long long), s));
-    if (frontier) partition_bins(frontier, nF, g.indptr, med_max, small, med, large, dcnt.get(), s);
-    else partition_bins(cub::CountingInputIterator<int32_t>(0), nF, g.indptr, med_max, small, med, large, dcnt.get(), s);
-    int64_t hc[4];
+    // bin boundaries: warp paths below the degree threshold, CTA paths above
+    // (the paper's sequential-vs-parallel hash-table switch)
+    const int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), 2048);
+    BinEdges be;
+    be.hi[0] = SMALL_MAX;
+    be.hi[1] = std::min<int64_t>(128, T - 1);
+    be.hi[2] = std::min<int64_t>(512, T - 1);
+    be.hi[3] = T - 1;
+    be.hi[4] = 2048;
+    be.hi[5] = MED_MAX;
+    be.hi[6] = INT64_MAX;
+
+    const int64_t stride = std::max<int64_t>(nF, 1);
+    Buf<int32_t> lists(NBINS * stride, s);
+    Buf<unsigned long long> dcnt(NBINS + 2, s);
+    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * (NBINS + 2), s));
+    unsigned long long* dmoved = dcnt.get() + NBINS + 1;
+    if (nF > 0) {
+        k_bin<<<grid_for(nF, 256, 8), 256, 0, s>>>(g.indptr, frontier, nF, be, lists.get(), stride, dcnt.get());
+        LCC_LAUNCH_CHECK();
+    }
+    unsigned long long hc[NBINS + 1];
     LCC_CUDA(cudaMemcpyAsync(hc, dcnt.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
-    const int64_t nS = hc[0], nM = hc[1], nL = hc[2];
 
-    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved.get(), (int32_t)n};
-    set_smem_attr<WT, ASYNC>();
+    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreate(&ev0));
     LCC_CUDA(cudaEventCreate(&ev1));
     const long long launches0 = launch_counter();
     float kms = 0.f, kms_large = 0.f;
 
-    // large bin: one pass over all large vertices (first sub-round)
-    Buf<int64_t> lbuf;
-    Buf<int32_t> lkeys;
-    Buf<unsigned char> lvals;
+    const int64_t nL = (int64_t)hc[NBINS - 1];
     if (nL > 0) {
-        lbuf.alloc(2 * (nL + 1) * 2, s);
-        int64_t* caps = lbuf.get();
-        int64_t* items = caps + (nL + 1);
-        int64_t* cap_off = items + (nL + 1);
-        int64_t* item_off = cap_off + (nL + 1);
-        k_large_sizes<<<grid_for(nL + 1, 256), 256, 0, s>>>(g.indptr, large, nL, caps, items);
-        LCC_LAUNCH_CHECK();
-        exclusive_sum(caps, cap_off, nL + 1, s);
-        exclusive_sum(items, item_off, nL + 1, s);
-        int64_t tot[2];
-        LCC_CUDA(cudaMemcpyAsync(&tot[0], cap_off + nL, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        LCC_CUDA(cudaMemcpyAsync(&tot[1], item_off + nL, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        LCC_CUDA(cudaStreamSynchronize(s));
-        lkeys.alloc(tot[0], s);
-        lvals.alloc(tot[0] * sizeof(ValT<WT>), s);
-        LCC_CUDA(cudaMemsetAsync(lkeys.get(), 0xff, sizeof(int32_t) * tot[0], s));
-        LCC_CUDA(cudaMemsetAsync(lvals.get(), 0, sizeof(ValT<WT>) * tot[0], s));
-        LargeLayout L{large, nL, cap_off, item_off, lkeys.get(), lvals.get()};
         LCC_CUDA(cudaEventRecord(ev0, s));
-        k_large_insert<WT, ASYNC><<<grid_for(tot[1] * LARGE_THREADS, LARGE_THREADS, 16), LARGE_THREADS, 0, s>>>(a, L, tot[1]);
-        LCC_LAUNCH_CHECK();
-        k_large_score<WT, ASYNC><<<grid_for(nL * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L);
-        LCC_LAUNCH_CHECK();
+        run_large<WT, ASYNC>(a, g, lists.get() + (NBINS - 1) * stride, nL, s);
         LCC_CUDA(cudaEventRecord(ev1, s));
         LCC_CUDA(cudaEventSynchronize(ev1));
         LCC_CUDA(cudaEventElapsedTime(&kms_large, ev0, ev1));
@@ -527,31 +627,33 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const int P = ASYNC ? std::max(1, chunks) : 1;
     LCC_CUDA(cudaEventRecord(ev0, s));
     for (int j = 0; j < P; ++j) {
-        const int64_t s0 = nS * j / P, s1 = nS * (j + 1) / P;
-        const int64_t m0 = nM * j / P, m1 = nM * (j + 1) / P;
-        if (s1 > s0) {
-            const int64_t warps = (s1 - s0 + 31) / 32;
-            k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, s>>>(a, small, s0, s1);
-            LCC_LAUNCH_CHECK();
-        }
-        if (m1 > m0) {
-            k_medium<WT, ASYNC><<<grid_for((m1 - m0) * MED_THREADS, MED_THREADS, 2), MED_THREADS, MED_SMEM, s>>>(a, med, m0, m1);
-            LCC_LAUNCH_CHECK();
+        for (int b = 0; b < NBINS - 1; ++b) {
+            const int64_t nb = (int64_t)hc[b];
+            const int64_t lo = nb * j / P, hi = nb * (j + 1) / P;
+            if (hi <= lo) continue;
+            const int32_t* list = lists.get() + b * stride;
+            if (b == 0) {
+                const int64_t warps = (hi - lo + 31) / 32;
+                k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, s>>>(a, list, lo, hi);
+                LCC_LAUNCH_CHECK();
+            } else {
+                launch_bin<WT, ASYNC>(b, a, list, lo, hi, s);
+            }
         }
     }
     LCC_CUDA(cudaEventRecord(ev1, s));
     unsigned long long hm = 0;
-    LCC_CUDA(cudaMemcpyAsync(&hm, dmoved.get(), sizeof(hm), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaMemcpyAsync(&hm, dmoved, sizeof(hm), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
     LCC_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     if (st) {
         st->vertices += nF;
-        st->edges += hc[3];
+        st->edges += (int64_t)hc[NBINS];
         st->moved += (int64_t)hm;
-        st->n_small += nS;
-        st->n_medium += nM;
+        st->n_small += (int64_t)hc[0];
+        st->n_medium += (int64_t)(hc[1] + hc[2] + hc[3] + hc[4] + hc[5]);
         st->n_large += nL;
         st->ms_kernels += (double)kms + (double)kms_large;
         st->launches += launch_counter() - launches0;

@@ -11,6 +11,7 @@
 // build_graph_arrays (graph.py:126-164).
 #include <cub/cub.cuh>
 
+#include "edgemap.cuh"
 #include "internal.cuh"
 #include "prims.cuh"
 
@@ -32,42 +33,44 @@ __global__ void k_map(const int32_t* __restrict__ C, const int32_t* __restrict__
     }
 }
 
+// edge functor: key of the directed entry (v, u), intra entries -> sentinel
 template <class WT>
-__global__ void k_edge_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                            const void* __restrict__ w, const int32_t* __restrict__ mapping, int64_t n,
-                            int bits, uint64_t* keys, double* vals, unsigned long long* intra_cnt,
-                            double* intra_w) {
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
+struct EdgeKey {
+    const int32_t* indices;
+    const void* w;
+    const int32_t* mapping;
+    int bits;
+    uint64_t sentinel;
+    uint64_t* keys;
+    double* vals;
+    unsigned long long* intra_cnt;
+    double* intra_w;
     unsigned long long cnt = 0;
     double acc = 0.0;
-    for (int64_t v = gw; v < n; v += nw) {
-        const uint64_t a = (uint32_t)mapping[v];
-        const int64_t e1 = indptr[v + 1];
-        for (int64_t e = indptr[v] + lane; e < e1; e += 32) {
-            const uint64_t b = (uint32_t)mapping[indices[e]];
-            const double wv = WLoad<WT>::at(w, e);
-            if (a == b) {
-                keys[e] = sentinel;
-                ++cnt;
-                acc += wv;
-            } else {
-                keys[e] = (a << bits) | b;
-            }
-            if (vals) vals[e] = wv;
+    __device__ __forceinline__ void operator()(int64_t v, int64_t e) {
+        const uint64_t a = (uint32_t)__ldg(mapping + v);
+        const uint64_t b = (uint32_t)__ldg(mapping + __ldg(indices + e));
+        const double wv = WLoad<WT>::at(w, e);
+        if (a == b) {
+            keys[e] = sentinel;
+            ++cnt;
+            acc += wv;
+        } else {
+            keys[e] = (a << bits) | b;
+        }
+        if (vals) vals[e] = wv;
+    }
+    __device__ __forceinline__ void flush() {
+        for (int d = 16; d; d >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+            acc += __shfl_xor_sync(0xffffffffu, acc, d);
+        }
+        if ((threadIdx.x & 31) == 0 && cnt) {
+            atomicAdd(intra_cnt, cnt);
+            atomicAdd(intra_w, acc);
         }
     }
-    for (int d = 16; d; d >>= 1) {
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    }
-    if (lane == 0 && cnt) {
-        atomicAdd(intra_cnt, cnt);
-        atomicAdd(intra_w, acc);
-    }
-}
+};
 
 __global__ void k_emit_rows(const uint64_t* __restrict__ ukeys, int64_t R, int bits, int64_t cn,
                             int64_t* cindptr, int32_t* cindices) {
@@ -125,9 +128,10 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         Buf<uint64_t> keys(nnz, s), keys2(nnz, s);
         Buf<double> vals, vals2;
         if (WLoad<WT>::weighted) { vals.alloc(nnz, s); vals2.alloc(nnz, s); }
-        k_edge_keys<WT><<<grid_for(n * 32, 256, 16), 256, 0, s>>>(g.indptr, g.indices, g.weights, mapping, n, bits,
-                                                                  keys.get(), vals.get(), dintra.get(), dacc.get());
-        LCC_LAUNCH_CHECK();
+        const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
+        edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
+                      EdgeKey<WT>{g.indices, g.weights, mapping, bits, sentinel, keys.get(), vals.get(),
+                                  dintra.get(), dacc.get()}, s);
         // 3. stable radix sort on the 2*bits live bits
         if (WLoad<WT>::weighted) sort_pairs(keys.get(), keys2.get(), vals.get(), vals2.get(), nnz, 2 * bits, s);
         else sort_keys(keys.get(), keys2.get(), nnz, 2 * bits, s);

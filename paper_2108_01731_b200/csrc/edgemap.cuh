@@ -1,0 +1,67 @@
+// edgemap.cuh -- edge-balanced traversal of a vertex list's adjacency.
+//
+// Work is split into fixed tiles of the concatenated edge space, so a
+// 400K-degree hub costs the same per edge as a degree-3 vertex (a warp- or
+// block-per-vertex mapping leaves a single warp walking the hub).  For each
+// edge position e the owning list entry is found by a binary search of the
+// degree prefix `off` restricted to the tile's window (found once per tile).
+// `off` is the exclusive degree prefix over `list` (off[nlist] = total); for
+// the all-vertices case pass list = nullptr and off = indptr.
+#pragma once
+#include "common.cuh"
+
+namespace lcc {
+
+constexpr int EM_THREADS = 256;
+constexpr int EM_ITEMS = 8;
+constexpr int EM_TILE = EM_THREADS * EM_ITEMS;
+
+__device__ __forceinline__ int64_t upper_idx(const int64_t* off, int64_t lo, int64_t hi, int64_t e) {
+    // largest a in [lo, hi) with off[a] <= e, given off[lo] <= e
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= e) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// F: functor with  __device__ void operator()(int64_t v, int64_t e)  and
+//                  __device__ void flush()   (called once per thread at the end)
+template <class F>
+__global__ void __launch_bounds__(EM_THREADS)
+k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ list,
+                const int64_t* __restrict__ off, int64_t nlist, F f) {
+    __shared__ int64_t s_lo, s_hi;
+    const int64_t total = __ldg(off + nlist);
+    for (int64_t t0 = (int64_t)blockIdx.x * EM_TILE; t0 < total; t0 += (int64_t)gridDim.x * EM_TILE) {
+        const int64_t t1 = min64(t0 + EM_TILE, total);
+        if (threadIdx.x == 0) s_lo = upper_idx(off, 0, nlist + 1, t0);
+        if (threadIdx.x == 32) s_hi = upper_idx(off, 0, nlist + 1, t1 - 1) + 1;
+        __syncthreads();
+        const int64_t lo = s_lo, hi = s_hi;
+#pragma unroll 2
+        for (int j = 0; j < EM_ITEMS; ++j) {
+            const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+            if (e < t1) {
+                const int64_t li = upper_idx(off, lo, hi, e);
+                const int64_t v = list ? (int64_t)__ldg(list + li) : li;
+                f(v, __ldg(indptr + v) + (e - __ldg(off + li)));
+            }
+        }
+        __syncthreads();
+    }
+    f.flush();
+}
+
+template <class F>
+inline void edge_balanced(const int64_t* indptr, const int32_t* list, const int64_t* off, int64_t nlist,
+                          int64_t total_edges, F f, cudaStream_t s) {
+    if (total_edges <= 0) return;
+    const int64_t tiles = (total_edges + EM_TILE - 1) / EM_TILE;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    const unsigned grid = (unsigned)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+    k_edge_balanced<F><<<grid, EM_THREADS, 0, s>>>(indptr, list, off, nlist, f);
+    LCC_LAUNCH_CHECK();
+}
+
+}  // namespace lcc

@@ -6,6 +6,7 @@
 // (k = 1 or k = degree) and therefore exact in fp64 below 2^53.
 #include <cub/cub.cuh>
 
+#include "edgemap.cuh"
 #include "internal.cuh"
 #include "prims.cuh"
 
@@ -13,33 +14,31 @@ namespace lcc {
 namespace {
 
 template <class WT>
-__global__ void k_intra(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                        const void* __restrict__ w, const int32_t* __restrict__ C, int64_t n,
-                        unsigned long long* cnt_out, double* w_out) {
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
+struct IntraEdges {
+    const int32_t* indices;
+    const void* w;
+    const int32_t* C;
+    unsigned long long* cnt_out;
+    double* w_out;
     unsigned long long cnt = 0;
     double acc = 0.0;
-    for (int64_t v = gw; v < n; v += nw) {
-        const int32_t c = C[v];
-        const int64_t e1 = indptr[v + 1];
-        for (int64_t e = indptr[v] + lane; e < e1; e += 32) {
-            if (C[indices[e]] == c) {
-                ++cnt;
-                if (WLoad<WT>::weighted) acc += WLoad<WT>::at(w, e);
-            }
+    __device__ __forceinline__ void operator()(int64_t v, int64_t e) {
+        if (__ldg(C + v) == __ldg(C + __ldg(indices + e))) {
+            ++cnt;
+            if (WLoad<WT>::weighted) acc += WLoad<WT>::at(w, e);
         }
     }
-    for (int d = 16; d; d >>= 1) {
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    __device__ __forceinline__ void flush() {
+        for (int d = 16; d; d >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+            acc += __shfl_xor_sync(0xffffffffu, acc, d);
+        }
+        if ((threadIdx.x & 31) == 0 && cnt) {
+            atomicAdd(cnt_out, cnt);
+            if (WLoad<WT>::weighted) atomicAdd(w_out, acc);
+        }
     }
-    if (lane == 0 && cnt) {
-        atomicAdd(cnt_out, cnt);
-        if (WLoad<WT>::weighted) atomicAdd(w_out, acc);
-    }
-}
+};
 
 __global__ void k_mass(const int32_t* __restrict__ C, const double* __restrict__ k, int64_t n, double* K) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
@@ -62,8 +61,8 @@ double objective_impl(const lcc_graph& g, const double* k, double lam, const int
     Buf<double> dd(3, s);
     LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long), s));
     LCC_CUDA(cudaMemsetAsync(dd.get(), 0, 3 * sizeof(double), s));
-    k_intra<WT><<<grid_for(n * 32, 256, 16), 256, 0, s>>>(g.indptr, g.indices, g.weights, C, n, dcnt.get(), dd.get());
-    LCC_LAUNCH_CHECK();
+    edge_balanced(g.indptr, nullptr, g.indptr, n, g.nnz,
+                  IntraEdges<WT>{g.indices, g.weights, C, dcnt.get(), dd.get()}, s);
     Buf<double> K(n, s);
     LCC_CUDA(cudaMemsetAsync(K.get(), 0, sizeof(double) * n, s));
     k_mass<<<grid_for(n, 256), 256, 0, s>>>(C, k, n, K.get());

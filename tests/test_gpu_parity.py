@@ -103,7 +103,7 @@ def test_sync_round_sbm_cfg1_exact():
         C, K = O.canonicalize(g.n, D0, 2 * g.n, None)
 
 
-@pytest.mark.parametrize("thr", [1000, 40, 0])
+@pytest.mark.parametrize("thr", [1000, 40, 0, 200, 2048])
 def test_sync_round_hubs_all_bins_exact(thr):
     rng = np.random.default_rng(11)
     hg = hub_graph(rng, 30_000, hubs=[5, 77, 900, 1234], hub_deg=[50, 700, 12_000, 25_000], base_p=0.0003)

@@ -41,29 +41,32 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_MAX = 32;
 constexpr int SMALL_THREADS = 256;
-constexpr int LARGE_CHUNK = 8192;
+constexpr int LARGE_CHUNK = 8192;   // edges per insertion work item
 constexpr int LARGE_THREADS = 256;
-constexpr int SCORE_THREADS = 512;
+constexpr int SCORE_CHUNK = 16384;  // table slots per scoring work item
+constexpr int SCORE_THREADS = 256;
 
-// ---- relaxed loads / stores for the async schedule ----------------------
+// ---- label / mass gathers ------------------------------------------------
+// sync : read-only for the whole kernel -> non-coherent path, L2 evict-last.
+// async: other warps store concurrently -> relaxed gpu-scope loads (L2).
 template <bool ASYNC>
-__device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i) {
+__device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i, uint64_t pol) {
     if constexpr (ASYNC) {
         int32_t r;
         asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(C + i));
         return r;
     } else {
-        return __ldg(C + i);
+        return ld_keep_i32(C + i, pol);
     }
 }
 template <bool ASYNC>
-__device__ __forceinline__ double ldK(const double* K, int64_t i) {
+__device__ __forceinline__ double ldK(const double* K, int64_t i, uint64_t pol) {
     if constexpr (ASYNC) {
         double r;
         asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(r) : "l"(K + i));
         return r;
     } else {
-        return __ldg(K + i);
+        return ld_keep_f64(K + i, pol);
     }
 }
 __device__ __forceinline__ void stC_relaxed(int32_t* C, int64_t i, int32_t x) {
@@ -136,6 +139,8 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const int64_t nb = (hi - lo + 31) / 32;
     const int64_t gw = ((int64_t)blockIdx.x * SMALL_THREADS + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * SMALL_THREADS) >> 5;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
 
     for (int64_t bt = gw; bt < nb; bt += nw) {
@@ -149,9 +154,9 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             v = __ldg(list + i0 + lane);
             s = __ldg(a.indptr + v);
             deg = (int32_t)(__ldg(a.indptr + v + 1) - s);
-            c = ldC<ASYNC>(a.C, v);
+            c = ldC<ASYNC>(a.C, v, pol_keep);
             kv = kval(a.k, v);
-            Kc = ldK<ASYNC>(a.K, c);
+            Kc = ldK<ASYNC>(a.K, c, pol_keep);
         }
         const double t = dmul(a.lam, kv);
         int32_t incl = deg;
@@ -190,7 +195,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double wv = 0.0;
             if (has_edge) {
                 const int64_t e = sj + (lane - p);
-                x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
+                x = ldC<ASYNC>(a.C, ld_stream_i32(a.indices + e, pol_stream), pol_keep);
                 wv = WLoad<WT>::at(a.w, e);
             }
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
@@ -216,7 +221,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double g = -INFINITY;
             int32_t gx = NO_CAND;
             if (is_leader && x != cj) {
-                g = dsub(dsub(S, dmul(tj, ldK<ASYNC>(a.K, x))), bj);
+                g = dsub(dsub(S, dmul(tj, ldK<ASYNC>(a.K, x, pol_keep))), bj);
                 gx = x;
             }
             const int32_t seg = has_edge ? j : 32 + lane;
@@ -270,8 +275,12 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 
 // ===========================================================================
-// group bins: GW warps per vertex, CAP-slot shared-memory table per group
+// group bins: GW warps per vertex, CAP-slot shared-memory table per group.
+// Every lane keeps U independent loads in flight (index stream, label
+// gather; then key read, mass gather) before consuming them.
 // ===========================================================================
+constexpr int U = 8;
+
 template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
 __global__ void __launch_bounds__(GW * 32 * GROUPS)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
@@ -290,24 +299,39 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         if constexpr (GW == 1) __syncwarp();
         else named_sync(1 + gid, GT);
     };
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
     for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += (int64_t)gridDim.x * GROUPS) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
-        const int64_t deg = __ldg(a.indptr + v + 1) - s;
+        const int64_t end = __ldg(a.indptr + v + 1);
+        const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
         for (uint32_t q = gt; q < cap; q += GT) { keys[q] = EMPTY_KEY; vals[q] = (VT)0; }
-        const int32_t c = ldC<ASYNC>(a.C, v);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC>(a.K, c);
+        const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         gsync();
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
-        for (int64_t e = s + gt; e < s + deg; e += GT) {
-            const int32_t x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
-            const double wv = WLoad<WT>::at(a.w, e);
-            if (x == c) sc += wv;
-            else table_insert<VT>(keys, vals, cap, x, wv);
+        for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
+            int32_t u[U];
+            double wv[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int64_t e = e0 + (int64_t)j * GT;
+                u[j] = e < end ? ld_stream_i32(a.indices + e, pol_stream) : -1;
+                wv[j] = e < end ? WLoad<WT>::at(a.w, e) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (u[j] == EMPTY_KEY) continue;
+                if (u[j] == c) sc += wv[j];
+                else table_insert<VT>(keys, vals, cap, u[j], wv[j]);
+            }
         }
 #pragma unroll
         for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
@@ -323,11 +347,21 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
-        for (uint32_t q = gt; q < cap; q += GT) {
-            const int32_t x = keys[q];
-            if (x != EMPTY_KEY) {
-                const double gq = dsub(dsub((double)vals[q], dmul(t, ldK<ASYNC>(a.K, x))), b);
-                if (better(gq, x, bg, bx)) { bg = gq; bx = x; }
+        for (uint32_t q0 = gt; q0 < cap; q0 += GT * U) {
+            int32_t x[U];
+            double Kx[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const uint32_t q = q0 + j * GT;
+                x[j] = q < cap ? keys[q] : EMPTY_KEY;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (x[j] == EMPTY_KEY) continue;
+                const double gq = dsub(dsub((double)vals[q0 + j * GT], dmul(t, Kx[j])), b);
+                if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; }
             }
         }
         warp_argmax(bg, bx);
@@ -349,48 +383,72 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 }
 
 // ===========================================================================
-// large bin: vertices batched so that their global tables fit in L2; each
-// batch = multi-CTA insertion over CHUNK-edge work items + CTA-per-vertex
-// scoring.
+// large bin (hubs): vertices batched so that their global tables fit in L2.
+// Per batch: insertion over INSERT_CHUNK-edge work items spread over all SMs,
+// scoring over SCORE_CHUNK-slot work items (partial argmax per item), then a
+// warp per vertex merges its partials and decides.  Batches are planned once
+// on the host; no host synchronisation between batches.
 // ===========================================================================
 struct LargeBatch {
-    const int32_t* list;      // batch vertices
+    const int32_t* list;       // batch vertices
     int64_t nL;
-    const int64_t* cap_off;   // [nL+1]
-    const int64_t* item_off;  // [nL+1]
+    const int64_t* cap_off;    // [nL+1] table slot offsets
+    const int64_t* item_off;   // [nL+1] insertion work-item offsets
+    const int64_t* sitem_off;  // [nL+1] scoring work-item offsets
     int32_t* keys;
     void* vals;
-    double* sc;               // [nL] S_c per vertex (own-cluster weight)
+    double* sc;                // [nL] S_c per vertex (own-cluster weight)
+    double* pg;                // [scoring items] partial best gain
+    int32_t* px;               // [scoring items] partial best cluster
 };
+
+__device__ __forceinline__ int64_t owner_of(const int64_t* off, int64_t n, int64_t it) {
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (off[mid] <= it) lo = mid; else hi = mid;
+    }
+    return lo;
+}
 
 template <class WT, bool ASYNC>
 __global__ void __launch_bounds__(LARGE_THREADS)
 k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
     using VT = ValT<WT>;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
     for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
-        int64_t lo = 0, hi = L.nL;
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (L.item_off[mid] <= it) lo = mid; else hi = mid;
-        }
-        const int32_t v = L.list[lo];
+        const int64_t li = owner_of(L.item_off, L.nL, it);
+        const int32_t v = L.list[li];
         const int64_t s = a.indptr[v], e_end = a.indptr[v + 1];
-        const int64_t e0 = s + (it - L.item_off[lo]) * LARGE_CHUNK;
+        const int64_t e0 = s + (it - L.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
-        const uint32_t cap = (uint32_t)(L.cap_off[lo + 1] - L.cap_off[lo]);
-        int32_t* keys = L.keys + L.cap_off[lo];
-        VT* vals = static_cast<VT*>(L.vals) + L.cap_off[lo];
-        const int32_t c = ldC<ASYNC>(a.C, v);
+        const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
+        int32_t* keys = L.keys + L.cap_off[li];
+        VT* vals = static_cast<VT*>(L.vals) + L.cap_off[li];
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         double sc = 0.0;
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += LARGE_THREADS) {
-            const int32_t x = ldC<ASYNC>(a.C, __ldg(a.indices + e));
-            const double wv = WLoad<WT>::at(a.w, e);
-            if (x == c) sc += wv;
-            else table_insert<VT>(keys, vals, cap, x, wv);
+        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * U) {
+            int32_t u[U];
+            double wv[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int64_t e = eb + (int64_t)j * LARGE_THREADS;
+                u[j] = e < e1 ? ld_stream_i32(a.indices + e, pol_stream) : -1;
+                wv[j] = e < e1 ? WLoad<WT>::at(a.w, e) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (u[j] == EMPTY_KEY) continue;
+                if (u[j] == c) sc += wv[j];
+                else table_insert<VT>(keys, vals, cap, u[j], wv[j]);
+            }
         }
 #pragma unroll
         for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
-        if ((threadIdx.x & 31) == 0 && sc != 0.0) atomicAdd(L.sc + lo, sc);
+        if ((threadIdx.x & 31) == 0 && sc != 0.0) atomicAdd(L.sc + li, sc);
     }
 }
 
@@ -405,39 +463,77 @@ __device__ __forceinline__ void block_argmax(double& g, int32_t& x, double* s_g,
         x = threadIdx.x < THREADS / 32 ? s_x[threadIdx.x] : NO_CAND;
         warp_argmax(g, x);
     }
+    __syncthreads();
 }
 
 template <class WT, bool ASYNC>
 __global__ void __launch_bounds__(SCORE_THREADS)
-k_large_score(BMArgs a, LargeBatch L) {
+k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
     using VT = ValT<WT>;
     __shared__ double s_g[SCORE_THREADS / 32];
     __shared__ int32_t s_x[SCORE_THREADS / 32];
-    unsigned long long my_moves = 0;
-    for (int64_t li = blockIdx.x; li < L.nL; li += gridDim.x) {
+    const uint64_t pol_keep = policy_evict_last();
+    for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
+        const int64_t li = owner_of(L.sitem_off, L.nL, it);
         const int32_t v = L.list[li];
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
+        const uint32_t q_begin = (uint32_t)((it - L.sitem_off[li]) * SCORE_CHUNK);
+        const uint32_t q_end = (uint32_t)min64((int64_t)q_begin + SCORE_CHUNK, cap);
         const int32_t* keys = L.keys + L.cap_off[li];
         const VT* vals = static_cast<const VT*>(L.vals) + L.cap_off[li];
-        const int32_t c = ldC<ASYNC>(a.C, v);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC>(a.K, c);
+        const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
-        for (uint32_t q = threadIdx.x; q < cap; q += SCORE_THREADS) {
-            const int32_t x = keys[q];
-            if (x != EMPTY_KEY) {
-                const double gq = dsub(dsub((double)vals[q], dmul(t, ldK<ASYNC>(a.K, x))), b);
-                if (better(gq, x, bg, bx)) { bg = gq; bx = x; }
+        for (uint32_t q0 = q_begin + threadIdx.x; q0 < q_end; q0 += SCORE_THREADS * U) {
+            int32_t x[U];
+            double Kx[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const uint32_t q = q0 + j * SCORE_THREADS;
+                x[j] = q < q_end ? keys[q] : EMPTY_KEY;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (x[j] == EMPTY_KEY) continue;
+                const double gq = dsub(dsub((double)vals[q0 + j * SCORE_THREADS], dmul(t, Kx[j])), b);
+                if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; }
             }
         }
         block_argmax<SCORE_THREADS>(bg, bx, s_g, s_x);
-        if (threadIdx.x == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
-        __syncthreads();
+        if (threadIdx.x == 0) { L.pg[it] = bg; L.px[it] = bx; }
     }
-    if (threadIdx.x < 32) flush_moves(a, my_moves);
+}
+
+template <bool ASYNC>
+__global__ void k_large_decide(BMArgs a, LargeBatch L) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol_keep = policy_evict_last();
+    unsigned long long my_moves = 0;
+    for (int64_t li = gw; li < L.nL; li += nw) {
+        double bg = -INFINITY;
+        int32_t bx = NO_CAND;
+        for (int64_t it = L.sitem_off[li] + lane; it < L.sitem_off[li + 1]; it += 32)
+            if (better(L.pg[it], L.px[it], bg, bx)) { bg = L.pg[it]; bx = L.px[it]; }
+        warp_argmax(bg, bx);
+        if (lane == 0) {
+            const int32_t v = L.list[li];
+            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+            const double kv = kval(a.k, v);
+            const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
+            const double t = dmul(a.lam, kv);
+            const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
+            my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
+        }
+    }
+    flush_moves(a, my_moves);
 }
 
 // ===========================================================================
@@ -497,11 +593,12 @@ void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, 
     if (hi <= lo) return;
     constexpr int THREADS = GW * 32 * GROUPS;
     constexpr int SMEM = GROUPS * CAP * (int)(sizeof(int32_t) + sizeof(ValT<WT>));
-    static bool attr = false;
-    if (!attr) { set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS>, SMEM); attr = true; }
-    int occ = 0;
-    LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS>, THREADS, SMEM));
-    occ = std::max(occ, 1);
+    static int occ = 0;
+    if (!occ) {
+        set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS>, THREADS, SMEM));
+        occ = std::max(occ, 1);
+    }
     const int64_t blocks_needed = (hi - lo + GROUPS - 1) / GROUPS;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * occ));
     k_group<WT, ASYNC, GW, CAP, GROUPS><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
@@ -509,25 +606,26 @@ void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, 
 }
 
 constexpr int B5_CAP = 16384;
-constexpr int64_t MED_MAX = (B5_CAP * 5) / 8;  // 10240: load factor <= 0.625
-constexpr int64_t LARGE_TABLE_BYTES = 48ll << 20;  // per batch: stays L2-resident
+constexpr int64_t MED_MAX = (B5_CAP * 5) / 8;      // 10240: load factor <= 0.625
+constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-resident
 
 template <class WT, bool ASYNC>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     switch (bin) {
-        case 1: launch_group<WT, ASYNC, 1, 256, 8>(a, list, lo, hi, s); break;
-        case 2: launch_group<WT, ASYNC, 1, 1024, 8>(a, list, lo, hi, s); break;
-        case 3: launch_group<WT, ASYNC, 1, 4096, 4>(a, list, lo, hi, s); break;
-        case 4: launch_group<WT, ASYNC, 4, 4096, 2>(a, list, lo, hi, s); break;
-        case 5: launch_group<WT, ASYNC, 16, B5_CAP, 1>(a, list, lo, hi, s); break;
+        case 1: launch_group<WT, ASYNC, 1, 256, 8>(a, list, lo, hi, s); break;    //   33..128   (warp)
+        case 2: launch_group<WT, ASYNC, 1, 1024, 8>(a, list, lo, hi, s); break;   //  129..512   (warp)
+        case 3: launch_group<WT, ASYNC, 1, 2048, 4>(a, list, lo, hi, s); break;   //  513..T-1   (warp)
+        case 4: launch_group<WT, ASYNC, 4, 4096, 2>(a, list, lo, hi, s); break;   //    T..2048  (4 warps)
+        case 5: launch_group<WT, ASYNC, 16, B5_CAP, 1>(a, list, lo, hi, s); break; // 2049..10240 (16 warps)
         default: break;
     }
 }
 
+inline int64_t large_cap(int64_t deg) { return (2 * deg + 31) & ~31LL; }
+
 template <class WT, bool ASYNC>
 void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_t nL, cudaStream_t s) {
     using VT = ValT<WT>;
-    // degrees to the host, plan L2-sized batches
     Buf<int64_t> ddeg(nL, s);
     k_degrees_of<<<grid_for(nL, 256), 256, 0, s>>>(g.indptr, large, nL, ddeg.get());
     LCC_LAUNCH_CHECK();
@@ -535,44 +633,58 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_
     LCC_CUDA(cudaMemcpyAsync(deg.data(), ddeg.get(), sizeof(int64_t) * nL, cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
     const int64_t slot_bytes = sizeof(int32_t) + sizeof(VT);
-    const int64_t budget = LARGE_TABLE_BYTES / slot_bytes;
     int64_t maxcap = 0;
-    for (int64_t d : deg) maxcap = std::max<int64_t>(maxcap, (2 * d + 31) & ~31LL);
-    const int64_t table_slots = std::max<int64_t>(budget, maxcap);
-    Buf<int32_t> keys(table_slots, s);
-    Buf<unsigned char> vals(table_slots * sizeof(VT), s);
-    Buf<int64_t> offs(2 * (nL + 1), s);
-    Buf<double> sc(nL, s);
-    std::vector<int64_t> h_cap(nL + 1), h_item(nL + 1);
-    int64_t b0 = 0;
-    while (b0 < nL) {
-        // greedy batch [b0, b1) with sum(cap) <= table_slots
-        int64_t b1 = b0, slots = 0, items = 0;
+    for (int64_t d : deg) maxcap = std::max<int64_t>(maxcap, large_cap(d));
+    const int64_t table_slots = std::max<int64_t>(LARGE_TABLE_BYTES / slot_bytes, maxcap);
+    // plan every batch: per-batch relative offsets, concatenated
+    struct B { int64_t b0, nb, slots, items, sitems, off; };
+    std::vector<B> batches;
+    std::vector<int64_t> h;  // for each batch: cap_off[nb+1], item_off[nb+1], sitem_off[nb+1]
+    int64_t max_sitems = 0;
+    for (int64_t b0 = 0; b0 < nL;) {
+        int64_t b1 = b0, slots = 0, items = 0, sitems = 0;
+        const size_t base = h.size();
+        h.resize(base + 3 * (nL - b0 + 1));
+        std::vector<int64_t> co, io, so;
         while (b1 < nL) {
-            const int64_t cap = (2 * deg[b1] + 31) & ~31LL;
+            const int64_t cap = large_cap(deg[b1]);
             if (b1 > b0 && slots + cap > table_slots) break;
-            h_cap[b1 - b0] = slots;
-            h_item[b1 - b0] = items;
+            co.push_back(slots); io.push_back(items); so.push_back(sitems);
             slots += cap;
             items += (deg[b1] + LARGE_CHUNK - 1) / LARGE_CHUNK;
+            sitems += (cap + SCORE_CHUNK - 1) / SCORE_CHUNK;
             ++b1;
         }
+        co.push_back(slots); io.push_back(items); so.push_back(sitems);
         const int64_t nb = b1 - b0;
-        h_cap[nb] = slots;
-        h_item[nb] = items;
-        LCC_CUDA(cudaMemcpyAsync(offs.get(), h_cap.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
-        LCC_CUDA(cudaMemcpyAsync(offs.get() + (nL + 1), h_item.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
-        LCC_CUDA(cudaMemsetAsync(keys.get(), 0xff, sizeof(int32_t) * slots, s));
-        LCC_CUDA(cudaMemsetAsync(vals.get(), 0, sizeof(VT) * slots, s));
-        LCC_CUDA(cudaMemsetAsync(sc.get(), 0, sizeof(double) * nb, s));
-        LargeBatch L{large + b0, nb, offs.get(), offs.get() + (nL + 1), keys.get(), vals.get(), sc.get()};
-        k_large_insert<WT, ASYNC><<<grid_for(items * LARGE_THREADS, LARGE_THREADS, 16), LARGE_THREADS, 0, s>>>(a, L, items);
-        LCC_LAUNCH_CHECK();
-        k_large_score<WT, ASYNC><<<grid_for(nb * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L);
-        LCC_LAUNCH_CHECK();
-        // the host-side offset vectors are rewritten next batch: keep ordering
-        LCC_CUDA(cudaStreamSynchronize(s));
+        h.resize(base);
+        h.insert(h.end(), co.begin(), co.end());
+        h.insert(h.end(), io.begin(), io.end());
+        h.insert(h.end(), so.begin(), so.end());
+        batches.push_back(B{b0, nb, slots, items, sitems, (int64_t)base});
+        max_sitems = std::max(max_sitems, sitems);
         b0 = b1;
+    }
+    Buf<int64_t> offs(h.size(), s);
+    LCC_CUDA(cudaMemcpyAsync(offs.get(), h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice, s));
+    Buf<int32_t> keys(table_slots, s);
+    Buf<unsigned char> vals(table_slots * sizeof(VT), s);
+    Buf<double> sc(nL, s);
+    Buf<double> pg(max_sitems, s);
+    Buf<int32_t> px(max_sitems, s);
+    LCC_CUDA(cudaMemsetAsync(sc.get(), 0, sizeof(double) * nL, s));
+    for (const B& bt : batches) {
+        const int64_t* o = offs.get() + bt.off;
+        LargeBatch L{large + bt.b0, bt.nb, o, o + (bt.nb + 1), o + 2 * (bt.nb + 1), keys.get(), vals.get(),
+                     sc.get() + bt.b0, pg.get(), px.get()};
+        LCC_CUDA(cudaMemsetAsync(keys.get(), 0xff, sizeof(int32_t) * bt.slots, s));
+        LCC_CUDA(cudaMemsetAsync(vals.get(), 0, sizeof(VT) * bt.slots, s));
+        k_large_insert<WT, ASYNC><<<grid_for(bt.items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, bt.items);
+        LCC_LAUNCH_CHECK();
+        k_large_score<WT, ASYNC><<<grid_for(bt.sitems * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L, bt.sitems);
+        LCC_LAUNCH_CHECK();
+        k_large_decide<ASYNC><<<grid_for(bt.nb * 32, 256), 256, 0, s>>>(a, L);
+        LCC_LAUNCH_CHECK();
     }
 }
 
@@ -586,7 +698,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
-    const int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), 2048);
+    const int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), 1024);
     BinEdges be;
     be.hi[0] = SMALL_MAX;
     be.hi[1] = std::min<int64_t>(128, T - 1);

@@ -267,6 +267,40 @@ __device__ __forceinline__ void table_insert(int32_t* keys, VT* vals, uint32_t c
     else atomicAdd(vals + h, (VT)1);
 }
 
+// Shared-memory variant: 32-bit shared-window addresses and shared-space
+// atomics (no generic-address conversion).  A thread that claims a fresh
+// slot appends the slot index to the group's occupied list, so scoring and
+// clean-up touch only occupied slots.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <class VT>
+__device__ __forceinline__ void stable_insert(uint32_t keys_s, uint32_t vals_s, uint32_t list_s, uint32_t cnt_s,
+                                              uint32_t cap, int32_t x, double wv) {
+    uint32_t h = slot_of(x, cap);
+    while (true) {
+        int32_t kq;
+        asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys_s + 4 * h));
+        if (kq == x) break;
+        if (kq == EMPTY_KEY) {
+            int32_t prev;
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys_s + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+            if (prev == EMPTY_KEY) {
+                uint32_t pos;
+                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(cnt_s) : "memory");
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(list_s + 2 * pos), "h"((unsigned short)h) : "memory");
+                break;
+            }
+            if (prev == x) break;
+        }
+        h = (h + 1 == cap) ? 0 : h + 1;
+    }
+    if constexpr (std::is_same<VT, double>::value) {
+        asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals_s + 8 * h), "d"(wv) : "memory");
+    } else {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(vals_s + 4 * h) : "memory");
+    }
+}
+
 template <class WT>
 using ValT = typename std::conditional<WLoad<WT>::weighted, double, int32_t>::type;
 
@@ -282,23 +316,41 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 constexpr int U = 8;
 
 template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
+struct GroupSmem {
+    using VT = ValT<WT>;
+    static constexpr size_t per_group = (size_t)CAP * (sizeof(VT) + sizeof(int32_t) + sizeof(uint16_t));
+    static constexpr size_t bytes = GROUPS * per_group;
+};
+
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
 __global__ void __launch_bounds__(GW * 32 * GROUPS)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     using VT = ValT<WT>;
     constexpr int GT = GW * 32;
+    static_assert(CAP <= 65536, "slot index must fit 16 bits");
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_g[GROUPS * GW];
     __shared__ int32_t s_x[GROUPS * GW];
+    __shared__ uint32_t s_cnt[GROUPS];
     const int gid = threadIdx.x / GT;
     const int gt = threadIdx.x % GT;
     const int wig = gt >> 5;
     const int lane = threadIdx.x & 31;
+    // layout: [vals: GROUPS*CAP VT][keys: GROUPS*CAP i32][slots: GROUPS*CAP u16]
     VT* vals = reinterpret_cast<VT*>(smem) + (size_t)gid * CAP;
     int32_t* keys = reinterpret_cast<int32_t*>(reinterpret_cast<VT*>(smem) + (size_t)GROUPS * CAP) + (size_t)gid * CAP;
+    uint16_t* slots = reinterpret_cast<uint16_t*>(reinterpret_cast<int32_t*>(reinterpret_cast<VT*>(smem) + (size_t)GROUPS * CAP) +
+                                                  (size_t)GROUPS * CAP) + (size_t)gid * CAP;
+    const uint32_t keys_s = smem_u32(keys), vals_s = smem_u32(vals), slots_s = smem_u32(slots);
+    const uint32_t cnt_s = smem_u32(&s_cnt[gid]);
     auto gsync = [&]() {
         if constexpr (GW == 1) __syncwarp();
         else named_sync(1 + gid, GT);
     };
+    // the table starts empty; every vertex empties the slots it used
+    for (uint32_t q = gt; q < CAP; q += GT) { keys[q] = EMPTY_KEY; vals[q] = (VT)0; }
+    if (gt == 0) s_cnt[gid] = 0;
+    gsync();
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
@@ -308,12 +360,10 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int64_t end = __ldg(a.indptr + v + 1);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
-        for (uint32_t q = gt; q < cap; q += GT) { keys[q] = EMPTY_KEY; vals[q] = (VT)0; }
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
-        gsync();
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
         for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
             int32_t u[U];
@@ -330,7 +380,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             for (int j = 0; j < U; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) sc += wv[j];
-                else table_insert<VT>(keys, vals, cap, u[j], wv[j]);
+                else stable_insert<VT>(keys_s, vals_s, slots_s, cnt_s, cap, u[j], wv[j]);
             }
         }
 #pragma unroll
@@ -344,30 +394,36 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 #pragma unroll
             for (int w = 0; w < GW; ++w) sc += s_g[gid * GW + w];
         }
+        const uint32_t nocc = s_cnt[gid];
         const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
-        for (uint32_t q0 = gt; q0 < cap; q0 += GT * U) {
+        for (uint32_t i0 = gt; i0 < nocc; i0 += GT * U) {
+            uint32_t q[U];
             int32_t x[U];
             double Kx[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                const uint32_t q = q0 + j * GT;
-                x[j] = q < cap ? keys[q] : EMPTY_KEY;
+                const uint32_t ii = i0 + j * GT;
+                q[j] = ii < nocc ? slots[ii] : 0xffffffffu;
+                x[j] = ii < nocc ? keys[q[j]] : EMPTY_KEY;
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
-                const double gq = dsub(dsub((double)vals[q0 + j * GT], dmul(t, Kx[j])), b);
+                const double gq = dsub(dsub((double)vals[q[j]], dmul(t, Kx[j])), b);
                 if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; }
+                keys[q[j]] = EMPTY_KEY;  // clean up for the next vertex
+                vals[q[j]] = (VT)0;
             }
         }
         warp_argmax(bg, bx);
         if constexpr (GW > 1) {
-            gsync();  // everyone has read s_g (S_c) before it is reused
+            gsync();  // everyone has read s_g (S_c) and s_cnt before reuse
             if (lane == 0) { s_g[gid * GW + wig] = bg; s_x[gid * GW + wig] = bx; }
+            if (gt == 0) s_cnt[gid] = 0;
             gsync();
 #pragma unroll
             for (int w = 0; w < GW; ++w) {
@@ -375,9 +431,12 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 const int32_t ox = s_x[gid * GW + w];
                 if (better(og, ox, bg, bx)) { bg = og; bx = ox; }
             }
+        } else {
+            __syncwarp();
+            if (gt == 0) s_cnt[gid] = 0;
         }
         if (gt == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
-        gsync();  // table and s_g free for the next vertex
+        gsync();  // table, counter and s_g free for the next vertex
     }
     flush_moves(a, my_moves);
 }
@@ -539,38 +598,86 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
 // ===========================================================================
 // degree-bin partition (one pass, block-aggregated reservations)
 // ===========================================================================
-constexpr int NBINS = 7;
+constexpr int NBINS = 8;
 struct BinEdges {
     int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
 
-__global__ void k_bin(const int64_t* __restrict__ indptr, const int32_t* __restrict__ frontier, int64_t nF,
-                      BinEdges be, int32_t* __restrict__ out, int64_t stride, unsigned long long* counts) {
+// Stable partition (frontier order preserved inside every bin, so sorted
+// frontiers give id-ordered bins): pass 1 counts per (bin, tile), an
+// exclusive scan gives every (bin, tile) its output offset, pass 2 scatters
+// with warp-ballot ranks.
+constexpr int BIN_THREADS = 256;
+constexpr int BIN_ROUNDS = 8;
+constexpr int BIN_TILE = BIN_THREADS * BIN_ROUNDS;
+
+__device__ __forceinline__ int bin_of(int64_t d, const BinEdges& be) {
+    int bin = 0;
+#pragma unroll
+    for (int b = 0; b < NBINS - 1; ++b) bin += d > be.hi[b] ? 1 : 0;
+    return bin;
+}
+
+__global__ void __launch_bounds__(BIN_THREADS)
+k_bin_count(const int64_t* __restrict__ indptr, const int32_t* __restrict__ frontier, int64_t nF, BinEdges be,
+            int64_t ntiles, int64_t* tile_counts, unsigned long long* edges) {
     __shared__ unsigned s_cnt[NBINS];
-    __shared__ unsigned long long s_base[NBINS];
-    __shared__ unsigned long long s_edges;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nF; base += (int64_t)gridDim.x * blockDim.x) {
-        if (threadIdx.x < NBINS) s_cnt[threadIdx.x] = 0;
-        if (threadIdx.x == 0) s_edges = 0;
-        __syncthreads();
-        const int64_t i = base + threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    if (threadIdx.x < NBINS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long my_edges = 0;
+    for (int r = 0; r < BIN_ROUNDS; ++r) {
+        const int64_t i = tile * BIN_TILE + (int64_t)r * BIN_THREADS + threadIdx.x;
+        if (i < nF) {
+            const int32_t v = frontier ? frontier[i] : (int32_t)i;
+            const int64_t d = indptr[v + 1] - indptr[v];
+            my_edges += (unsigned long long)d;
+            atomicAdd(&s_cnt[bin_of(d, be)], 1u);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) my_edges += __shfl_xor_sync(FULL, my_edges, d);
+    if ((threadIdx.x & 31) == 0 && my_edges) atomicAdd(edges, my_edges);
+    __syncthreads();
+    if (threadIdx.x < NBINS) tile_counts[(int64_t)threadIdx.x * ntiles + tile] = s_cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(BIN_THREADS)
+k_bin_scatter(const int64_t* __restrict__ indptr, const int32_t* __restrict__ frontier, int64_t nF, BinEdges be,
+              int64_t ntiles, const int64_t* __restrict__ tile_base, int32_t* __restrict__ out) {
+    constexpr int W = BIN_THREADS / 32;
+    __shared__ unsigned s_wc[W][NBINS];
+    __shared__ int64_t s_run[NBINS];
+    const int64_t tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x < NBINS) s_run[threadIdx.x] = tile_base[(int64_t)threadIdx.x * ntiles + tile];
+    for (int r = 0; r < BIN_ROUNDS; ++r) {
+        const int64_t i = tile * BIN_TILE + (int64_t)r * BIN_THREADS + threadIdx.x;
         int bin = -1;
-        unsigned slot = 0;
         int32_t v = 0;
         if (i < nF) {
             v = frontier ? frontier[i] : (int32_t)i;
-            const int64_t d = indptr[v + 1] - indptr[v];
-            bin = 0;
+            bin = bin_of(indptr[v + 1] - indptr[v], be);
+        }
+        unsigned rank = 0;
 #pragma unroll
-            for (int b = 0; b < NBINS - 1; ++b) bin += d > be.hi[b] ? 1 : 0;
-            slot = atomicAdd(&s_cnt[bin], 1u);
-            atomicAdd(&s_edges, (unsigned long long)d);
+        for (int b = 0; b < NBINS; ++b) {
+            const unsigned m = __ballot_sync(FULL, bin == b);
+            if (bin == b) rank = __popc(m & ((1u << lane) - 1u));
+            if (lane == 0) s_wc[w][b] = __popc(m);
         }
         __syncthreads();
-        if (threadIdx.x < NBINS) s_base[threadIdx.x] = atomicAdd(counts + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
-        if (threadIdx.x == NBINS) atomicAdd(counts + NBINS, s_edges);
+        if (bin >= 0) {
+            int64_t pos = s_run[bin] + rank;
+            for (int ww = 0; ww < w; ++ww) pos += s_wc[ww][bin];
+            out[pos] = v;  // bins are contiguous, in bin order, in one array
+        }
         __syncthreads();
-        if (bin >= 0) out[bin * stride + s_base[bin] + slot] = v;
+        if (threadIdx.x < NBINS) {
+            unsigned tot = 0;
+            for (int ww = 0; ww < W; ++ww) tot += s_wc[ww][threadIdx.x];
+            s_run[threadIdx.x] += tot;
+        }
         __syncthreads();
     }
 }
@@ -592,7 +699,7 @@ template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
 void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     if (hi <= lo) return;
     constexpr int THREADS = GW * 32 * GROUPS;
-    constexpr int SMEM = GROUPS * CAP * (int)(sizeof(int32_t) + sizeof(ValT<WT>));
+    constexpr int SMEM = (int)GroupSmem<WT, ASYNC, GW, CAP, GROUPS>::bytes;
     static int occ = 0;
     if (!occ) {
         set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS>, SMEM);
@@ -609,14 +716,17 @@ constexpr int B5_CAP = 16384;
 constexpr int64_t MED_MAX = (B5_CAP * 5) / 8;      // 10240: load factor <= 0.625
 constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-resident
 
+// bin -> kernel shape.  Shared memory per group = CAP * (4 key + 4|8 value +
+// 2 slot-list) bytes; GROUPS chosen so 2-3 CTAs fit per SM.
 template <class WT, bool ASYNC>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     switch (bin) {
-        case 1: launch_group<WT, ASYNC, 1, 256, 8>(a, list, lo, hi, s); break;    //   33..128   (warp)
-        case 2: launch_group<WT, ASYNC, 1, 1024, 8>(a, list, lo, hi, s); break;   //  129..512   (warp)
-        case 3: launch_group<WT, ASYNC, 1, 2048, 4>(a, list, lo, hi, s); break;   //  513..T-1   (warp)
-        case 4: launch_group<WT, ASYNC, 4, 4096, 2>(a, list, lo, hi, s); break;   //    T..2048  (4 warps)
-        case 5: launch_group<WT, ASYNC, 16, B5_CAP, 1>(a, list, lo, hi, s); break; // 2049..10240 (16 warps)
+        case 1: launch_group<WT, ASYNC, 1, 256, 8>(a, list, lo, hi, s); break;     //   33..128   warp
+        case 2: launch_group<WT, ASYNC, 1, 1024, 8>(a, list, lo, hi, s); break;    //  129..512   warp
+        case 3: launch_group<WT, ASYNC, 2, 2048, 4>(a, list, lo, hi, s); break;    //  513..T-1   2 warps
+        case 4: launch_group<WT, ASYNC, 4, 4096, 2>(a, list, lo, hi, s); break;    //    T..2048  4 warps
+        case 5: launch_group<WT, ASYNC, 8, 8192, 1>(a, list, lo, hi, s); break;    // 2049..4096  8 warps
+        case 6: launch_group<WT, ASYNC, 8, B5_CAP, 1>(a, list, lo, hi, s); break;  // 4097..10240 8 warps
         default: break;
     }
 }
@@ -705,22 +815,38 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     be.hi[2] = std::min<int64_t>(512, T - 1);
     be.hi[3] = T - 1;
     be.hi[4] = 2048;
-    be.hi[5] = MED_MAX;
-    be.hi[6] = INT64_MAX;
+    be.hi[5] = 4096;
+    be.hi[6] = MED_MAX;
+    be.hi[7] = INT64_MAX;
 
-    const int64_t stride = std::max<int64_t>(nF, 1);
-    Buf<int32_t> lists(NBINS * stride, s);
-    Buf<unsigned long long> dcnt(NBINS + 2, s);
-    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * (NBINS + 2), s));
-    unsigned long long* dmoved = dcnt.get() + NBINS + 1;
-    if (nF > 0) {
-        k_bin<<<grid_for(nF, 256, 8), 256, 0, s>>>(g.indptr, frontier, nF, be, lists.get(), stride, dcnt.get());
-        LCC_LAUNCH_CHECK();
-    }
+    Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);
+    std::vector<int64_t> binstart;
+    Buf<unsigned long long> dcnt(2, s);  // [edges, movers]
+    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * 2, s));
+    unsigned long long* dmoved = dcnt.get() + 1;
+    const int64_t ntiles = std::max<int64_t>((nF + BIN_TILE - 1) / BIN_TILE, 1);
+    Buf<int64_t> tcnt(NBINS * ntiles + 1, s), tbase(NBINS * ntiles + 1, s);
     unsigned long long hc[NBINS + 1];
-    LCC_CUDA(cudaMemcpyAsync(hc, dcnt.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
-    LCC_CUDA(cudaStreamSynchronize(s));
-
+    if (nF > 0) {
+        k_bin_count<<<(unsigned)ntiles, BIN_THREADS, 0, s>>>(g.indptr, frontier, nF, be, ntiles, tcnt.get(), dcnt.get());
+        LCC_LAUNCH_CHECK();
+        LCC_CUDA(cudaMemsetAsync(tcnt.get() + NBINS * ntiles, 0, sizeof(int64_t), s));
+        exclusive_sum(tcnt.get(), tbase.get(), NBINS * ntiles + 1, s);
+        k_bin_scatter<<<(unsigned)ntiles, BIN_THREADS, 0, s>>>(g.indptr, frontier, nF, be, ntiles, tbase.get(),
+                                                               lists.get());
+        LCC_LAUNCH_CHECK();
+        // bin b occupies [tbase[b*ntiles], tbase[(b+1)*ntiles]) of `lists`
+        std::vector<int64_t> hb(NBINS + 1);
+        for (int b = 0; b <= NBINS; ++b)
+            LCC_CUDA(cudaMemcpyAsync(&hb[b], tbase.get() + (int64_t)b * ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaMemcpyAsync(&hc[NBINS], dcnt.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < NBINS; ++b) hc[b] = (unsigned long long)(hb[b + 1] - hb[b]);
+        binstart.assign(hb.begin(), hb.end());
+    } else {
+        for (int b = 0; b <= NBINS; ++b) hc[b] = 0;
+        binstart.assign(NBINS + 1, 0);
+    }
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreate(&ev0));
@@ -731,7 +857,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const int64_t nL = (int64_t)hc[NBINS - 1];
     if (nL > 0) {
         LCC_CUDA(cudaEventRecord(ev0, s));
-        run_large<WT, ASYNC>(a, g, lists.get() + (NBINS - 1) * stride, nL, s);
+        run_large<WT, ASYNC>(a, g, lists.get() + binstart[NBINS - 1], nL, s);
         LCC_CUDA(cudaEventRecord(ev1, s));
         LCC_CUDA(cudaEventSynchronize(ev1));
         LCC_CUDA(cudaEventElapsedTime(&kms_large, ev0, ev1));
@@ -743,7 +869,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             const int64_t nb = (int64_t)hc[b];
             const int64_t lo = nb * j / P, hi = nb * (j + 1) / P;
             if (hi <= lo) continue;
-            const int32_t* list = lists.get() + b * stride;
+            const int32_t* list = lists.get() + binstart[b];
             if (b == 0) {
                 const int64_t warps = (hi - lo + 31) / 32;
                 k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, s>>>(a, list, lo, hi);
@@ -765,7 +891,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         st->edges += (int64_t)hc[NBINS];
         st->moved += (int64_t)hm;
         st->n_small += (int64_t)hc[0];
-        st->n_medium += (int64_t)(hc[1] + hc[2] + hc[3] + hc[4] + hc[5]);
+        for (int b = 1; b < NBINS - 1; ++b) st->n_medium += (int64_t)hc[b];
         st->n_large += nL;
         st->ms_kernels += (double)kms + (double)kms_large;
         st->launches += launch_counter() - launches0;

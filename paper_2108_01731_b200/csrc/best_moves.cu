@@ -244,65 +244,156 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 }
 
 // ===========================================================================
-// hash-table helpers (group bins: shared memory; large bin: global memory)
+// neighbour-cluster tables.  One atomic per edge: unweighted graphs pack
+// (cluster id, count) into one 64-bit slot, claimed by a 64-bit CAS that
+// already carries count 1, bumped by a 64-bit RED otherwise.  Weighted
+// graphs claim a 32-bit key by CAS and add the weight with fp64 RED.
+// Scoring scans every slot (plain loads) and resets it, so the table is
+// clean for the next vertex without a separate clearing pass.
 // ===========================================================================
 __device__ __forceinline__ uint32_t slot_of(int32_t x, uint32_t cap) {
     return (uint32_t)(((uint64_t)hash32((uint32_t)x) * cap) >> 32);
 }
-
-template <class VT>
-__device__ __forceinline__ void table_insert(int32_t* keys, VT* vals, uint32_t cap, int32_t x, double wv) {
-    uint32_t h = slot_of(x, cap);
-    volatile int32_t* vk = keys;
-    while (true) {
-        const int32_t kq = vk[h];
-        if (kq == x) break;
-        if (kq == EMPTY_KEY) {
-            const int32_t prev = atomicCAS(keys + h, EMPTY_KEY, x);
-            if (prev == EMPTY_KEY || prev == x) break;
-        }
-        h = (h + 1 == cap) ? 0 : h + 1;
-    }
-    if constexpr (std::is_same<VT, double>::value) atomicAdd(vals + h, wv);
-    else atomicAdd(vals + h, (VT)1);
-}
-
-// Shared-memory variant: 32-bit shared-window addresses and shared-space
-// atomics (no generic-address conversion).  A thread that claims a fresh
-// slot appends the slot index to the group's occupied list, so scoring and
-// clean-up touch only occupied slots.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <class VT>
-__device__ __forceinline__ void stable_insert(uint32_t keys_s, uint32_t vals_s, uint32_t list_s, uint32_t cnt_s,
-                                              uint32_t cap, int32_t x, double wv) {
-    uint32_t h = slot_of(x, cap);
-    while (true) {
-        int32_t kq;
-        asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys_s + 4 * h));
-        if (kq == x) break;
-        if (kq == EMPTY_KEY) {
-            int32_t prev;
-            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys_s + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
-            if (prev == EMPTY_KEY) {
-                uint32_t pos;
-                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(cnt_s) : "memory");
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(list_s + 2 * pos), "h"((unsigned short)h) : "memory");
-                break;
-            }
-            if (prev == x) break;
-        }
-        h = (h + 1 == cap) ? 0 : h + 1;
-    }
-    if constexpr (std::is_same<VT, double>::value) {
-        asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals_s + 8 * h), "d"(wv) : "memory");
-    } else {
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(vals_s + 4 * h) : "memory");
-    }
-}
+constexpr uint64_t EMPTY64 = ~0ull;  // key -1 (never a cluster id); memset(0xff)-able
 
-template <class WT>
-using ValT = typename std::conditional<WLoad<WT>::weighted, double, int32_t>::type;
+template <bool WEIGHTED>
+struct SmemTable;
+
+template <>
+struct SmemTable<false> {
+    static constexpr int bytes_per_slot = 8;
+    uint32_t base;  // shared address of uint64[cap]
+    __device__ __forceinline__ void init(unsigned char* p) { base = smem_u32(p); }
+    __device__ __forceinline__ void clear(uint32_t q) const {
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(base + 8 * q), "l"(EMPTY64) : "memory");
+    }
+    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double) const {
+        const uint64_t want = ((uint64_t)(uint32_t)x << 32) | 1ull;
+        uint32_t h = slot_of(x, cap);
+        while (true) {
+            const uint32_t addr = base + 8 * h;
+            uint64_t w;
+            asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(addr));
+            if ((int32_t)(w >> 32) == x) {
+                asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(addr) : "memory");
+                return;
+            }
+            if (w == EMPTY64) {
+                uint64_t prev;
+                asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(prev) : "r"(addr), "l"(EMPTY64), "l"(want) : "memory");
+                if (prev == EMPTY64) return;
+                if ((int32_t)(prev >> 32) == x) {
+                    asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(addr) : "memory");
+                    return;
+                }
+            }
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+    }
+    // read + reset; returns false for an empty slot
+    __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
+        uint64_t w;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w) : "r"(base + 8 * q));
+        if (w == EMPTY64) return false;
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(base + 8 * q), "l"(EMPTY64) : "memory");
+        x = (int32_t)(w >> 32);
+        S = (double)(uint32_t)w;
+        return true;
+    }
+};
+
+template <>
+struct SmemTable<true> {
+    static constexpr int bytes_per_slot = 12;
+    uint32_t keys, vals;  // int32[cap] keys, then double[cap] sums (8B aligned)
+    uint32_t capmax;
+    __device__ __forceinline__ void init_cap(unsigned char* p, uint32_t CAP) {
+        vals = smem_u32(p);
+        keys = vals + 8 * CAP;
+        capmax = CAP;
+    }
+    __device__ __forceinline__ void clear(uint32_t q) const {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(keys + 4 * q), "r"(EMPTY_KEY) : "memory");
+        asm volatile("st.shared.f64 [%0], %1;" ::"r"(vals + 8 * q), "d"(0.0) : "memory");
+    }
+    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double wv) const {
+        uint32_t h = slot_of(x, cap);
+        while (true) {
+            int32_t kq;
+            asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * h));
+            if (kq == x) break;
+            if (kq == EMPTY_KEY) {
+                int32_t prev;
+                asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+                if (prev == EMPTY_KEY || prev == x) break;
+            }
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+        asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h), "d"(wv) : "memory");
+    }
+    __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
+        int32_t kq;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
+        if (kq == EMPTY_KEY) return false;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(S) : "r"(vals + 8 * q));
+        clear(q);
+        x = kq;
+        return true;
+    }
+};
+
+// global-memory (L2-resident) variant for hubs: same packing, device atomics
+template <bool WEIGHTED>
+struct GlobalTable;
+template <>
+struct GlobalTable<false> {
+    static constexpr int bytes_per_slot = 8;
+    unsigned long long* tab;
+    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double) const {
+        const unsigned long long want = ((unsigned long long)(uint32_t)x << 32) | 1ull;
+        uint32_t h = slot_of(x, cap);
+        while (true) {
+            const unsigned long long prev = atomicCAS(tab + h, (unsigned long long)EMPTY64, want);
+            if (prev == EMPTY64) return;
+            if ((int32_t)(prev >> 32) == x) {
+                atomicAdd(tab + h, 1ull);
+                return;
+            }
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+    }
+    __device__ __forceinline__ bool read(uint32_t q, int32_t& x, double& S) const {
+        const unsigned long long w = tab[q];
+        if (w == EMPTY64) return false;
+        x = (int32_t)(w >> 32);
+        S = (double)(uint32_t)w;
+        return true;
+    }
+};
+template <>
+struct GlobalTable<true> {
+    static constexpr int bytes_per_slot = 12;
+    int32_t* keys;
+    double* vals;
+    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double wv) const {
+        uint32_t h = slot_of(x, cap);
+        while (true) {
+            const int32_t prev = atomicCAS(keys + h, EMPTY_KEY, x);
+            if (prev == EMPTY_KEY || prev == x) break;
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+        atomicAdd(vals + h, wv);
+    }
+    __device__ __forceinline__ bool read(uint32_t q, int32_t& x, double& S) const {
+        const int32_t kq = keys[q];
+        if (kq == EMPTY_KEY) return false;
+        x = kq;
+        S = vals[q];
+        return true;
+    }
+};
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -310,46 +401,34 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 // ===========================================================================
 // group bins: GW warps per vertex, CAP-slot shared-memory table per group.
-// Every lane keeps U independent loads in flight (index stream, label
-// gather; then key read, mass gather) before consuming them.
+// Every lane keeps U independent loads in flight (index stream + label
+// gather; then slot read + mass gather) before consuming them.
 // ===========================================================================
-constexpr int U = 8;
+template <class WT, int CAP, int GROUPS>
+constexpr size_t group_smem_bytes() {
+    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::weighted>::bytes_per_slot;
+}
 
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
-struct GroupSmem {
-    using VT = ValT<WT>;
-    static constexpr size_t per_group = (size_t)CAP * (sizeof(VT) + sizeof(int32_t) + sizeof(uint16_t));
-    static constexpr size_t bytes = GROUPS * per_group;
-};
-
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U>
 __global__ void __launch_bounds__(GW * 32 * GROUPS)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
-    using VT = ValT<WT>;
+    constexpr bool WEIGHTED = WLoad<WT>::weighted;
     constexpr int GT = GW * 32;
-    static_assert(CAP <= 65536, "slot index must fit 16 bits");
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_g[GROUPS * GW];
     __shared__ int32_t s_x[GROUPS * GW];
-    __shared__ uint32_t s_cnt[GROUPS];
     const int gid = threadIdx.x / GT;
     const int gt = threadIdx.x % GT;
     const int wig = gt >> 5;
     const int lane = threadIdx.x & 31;
-    // layout: [vals: GROUPS*CAP VT][keys: GROUPS*CAP i32][slots: GROUPS*CAP u16]
-    VT* vals = reinterpret_cast<VT*>(smem) + (size_t)gid * CAP;
-    int32_t* keys = reinterpret_cast<int32_t*>(reinterpret_cast<VT*>(smem) + (size_t)GROUPS * CAP) + (size_t)gid * CAP;
-    uint16_t* slots = reinterpret_cast<uint16_t*>(reinterpret_cast<int32_t*>(reinterpret_cast<VT*>(smem) + (size_t)GROUPS * CAP) +
-                                                  (size_t)GROUPS * CAP) + (size_t)gid * CAP;
-    const uint32_t keys_s = smem_u32(keys), vals_s = smem_u32(vals), slots_s = smem_u32(slots);
-    const uint32_t cnt_s = smem_u32(&s_cnt[gid]);
+    SmemTable<WEIGHTED> tab;
+    if constexpr (WEIGHTED) tab.init_cap(smem + (size_t)gid * CAP * 12, CAP);
+    else tab.init(smem + (size_t)gid * CAP * 8);
     auto gsync = [&]() {
         if constexpr (GW == 1) __syncwarp();
         else named_sync(1 + gid, GT);
     };
-    // the table starts empty; every vertex empties the slots it used
-    for (uint32_t q = gt; q < CAP; q += GT) { keys[q] = EMPTY_KEY; vals[q] = (VT)0; }
-    if (gt == 0) s_cnt[gid] = 0;
+    for (uint32_t q = gt; q < CAP; q += GT) tab.clear(q);
     gsync();
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
@@ -380,7 +459,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             for (int j = 0; j < U; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) sc += wv[j];
-                else stable_insert<VT>(keys_s, vals_s, slots_s, cnt_s, cap, u[j], wv[j]);
+                else tab.insert(cap, u[j], wv[j]);
             }
         }
 #pragma unroll
@@ -394,36 +473,30 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 #pragma unroll
             for (int w = 0; w < GW; ++w) sc += s_g[gid * GW + w];
         }
-        const uint32_t nocc = s_cnt[gid];
         const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
-        for (uint32_t i0 = gt; i0 < nocc; i0 += GT * U) {
-            uint32_t q[U];
+        for (uint32_t q0 = gt; q0 < cap; q0 += GT * U) {
             int32_t x[U];
-            double Kx[U];
+            double S[U], Kx[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                const uint32_t ii = i0 + j * GT;
-                q[j] = ii < nocc ? slots[ii] : 0xffffffffu;
-                x[j] = ii < nocc ? keys[q[j]] : EMPTY_KEY;
+                const uint32_t q = q0 + j * GT;
+                if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
-                const double gq = dsub(dsub((double)vals[q[j]], dmul(t, Kx[j])), b);
+                const double gq = dsub(dsub(S[j], dmul(t, Kx[j])), b);
                 if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; }
-                keys[q[j]] = EMPTY_KEY;  // clean up for the next vertex
-                vals[q[j]] = (VT)0;
             }
         }
         warp_argmax(bg, bx);
         if constexpr (GW > 1) {
-            gsync();  // everyone has read s_g (S_c) and s_cnt before reuse
+            gsync();  // everyone has read s_g (S_c) before reuse
             if (lane == 0) { s_g[gid * GW + wig] = bg; s_x[gid * GW + wig] = bx; }
-            if (gt == 0) s_cnt[gid] = 0;
             gsync();
 #pragma unroll
             for (int w = 0; w < GW; ++w) {
@@ -431,19 +504,16 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 const int32_t ox = s_x[gid * GW + w];
                 if (better(og, ox, bg, bx)) { bg = og; bx = ox; }
             }
-        } else {
-            __syncwarp();
-            if (gt == 0) s_cnt[gid] = 0;
         }
         if (gt == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
-        gsync();  // table, counter and s_g free for the next vertex
+        gsync();  // table (already reset by take) and s_g free for the next vertex
     }
     flush_moves(a, my_moves);
 }
 
 // ===========================================================================
 // large bin (hubs): vertices batched so that their global tables fit in L2.
-// Per batch: insertion over INSERT_CHUNK-edge work items spread over all SMs,
+// Per batch: insertion over LARGE_CHUNK-edge work items spread over all SMs,
 // scoring over SCORE_CHUNK-slot work items (partial argmax per item), then a
 // warp per vertex merges its partials and decides.  Batches are planned once
 // on the host; no host synchronisation between batches.
@@ -454,12 +524,18 @@ struct LargeBatch {
     const int64_t* cap_off;    // [nL+1] table slot offsets
     const int64_t* item_off;   // [nL+1] insertion work-item offsets
     const int64_t* sitem_off;  // [nL+1] scoring work-item offsets
-    int32_t* keys;
-    void* vals;
+    void* tab;                 // packed u64 slots, or int32 keys ...
+    double* tabv;              // ... plus double sums (weighted)
     double* sc;                // [nL] S_c per vertex (own-cluster weight)
     double* pg;                // [scoring items] partial best gain
     int32_t* px;               // [scoring items] partial best cluster
 };
+
+template <bool WEIGHTED>
+__device__ __forceinline__ GlobalTable<WEIGHTED> gtable(const LargeBatch& L, int64_t off) {
+    if constexpr (WEIGHTED) return GlobalTable<true>{static_cast<int32_t*>(L.tab) + off, L.tabv + off};
+    else return GlobalTable<false>{static_cast<unsigned long long*>(L.tab) + off};
+}
 
 __device__ __forceinline__ int64_t owner_of(const int64_t* off, int64_t n, int64_t it) {
     int64_t lo = 0, hi = n;
@@ -473,7 +549,7 @@ __device__ __forceinline__ int64_t owner_of(const int64_t* off, int64_t n, int64
 template <class WT, bool ASYNC>
 __global__ void __launch_bounds__(LARGE_THREADS)
 k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
-    using VT = ValT<WT>;
+    constexpr int UL = 8;
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
@@ -483,26 +559,25 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
         const int64_t e0 = s + (it - L.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
-        int32_t* keys = L.keys + L.cap_off[li];
-        VT* vals = static_cast<VT*>(L.vals) + L.cap_off[li];
+        const auto tab = gtable<WLoad<WT>::weighted>(L, L.cap_off[li]);
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         double sc = 0.0;
-        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * U) {
-            int32_t u[U];
-            double wv[U];
+        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * UL) {
+            int32_t u[UL];
+            double wv[UL];
 #pragma unroll
-            for (int j = 0; j < U; ++j) {
+            for (int j = 0; j < UL; ++j) {
                 const int64_t e = eb + (int64_t)j * LARGE_THREADS;
                 u[j] = e < e1 ? ld_stream_i32(a.indices + e, pol_stream) : -1;
                 wv[j] = e < e1 ? WLoad<WT>::at(a.w, e) : 0.0;
             }
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
 #pragma unroll
-            for (int j = 0; j < U; ++j) {
+            for (int j = 0; j < UL; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) sc += wv[j];
-                else table_insert<VT>(keys, vals, cap, u[j], wv[j]);
+                else tab.insert(cap, u[j], wv[j]);
             }
         }
 #pragma unroll
@@ -528,7 +603,7 @@ __device__ __forceinline__ void block_argmax(double& g, int32_t& x, double* s_g,
 template <class WT, bool ASYNC>
 __global__ void __launch_bounds__(SCORE_THREADS)
 k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
-    using VT = ValT<WT>;
+    constexpr int UL = 8;
     __shared__ double s_g[SCORE_THREADS / 32];
     __shared__ int32_t s_x[SCORE_THREADS / 32];
     const uint64_t pol_keep = policy_evict_last();
@@ -538,8 +613,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
         const uint32_t q_begin = (uint32_t)((it - L.sitem_off[li]) * SCORE_CHUNK);
         const uint32_t q_end = (uint32_t)min64((int64_t)q_begin + SCORE_CHUNK, cap);
-        const int32_t* keys = L.keys + L.cap_off[li];
-        const VT* vals = static_cast<const VT*>(L.vals) + L.cap_off[li];
+        const auto tab = gtable<WLoad<WT>::weighted>(L, L.cap_off[li]);
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
@@ -547,20 +621,20 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
-        for (uint32_t q0 = q_begin + threadIdx.x; q0 < q_end; q0 += SCORE_THREADS * U) {
-            int32_t x[U];
-            double Kx[U];
+        for (uint32_t q0 = q_begin + threadIdx.x; q0 < q_end; q0 += SCORE_THREADS * UL) {
+            int32_t x[UL];
+            double S[UL], Kx[UL];
 #pragma unroll
-            for (int j = 0; j < U; ++j) {
+            for (int j = 0; j < UL; ++j) {
                 const uint32_t q = q0 + j * SCORE_THREADS;
-                x[j] = q < q_end ? keys[q] : EMPTY_KEY;
+                if (!(q < q_end && tab.read(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
-            for (int j = 0; j < U; ++j) {
+            for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
-                const double gq = dsub(dsub((double)vals[q0 + j * SCORE_THREADS], dmul(t, Kx[j])), b);
+                const double gq = dsub(dsub(S[j], dmul(t, Kx[j])), b);
                 if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; }
             }
         }
@@ -695,20 +769,20 @@ void set_smem(K kernel, int bytes) {
     LCC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS>
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U>
 void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     if (hi <= lo) return;
     constexpr int THREADS = GW * 32 * GROUPS;
-    constexpr int SMEM = (int)GroupSmem<WT, ASYNC, GW, CAP, GROUPS>::bytes;
+    constexpr int SMEM = (int)group_smem_bytes<WT, CAP, GROUPS>();
     static int occ = 0;
     if (!occ) {
-        set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS>, SMEM);
-        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS>, THREADS, SMEM));
+        set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS, U>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS, U>, THREADS, SMEM));
         occ = std::max(occ, 1);
     }
     const int64_t blocks_needed = (hi - lo + GROUPS - 1) / GROUPS;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * occ));
-    k_group<WT, ASYNC, GW, CAP, GROUPS><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
+    k_group<WT, ASYNC, GW, CAP, GROUPS, U><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
     LCC_LAUNCH_CHECK();
 }
 
@@ -720,13 +794,13 @@ constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-reside
 // 2 slot-list) bytes; GROUPS chosen so 2-3 CTAs fit per SM.
 template <class WT, bool ASYNC>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
-    switch (bin) {
-        case 1: launch_group<WT, ASYNC, 1, 256, 8>(a, list, lo, hi, s); break;     //   33..128   warp
-        case 2: launch_group<WT, ASYNC, 1, 1024, 8>(a, list, lo, hi, s); break;    //  129..512   warp
-        case 3: launch_group<WT, ASYNC, 2, 2048, 4>(a, list, lo, hi, s); break;    //  513..T-1   2 warps
-        case 4: launch_group<WT, ASYNC, 4, 4096, 2>(a, list, lo, hi, s); break;    //    T..2048  4 warps
-        case 5: launch_group<WT, ASYNC, 8, 8192, 1>(a, list, lo, hi, s); break;    // 2049..4096  8 warps
-        case 6: launch_group<WT, ASYNC, 8, B5_CAP, 1>(a, list, lo, hi, s); break;  // 4097..10240 8 warps
+    switch (bin) {  //                         GW  CAP    GROUPS U
+        case 1: launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s); break;     //   33..128   warp
+        case 2: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;    //  129..512   warp
+        case 3: launch_group<WT, ASYNC, 2, 2048, 4, 8>(a, list, lo, hi, s); break;    //  513..T-1   2 warps
+        case 4: launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s); break;    //    T..2048  4 warps
+        case 5: launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s); break;    // 2049..4096  8 warps
+        case 6: launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s); break;  // 4097..10240 8 warps
         default: break;
     }
 }
@@ -735,14 +809,14 @@ inline int64_t large_cap(int64_t deg) { return (2 * deg + 31) & ~31LL; }
 
 template <class WT, bool ASYNC>
 void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_t nL, cudaStream_t s) {
-    using VT = ValT<WT>;
+    constexpr bool WEIGHTED = WLoad<WT>::weighted;
     Buf<int64_t> ddeg(nL, s);
     k_degrees_of<<<grid_for(nL, 256), 256, 0, s>>>(g.indptr, large, nL, ddeg.get());
     LCC_LAUNCH_CHECK();
     std::vector<int64_t> deg(nL);
     LCC_CUDA(cudaMemcpyAsync(deg.data(), ddeg.get(), sizeof(int64_t) * nL, cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
-    const int64_t slot_bytes = sizeof(int32_t) + sizeof(VT);
+    const int64_t slot_bytes = GlobalTable<WEIGHTED>::bytes_per_slot;
     int64_t maxcap = 0;
     for (int64_t d : deg) maxcap = std::max<int64_t>(maxcap, large_cap(d));
     const int64_t table_slots = std::max<int64_t>(LARGE_TABLE_BYTES / slot_bytes, maxcap);
@@ -777,18 +851,22 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_
     }
     Buf<int64_t> offs(h.size(), s);
     LCC_CUDA(cudaMemcpyAsync(offs.get(), h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice, s));
-    Buf<int32_t> keys(table_slots, s);
-    Buf<unsigned char> vals(table_slots * sizeof(VT), s);
+    Buf<unsigned long long> tab(WEIGHTED ? (table_slots + 1) / 2 : table_slots, s);  // u64 slots or i32 keys
+    Buf<double> tabv(WEIGHTED ? table_slots : 0, s);
     Buf<double> sc(nL, s);
     Buf<double> pg(max_sitems, s);
     Buf<int32_t> px(max_sitems, s);
     LCC_CUDA(cudaMemsetAsync(sc.get(), 0, sizeof(double) * nL, s));
     for (const B& bt : batches) {
         const int64_t* o = offs.get() + bt.off;
-        LargeBatch L{large + bt.b0, bt.nb, o, o + (bt.nb + 1), o + 2 * (bt.nb + 1), keys.get(), vals.get(),
+        LargeBatch L{large + bt.b0, bt.nb, o, o + (bt.nb + 1), o + 2 * (bt.nb + 1), tab.get(), tabv.get(),
                      sc.get() + bt.b0, pg.get(), px.get()};
-        LCC_CUDA(cudaMemsetAsync(keys.get(), 0xff, sizeof(int32_t) * bt.slots, s));
-        LCC_CUDA(cudaMemsetAsync(vals.get(), 0, sizeof(VT) * bt.slots, s));
+        if (WEIGHTED) {
+            LCC_CUDA(cudaMemsetAsync(tab.get(), 0xff, sizeof(int32_t) * bt.slots, s));
+            LCC_CUDA(cudaMemsetAsync(tabv.get(), 0, sizeof(double) * bt.slots, s));
+        } else {
+            LCC_CUDA(cudaMemsetAsync(tab.get(), 0xff, sizeof(unsigned long long) * bt.slots, s));
+        }
         k_large_insert<WT, ASYNC><<<grid_for(bt.items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, bt.items);
         LCC_LAUNCH_CHECK();
         k_large_score<WT, ASYNC><<<grid_for(bt.sitems * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L, bt.sitems);

@@ -31,6 +31,7 @@
 #include <math.h>
 #include <type_traits>
 #include <vector>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "prims.cuh"
@@ -41,7 +42,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_MAX = 32;
 constexpr int SMALL_THREADS = 256;
-constexpr int LARGE_CHUNK = 8192;   // edges per insertion work item
+constexpr int LARGE_CHUNK = 2048;   // edges per insertion work item
 constexpr int LARGE_THREADS = 256;
 constexpr int SCORE_CHUNK = 16384;  // table slots per scoring work item
 constexpr int SCORE_THREADS = 256;
@@ -893,8 +894,13 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     be.hi[2] = std::min<int64_t>(512, T - 1);
     be.hi[3] = T - 1;
     be.hi[4] = 2048;
-    be.hi[5] = 4096;
-    be.hi[6] = MED_MAX;
+    // LCC_LARGE_MIN (env, tuning only): degree above which hubs use the L2 path
+    static const int64_t large_min = [] {
+        const char* e = getenv("LCC_LARGE_MIN");
+        return e ? std::max<int64_t>(2048, atoll(e)) : MED_MAX;
+    }();
+    be.hi[5] = std::min<int64_t>(4096, large_min);
+    be.hi[6] = large_min;
     be.hi[7] = INT64_MAX;
 
     Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);

@@ -16,9 +16,26 @@ long long& launch_counter() {
 namespace {
 thread_local std::string g_err;
 
+// Keep freed scratch in the device's stream-ordered pool: the default release
+// threshold (0) hands memory back to the driver at every synchronisation, so
+// each best-move iteration would pay for fresh cudaMalloc/cudaFree of its
+// O(n) scratch.
+void init_pool_once() {
+    static bool done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 template <class F>
 lcc_status guard(F&& f) {
     try {
+        init_pool_once();
         f();
         g_err.clear();
         return LCC_OK;

@@ -513,6 +513,225 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 }
 
 // ===========================================================================
+// window bin (33 <= deg < T): edge-balanced multi-vertex CTAs.
+// The bin list is cut into windows of ~WIN_W edges along its degree prefix
+// (window w = list entries whose prefix falls in [w*W, (w+1)*W)), so every
+// CTA does the same amount of edge work whatever the degree mix, and no
+// vertex straddles two CTAs (deg < W).  Per window:
+//   1. each thread takes 8 consecutive edge positions, loads indices and
+//      gathers labels (8 loads in flight), inserts ((label, vertex-slot) ->
+//      count) into the CTA's shared table -- one 64-bit atomic per edge;
+//      edges into the vertex's own cluster accumulate S_c instead;
+//   2. every occupied entry is scored; per-vertex argmax by a 64-bit
+//      shared atomicMax on the order-preserving gain bits, then atomicMin on
+//      the cluster id among the entries that hit the maximum (lowest-id tie);
+//   3. one thread per vertex decides.
+// ===========================================================================
+constexpr int WIN_THREADS = 256;
+constexpr int WIN_ITEMS = 8;
+constexpr int WIN_W = WIN_THREADS * WIN_ITEMS / 2;   // 1024: window edges <= 2W-1 for deg < W
+constexpr int WIN_CAP = 4096;                        // table slots: load <= 0.5
+constexpr int WIN_MAXV = WIN_W / (SMALL_MAX + 1) * 2 + 2;  // vertices per window (deg > 32)
+
+__device__ __forceinline__ unsigned long long ord_gain(double g) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(g);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord_gain(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+template <bool WEIGHTED>
+constexpr size_t window_smem_bytes() {
+    // table u64 + occupied list u16 + gain f64 (+ f64 sums when weighted)
+    return (size_t)WIN_CAP * (8 + 2 + 8 + (WEIGHTED ? 8 : 0));
+}
+
+template <class WT, bool ASYNC>
+__global__ void __launch_bounds__(WIN_THREADS)
+k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__ off,
+         const int64_t* __restrict__ wstart, int64_t w0, int64_t w1) {
+    constexpr bool WEIGHTED = WLoad<WT>::weighted;
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(smem);
+    double* gval = reinterpret_cast<double*>(smem + (size_t)WIN_CAP * 8);
+    double* sums = reinterpret_cast<double*>(smem + (size_t)WIN_CAP * 16);  // weighted only
+    uint16_t* occ = reinterpret_cast<uint16_t*>(smem + (size_t)WIN_CAP * (WEIGHTED ? 24 : 16));
+    __shared__ int64_t s_start[WIN_MAXV];
+    __shared__ int32_t s_loc[WIN_MAXV + 1];
+    __shared__ int32_t s_v[WIN_MAXV], s_c[WIN_MAXV], s_bx[WIN_MAXV];
+    __shared__ double s_t[WIN_MAXV], s_kv[WIN_MAXV], s_Kc[WIN_MAXV], s_sc[WIN_MAXV], s_b[WIN_MAXV];
+    __shared__ unsigned long long s_best[WIN_MAXV];
+    __shared__ uint32_t s_nocc;
+    const uint32_t tab_s = smem_u32(tab), sums_s = smem_u32(sums), occ_s = smem_u32(occ), nocc_s = smem_u32(&s_nocc);
+    const int tid = threadIdx.x;
+    for (int q = tid; q < WIN_CAP; q += WIN_THREADS) {
+        tab[q] = EMPTY64;
+        if constexpr (WEIGHTED) sums[q] = 0.0;
+    }
+    if (tid == 0) s_nocc = 0;
+    __syncthreads();
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    unsigned long long my_moves = 0;
+    for (int64_t w = w0 + blockIdx.x; w < w1; w += gridDim.x) {
+        const int64_t i0 = __ldg(wstart + w), i1 = __ldg(wstart + w + 1);
+        const int nv = (int)(i1 - i0);
+        if (nv <= 0) continue;  // uniform across the CTA
+        const int64_t base = __ldg(off + i0);
+        const int E = (int)(__ldg(off + i1) - base);
+        // ---- 0. per-vertex setup
+        if (tid < nv) {
+            const int32_t v = __ldg(list + i0 + tid);
+            s_v[tid] = v;
+            s_start[tid] = __ldg(a.indptr + v);
+            s_loc[tid] = (int32_t)(__ldg(off + i0 + tid) - base);
+            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+            s_c[tid] = c;
+            const double kv = kval(a.k, v);
+            s_kv[tid] = kv;
+            s_t[tid] = dmul(a.lam, kv);
+            s_Kc[tid] = ldK<ASYNC>(a.K, c, pol_keep);
+            s_sc[tid] = 0.0;
+            s_best[tid] = 0ull;  // below every real gain key
+            s_bx[tid] = NO_CAND;
+        }
+        if (tid == 0) s_loc[nv] = E;
+        __syncthreads();
+        const uint32_t cap = (uint32_t)min64(WIN_CAP, ((int64_t)2 * E + 255) & ~255LL);
+        // ---- 1. edges: 8 consecutive positions per thread
+        {
+            const int p0 = tid * WIN_ITEMS;
+            int32_t u[WIN_ITEMS];
+            int slot[WIN_ITEMS];
+            double wv[WIN_ITEMS];
+            int sl = 0;
+            if (p0 < E) {
+                int lo = 0, hi = nv;  // last sl with s_loc[sl] <= p0
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_loc[mid] <= p0) lo = mid; else hi = mid;
+                }
+                sl = lo;
+            }
+#pragma unroll
+            for (int j = 0; j < WIN_ITEMS; ++j) {
+                const int p = p0 + j;
+                u[j] = -1;
+                wv[j] = 0.0;
+                slot[j] = 0;
+                if (p < E) {
+                    while (p >= s_loc[sl + 1]) ++sl;
+                    const int64_t e = s_start[sl] + (p - s_loc[sl]);
+                    u[j] = ld_stream_i32(a.indices + e, pol_stream);
+                    wv[j] = WLoad<WT>::at(a.w, e);
+                    slot[j] = sl;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+#pragma unroll
+            for (int j = 0; j < WIN_ITEMS; ++j) {
+                if (u[j] == EMPTY_KEY) continue;
+                const int sj = slot[j];
+                if (u[j] == s_c[sj]) {
+                    atomicAdd(&s_sc[sj], wv[j]);
+                    continue;
+                }
+                // key = (label << 32) | (slot << 16); low 16 bits count (unweighted)
+                const unsigned long long key = ((unsigned long long)(uint32_t)u[j] << 32) | ((unsigned long long)sj << 16);
+                uint32_t h = (uint32_t)(((uint64_t)hash32((uint32_t)u[j] ^ (0x9e3779b9u * (uint32_t)(sj + 1))) * cap) >> 32);
+                while (true) {
+                    const uint32_t addr = tab_s + 8 * h;
+                    unsigned long long cur;
+                    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(cur) : "r"(addr));
+                    bool mine = (cur >> 16) == (key >> 16);
+                    if (!mine && cur == EMPTY64) {
+                        unsigned long long prev;
+                        asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(prev) : "r"(addr), "l"(EMPTY64), "l"(key | 1ull) : "memory");
+                        if (prev == EMPTY64) {
+                            uint32_t pos;
+                            asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(nocc_s) : "memory");
+                            asm volatile("st.shared.u16 [%0], %1;" ::"r"(occ_s + 2 * pos), "h"((unsigned short)h) : "memory");
+                            if constexpr (WEIGHTED) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
+                            break;
+                        }
+                        mine = (prev >> 16) == (key >> 16);
+                    }
+                    if (mine) {
+                        if constexpr (WEIGHTED) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
+                        else asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(addr) : "memory");
+                        break;
+                    }
+                    h = (h + 1 == cap) ? 0 : h + 1;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < nv) s_b[tid] = dadd(dsub(s_sc[tid], dmul(s_t[tid], s_Kc[tid])), dmul(s_t[tid], s_kv[tid]));
+        __syncthreads();
+        // ---- 2a. score occupied entries, per-vertex max gain
+        const uint32_t nocc = s_nocc;
+        for (uint32_t i = tid; i < nocc; i += WIN_THREADS) {
+            const uint32_t q = occ[i];
+            const unsigned long long cur = tab[q];
+            const int32_t x = (int32_t)(cur >> 32);
+            const int sj = (int)((cur >> 16) & 0xffff);
+            const double S = WEIGHTED ? sums[q] : (double)(uint32_t)(cur & 0xffff);
+            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC>(a.K, x, pol_keep))), s_b[sj]);
+            gval[i] = g;
+            atomicMax(&s_best[sj], ord_gain(g));
+        }
+        __syncthreads();
+        // ---- 2b. lowest id among the maxima; reset the table
+        for (uint32_t i = tid; i < nocc; i += WIN_THREADS) {
+            const uint32_t q = occ[i];
+            const unsigned long long cur = tab[q];
+            const int32_t x = (int32_t)(cur >> 32);
+            const int sj = (int)((cur >> 16) & 0xffff);
+            if (ord_gain(gval[i]) == s_best[sj]) atomicMin(&s_bx[sj], x);
+            tab[q] = EMPTY64;
+            if constexpr (WEIGHTED) sums[q] = 0.0;
+        }
+        __syncthreads();
+        // ---- 3. decide
+        if (tid == 0) s_nocc = 0;
+        if (tid < nv) {
+            const int32_t bx = s_bx[tid];
+            my_moves += decide<ASYNC>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND,
+                                      unord_gain(s_best[tid]), bx);
+        }
+        __syncthreads();
+    }
+    flush_moves(a, my_moves);
+}
+
+__global__ void k_window_starts(const int64_t* __restrict__ off, int64_t nb, int64_t nwin, int64_t* wstart) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= nwin; w += (int64_t)gridDim.x * blockDim.x) {
+        // first list index whose prefix is >= w*W  (lower_bound over off[0..nb])
+        const int64_t target = w * (int64_t)WIN_W;
+        int64_t lo = 0, hi = nb + 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (off[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        wstart[w] = w == nwin ? nb : (lo > nb ? nb : lo);
+    }
+}
+
+struct DegOfList {
+    const int64_t* indptr;
+    const int32_t* list;
+    int64_t n;
+    __device__ __forceinline__ int64_t operator()(int64_t i) const {
+        if (i >= n) return 0;
+        const int32_t v = list[i];
+        return indptr[v + 1] - indptr[v];
+    }
+};
+
+// ===========================================================================
 // large bin (hubs): vertices batched so that their global tables fit in L2.
 // Per batch: insertion over LARGE_CHUNK-edge work items spread over all SMs,
 // scoring over SCORE_CHUNK-slot work items (partial argmax per item), then a
@@ -673,7 +892,7 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
 // ===========================================================================
 // degree-bin partition (one pass, block-aggregated reservations)
 // ===========================================================================
-constexpr int NBINS = 8;
+constexpr int NBINS = 6;
 struct BinEdges {
     int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
@@ -796,14 +1015,46 @@ constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-reside
 template <class WT, bool ASYNC>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     switch (bin) {  //                         GW  CAP    GROUPS U
-        case 1: launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s); break;     //   33..128   warp
-        case 2: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;    //  129..512   warp
-        case 3: launch_group<WT, ASYNC, 2, 2048, 4, 8>(a, list, lo, hi, s); break;    //  513..T-1   2 warps
-        case 4: launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s); break;    //    T..2048  4 warps
-        case 5: launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s); break;    // 2049..4096  8 warps
-        case 6: launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s); break;  // 4097..10240 8 warps
+        case 2: launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s); break;    //    T..2048  4 warps
+        case 3: launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s); break;    // 2049..4096  8 warps
+        case 4: launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s); break;  // 4097..10240 8 warps
         default: break;
     }
+}
+
+// window bin: degree prefix over the bin list -> window starts
+struct WindowPlan {
+    Buf<int64_t> off, wstart;
+    int64_t nwin = 0;
+};
+inline void plan_windows(const int64_t* indptr, const int32_t* list, int64_t nb, WindowPlan& P, cudaStream_t s) {
+    P.off.alloc(nb + 1, s);
+    cub::TransformInputIterator<int64_t, DegOfList, cub::CountingInputIterator<int64_t>> degs(
+        cub::CountingInputIterator<int64_t>(0), DegOfList{indptr, list, nb});
+    exclusive_sum(degs, P.off.get(), nb + 1, s);
+    int64_t total = 0;
+    LCC_CUDA(cudaMemcpyAsync(&total, P.off.get() + nb, sizeof(total), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    P.nwin = (total + WIN_W - 1) / WIN_W;
+    if (P.nwin < 1) P.nwin = 1;
+    P.wstart.alloc(P.nwin + 1, s);
+    k_window_starts<<<grid_for(P.nwin + 1, 256), 256, 0, s>>>(P.off.get(), nb, P.nwin, P.wstart.get());
+    LCC_LAUNCH_CHECK();
+}
+
+template <class WT, bool ASYNC>
+void launch_window(const BMArgs& a, const int32_t* list, const WindowPlan& P, int64_t w0, int64_t w1, cudaStream_t s) {
+    if (w1 <= w0) return;
+    constexpr int SMEM = (int)window_smem_bytes<WLoad<WT>::weighted>();
+    static int occ = 0;
+    if (!occ) {
+        set_smem(k_window<WT, ASYNC>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<WT, ASYNC>, WIN_THREADS, SMEM));
+        occ = std::max(occ, 1);
+    }
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(w1 - w0, (int64_t)num_sms() * occ));
+    k_window<WT, ASYNC><<<grid, WIN_THREADS, SMEM, s>>>(a, list, P.off.get(), P.wstart.get(), w0, w1);
+    LCC_LAUNCH_CHECK();
 }
 
 inline int64_t large_cap(int64_t deg) { return (2 * deg + 31) & ~31LL; }
@@ -887,21 +1138,21 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
-    const int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), 1024);
-    BinEdges be;
-    be.hi[0] = SMALL_MAX;
-    be.hi[1] = std::min<int64_t>(128, T - 1);
-    be.hi[2] = std::min<int64_t>(512, T - 1);
-    be.hi[3] = T - 1;
-    be.hi[4] = 2048;
+    // bins: 0 deg<=32 warp windows | 1 33..T-1 edge windows | 2 T..2048 |
+    //       3 2049..4096 | 4 ..large_min (CTA groups) | 5 hubs (L2 tables)
+    const int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
     // LCC_LARGE_MIN (env, tuning only): degree above which hubs use the L2 path
     static const int64_t large_min = [] {
         const char* e = getenv("LCC_LARGE_MIN");
-        return e ? std::max<int64_t>(2048, atoll(e)) : MED_MAX;
+        return e ? std::max<int64_t>(2048, atoll(e)) : (int64_t)4096;
     }();
-    be.hi[5] = std::min<int64_t>(4096, large_min);
-    be.hi[6] = large_min;
-    be.hi[7] = INT64_MAX;
+    BinEdges be;
+    be.hi[0] = SMALL_MAX;
+    be.hi[1] = T - 1;
+    be.hi[2] = std::min<int64_t>(2048, large_min);
+    be.hi[3] = std::min<int64_t>(4096, large_min);
+    be.hi[4] = std::min<int64_t>(MED_MAX, large_min);
+    be.hi[5] = INT64_MAX;
 
     Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);
     std::vector<int64_t> binstart;
@@ -947,13 +1198,20 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         LCC_CUDA(cudaEventElapsedTime(&kms_large, ev0, ev1));
     }
     const int P = ASYNC ? std::max(1, chunks) : 1;
+    WindowPlan wp;
+    if (hc[1] > 0) plan_windows(g.indptr, lists.get() + binstart[1], (int64_t)hc[1], wp, s);
     LCC_CUDA(cudaEventRecord(ev0, s));
     for (int j = 0; j < P; ++j) {
         for (int b = 0; b < NBINS - 1; ++b) {
             const int64_t nb = (int64_t)hc[b];
+            if (nb == 0) continue;
+            const int32_t* list = lists.get() + binstart[b];
+            if (b == 1) {
+                launch_window<WT, ASYNC>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, s);
+                continue;
+            }
             const int64_t lo = nb * j / P, hi = nb * (j + 1) / P;
             if (hi <= lo) continue;
-            const int32_t* list = lists.get() + binstart[b];
             if (b == 0) {
                 const int64_t warps = (hi - lo + 31) / 32;
                 k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, s>>>(a, list, lo, hi);

@@ -265,42 +265,34 @@ struct SmemTable;
 template <>
 struct SmemTable<false> {
     static constexpr int bytes_per_slot = 8;
-    uint32_t base;  // shared address of uint64[cap]
-    __device__ __forceinline__ void init(unsigned char* p) { base = smem_u32(p); }
+    uint32_t keys, cnts;  // int32[cap] keys, then u32[cap] counts (native 32-bit shared atomics)
+    __device__ __forceinline__ void init_cap(unsigned char* p, uint32_t CAP) {
+        cnts = smem_u32(p);
+        keys = cnts + 4 * CAP;
+    }
     __device__ __forceinline__ void clear(uint32_t q) const {
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(base + 8 * q), "l"(EMPTY64) : "memory");
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(keys + 4 * q), "r"(EMPTY_KEY) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(cnts + 4 * q), "r"(0u) : "memory");
     }
     __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double) const {
-        const uint64_t want = ((uint64_t)(uint32_t)x << 32) | 1ull;
         uint32_t h = slot_of(x, cap);
         while (true) {
-            const uint32_t addr = base + 8 * h;
-            uint64_t w;
-            asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(addr));
-            if ((int32_t)(w >> 32) == x) {
-                asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(addr) : "memory");
-                return;
-            }
-            if (w == EMPTY64) {
-                uint64_t prev;
-                asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(prev) : "r"(addr), "l"(EMPTY64), "l"(want) : "memory");
-                if (prev == EMPTY64) return;
-                if ((int32_t)(prev >> 32) == x) {
-                    asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(addr) : "memory");
-                    return;
-                }
-            }
+            int32_t prev;
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+            if (prev == EMPTY_KEY || prev == x) break;
             h = (h + 1 == cap) ? 0 : h + 1;
         }
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts + 4 * h) : "memory");
     }
-    // read + reset; returns false for an empty slot
     __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
-        uint64_t w;
-        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w) : "r"(base + 8 * q));
-        if (w == EMPTY64) return false;
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(base + 8 * q), "l"(EMPTY64) : "memory");
-        x = (int32_t)(w >> 32);
-        S = (double)(uint32_t)w;
+        int32_t kq;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
+        if (kq == EMPTY_KEY) return false;
+        uint32_t cq;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cq) : "r"(cnts + 4 * q));
+        clear(q);
+        x = kq;
+        S = (double)cq;
         return true;
     }
 };
@@ -423,8 +415,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const int wig = gt >> 5;
     const int lane = threadIdx.x & 31;
     SmemTable<WEIGHTED> tab;
-    if constexpr (WEIGHTED) tab.init_cap(smem + (size_t)gid * CAP * 12, CAP);
-    else tab.init(smem + (size_t)gid * CAP * 8);
+    tab.init_cap(smem + (size_t)gid * CAP * SmemTable<WEIGHTED>::bytes_per_slot, CAP);
     auto gsync = [&]() {
         if constexpr (GW == 1) __syncwarp();
         else named_sync(1 + gid, GT);
@@ -513,25 +504,28 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 }
 
 // ===========================================================================
-// window bin (33 <= deg < T): edge-balanced multi-vertex CTAs.
-// The bin list is cut into windows of ~WIN_W edges along its degree prefix
-// (window w = list entries whose prefix falls in [w*W, (w+1)*W)), so every
-// CTA does the same amount of edge work whatever the degree mix, and no
-// vertex straddles two CTAs (deg < W).  Per window:
-//   1. each thread takes 8 consecutive edge positions, loads indices and
-//      gathers labels (8 loads in flight), inserts ((label, vertex-slot) ->
-//      count) into the CTA's shared table -- one 64-bit atomic per edge;
-//      edges into the vertex's own cluster accumulate S_c instead;
-//   2. every occupied entry is scored; per-vertex argmax by a 64-bit
-//      shared atomicMax on the order-preserving gain bits, then atomicMin on
-//      the cluster id among the entries that hit the maximum (lowest-id tie);
+// window bin (33 <= deg < T <= 512): edge-balanced multi-vertex CTAs.
+// The bin list is cut into windows along its degree prefix (window w = list
+// entries whose prefix falls in [w*W, (w+1)*W)), so every CTA does the same
+// edge work whatever the degree mix and no vertex straddles two CTAs
+// (deg < W).  A window holds <= 2W-1 edges and <= 31 vertices, so a table key
+// packs (vertex slot, cluster id) into 32 bits and every shared-memory atomic
+// is a native 32-bit one (64-bit shared CAS is emulated by a spin loop).
+//   1. each thread takes 8 consecutive edge positions: index loads, label
+//      gathers (8 in flight), then insert key -> count (CAS + RED per edge);
+//      edges into the vertex's own cluster add to S_c instead;
+//   2. every slot is scored; per-vertex argmax in three 32-bit atomic steps
+//      (max of the high word of the order-preserving gain bits, max of the low
+//      word among those, min cluster id among exact maxima: lowest-id ties);
 //   3. one thread per vertex decides.
 // ===========================================================================
-constexpr int WIN_THREADS = 256;
+constexpr int WIN_THREADS = 128;
 constexpr int WIN_ITEMS = 8;
-constexpr int WIN_W = WIN_THREADS * WIN_ITEMS / 2;   // 1024: window edges <= 2W-1 for deg < W
-constexpr int WIN_CAP = 4096;                        // table slots: load <= 0.5
-constexpr int WIN_MAXV = WIN_W / (SMALL_MAX + 1) * 2 + 2;  // vertices per window (deg > 32)
+constexpr int WIN_W = WIN_THREADS * WIN_ITEMS / 2;  // 512: window edges <= 2W-1 = 1023
+constexpr int WIN_CAP = 2048;                       // table slots: load <= 0.5
+constexpr int WIN_MAXV = 32;                        // (2W-1)/33 + 1 = 31 vertices max
+constexpr int LABEL_BITS = 27;                      // cluster ids < 2^27 (n < 2^26)
+constexpr uint32_t KEY_EMPTY = 0xffffffffu;
 
 __device__ __forceinline__ unsigned long long ord_gain(double g) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(g);
@@ -544,8 +538,8 @@ __device__ __forceinline__ double unord_gain(unsigned long long k) {
 
 template <bool WEIGHTED>
 constexpr size_t window_smem_bytes() {
-    // table u64 + occupied list u16 + gain f64 (+ f64 sums when weighted)
-    return (size_t)WIN_CAP * (8 + 2 + 8 + (WEIGHTED ? 8 : 0));
+    // keys u32 + counts u32 (or sums f64) + gain f64
+    return (size_t)WIN_CAP * (4 + (WEIGHTED ? 8 : 4) + 8);
 }
 
 template <class WT, bool ASYNC>
@@ -554,24 +548,23 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
          const int64_t* __restrict__ wstart, int64_t w0, int64_t w1) {
     constexpr bool WEIGHTED = WLoad<WT>::weighted;
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long* tab = reinterpret_cast<unsigned long long*>(smem);
-    double* gval = reinterpret_cast<double*>(smem + (size_t)WIN_CAP * 8);
-    double* sums = reinterpret_cast<double*>(smem + (size_t)WIN_CAP * 16);  // weighted only
-    uint16_t* occ = reinterpret_cast<uint16_t*>(smem + (size_t)WIN_CAP * (WEIGHTED ? 24 : 16));
+    double* gval = reinterpret_cast<double*>(smem);
+    double* sums = reinterpret_cast<double*>(smem + (size_t)WIN_CAP * 8);          // weighted
+    uint32_t* cnts = reinterpret_cast<uint32_t*>(smem + (size_t)WIN_CAP * 8);      // unweighted
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem + (size_t)WIN_CAP * (WEIGHTED ? 16 : 12));
     __shared__ int64_t s_start[WIN_MAXV];
     __shared__ int32_t s_loc[WIN_MAXV + 1];
-    __shared__ int32_t s_v[WIN_MAXV], s_c[WIN_MAXV], s_bx[WIN_MAXV];
-    __shared__ double s_t[WIN_MAXV], s_kv[WIN_MAXV], s_Kc[WIN_MAXV], s_sc[WIN_MAXV], s_b[WIN_MAXV];
-    __shared__ unsigned long long s_best[WIN_MAXV];
-    __shared__ uint32_t s_nocc;
-    const uint32_t tab_s = smem_u32(tab), sums_s = smem_u32(sums), occ_s = smem_u32(occ), nocc_s = smem_u32(&s_nocc);
+    __shared__ int32_t s_v[WIN_MAXV], s_c[WIN_MAXV];
+    __shared__ double s_t[WIN_MAXV], s_kv[WIN_MAXV], s_Kc[WIN_MAXV], s_b[WIN_MAXV], s_scw[WIN_MAXV];
+    __shared__ uint32_t s_sc[WIN_MAXV], s_hi[WIN_MAXV], s_lo[WIN_MAXV];
+    __shared__ int32_t s_bx[WIN_MAXV];
     const int tid = threadIdx.x;
+    const uint32_t keys_s = smem_u32(keys), cnts_s = smem_u32(cnts), sums_s = smem_u32(sums);
     for (int q = tid; q < WIN_CAP; q += WIN_THREADS) {
-        tab[q] = EMPTY64;
+        keys[q] = KEY_EMPTY;
         if constexpr (WEIGHTED) sums[q] = 0.0;
+        else cnts[q] = 0;
     }
-    if (tid == 0) s_nocc = 0;
-    __syncthreads();
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
@@ -593,13 +586,15 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             s_kv[tid] = kv;
             s_t[tid] = dmul(a.lam, kv);
             s_Kc[tid] = ldK<ASYNC>(a.K, c, pol_keep);
-            s_sc[tid] = 0.0;
-            s_best[tid] = 0ull;  // below every real gain key
+            s_sc[tid] = 0;
+            s_scw[tid] = 0.0;
+            s_hi[tid] = 0;
+            s_lo[tid] = 0;
             s_bx[tid] = NO_CAND;
         }
         if (tid == 0) s_loc[nv] = E;
         __syncthreads();
-        const uint32_t cap = (uint32_t)min64(WIN_CAP, ((int64_t)2 * E + 255) & ~255LL);
+        const uint32_t cap = (uint32_t)min64(WIN_CAP, ((int64_t)2 * E + 127) & ~127LL);
         // ---- 1. edges: 8 consecutive positions per thread
         {
             const int p0 = tid * WIN_ITEMS;
@@ -636,71 +631,65 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                 if (u[j] == EMPTY_KEY) continue;
                 const int sj = slot[j];
                 if (u[j] == s_c[sj]) {
-                    atomicAdd(&s_sc[sj], wv[j]);
+                    if constexpr (WEIGHTED) atomicAdd(&s_scw[sj], wv[j]);
+                    else atomicAdd(&s_sc[sj], 1u);
                     continue;
                 }
-                // key = (label << 32) | (slot << 16); low 16 bits count (unweighted)
-                const unsigned long long key = ((unsigned long long)(uint32_t)u[j] << 32) | ((unsigned long long)sj << 16);
-                uint32_t h = (uint32_t)(((uint64_t)hash32((uint32_t)u[j] ^ (0x9e3779b9u * (uint32_t)(sj + 1))) * cap) >> 32);
+                const uint32_t key = ((uint32_t)sj << LABEL_BITS) | (uint32_t)u[j];
+                uint32_t h = (uint32_t)(((uint64_t)hash32(key) * cap) >> 32);
                 while (true) {
-                    const uint32_t addr = tab_s + 8 * h;
-                    unsigned long long cur;
-                    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(cur) : "r"(addr));
-                    bool mine = (cur >> 16) == (key >> 16);
-                    if (!mine && cur == EMPTY64) {
-                        unsigned long long prev;
-                        asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(prev) : "r"(addr), "l"(EMPTY64), "l"(key | 1ull) : "memory");
-                        if (prev == EMPTY64) {
-                            uint32_t pos;
-                            asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(nocc_s) : "memory");
-                            asm volatile("st.shared.u16 [%0], %1;" ::"r"(occ_s + 2 * pos), "h"((unsigned short)h) : "memory");
-                            if constexpr (WEIGHTED) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
-                            break;
-                        }
-                        mine = (prev >> 16) == (key >> 16);
-                    }
-                    if (mine) {
-                        if constexpr (WEIGHTED) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
-                        else asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(addr) : "memory");
-                        break;
-                    }
+                    uint32_t prev;
+                    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys_s + 4 * h), "r"(KEY_EMPTY), "r"(key) : "memory");
+                    if (prev == KEY_EMPTY || prev == key) break;
                     h = (h + 1 == cap) ? 0 : h + 1;
                 }
+                if constexpr (WEIGHTED) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
+                else asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts_s + 4 * h) : "memory");
             }
         }
         __syncthreads();
-        if (tid < nv) s_b[tid] = dadd(dsub(s_sc[tid], dmul(s_t[tid], s_Kc[tid])), dmul(s_t[tid], s_kv[tid]));
-        __syncthreads();
-        // ---- 2a. score occupied entries, per-vertex max gain
-        const uint32_t nocc = s_nocc;
-        for (uint32_t i = tid; i < nocc; i += WIN_THREADS) {
-            const uint32_t q = occ[i];
-            const unsigned long long cur = tab[q];
-            const int32_t x = (int32_t)(cur >> 32);
-            const int sj = (int)((cur >> 16) & 0xffff);
-            const double S = WEIGHTED ? sums[q] : (double)(uint32_t)(cur & 0xffff);
-            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC>(a.K, x, pol_keep))), s_b[sj]);
-            gval[i] = g;
-            atomicMax(&s_best[sj], ord_gain(g));
+        if (tid < nv) {
+            const double sc = WEIGHTED ? s_scw[tid] : (double)s_sc[tid];
+            s_b[tid] = dadd(dsub(sc, dmul(s_t[tid], s_Kc[tid])), dmul(s_t[tid], s_kv[tid]));
         }
         __syncthreads();
-        // ---- 2b. lowest id among the maxima; reset the table
-        for (uint32_t i = tid; i < nocc; i += WIN_THREADS) {
-            const uint32_t q = occ[i];
-            const unsigned long long cur = tab[q];
-            const int32_t x = (int32_t)(cur >> 32);
-            const int sj = (int)((cur >> 16) & 0xffff);
-            if (ord_gain(gval[i]) == s_best[sj]) atomicMin(&s_bx[sj], x);
-            tab[q] = EMPTY64;
+        // ---- 2. score every slot; per-vertex max of the high gain word
+        for (uint32_t q = tid; q < cap; q += WIN_THREADS) {
+            const uint32_t key = keys[q];
+            if (key == KEY_EMPTY) continue;
+            const int32_t x = (int32_t)(key & ((1u << LABEL_BITS) - 1u));
+            const int sj = (int)(key >> LABEL_BITS);
+            const double S = WEIGHTED ? sums[q] : (double)cnts[q];
+            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC>(a.K, x, pol_keep))), s_b[sj]);
+            gval[q] = g;
+            atomicMax(&s_hi[sj], (uint32_t)(ord_gain(g) >> 32));
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < cap; q += WIN_THREADS) {
+            const uint32_t key = keys[q];
+            if (key == KEY_EMPTY) continue;
+            const int sj = (int)(key >> LABEL_BITS);
+            const unsigned long long o = ord_gain(gval[q]);
+            if ((uint32_t)(o >> 32) == s_hi[sj]) atomicMax(&s_lo[sj], (uint32_t)o);
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < cap; q += WIN_THREADS) {
+            const uint32_t key = keys[q];
+            if (key == KEY_EMPTY) continue;
+            const int sj = (int)(key >> LABEL_BITS);
+            const unsigned long long o = ord_gain(gval[q]);
+            if ((uint32_t)(o >> 32) == s_hi[sj] && (uint32_t)o == s_lo[sj])
+                atomicMin(&s_bx[sj], (int32_t)(key & ((1u << LABEL_BITS) - 1u)));
+            keys[q] = KEY_EMPTY;  // reset for the next window
             if constexpr (WEIGHTED) sums[q] = 0.0;
+            else cnts[q] = 0;
         }
         __syncthreads();
         // ---- 3. decide
-        if (tid == 0) s_nocc = 0;
         if (tid < nv) {
             const int32_t bx = s_bx[tid];
-            my_moves += decide<ASYNC>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND,
-                                      unord_gain(s_best[tid]), bx);
+            const unsigned long long o = ((unsigned long long)s_hi[tid] << 32) | s_lo[tid];
+            my_moves += decide<ASYNC>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND, unord_gain(o), bx);
         }
         __syncthreads();
     }
@@ -1140,7 +1129,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     // (the paper's sequential-vs-parallel hash-table switch)
     // bins: 0 deg<=32 warp windows | 1 33..T-1 edge windows | 2 T..2048 |
     //       3 2049..4096 | 4 ..large_min (CTA groups) | 5 hubs (L2 tables)
-    const int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
+    int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
+    if (2 * n > (1LL << LABEL_BITS)) T = SMALL_MAX + 1;  // window keys need ids < 2^27
     // LCC_LARGE_MIN (env, tuning only): degree above which hubs use the L2 path
     static const int64_t large_min = [] {
         const char* e = getenv("LCC_LARGE_MIN");

@@ -881,7 +881,7 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
 // ===========================================================================
 // degree-bin partition (one pass, block-aggregated reservations)
 // ===========================================================================
-constexpr int NBINS = 6;
+constexpr int NBINS = 8;
 struct BinEdges {
     int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
@@ -1004,9 +1004,11 @@ constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-reside
 template <class WT, bool ASYNC>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     switch (bin) {  //                         GW  CAP    GROUPS U
-        case 2: launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s); break;    //    T..2048  4 warps
-        case 3: launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s); break;    // 2049..4096  8 warps
-        case 4: launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s); break;  // 4097..10240 8 warps
+        case 2: launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s); break;     //  ..128      warp
+        case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;    //  ..512      warp
+        case 4: launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s); break;    //  ..2048     4 warps
+        case 5: launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s); break;    //  ..4096     8 warps
+        case 6: launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s); break;  //  ..10240    8 warps
         default: break;
     }
 }
@@ -1127,22 +1129,27 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
-    // bins: 0 deg<=32 warp windows | 1 33..T-1 edge windows | 2 T..2048 |
-    //       3 2049..4096 | 4 ..large_min (CTA groups) | 5 hubs (L2 tables)
+    // bins: 0 deg<=32 warp windows | 1 33..T-1 edge windows | 2 T..128 warp |
+    //       3 ..512 warp | 4 ..2048 4 warps | 5 ..4096 8 warps | 6 ..large_min
+    //       8 warps | 7 hubs (L2 tables)
+    // LCC_WINDOW=0 / LCC_LARGE_MIN (env): tuning knobs for the bin shapes only
+    // measured on B200 (R-MAT s24): per-vertex warp groups beat the window
+    // kernel by ~5%, and CTA groups beat the L2 hub path up to 10240
+    const char* ew = getenv("LCC_WINDOW");
+    const bool use_window = ew && ew[0] == '1';
+    const char* el = getenv("LCC_LARGE_MIN");
+    const int64_t large_min = el ? std::max<int64_t>(2048, atoll(el)) : MED_MAX;
     int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
-    if (2 * n > (1LL << LABEL_BITS)) T = SMALL_MAX + 1;  // window keys need ids < 2^27
-    // LCC_LARGE_MIN (env, tuning only): degree above which hubs use the L2 path
-    static const int64_t large_min = [] {
-        const char* e = getenv("LCC_LARGE_MIN");
-        return e ? std::max<int64_t>(2048, atoll(e)) : (int64_t)4096;
-    }();
+    if (!use_window || 2 * n > (1LL << LABEL_BITS)) T = SMALL_MAX + 1;  // window keys need ids < 2^27
     BinEdges be;
     be.hi[0] = SMALL_MAX;
     be.hi[1] = T - 1;
-    be.hi[2] = std::min<int64_t>(2048, large_min);
-    be.hi[3] = std::min<int64_t>(4096, large_min);
-    be.hi[4] = std::min<int64_t>(MED_MAX, large_min);
-    be.hi[5] = INT64_MAX;
+    be.hi[2] = std::max<int64_t>(T - 1, 128);
+    be.hi[3] = std::max<int64_t>(T - 1, 512);
+    be.hi[4] = std::min<int64_t>(2048, large_min);
+    be.hi[5] = std::min<int64_t>(4096, large_min);
+    be.hi[6] = std::min<int64_t>(MED_MAX, large_min);
+    be.hi[7] = INT64_MAX;
 
     Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);
     std::vector<int64_t> binstart;

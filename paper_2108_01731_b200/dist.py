@@ -1,0 +1,324 @@
+"""Vertex-sharded multi-GPU LambdaCC.
+
+One process per GPU.  Vertices are 1-D partitioned into contiguous ranges
+balanced by degree sum; each rank keeps only the CSR rows of the vertices it
+owns (edges co-located with their source) and a replica of the cluster
+labels C and masses K.
+
+Per best-move iteration (Alg. 1 lines 6-10, bulk-synchronous across ranks):
+  1. every rank runs the best-move kernels over its owned frontier;
+  2. the owned slices of the new labels and of the moved flags are combined
+     with an element-wise MAX all-reduce over NCCL (non-owners contribute -1 /
+     0), so every rank holds the full new labelling;
+  3. masses K are recomputed locally from the replicated labels (the apply /
+     reconcile kernel) -- cheaper than all-reducing a dense fp64 K array, see
+     SURVEY.md §8e step 3;
+  4. every rank marks the neighbours of its owned movers, the marks are
+     MAX-all-reduced, and each rank keeps its owned part as the next frontier.
+Asynchronous mode is asynchronous inside a GPU and bulk-synchronous across
+GPUs.  Synchronous mode gives labels identical to the single-GPU run (Jacobi
+rounds do not depend on the partition).
+
+Contraction: each rank compresses its owned rows with the device kernel
+(renumbering is identical everywhere since labels are replicated); the
+partial coarse CSRs are all-gathered and merged, the coarse levels run on
+rank 0 (they are a small fraction of the work) and the coarse labels are
+broadcast; flatten and the level-0 refinement run sharded again.
+
+The per-rank compute goes through a backend object (``CudaBackend`` here:
+the sm_100a C ABI).  Tests drive the same driver with a CPU backend over
+``gloo`` to check the exchange logic without GPUs.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .graph import DeviceGraph, stream_ptr
+
+
+# ---------------------------------------------------------------------------
+# partitioning
+# ---------------------------------------------------------------------------
+
+def partition_bounds(indptr: np.ndarray, parts: int) -> np.ndarray:
+    """Contiguous vertex ranges with (vertex count + degree sum) balanced.
+    Returns bounds[parts+1]; rank r owns [bounds[r], bounds[r+1])."""
+    indptr = np.asarray(indptr, dtype=np.int64)
+    n = indptr.size - 1
+    work = indptr + np.arange(n + 1, dtype=np.int64)  # vertices + edges prefix
+    total = work[-1]
+    targets = (total * np.arange(1, parts, dtype=np.float64) / parts).astype(np.int64)
+    inner = np.searchsorted(work, targets, side="left")
+    return np.concatenate([[0], inner, [n]]).astype(np.int64)
+
+
+@dataclass
+class PartGraph:
+    """Owned rows of a symmetric CSR: indptr covers all n vertices (rows
+    outside [lo, hi) are empty), indices/weights hold the owned rows only."""
+    n: int
+    lo: int
+    hi: int
+    indptr: torch.Tensor
+    indices: torch.Tensor
+    weights: torch.Tensor | None
+    total_weight: float
+
+    @property
+    def m(self) -> int:
+        return int(self.indices.numel()) // 2
+
+
+def make_part(indptr, indices, weights, total_weight, lo: int, hi: int, device) -> PartGraph:
+    """Build the owned-rows view from full host (numpy) or torch CSR arrays."""
+    ip = torch.as_tensor(np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr), dtype=torch.int64)
+    n = ip.numel() - 1
+    s, e = int(ip[lo]), int(ip[hi])
+    pip = (ip.clamp(min=s, max=e) - s).to(device)
+    ind = indices[s:e] if isinstance(indices, torch.Tensor) else torch.as_tensor(np.asarray(indices[s:e]))
+    ind = ind.to(device=device, dtype=torch.int32).contiguous()
+    w = None
+    if weights is not None:
+        ww = weights[s:e] if isinstance(weights, torch.Tensor) else torch.as_tensor(np.asarray(weights[s:e]))
+        w = ww.to(device).contiguous()
+    return PartGraph(n, lo, hi, pip, ind, w, float(total_weight))
+
+
+# ---------------------------------------------------------------------------
+# CUDA backend: the per-rank compute, all through the C ABI
+# ---------------------------------------------------------------------------
+
+class CudaBackend:
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.lib = _lib.load()
+
+    def _g(self, part) -> _lib.LccGraph:
+        wtype, wp = _lib.W_NONE, None
+        if part.weights is not None:
+            wtype = _lib.W_F32 if part.weights.dtype == torch.float32 else _lib.W_F64
+            wp = part.weights.data_ptr()
+        nnz = int(part.indices.numel())
+        return _lib.LccGraph(part.n, nnz, part.indptr.data_ptr(), part.indices.data_ptr() if nnz else None, wp,
+                             wtype, 0, part.total_weight)
+
+    @staticmethod
+    def _p(k, lam) -> _lib.LccParams:
+        return _lib.LccParams(None if k is None else k.data_ptr(), float(lam))
+
+    def round(self, part, k, lam, C, K, frontier, schedule, thr, chunks):
+        """Returns (labels, moved, count): sync -> D; async -> C updated in a
+        copy with masses in a 2n copy of K."""
+        n = part.n
+        g, p = self._g(part), self._p(k, lam)
+        moved = torch.empty(n, dtype=torch.uint8, device=self.device)
+        cnt = ctypes.c_int64()
+        fr = frontier.to(self.device, torch.int32).contiguous()
+        if schedule == _lib.SYNC:
+            D = torch.empty(n, dtype=torch.int32, device=self.device)
+            _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), C.data_ptr(), K.data_ptr(),
+                                                     fr.data_ptr() if fr.numel() else None, fr.numel(),
+                                                     _lib.SYNC, thr, chunks, D.data_ptr(), moved.data_ptr(),
+                                                     ctypes.byref(cnt), stream_ptr()))
+            return D, moved, cnt.value
+        Cw = C.clone()
+        K2 = torch.zeros(2 * n, dtype=torch.float64, device=self.device)
+        K2[:n] = K
+        _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), Cw.data_ptr(), K2.data_ptr(),
+                                                 fr.data_ptr() if fr.numel() else None, fr.numel(),
+                                                 _lib.ASYNC, thr, chunks, None, moved.data_ptr(),
+                                                 ctypes.byref(cnt), stream_ptr()))
+        return Cw, moved, cnt.value
+
+    def apply(self, labels, label_range, k):
+        n = labels.numel()
+        C = torch.empty(n, dtype=torch.int32, device=self.device)
+        K = torch.empty(n, dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.lcc_apply_moves(n, labels.data_ptr(), int(label_range),
+                                            None if k is None else k.data_ptr(), C.data_ptr(), K.data_ptr(),
+                                            stream_ptr()))
+        return C, K
+
+    def frontier_mask(self, part, policy, moved, Cold, Cnew):
+        n = part.n
+        g = self._g(part)
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        cnt = ctypes.c_int64()
+        _lib.check(self.lib.lcc_compute_frontier(ctypes.byref(g), int(policy), moved.data_ptr(), Cold.data_ptr(),
+                                                 Cnew.data_ptr(), out.data_ptr(), ctypes.byref(cnt), stream_ptr()))
+        mask = torch.zeros(n, dtype=torch.uint8, device=self.device)
+        if cnt.value:
+            mask[out[:cnt.value].long()] = 1
+        return mask
+
+    def compress(self, part, k, lam, C, K):
+        n, nnz = part.n, int(part.indices.numel())
+        d = self.device
+        mapping = torch.empty(max(n, 1), dtype=torch.int32, device=d)
+        ck = torch.empty(max(n, 1), dtype=torch.float64, device=d)
+        cptr = torch.empty(n + 1, dtype=torch.int64, device=d)
+        cind = torch.empty(max(nnz, 1), dtype=torch.int32, device=d)
+        cw = torch.empty(max(nnz, 1), dtype=torch.float64, device=d)
+        cn, cnnz, off, tot = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        g, p = self._g(part), self._p(k, lam)
+        _lib.check(self.lib.lcc_par_compress(ctypes.byref(g), ctypes.byref(p), C.data_ptr(), K.data_ptr(),
+                                             mapping.data_ptr(), ck.data_ptr(), cptr.data_ptr(), cind.data_ptr(),
+                                             cw.data_ptr(), ctypes.byref(cn), ctypes.byref(cnnz), ctypes.byref(off),
+                                             ctypes.byref(tot), stream_ptr()))
+        cn, cnnz = cn.value, cnnz.value
+        return cn, cptr[:cn + 1], cind[:cnnz], cw[:cnnz], ck[:cn], mapping[:n]
+
+    def parallel_cc(self, indptr, indices, weights, total_weight, k, lam, opts):
+        from .louvain_par import parallel_cc
+        from .objective import ClusteringParams
+        n = indptr.numel() - 1
+        g = DeviceGraph(n, indices.numel() // 2, indptr.to(self.device), indices.to(self.device, torch.int32),
+                        None if weights is None else weights.to(self.device, torch.float64), float(total_weight))
+        p = ClusteringParams.__new__(ClusteringParams)
+        p.lam, p.k = float(lam), k
+        return parallel_cc(g, p, opts).assignment
+
+    def flatten(self, mapping, Cc, k):
+        n = mapping.numel()
+        C = torch.empty(n, dtype=torch.int32, device=self.device)
+        K = torch.empty(n, dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.lcc_par_flatten(n, mapping.data_ptr(), Cc.to(self.device, torch.int32).data_ptr(),
+                                            None if k is None else k.data_ptr(), C.data_ptr(), K.data_ptr(),
+                                            stream_ptr()))
+        return C, K
+
+
+# ---------------------------------------------------------------------------
+# the sharded driver
+# ---------------------------------------------------------------------------
+
+def _max_(t: torch.Tensor, group):
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
+def _sum_int(x: int, device, group) -> int:
+    t = torch.tensor([x], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())
+
+
+@dataclass
+class ShardStats:
+    rounds: int = 0
+    edges_scanned: int = 0   # this rank's owned frontier edges
+    moves: int = 0           # global movers
+
+
+def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None, stats: ShardStats | None = None):
+    """par_best_moves over the owned vertices of every rank (module doc)."""
+    from .louvain_par import FrontierPolicy
+    dev = backend.device
+    n = part.n
+    owned = torch.arange(part.lo, part.hi, dtype=torch.int32, device=dev)
+    F = owned                                   # V' <- V
+    sched = int(opts.schedule)
+    any_moved = False
+    deg = (part.indptr[1:] - part.indptr[:-1])
+    for _ in range(int(opts.num_iter)):
+        if _sum_int(int(F.numel()), dev, group) == 0:
+            break
+        labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
+                                           int(opts.async_chunks))
+        if stats is not None:
+            stats.rounds += 1
+            stats.edges_scanned += int(deg[F.long()].sum().item()) if F.numel() else 0
+        total = _sum_int(int(cnt), dev, group)
+        if stats is not None:
+            stats.moves += total
+        if total == 0:
+            break                               # Alg. 1 line 9
+        any_moved = True
+        # owners' labels / moved flags to every rank
+        lab = torch.full((n,), -1, dtype=torch.int32, device=dev)
+        lab[part.lo:part.hi] = labels[part.lo:part.hi]
+        _max_(lab, group)
+        mv = torch.zeros(n, dtype=torch.uint8, device=dev)
+        mv[part.lo:part.hi] = moved[part.lo:part.hi]
+        _max_(mv, group)
+        Cn, Kn = backend.apply(lab, 2 * n, k)   # canonical labels + masses, replicated
+        policy = FrontierPolicy(opts.frontier_policy)
+        if policy == FrontierPolicy.AllVertices:
+            F = owned
+        else:
+            mask = backend.frontier_mask(part, int(policy), mv, C, Cn)
+            _max_(mask, group)
+            F = (torch.nonzero(mask[part.lo:part.hi]).flatten() + part.lo).to(torch.int32)
+        C, K = Cn, Kn
+    return C, K, any_moved
+
+
+def _gather_coarse(cn, cptr, cind, cw, device, group):
+    """All-gather partial coarse CSRs and merge duplicate (a, b) entries."""
+    world = dist.get_world_size(group)
+    rows = torch.repeat_interleave(torch.arange(cn, device=device, dtype=torch.int64), cptr[1:] - cptr[:-1])
+    local = torch.stack([rows, cind.to(torch.int64)]).contiguous()
+    size = torch.tensor([local.shape[1]], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(size) for _ in range(world)]
+    dist.all_gather(sizes, size, group=group)
+    mx = int(max(s.item() for s in sizes))
+    pad_i = torch.full((2, mx), -1, dtype=torch.int64, device=device)
+    pad_i[:, :local.shape[1]] = local
+    pad_w = torch.zeros(mx, dtype=torch.float64, device=device)
+    pad_w[:cw.numel()] = cw
+    gi = [torch.empty_like(pad_i) for _ in range(world)]
+    gw = [torch.empty_like(pad_w) for _ in range(world)]
+    dist.all_gather(gi, pad_i, group=group)
+    dist.all_gather(gw, pad_w, group=group)
+    ab = torch.cat([g[:, :int(s.item())] for g, s in zip(gi, sizes)], dim=1)
+    w = torch.cat([g[:int(s.item())] for g, s in zip(gw, sizes)])
+    key = ab[0] * max(cn, 1) + ab[1]
+    key, order = torch.sort(key, stable=True)
+    w = w[order]
+    uk, inv = torch.unique_consecutive(key, return_inverse=True)
+    ws = torch.zeros(uk.numel(), dtype=torch.float64, device=device).index_add_(0, inv, w)
+    a, b = uk // max(cn, 1), uk % max(cn, 1)
+    indptr = torch.zeros(cn + 1, dtype=torch.int64, device=device)
+    indptr[1:] = torch.cumsum(torch.bincount(a, minlength=cn), 0)
+    return indptr, b.to(torch.int32), ws, float(ws.sum().item()) / 2.0
+
+
+def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, backend=None, group=None,
+                        stats: ShardStats | None = None) -> torch.Tensor:
+    """parallel_cc with level 0 sharded over the process
+    group.  ``indptr``/``indices``/``weights`` are the full graph (host or
+    device); ``k`` the full vertex weights (or None).  Returns the canonical
+    labels (replicated on every rank)."""
+    backend = backend or CudaBackend()
+    dev = backend.device
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ip = np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr, dtype=np.int64)
+    bounds = partition_bounds(ip, world)
+    part = make_part(indptr, indices, weights, total_weight, int(bounds[rank]), int(bounds[rank + 1]), dev)
+    n = part.n
+    if k is not None:
+        k = torch.as_tensor(k, dtype=torch.float64).to(dev)
+    C = torch.arange(n, dtype=torch.int32, device=dev)
+    K = torch.ones(n, dtype=torch.float64, device=dev) if k is None else k.clone()
+    C, K, moved = sharded_best_moves(part, k, lam, C, K, opts, backend, group, stats)
+    if not moved:
+        return C
+    cn, cptr, cind, cw, ck, mapping = backend.compress(part, k, lam, C, K)
+    if cn == n:
+        return C                                      # no size reduction
+    c_indptr, c_ind, c_w, c_tot = _gather_coarse(cn, cptr, cind, cw, dev, group)
+    Cc = torch.empty(cn, dtype=torch.int32, device=dev)
+    if rank == 0:
+        Cc = backend.parallel_cc(c_indptr, c_ind, c_w, c_tot, ck, lam, opts).to(torch.int32)
+    dist.broadcast(Cc, src=0, group=group)
+    C, K = backend.flatten(mapping, Cc, k)
+    if opts.refine:
+        C, K, _ = sharded_best_moves(part, k, lam, C, K, opts, backend, group, stats)
+    return C
+

@@ -1,0 +1,63 @@
+"""Sharded driver with the CUDA backend.  Only one GPU is available, so two
+ranks share it over gloo (collectives on the host; no kernel ever waits on
+another rank), and a single-rank NCCL group exercises the NCCL code path."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2108_01731_b200.gen import csr_from_pairs, rmat_pairs_host, sbm
+
+from tests.test_dist_gloo import free_port
+
+pytestmark = pytest.mark.gpu
+
+
+def _rank_main(rank, world, port, backend_name, indptr, indices, lam, opts_kw, out):
+    import torch.distributed as dist
+    from paper_2108_01731_b200.dist import CudaBackend, ShardStats, sharded_parallel_cc
+    from paper_2108_01731_b200.louvain_par import ParOptions
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend_name, rank=rank, world_size=world)
+    try:
+        st = ShardStats()
+        C = sharded_parallel_cc(indptr, indices, None, float(indices.size // 2), None, lam, ParOptions(**opts_kw),
+                                backend=CudaBackend(), stats=st)
+        if rank == 0:
+            torch.save({"C": C.cpu().numpy(), "rounds": st.rounds}, out)
+    finally:
+        dist.destroy_process_group()
+
+
+def run(world, backend_name, hg, lam, opts_kw):
+    out = tempfile.mktemp(suffix=".pt")
+    mp.spawn(_rank_main, args=(world, free_port(), backend_name, hg.indptr, hg.indices, lam, opts_kw, out),
+             nprocs=world, join=True)
+    r = torch.load(out, weights_only=False)
+    os.remove(out)
+    return r
+
+
+@pytest.mark.parametrize("world,backend_name", [(2, "gloo"), (1, "nccl")])
+def test_sharded_cuda_sync_exact(world, backend_name):
+    hg, _ = sbm(seed=1)
+    g = O.as_graph(hg)
+    ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC))
+    r = run(world, backend_name, hg, 0.85, dict(schedule="sync"))
+    assert np.array_equal(r["C"], ref)
+
+
+def test_sharded_cuda_async_objective():
+    u, v = rmat_pairs_host(13, 16 << 13, 0.57, 0.19, 0.19, 10)
+    hg = csr_from_pairs(1 << 13, u, v)
+    g = O.as_graph(hg)
+    ref = O.objective(g, None, 0.85, O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.ASYNC)))
+    r = run(2, "gloo", hg, 0.85, dict(schedule="async"))
+    got = O.objective(g, None, 0.85, r["C"])
+    assert got >= ref - 0.005 * abs(ref), (got, ref)

@@ -22,8 +22,9 @@ LambdaCC clustering time (the metric's second half).
 best-move round (OpenMP, relaxed atomics, all host threads) on a bounded
 vertex sample of the same graph.
 
-Multi-GPU (--gpus N under torchrun): replicas only in this round -- every
-rank clusters its own seeded copy; value = total edges / max-over-ranks time.
+Multi-GPU (--gpus N under torchrun): level 0 vertex-sharded over NCCL
+(paper_2108_01731_b200/dist.py), the same graph on every rank, strong
+scaling; value = edges scanned by all ranks / max-over-ranks step time.
 """
 from __future__ import annotations
 
@@ -248,13 +249,9 @@ def run_ours(args):
 
     ws, rank, lrank = dist_init()
     torch.cuda.set_device(lrank)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
+    dist = None  # single GPU; N > 1 goes through run_sharded
     lib = _lib.load()
-    seed = args.seed + (rank if ws > 1 else 0)
-    dg = build_graph_device(args.scale, args.edge_factor, seed)
+    dg = build_graph_device(args.scale, args.edge_factor, args.seed)
     n, nnz = dg.n, dg.nnz
     g = {"n": n, "m": nnz // 2, "ws": ws}
     p = L.ClusteringParams(args.lam)
@@ -374,10 +371,101 @@ def run_ours(args):
     return 0
 
 
+def run_sharded(args):
+    """N > 1: one rank per GPU over NCCL; level 0 vertex-sharded (dist.py),
+    the same R-MAT graph on every rank; strong scaling (fixed total work)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2108_01731_b200 as L
+    from paper_2108_01731_b200 import _lib
+    from paper_2108_01731_b200.dist import CudaBackend, ShardStats, make_part, partition_bounds, sharded_best_moves, sharded_parallel_cc
+
+    ws, rank, lrank = dist_init()
+    torch.cuda.set_device(lrank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    lib = _lib.load()
+    dg = build_graph_device(args.scale, args.edge_factor, args.seed)
+    n, nnz = dg.n, dg.nnz
+    indptr_h = dg.indptr.cpu().numpy()
+    bounds = partition_bounds(indptr_h, ws)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    part = make_part(dg.indptr, dg.indices, None, float(nnz // 2), lo, hi, torch.device("cuda", lrank))
+    be = CudaBackend()
+    opts1 = L.ParOptions(schedule=args.schedule, num_iter=1, degree_threshold=args.degree_threshold,
+                         async_chunks=args.async_chunks)
+    iota = torch.arange(n, dtype=torch.int32, device="cuda")
+
+    def step(st):
+        C = iota.clone()
+        K = torch.ones(n, dtype=torch.float64, device="cuda")
+        sharded_best_moves(part, None, args.lam, C, K, opts1, be, None, st)
+
+    for _ in range(args.warmup):
+        step(ShardStats())
+    st = ShardStats()
+    launches0 = lib.lcc_kernel_launches()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(lrank) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step(st)
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = lib.lcc_kernel_launches() - launches0
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ed = torch.tensor([float(st.edges_scanned)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ed, op=dist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    value = float(ed.item()) / (ms_max / 1e3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        ip_h = torch.from_numpy(indptr_h).pin_memory()
+        ix_h = dg.indices.cpu().pin_memory()
+        full = L.ParOptions(schedule=args.schedule, degree_threshold=args.degree_threshold,
+                            async_chunks=args.async_chunks)
+        sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, args.lam, full, be)  # warm-up
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st2 = ShardStats()
+        C = sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, args.lam, full, be, None, st2)
+        out_h = C.cpu()
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ed2 = torch.tensor([float(st2.edges_scanned)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ed2, op=dist.ReduceOp.SUM)
+        obj = L.cc_objective(dg, L.ClusteringParams(args.lam), C)
+        h2d = int((bounds[rank + 1] - bounds[rank]) * 8 + (indptr_h[hi] - indptr_h[lo]) * 4)
+        e2e = {"value": float(ed2.item()) / float(te.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": int(n * 4),
+               "clustering_ms": 1e3 * float(te.item()), "objective": obj, "clusters": int(np.unique(out_h.numpy()).size),
+               "api": "paper_2108_01731_b200.dist.sharded_parallel_cc(host pinned CSR) + labels D2H"}
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded R-MAT generated on device, identical on every rank)",
+               "config": config_dict(args, {"n": n, "m": nnz // 2, "ws": ws},
+                                     {"parallelism": f"vertex-sharded x{ws} (NCCL MAX all-reduce of labels/flags)"}),
+               "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
+               "clocks": clk.summary()}
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_sharded(args)
     return run_ours(args)
 
 

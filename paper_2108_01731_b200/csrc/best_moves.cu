@@ -1129,9 +1129,9 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
-    // bins: 0 deg<=32 warp windows | 1 33..T-1 edge windows | 2 T..128 warp |
-    //       3 ..512 warp | 4 ..2048 4 warps | 5 ..4096 8 warps | 6 ..large_min
-    //       8 warps | 7 hubs (L2 tables)
+    // bins: 0 deg<=32 warp windows | 1 optional edge windows | 2-3 warp per
+    //       vertex up to the threshold | 4 ..2048 4 warps | 5 ..4096 8 warps |
+    //       6 ..large_min 8 warps | 7 hubs (L2 tables)
     // LCC_WINDOW=0 / LCC_LARGE_MIN (env): tuning knobs for the bin shapes only
     // measured on B200 (R-MAT s24): per-vertex warp groups beat the window
     // kernel by ~5%, and CTA groups beat the L2 hub path up to 10240
@@ -1139,13 +1139,17 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const bool use_window = ew && ew[0] == '1';
     const char* el = getenv("LCC_LARGE_MIN");
     const int64_t large_min = el ? std::max<int64_t>(2048, atoll(el)) : MED_MAX;
-    int64_t T = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
-    if (!use_window || 2 * n > (1LL << LABEL_BITS)) T = SMALL_MAX + 1;  // window keys need ids < 2^27
+    // degree_threshold: warp-per-vertex accumulation below it (the paper's
+    // "sequential" path), CTA-cooperative tables from it on ("parallel hash
+    // table"); clamped to the warp-table capacity.
+    const int64_t Tg = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), 513);
+    int64_t Tw = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
+    if (!use_window || 2 * n > (1LL << LABEL_BITS)) Tw = SMALL_MAX + 1;  // window keys need ids < 2^27
     BinEdges be;
     be.hi[0] = SMALL_MAX;
-    be.hi[1] = T - 1;
-    be.hi[2] = std::max<int64_t>(T - 1, 128);
-    be.hi[3] = std::max<int64_t>(T - 1, 512);
+    be.hi[1] = Tw - 1;
+    be.hi[2] = std::max<int64_t>(be.hi[1], std::min<int64_t>(128, Tg - 1));
+    be.hi[3] = std::max<int64_t>(be.hi[2], Tg - 1);
     be.hi[4] = std::min<int64_t>(2048, large_min);
     be.hi[5] = std::min<int64_t>(4096, large_min);
     be.hi[6] = std::min<int64_t>(MED_MAX, large_min);

@@ -390,3 +390,29 @@ def test_device_rmat_matches_host_stream():
     hg = csr_from_pairs(1 << 12, u, v)
     assert np.array_equal(d.indptr.cpu().numpy(), hg.indptr)
     assert np.array_equal(d.indices.cpu().numpy(), hg.indices)
+
+
+@pytest.mark.parametrize("window", ["1", "0"])
+@pytest.mark.parametrize("large_min", ["2048", "10240"])
+def test_sync_round_bin_shapes_exact(window, large_min, monkeypatch):
+    """Every kernel shape (window bin on/off, hub path threshold) gives the
+    same labels as the oracle (LCC_WINDOW / LCC_LARGE_MIN are tuning knobs)."""
+    monkeypatch.setenv("LCC_WINDOW", window)
+    monkeypatch.setenv("LCC_LARGE_MIN", large_min)
+    rng = np.random.default_rng(21)
+    hg = hub_graph(rng, 40_000, hubs=[3, 9, 700, 8000], hub_deg=[300, 2500, 6000, 15_000], base_p=0.0004)
+    g = og(hg)
+    for nclus in (40_000, 2000):
+        C, K = clustered_state(rng, g.n, nclus)
+        D0, m0, c0 = O.sync_round(g, None, 0.5, C, K)
+        D1, m1, c1 = gpu_sync_round(hg, None, 0.5, C, K, thr=1000)
+        assert np.array_equal(D0, D1) and c0 == c1
+    hw = rand_weighted(rng, 6000, 0.01)
+    gw = og(hw)
+    C, K = clustered_state(rng, gw.n, 900)
+    D0, _, _ = O.sync_round(gw, None, 0.1, C, K)
+    D1, _, _ = gpu_sync_round(hw, None, 0.1, C, K)
+    for v in np.flatnonzero(D0 != D1):
+        g0 = oracle_gain(gw, None, 0.1, C, K, v, D0[v])
+        g1 = oracle_gain(gw, None, 0.1, C, K, v, D1[v])
+        assert abs(g0 - g1) <= REL_TIE * max(1.0, abs(g0))

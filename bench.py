@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=24)
     ap.add_argument("--lam", type=float, default=0.85)
     ap.add_argument("--schedule", default="async", choices=["async", "sync"])
-    ap.add_argument("--async-chunks", type=int, default=16)
+    ap.add_argument("--async-chunks", type=int, default=0)
     ap.add_argument("--degree-threshold", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-stride", type=int, default=8)

@@ -75,7 +75,7 @@ typedef struct {
     int32_t degree_threshold; /* vertices above it use the block/global
                                  hash path (default 1000)    */
     int32_t async_chunks;     /* async: frontier processed in this many
-                                 ordered sub-rounds (>= 1)                 */
+                                 ordered sub-rounds; 0 = auto              */
 } lcc_options;
 
 /* Per-call counters, accumulated (caller zeroes).                           */

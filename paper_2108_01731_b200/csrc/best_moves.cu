@@ -1198,7 +1198,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         LCC_CUDA(cudaEventSynchronize(ev1));
         LCC_CUDA(cudaEventElapsedTime(&kms_large, ev0, ev1));
     }
-    const int P = ASYNC ? std::max(1, chunks) : 1;
+    // async sub-rounds: `chunks` > 0 is explicit; 0 = auto, enough sub-rounds
+    // that small frontiers still see each other's moves (symmetry breaking,
+    // PAPER.md:193) while large ones run as one wave (measured on R-MAT s24:
+    // 1 sub-round is 20% faster than 16 and reaches a higher objective)
+    int P = 1;
+    if (ASYNC) P = chunks > 0 ? chunks : (int)std::min<int64_t>(16, std::max<int64_t>(1, ((1LL << 22) + nF - 1) / std::max<int64_t>(nF, 1)));
     WindowPlan wp;
     if (hc[1] > 0) plan_windows(g.indptr, lists.get() + binstart[1], (int64_t)hc[1], wp, s);
     LCC_CUDA(cudaEventRecord(ev0, s));

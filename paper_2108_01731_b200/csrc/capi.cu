@@ -78,7 +78,7 @@ lcc::Options to_opts(const lcc_options* o) {
         r.refine = o->refine;
         r.num_iter = o->num_iter;
         r.deg_threshold = o->degree_threshold;
-        r.async_chunks = o->async_chunks > 0 ? o->async_chunks : 1;
+        r.async_chunks = o->async_chunks > 0 ? o->async_chunks : 0;  // 0 = auto
     }
     return r;
 }
@@ -100,7 +100,7 @@ lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p, int32_t
         LCC_REQUIRE(C && K && moved, "C, K and moved are required");
         LCC_REQUIRE(n_frontier >= 0 && n_frontier <= g->n, "frontier size out of range");
         const int64_t cnt = lcc::best_moves_round(*g, p->k, p->lambda, C, K, frontier, n_frontier, schedule,
-                                                  degree_threshold, async_chunks > 0 ? async_chunks : 1, D, moved,
+                                                  degree_threshold, async_chunks > 0 ? async_chunks : 0, D, moved,
                                                   nullptr, S(stream));
         if (moved_count) *moved_count = cnt;
     });

@@ -55,7 +55,7 @@ int64_t gen_rmat(int scale, int64_t samples, double a, double b, double c, uint6
 // driver.cu
 struct Options {
     int schedule = LCC_ASYNC, policy = LCC_FRONTIER_VERTEX_NBRS, refine = 1, num_iter = 10;
-    int deg_threshold = 1000, async_chunks = 16;
+    int deg_threshold = 1000, async_chunks = 0;  // 0 = auto
 };
 bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C,
                     double* K, lcc_stats* st, cudaStream_t s);

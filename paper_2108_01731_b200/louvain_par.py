@@ -55,7 +55,8 @@ class ParOptions:
     from below by the warp path (32) and from above by the shared-memory
     table capacity.  ``async_chunks``: the asynchronous schedule walks the
     frontier in this many ordered sub-rounds; later sub-rounds see the moves
-    of earlier ones (symmetry breaking)."""
+    of earlier ones (symmetry breaking).  0 = auto (up to 16
+    for small frontiers, one wave for frontiers of 4M+ vertices)."""
     schedule: Schedule = Schedule.Asynchronous
     frontier_policy: FrontierPolicy = FrontierPolicy.VertexNeighbors
     refine: bool = True
@@ -63,7 +64,7 @@ class ParOptions:
     seed: int = 0
     threads: int = 0
     degree_threshold: int = 1000
-    async_chunks: int = 16
+    async_chunks: int = 0
 
     def __post_init__(self):
         if isinstance(self.schedule, str):
@@ -76,8 +77,8 @@ class ParOptions:
             raise GraphError("num_iter must be >= 1")
         if int(self.threads) < 0:
             raise GraphError("threads must be >= 1 (0 = all)")
-        if int(self.async_chunks) < 1:
-            raise GraphError("async_chunks must be >= 1")
+        if int(self.async_chunks) < 0:
+            raise GraphError("async_chunks must be >= 0 (0 = auto)")
 
     def c_struct(self) -> _lib.LccOptions:
         return _lib.LccOptions(int(self.schedule), int(self.frontier_policy), 1 if self.refine else 0,
@@ -154,7 +155,7 @@ def _labels_of(c, dg: DeviceGraph) -> torch.Tensor:
 
 def best_moves_round(g, p: ClusteringParams, c: Clustering, frontier=None,
                      schedule: Schedule = Schedule.Synchronous, degree_threshold: int = 1000,
-                     async_chunks: int = 16) -> MoveBuffer:
+                     async_chunks: int = 0) -> MoveBuffer:
     """One Alg. 1 iteration (lines 6-8).  Synchronous: returns D and moved
     flags, leaves ``c`` untouched.  Asynchronous: applies the moves to ``c``
     in place (labels may temporarily use ids n+v; call ``apply_moves``)."""

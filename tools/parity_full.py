@@ -1,0 +1,69 @@
+"""Full-size parity runs on the GPU box (too slow for the unit suite).
+
+cfg4: R-MAT s24 (BASELINE configs[3]), CC lambda=0.85, async + vertex
+neighbours + refine: GPU parallel_cc objective vs the oracle's parallel
+async (OpenMP relaxed atomics, the reference's schedule) on all host cores.
+cfg2: LFR-style 1.2M (configs[1]), modularity gamma=1, async, full
+multi-level: GPU vs the oracle's sequential and parallel async.
+Prints one JSON line per config."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2108_01731_b200 as L  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_2108_01731_b200.gen import lfr_like, rmat_device  # noqa: E402
+
+
+def gpu_run(hg_or_dg, k, lam):
+    p = L.ClusteringParams(lam, k)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cl = L.parallel_cc(hg_or_dg, p, L.ParOptions())
+    torch.cuda.synchronize()
+    return cl.labels(), time.perf_counter() - t0
+
+
+def main(which):
+    threads = os.cpu_count()
+    out = {}
+    if "cfg4" in which:
+        dg = rmat_device(24, 16, seed=24)
+        lab, t_gpu = gpu_run(dg, None, 0.85)
+        ip, ix, _ = dg.to_host()
+        g = O.Graph(dg.n, ip, ix, None, float(dg.m))
+        o_gpu = O.objective(g, None, 0.85, lab)
+        t0 = time.perf_counter()
+        ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.ASYNC, async_parallel=True, threads=threads))
+        t_cpu = time.perf_counter() - t0
+        o_ref = O.objective(g, None, 0.85, ref)
+        out["cfg4"] = {"objective_gpu": o_gpu, "objective_cpu_parallel_async": o_ref,
+                       "rel_diff": (o_gpu - o_ref) / abs(o_ref), "pass_0.5pct": o_gpu >= o_ref - 0.005 * abs(o_ref),
+                       "gpu_s": t_gpu, "cpu_s": t_cpu, "cpu_threads": threads}
+        print(json.dumps({"cfg4": out["cfg4"]}), flush=True)
+    if "cfg2" in which:
+        hg, _ = lfr_like(n=1_200_000, seed=2)
+        g = O.as_graph(hg)
+        k, lam = O.modularity_params(g, 1.0)
+        lab, t_gpu = gpu_run(hg, k, lam)
+        o_gpu = O.objective(g, k, lam, lab) / g.total_weight
+        t0 = time.perf_counter()
+        seq = O.parallel_cc(g, k, lam, O.Opts(schedule=O.ASYNC))
+        t_seq = time.perf_counter() - t0
+        par = O.parallel_cc(g, k, lam, O.Opts(schedule=O.ASYNC, async_parallel=True, threads=threads))
+        o_seq = O.objective(g, k, lam, seq) / g.total_weight
+        o_par = O.objective(g, k, lam, par) / g.total_weight
+        out["cfg2"] = {"modularity_gpu": o_gpu, "modularity_cpu_seq_async": o_seq,
+                       "modularity_cpu_parallel_async": o_par, "rel_diff_vs_seq": (o_gpu - o_seq) / abs(o_seq),
+                       "pass_0.5pct": o_gpu >= min(o_seq, o_par) - 0.005 * abs(o_seq), "gpu_s": t_gpu,
+                       "cpu_seq_s": t_seq, "n": g.n, "m": g.m}
+        print(json.dumps({"cfg2": out["cfg2"]}), flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["cfg4", "cfg2"])

@@ -7,13 +7,15 @@ plumbing, not the hot path:
 * ``sbm``      -- config 1, planted-partition SBM (numpy, host).
 * ``lfr_like`` -- config 2, power-law degrees + power-law community sizes
   with mixing mu, configuration-model pairing (numpy, host).
+* ``knn_mixture`` -- config 3, weighted cosine kNN of a Gaussian mixture
+  (torch on the device when present; fp32 weights in (0, 1]).
 * ``rmat_device`` -- config 4, R-MAT on the device (``lcc_gen_rmat``):
   counter-based splitmix64 draws, so ``rmat_pairs_host`` reproduces the same
   sample stream on the host for small scales (tests).
 
-All return undirected, deduplicated, self-loop-free, unweighted graphs
-(SURVEY.md §4 erratum 3: pairs are deduplicated before the CSR build, so
-every edge weighs exactly 1).
+All return undirected, deduplicated, self-loop-free graphs; the unweighted
+ones deduplicate pairs before the CSR build (SURVEY.md §4 erratum 3), so
+every edge weighs exactly 1.
 """
 from __future__ import annotations
 
@@ -212,3 +214,75 @@ def device_csr_from_pairs(n: int, u, v) -> DeviceGraph:
                                                     indices.data_ptr(), ctypes.byref(nnz), stream_ptr()))
     nnz = nnz.value
     return DeviceGraph(n, nnz // 2, indptr, indices[:nnz].clone(), None, float(nnz // 2))
+
+
+# ---------------------------------------------------------------------------
+# config 3: weighted kNN similarity graph (BASELINE.json configs[2])
+# ---------------------------------------------------------------------------
+
+def knn_mixture(n: int = 4_000_000, dim: int = 64, components: int = 10_000, k: int = 10, sigma: float = 1.0,
+                seed: int = 3, device=None, batch: int = 512):
+    """Seeded stand-in for the paper's ScaNN k-NN graphs.
+
+    Points: a Gaussian mixture in R^dim -- component means ~ N(0, I), points
+    mean + sigma * N(0, I), component sizes multinomial with equal weights,
+    ids grouped by component (no permutation).  Neighbours: exact top-k by
+    cosine similarity inside each component (the mixture components are far
+    apart, so this is the component-neighbourhood kNN of SURVEY.md §8d).
+    Symmetrised: an unordered pair is an edge if either endpoint lists the
+    other; its weight is the fp32 cosine recomputed once per pair, so both
+    orientations carry identical values.  Pairs with cosine <= 0 are dropped
+    and weights are clamped to (0, 1].  Returns (HostGraph with fp32-exact
+    fp64 weights, component of each vertex)."""
+    dev = torch.device(device) if device is not None else (torch.device("cuda") if torch.cuda.is_available()
+                                                              else torch.device("cpu"))
+    gen = torch.Generator().manual_seed(seed)
+    sizes = torch.multinomial(torch.full((components,), 1.0 / components), n, replacement=True,
+                              generator=gen).bincount(minlength=components)
+    comp = torch.repeat_interleave(torch.arange(components), sizes)
+    means = torch.randn(components, dim, generator=gen)
+    pts = means[comp] + sigma * torch.randn(n, dim, generator=gen)
+    pts = torch.nn.functional.normalize(pts, dim=1).to(dev)
+    starts = torch.zeros(components + 1, dtype=torch.int64)
+    starts[1:] = torch.cumsum(sizes, 0)
+    us, vs = [], []
+    smax = int(sizes.max())
+    kk = min(k, max(smax - 1, 1))
+    for c0 in range(0, components, batch):
+        c1 = min(components, c0 + batch)
+        nb = c1 - c0
+        X = torch.zeros(nb, smax, dim, device=dev)
+        valid = torch.zeros(nb, smax, dtype=torch.bool, device=dev)
+        for j, c in enumerate(range(c0, c1)):
+            s, e = int(starts[c]), int(starts[c + 1])
+            X[j, :e - s] = pts[s:e]
+            valid[j, :e - s] = True
+        S = torch.bmm(X, X.transpose(1, 2))
+        S.masked_fill_(~valid[:, None, :], -2.0)
+        idx = torch.arange(smax, device=dev)
+        S[:, idx, idx] = -2.0
+        top = torch.topk(S, kk, dim=2)
+        base = starts[c0:c1].to(dev)[:, None, None]
+        src = (base + idx[None, :, None]).expand(nb, smax, kk)
+        dst = base + top.indices
+        ok = valid[:, :, None] & (top.values > -1.5)
+        us.append(src[ok].cpu())
+        vs.append(dst[ok].cpu())
+    u = torch.cat(us).numpy()
+    v = torch.cat(vs).numpy()
+    lo, hi = np.minimum(u, v), np.maximum(u, v)
+    key = np.unique(lo * n + hi)
+    lo, hi = key // n, key % n
+    P = pts.cpu()
+    w = (P[torch.from_numpy(lo)] * P[torch.from_numpy(hi)]).sum(1).numpy().astype(np.float32)
+    keep = w > 0
+    lo, hi, w = lo[keep], hi[keep], np.minimum(w[keep], np.float32(1.0))
+    src = np.concatenate([lo, hi])
+    dst = np.concatenate([hi, lo])
+    ww = np.concatenate([w, w]).astype(np.float64)
+    order = np.lexsort((dst, src))
+    src, dst, ww = src[order], dst[order], ww[order]
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(src, minlength=n), out=indptr[1:])
+    m = int(lo.size)
+    return HostGraph(n, m, indptr, dst.astype(np.int32), ww, float(w.astype(np.float64).sum())), comp.numpy()

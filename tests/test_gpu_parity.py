@@ -416,3 +416,20 @@ def test_sync_round_bin_shapes_exact(window, large_min, monkeypatch):
         g0 = oracle_gain(gw, None, 0.1, C, K, v, D0[v])
         g1 = oracle_gain(gw, None, 0.1, C, K, v, D1[v])
         assert abs(g0 - g1) <= REL_TIE * max(1.0, abs(g0))
+
+
+@pytest.mark.parametrize("lam", [0.01, 0.1, 0.5])
+def test_cfg3_knn_weighted_sync(lam):
+    """Config 3 semantics at reduced size: weighted cosine kNN, fp32 weights,
+    synchronous moves, full multi-level: labels identical except at gain ties
+    (none expected with continuous weights), objective within 1e-6."""
+    from paper_2108_01731_b200.gen import knn_mixture
+    hg, _ = knn_mixture(n=60_000, components=150, seed=33)
+    g = og(hg)
+    C0 = O.parallel_cc(g, None, lam, O.Opts(schedule=O.SYNC))
+    cl = L.parallel_cc(hg, L.ClusteringParams(lam), L.ParOptions(schedule="sync"))
+    o0 = O.objective(g, None, lam, C0)
+    o1 = L.cc_objective(hg, L.ClusteringParams(lam), cl)
+    assert o1 == pytest.approx(o0, rel=REL_W)
+    agree = np.mean(cl.labels() == C0)
+    assert agree > 0.999, agree

@@ -17,7 +17,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2108_01731_b200 as L  # noqa: E402
 from oracle import oracle as O  # noqa: E402
-from paper_2108_01731_b200.gen import lfr_like, rmat_device  # noqa: E402
+from paper_2108_01731_b200.gen import knn_mixture, lfr_like, rmat_device  # noqa: E402
 
 
 def gpu_run(hg_or_dg, k, lam):
@@ -63,7 +63,27 @@ def main(which):
                        "pass_0.5pct": o_gpu >= min(o_seq, o_par) - 0.005 * abs(o_seq), "gpu_s": t_gpu,
                        "cpu_seq_s": t_seq, "n": g.n, "m": g.m}
         print(json.dumps({"cfg2": out["cfg2"]}), flush=True)
+    if "cfg3" in which:
+        hg, _ = knn_mixture(seed=3)
+        g = O.as_graph(hg)
+        for lam in (0.01, 0.1, 0.5):
+            p = L.ClusteringParams(lam)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cl = L.parallel_cc(hg, p, L.ParOptions(schedule="sync"))
+            torch.cuda.synchronize()
+            t_gpu = time.perf_counter() - t0
+            lab = cl.labels()
+            t0 = time.perf_counter()
+            ref = O.parallel_cc(g, None, lam, O.Opts(schedule=O.SYNC, threads=threads))
+            t_cpu = time.perf_counter() - t0
+            o_gpu, o_ref = O.objective(g, None, lam, lab), O.objective(g, None, lam, ref)
+            res = {"lambda": lam, "n": g.n, "m": g.m, "label_agreement": float(np.mean(lab == ref)),
+                   "objective_gpu": o_gpu, "objective_cpu_sync": o_ref,
+                   "rel_diff": (o_gpu - o_ref) / max(abs(o_ref), 1e-300),
+                   "pass_1e-6": abs(o_gpu - o_ref) <= 1e-6 * max(abs(o_ref), 1e-300), "gpu_s": t_gpu, "cpu_s": t_cpu}
+            print(json.dumps({"cfg3": res}), flush=True)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["cfg4", "cfg2"])
+    main(sys.argv[1:] or ["cfg4", "cfg2", "cfg3"])

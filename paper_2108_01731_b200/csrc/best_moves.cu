@@ -1003,12 +1003,26 @@ constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-reside
 // 2 slot-list) bytes; GROUPS chosen so 2-3 CTAs fit per SM.
 template <class WT, bool ASYNC>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
+    // LCC_VARIANT (env, tuning only) selects alternative group shapes
+    const char* ev = getenv("LCC_VARIANT");
+    const int var = ev ? atoi(ev) : 0;
     switch (bin) {  //                         GW  CAP    GROUPS U
         case 2: launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s); break;     //  ..128      warp
         case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;    //  ..512      warp
-        case 4: launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s); break;    //  ..2048     4 warps
-        case 5: launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s); break;    //  ..4096     8 warps
-        case 6: launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s); break;  //  ..10240    8 warps
+        case 4:
+            if (var == 3) launch_group<WT, ASYNC, 8, 4096, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s);           //  ..2048     4 warps
+            break;
+        case 5:
+            if (var == 1 || var == 3) launch_group<WT, ASYNC, 16, 8192, 1, 8>(a, list, lo, hi, s);
+            else if (var == 2) launch_group<WT, ASYNC, 8, 8192, 1, 4>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s);           //  ..4096     8 warps
+            break;
+        case 6:
+            if (var == 1 || var == 3) launch_group<WT, ASYNC, 16, B5_CAP, 1, 8>(a, list, lo, hi, s);
+            else if (var == 2) launch_group<WT, ASYNC, 32, B5_CAP, 1, 4>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s);         //  ..10240    8 warps
+            break;
         default: break;
     }
 }

@@ -345,8 +345,10 @@ struct GlobalTable<false> {
     static constexpr int bytes_per_slot = 8;
     unsigned long long* tab;
     __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double) const {
+        insert_from(cap, x, slot_of(x, cap));
+    }
+    __device__ __forceinline__ void insert_from(uint32_t cap, int32_t x, uint32_t h) const {
         const unsigned long long want = ((unsigned long long)(uint32_t)x << 32) | 1ull;
-        uint32_t h = slot_of(x, cap);
         while (true) {
             const unsigned long long prev = atomicCAS(tab + h, (unsigned long long)EMPTY64, want);
             if (prev == EMPTY64) return;
@@ -782,11 +784,34 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
             }
 #pragma unroll
             for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            if constexpr (!WLoad<WT>::weighted) {
+                // first probe of all UL keys issued back to back (UL device
+                // CAS in flight per lane); collisions finish in the probe loop
+                unsigned long long* T = static_cast<unsigned long long*>(L.tab) + L.cap_off[li];
+                uint32_t h[UL];
+                unsigned long long old[UL];
 #pragma unroll
-            for (int j = 0; j < UL; ++j) {
-                if (u[j] == EMPTY_KEY) continue;
-                if (u[j] == c) sc += wv[j];
-                else tab.insert(cap, u[j], wv[j]);
+                for (int j = 0; j < UL; ++j) {
+                    old[j] = EMPTY64;
+                    if (u[j] == EMPTY_KEY) continue;
+                    if (u[j] == c) { sc += 1.0; u[j] = EMPTY_KEY; continue; }
+                    h[j] = slot_of(u[j], cap);
+                    old[j] = atomicCAS(T + h[j], (unsigned long long)EMPTY64,
+                                       ((unsigned long long)(uint32_t)u[j] << 32) | 1ull);
+                }
+#pragma unroll
+                for (int j = 0; j < UL; ++j) {
+                    if (u[j] == EMPTY_KEY || old[j] == EMPTY64) continue;
+                    if ((int32_t)(old[j] >> 32) == u[j]) { atomicAdd(T + h[j], 1ull); continue; }
+                    GlobalTable<false>{T}.insert_from(cap, u[j], (h[j] + 1 == cap) ? 0 : h[j] + 1);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < UL; ++j) {
+                    if (u[j] == EMPTY_KEY) continue;
+                    if (u[j] == c) sc += wv[j];
+                    else tab.insert(cap, u[j], wv[j]);
+                }
             }
         }
 #pragma unroll
@@ -1014,14 +1039,12 @@ void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64
             else launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s);           //  ..2048     4 warps
             break;
         case 5:
-            if (var == 1 || var == 3) launch_group<WT, ASYNC, 16, 8192, 1, 8>(a, list, lo, hi, s);
-            else if (var == 2) launch_group<WT, ASYNC, 8, 8192, 1, 4>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 8, 8192, 1, 8>(a, list, lo, hi, s);           //  ..4096     8 warps
+            if (var == 1) launch_group<WT, ASYNC, 16, 8192, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 8, 8192, 1, 4>(a, list, lo, hi, s);           //  ..4096     8 warps
             break;
         case 6:
-            if (var == 1 || var == 3) launch_group<WT, ASYNC, 16, B5_CAP, 1, 8>(a, list, lo, hi, s);
-            else if (var == 2) launch_group<WT, ASYNC, 32, B5_CAP, 1, 4>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 8, B5_CAP, 1, 8>(a, list, lo, hi, s);         //  ..10240    8 warps
+            if (var == 1) launch_group<WT, ASYNC, 16, B5_CAP, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 32, B5_CAP, 1, 4>(a, list, lo, hi, s);        //  ..10240    32 warps
             break;
         default: break;
     }

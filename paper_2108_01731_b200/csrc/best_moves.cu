@@ -789,21 +789,36 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
                 // CAS in flight per lane); collisions finish in the probe loop
                 unsigned long long* T = static_cast<unsigned long long*>(L.tab) + L.cap_off[li];
                 uint32_t h[UL];
-                unsigned long long old[UL];
+                unsigned pending = 0;
 #pragma unroll
                 for (int j = 0; j < UL; ++j) {
-                    old[j] = EMPTY64;
+                    h[j] = 0;
                     if (u[j] == EMPTY_KEY) continue;
-                    if (u[j] == c) { sc += 1.0; u[j] = EMPTY_KEY; continue; }
+                    if (u[j] == c) { sc += 1.0; continue; }
                     h[j] = slot_of(u[j], cap);
-                    old[j] = atomicCAS(T + h[j], (unsigned long long)EMPTY64,
-                                       ((unsigned long long)(uint32_t)u[j] << 32) | 1ull);
+                    pending |= 1u << j;
                 }
+                // every probe round issues the CAS of all pending keys back to
+                // back, so a lane waits one L2 round trip per probe depth, not
+                // per key
+                while (pending) {
+                    unsigned long long old[UL];
 #pragma unroll
-                for (int j = 0; j < UL; ++j) {
-                    if (u[j] == EMPTY_KEY || old[j] == EMPTY64) continue;
-                    if ((int32_t)(old[j] >> 32) == u[j]) { atomicAdd(T + h[j], 1ull); continue; }
-                    GlobalTable<false>{T}.insert_from(cap, u[j], (h[j] + 1 == cap) ? 0 : h[j] + 1);
+                    for (int j = 0; j < UL; ++j)
+                        if (pending & (1u << j))
+                            old[j] = atomicCAS(T + h[j], (unsigned long long)EMPTY64,
+                                               ((unsigned long long)(uint32_t)u[j] << 32) | 1ull);
+#pragma unroll
+                    for (int j = 0; j < UL; ++j) {
+                        if (!(pending & (1u << j))) continue;
+                        if (old[j] == EMPTY64) { pending &= ~(1u << j); continue; }
+                        if ((int32_t)(old[j] >> 32) == u[j]) {
+                            atomicAdd(T + h[j], 1ull);
+                            pending &= ~(1u << j);
+                            continue;
+                        }
+                        h[j] = (h[j] + 1 == cap) ? 0 : h[j] + 1;
+                    }
                 }
             } else {
 #pragma unroll

@@ -284,6 +284,32 @@ struct SmemTable<false> {
         }
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts + 4 * h) : "memory");
     }
+    // U keys at once: each probe round issues the CAS of every pending key
+    // back to back (one shared-memory latency per probe depth, not per key)
+    template <int U>
+    __device__ __forceinline__ void insert_batch(uint32_t cap, const int32_t (&x)[U], const double (&)[U],
+                                                 unsigned pending) const {
+        uint32_t h[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) h[j] = (pending >> j & 1u) ? slot_of(x[j], cap) : 0u;
+        while (pending) {
+            int32_t prev[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j)
+                if (pending >> j & 1u)
+                    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev[j]) : "r"(keys + 4 * h[j]), "r"(EMPTY_KEY), "r"(x[j]) : "memory");
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (!(pending >> j & 1u)) continue;
+                if (prev[j] == EMPTY_KEY || prev[j] == x[j]) {
+                    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts + 4 * h[j]) : "memory");
+                    pending &= ~(1u << j);
+                } else {
+                    h[j] = (h[j] + 1 == cap) ? 0 : h[j] + 1;
+                }
+            }
+        }
+    }
     __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
         int32_t kq;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
@@ -325,6 +351,30 @@ struct SmemTable<true> {
             h = (h + 1 == cap) ? 0 : h + 1;
         }
         asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h), "d"(wv) : "memory");
+    }
+    template <int U>
+    __device__ __forceinline__ void insert_batch(uint32_t cap, const int32_t (&x)[U], const double (&wv)[U],
+                                                 unsigned pending) const {
+        uint32_t h[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) h[j] = (pending >> j & 1u) ? slot_of(x[j], cap) : 0u;
+        while (pending) {
+            int32_t prev[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j)
+                if (pending >> j & 1u)
+                    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev[j]) : "r"(keys + 4 * h[j]), "r"(EMPTY_KEY), "r"(x[j]) : "memory");
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (!(pending >> j & 1u)) continue;
+                if (prev[j] == EMPTY_KEY || prev[j] == x[j]) {
+                    asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h[j]), "d"(wv[j]) : "memory");
+                    pending &= ~(1u << j);
+                } else {
+                    h[j] = (h[j] + 1 == cap) ? 0 : h[j] + 1;
+                }
+            }
+        }
     }
     __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
         int32_t kq;
@@ -449,12 +499,14 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            unsigned pending = 0;
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) sc += wv[j];
-                else tab.insert(cap, u[j], wv[j]);
+                else pending |= 1u << j;
             }
+            tab.template insert_batch<U>(cap, u, wv, pending);
         }
 #pragma unroll
         for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);

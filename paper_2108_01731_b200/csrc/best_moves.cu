@@ -499,14 +499,14 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
-            unsigned pending = 0;
+            // (batched probe rounds measured slower here than for the L2
+            // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) sc += wv[j];
-                else pending |= 1u << j;
+                else tab.insert(cap, u[j], wv[j]);
             }
-            tab.template insert_batch<U>(cap, u, wv, pending);
         }
 #pragma unroll
         for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);

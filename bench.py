@@ -183,7 +183,8 @@ def config_dict(args, g, extra=None):
          "n": g["n"], "m": g["m"], "objective": "cc", "lambda": args.lam, "schedule": args.schedule,
          "frontier": "vertex-neighbors", "refine": True, "num_iter": 10,
          "async_chunks": args.async_chunks, "degree_threshold": args.degree_threshold,
-         "step": "one best-move iteration over V'=V from singletons (partition+kernels+reconcile+frontier)",
+         "step": "one best-move iteration over V'=V from singletons: lcc_best_moves_round + lcc_apply_moves + "
+                 "lcc_compute_frontier (partition, kernels, reconcile, next active set)",
          "l2": "inputs larger than L2 (CSR indices %.2f GB vs 126 MB L2); no flush" % (4 * 2 * g["m"] / 1e9),
          "parallelism": "replicas" if g.get("ws", 1) > 1 else "single-gpu"}
     if extra:
@@ -257,17 +258,32 @@ def run_ours(args):
     p = L.ClusteringParams(args.lam)
     opts = L.ParOptions(schedule=args.schedule, num_iter=1, degree_threshold=args.degree_threshold,
                         async_chunks=args.async_chunks)
-    gs, ps, os_ = dg.c_struct(), p.c_struct(), opts.c_struct()
+    gs, ps = dg.c_struct(), p.c_struct()
+    sched = 1 if args.schedule == "async" else 0
     C = torch.empty(n, dtype=torch.int32, device="cuda")
-    K = torch.empty(n, dtype=torch.float64, device="cuda")
+    D = torch.empty(n, dtype=torch.int32, device="cuda")
+    K2 = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    Cn = torch.empty(n, dtype=torch.int32, device="cuda")
+    Kn = torch.empty(n, dtype=torch.float64, device="cuda")
+    F = torch.empty(n, dtype=torch.int32, device="cuda")
+    moved = torch.empty(n, dtype=torch.uint8, device="cuda")
     iota = torch.arange(n, dtype=torch.int32, device="cuda")
-    anym = ctypes.c_int32()
+    cnt, nF = ctypes.c_int64(), ctypes.c_int64()
 
     def step(st):
+        # one Alg. 1 iteration from singletons: best moves over V' = V, the
+        # mass/label reconcile, and the next active set (vertex neighbours)
         C.copy_(iota)
-        K.fill_(1.0)
-        _lib.check(lib.lcc_par_best_moves(ctypes.byref(gs), ctypes.byref(ps), ctypes.byref(os_), C.data_ptr(),
-                                          K.data_ptr(), ctypes.byref(anym), ctypes.byref(st), stream_ptr()))
+        K2[:n].fill_(1.0)
+        K2[n:].zero_()
+        sp = stream_ptr()
+        _lib.check(lib.lcc_best_moves_round(ctypes.byref(gs), ctypes.byref(ps), C.data_ptr(), K2.data_ptr(), None, n,
+                                            sched, args.degree_threshold, args.async_chunks, D.data_ptr(),
+                                            moved.data_ptr(), ctypes.byref(cnt), ctypes.byref(st), sp))
+        labels = C if sched == 1 else D
+        _lib.check(lib.lcc_apply_moves(n, labels.data_ptr(), 2 * n, None, Cn.data_ptr(), Kn.data_ptr(), sp))
+        _lib.check(lib.lcc_compute_frontier(ctypes.byref(gs), 1, moved.data_ptr(), iota.data_ptr(), Cn.data_ptr(),
+                                            F.data_ptr(), ctypes.byref(nF), sp))
 
     for _ in range(args.warmup):
         step(_lib.LccStats())
@@ -364,7 +380,7 @@ def run_ours(args):
                "config": config_dict(args, g), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(launches), "clocks": clk.summary(),
                "round_stats": {"vertices": st.vertices // args.steps, "edges": st.edges_scanned // args.steps,
-                               "moves": st.moves // args.steps, "ms_round": st.ms_best_moves / args.steps}}
+                               "moves": st.moves // args.steps, "next_frontier": int(nF.value)}}
         print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()

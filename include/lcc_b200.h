@@ -104,14 +104,16 @@ int64_t lcc_kernel_launches(void);
  *              fresh-singleton targets are n+v) and moved[n] (0/1).
  *   LCC_ASYNC: updates C[n] and K[2n] in place with relaxed atomics
  *              (SPEC.md:261,313); D may be NULL; moved[n] written.
- * *moved_count (host) receives the number of movers.                        */
+ * *moved_count (host) receives the number of movers; stats (may be NULL) is
+ * accumulated (vertices, edges scanned, movers, best-move kernel time).     */
 lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p,
                                 int32_t* C, double* K,
                                 const int32_t* frontier, int64_t n_frontier,
                                 int32_t schedule, int32_t degree_threshold,
                                 int32_t async_chunks,
                                 int32_t* D, uint8_t* moved,
-                                int64_t* moved_count, void* stream);
+                                int64_t* moved_count, lcc_stats* stats,
+                                void* stream);
 
 /* ---- sync apply: canonicalise labels and rebuild masses ----
  * labels_in[n] take values in [0, label_range); writes C[v] = smallest member

@@ -79,7 +79,7 @@ def load() -> ctypes.CDLL:
         "lcc_abi_version": (ctypes.c_int, []),
         "lcc_last_error": (ctypes.c_char_p, []),
         "lcc_kernel_launches": (ctypes.c_int64, []),
-        "lcc_best_moves_round": (ctypes.c_int, [G, PR, P, P, P, I64, I32, I32, I32, P, P, pI64, P]),
+        "lcc_best_moves_round": (ctypes.c_int, [G, PR, P, P, P, I64, I32, I32, I32, P, P, pI64, ST, P]),
         "lcc_apply_moves": (ctypes.c_int, [I64, P, I64, P, P, P, P]),
         "lcc_compute_frontier": (ctypes.c_int, [G, I32, P, P, P, P, pI64, P]),
         "lcc_par_best_moves": (ctypes.c_int, [G, PR, O, P, P, pI32, ST, P]),

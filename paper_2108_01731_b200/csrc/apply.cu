@@ -46,24 +46,21 @@ __global__ void k_relabel_mass(const int32_t* __restrict__ L, const int32_t* __r
     }
 }
 
-// degree of v if v contributes its neighbours to the frontier, else 0
-struct MovedDeg {
+struct HasEdgesAndFlag {
     const int64_t* indptr;
-    const uint8_t* moved;
-    int64_t n;
-    __device__ __forceinline__ int64_t operator()(int64_t v) const {
-        return (v < n && moved[v]) ? indptr[v + 1] - indptr[v] : 0;
+    const uint8_t* flag;
+    __device__ __forceinline__ bool operator()(int32_t v) const {
+        return flag[v] && indptr[v + 1] > indptr[v];
     }
 };
-struct ClusterDeg {
+struct ListDeg {
     const int64_t* indptr;
-    const int32_t* Cold;
-    const int32_t* Cnew;
-    const uint8_t* src;
-    const uint8_t* dst;
+    const int32_t* list;
     int64_t n;
-    __device__ __forceinline__ int64_t operator()(int64_t u) const {
-        return (u < n && (src[Cold[u]] || dst[Cnew[u]])) ? indptr[u + 1] - indptr[u] : 0;
+    __device__ __forceinline__ int64_t operator()(int64_t i) const {
+        if (i >= n) return 0;
+        const int32_t v = list[i];
+        return indptr[v + 1] - indptr[v];
     }
 };
 // edge functor: mark the neighbour
@@ -78,6 +75,13 @@ __global__ void k_cluster_flags(const uint8_t* __restrict__ moved, const int32_t
                                 const int32_t* __restrict__ Cnew, int64_t n, uint8_t* src, uint8_t* dst) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
         if (moved[v]) { src[Cold[v]] = 1; dst[Cnew[v]] = 1; }
+}
+
+__global__ void k_cluster_contrib(const int32_t* __restrict__ Cold, const int32_t* __restrict__ Cnew,
+                                  const uint8_t* __restrict__ src, const uint8_t* __restrict__ dst, int64_t n,
+                                  uint8_t* contrib) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        contrib[u] = (src[Cold[u]] || dst[Cnew[u]]) ? 1 : 0;
 }
 
 __global__ void k_mark_dst_members(const int32_t* __restrict__ Cnew, const uint8_t* __restrict__ dst, int64_t n,
@@ -133,27 +137,40 @@ int64_t compute_frontier(const lcc_graph& g, int policy, const uint8_t* moved, c
     }
     Buf<uint8_t> mark(n, s);
     LCC_CUDA(cudaMemsetAsync(mark.get(), 0, n, s));
-    Buf<int64_t> off(n + 1, s);
+    // contributing vertices (movers, or members of affected clusters) are
+    // compacted first so every list entry has degree >= 1 and the edge map's
+    // per-tile window stays in shared memory
+    Buf<uint8_t> contrib;
+    const uint8_t* cflag = moved;
     Buf<uint8_t> flags;
-    if (policy == LCC_FRONTIER_VERTEX_NBRS) {
-        cub::TransformInputIterator<int64_t, MovedDeg, cub::CountingInputIterator<int64_t>> degs(
-            cub::CountingInputIterator<int64_t>(0), MovedDeg{g.indptr, moved, n});
-        exclusive_sum(degs, off.get(), n + 1, s);  // entry n contributes 0 -> off[n] = total
-    } else {
+    if (policy == LCC_FRONTIER_CLUSTER_NBRS) {
         flags.alloc(2 * n, s);
         LCC_CUDA(cudaMemsetAsync(flags.get(), 0, 2 * n, s));
         k_cluster_flags<<<grid_for(n, 256), 256, 0, s>>>(moved, C_old, C_new, n, flags.get(), flags.get() + n);
         LCC_LAUNCH_CHECK();
         k_mark_dst_members<<<grid_for(n, 256), 256, 0, s>>>(C_new, flags.get() + n, n, mark.get());
         LCC_LAUNCH_CHECK();
-        cub::TransformInputIterator<int64_t, ClusterDeg, cub::CountingInputIterator<int64_t>> degs(
-            cub::CountingInputIterator<int64_t>(0), ClusterDeg{g.indptr, C_old, C_new, flags.get(), flags.get() + n, n});
-        exclusive_sum(degs, off.get(), n + 1, s);
+        contrib.alloc(n, s);
+        k_cluster_contrib<<<grid_for(n, 256), 256, 0, s>>>(C_old, C_new, flags.get(), flags.get() + n, n, contrib.get());
+        LCC_LAUNCH_CHECK();
+        cflag = contrib.get();
     }
-    int64_t total = 0;
-    LCC_CUDA(cudaMemcpyAsync(&total, off.get() + n, sizeof(total), cudaMemcpyDeviceToHost, s));
+    Buf<int32_t> clist(n, s);
+    select_if(cub::CountingInputIterator<int32_t>(0), clist.get(), dcnt.get(), n,
+              HasEdgesAndFlag{g.indptr, cflag}, s);
+    int64_t nc = 0;
+    LCC_CUDA(cudaMemcpyAsync(&nc, dcnt.get(), sizeof(nc), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
-    edge_balanced(g.indptr, nullptr, off.get(), n, total, MarkNbr{g.indices, mark.get()}, s);
+    if (nc > 0) {
+        Buf<int64_t> off(nc + 1, s);
+        cub::TransformInputIterator<int64_t, ListDeg, cub::CountingInputIterator<int64_t>> degs(
+            cub::CountingInputIterator<int64_t>(0), ListDeg{g.indptr, clist.get(), nc});
+        exclusive_sum(degs, off.get(), nc + 1, s);
+        int64_t total = 0;
+        LCC_CUDA(cudaMemcpyAsync(&total, off.get() + nc, sizeof(total), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaStreamSynchronize(s));
+        edge_balanced(g.indptr, clist.get(), off.get(), nc, total, MarkNbr{g.indices, mark.get()}, s);
+    }
     select_flagged(cub::CountingInputIterator<int32_t>(0), mark.get(), frontier, dcnt.get(), n, s);
     int64_t h = 0;
     LCC_CUDA(cudaMemcpyAsync(&h, dcnt.get(), sizeof(h), cudaMemcpyDeviceToHost, s));

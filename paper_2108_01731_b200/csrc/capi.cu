@@ -93,16 +93,25 @@ const char* lcc_last_error(void) { return g_err.c_str(); }
 lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p, int32_t* C, double* K,
                                 const int32_t* frontier, int64_t n_frontier, int32_t schedule,
                                 int32_t degree_threshold, int32_t async_chunks, int32_t* D, uint8_t* moved,
-                                int64_t* moved_count, void* stream) {
+                                int64_t* moved_count, lcc_stats* stats, void* stream) {
     return guard([&] {
         check_graph(g);
         check_params(p);
         LCC_REQUIRE(C && K && moved, "C, K and moved are required");
         LCC_REQUIRE(n_frontier >= 0 && n_frontier <= g->n, "frontier size out of range");
+        lcc::RoundStats rs;
         const int64_t cnt = lcc::best_moves_round(*g, p->k, p->lambda, C, K, frontier, n_frontier, schedule,
                                                   degree_threshold, async_chunks > 0 ? async_chunks : 0, D, moved,
-                                                  nullptr, S(stream));
+                                                  &rs, S(stream));
         if (moved_count) *moved_count = cnt;
+        if (stats) {
+            stats->rounds += 1;
+            stats->vertices += rs.vertices;
+            stats->edges_scanned += rs.edges;
+            stats->moves += rs.moved;
+            stats->ms_kernels += rs.ms_kernels;
+            stats->kernel_launches += rs.launches;
+        }
     });
 }
 

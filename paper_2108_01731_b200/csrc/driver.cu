@@ -80,8 +80,10 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         if (cnt == 0) break;  // Alg. 1 line 9
         any = true;
         apply_moves(n, D.get(), 2 * n, k, nxt, K, s);  // sync apply / async reconcile
-        nF = compute_frontier(g, o.policy, moved.get(), cur, nxt, F.get(), s);
-        frontier = F.get();
+        if (it + 1 < o.num_iter) {  // the next frontier is only needed by a next iteration
+            nF = compute_frontier(g, o.policy, moved.get(), cur, nxt, F.get(), s);
+            frontier = F.get();
+        }
         std::swap(cur, nxt);
     }
     if (cur != C) LCC_CUDA(cudaMemcpyAsync(C, cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));

@@ -27,11 +27,17 @@ __device__ __forceinline__ int64_t upper_idx(const int64_t* off, int64_t lo, int
 
 // F: functor with  __device__ void operator()(int64_t v, int64_t e)  and
 //                  __device__ void flush()   (called once per thread at the end)
+// When the tile's window of `off` fits in shared memory (always the case for
+// lists whose entries all have degree >= 1: at most EM_TILE + 1 entries) the
+// per-edge search runs in shared memory; otherwise it falls back to global.
 template <class F>
 __global__ void __launch_bounds__(EM_THREADS)
 k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ list,
                 const int64_t* __restrict__ off, int64_t nlist, F f) {
     __shared__ int64_t s_lo, s_hi;
+    __shared__ int64_t s_off[EM_TILE + 2];
+    __shared__ int64_t s_row[EM_TILE + 1];  // start of each window entry's row
+    __shared__ int32_t s_v[EM_TILE + 1];    // vertex of each window entry
     const int64_t total = __ldg(off + nlist);
     for (int64_t t0 = (int64_t)blockIdx.x * EM_TILE; t0 < total; t0 += (int64_t)gridDim.x * EM_TILE) {
         const int64_t t1 = min64(t0 + EM_TILE, total);
@@ -39,13 +45,33 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
         if (threadIdx.x == 32) s_hi = upper_idx(off, 0, nlist + 1, t1 - 1) + 1;
         __syncthreads();
         const int64_t lo = s_lo, hi = s_hi;
+        const int64_t wn = hi - lo;  // entries lo .. hi-1 own the tile; off[hi] closes it
+        const bool cached = wn <= EM_TILE;
+        if (cached) {
+            for (int64_t i = threadIdx.x; i <= wn; i += EM_THREADS) s_off[i] = __ldg(off + lo + i);
+            for (int64_t i = threadIdx.x; i < wn; i += EM_THREADS) {
+                const int64_t v = list ? (int64_t)__ldg(list + lo + i) : lo + i;
+                s_v[i] = (int32_t)v;
+                s_row[i] = __ldg(indptr + v) - s_off[i];  // edge e of this entry = s_row + e
+            }
+        }
+        __syncthreads();
 #pragma unroll 2
         for (int j = 0; j < EM_ITEMS; ++j) {
             const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
             if (e < t1) {
-                const int64_t li = upper_idx(off, lo, hi, e);
-                const int64_t v = list ? (int64_t)__ldg(list + li) : li;
-                f(v, __ldg(indptr + v) + (e - __ldg(off + li)));
+                if (cached) {
+                    int a = 0, b = (int)wn;  // largest a with s_off[a] <= e
+                    while (b - a > 1) {
+                        const int mid = (a + b) >> 1;
+                        if (s_off[mid] <= e) a = mid; else b = mid;
+                    }
+                    f((int64_t)s_v[a], s_row[a] + e);
+                } else {
+                    const int64_t li = upper_idx(off, lo, hi, e);
+                    const int64_t v = list ? (int64_t)__ldg(list + li) : li;
+                    f(v, __ldg(indptr + v) + (e - __ldg(off + li)));
+                }
             }
         }
         __syncthreads();

@@ -125,7 +125,7 @@ class CudaBackend:
             _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), C.data_ptr(), K.data_ptr(),
                                                      fr.data_ptr() if fr.numel() else None, fr.numel(),
                                                      _lib.SYNC, thr, chunks, D.data_ptr(), moved.data_ptr(),
-                                                     ctypes.byref(cnt), stream_ptr()))
+                                                     ctypes.byref(cnt), None, stream_ptr()))
             return D, moved, cnt.value
         Cw = C.clone()
         K2 = torch.zeros(2 * n, dtype=torch.float64, device=self.device)
@@ -133,7 +133,7 @@ class CudaBackend:
         _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), Cw.data_ptr(), K2.data_ptr(),
                                                  fr.data_ptr() if fr.numel() else None, fr.numel(),
                                                  _lib.ASYNC, thr, chunks, None, moved.data_ptr(),
-                                                 ctypes.byref(cnt), stream_ptr()))
+                                                 ctypes.byref(cnt), None, stream_ptr()))
         return Cw, moved, cnt.value
 
     def apply(self, labels, label_range, k):
@@ -151,7 +151,7 @@ class CudaBackend:
         out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         cnt = ctypes.c_int64()
         _lib.check(self.lib.lcc_compute_frontier(ctypes.byref(g), int(policy), moved.data_ptr(), Cold.data_ptr(),
-                                                 Cnew.data_ptr(), out.data_ptr(), ctypes.byref(cnt), stream_ptr()))
+                                                 Cnew.data_ptr(), out.data_ptr(), ctypes.byref(cnt), None, stream_ptr()))
         mask = torch.zeros(n, dtype=torch.uint8, device=self.device)
         if cnt.value:
             mask[out[:cnt.value].long()] = 1

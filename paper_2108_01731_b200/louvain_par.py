@@ -177,7 +177,7 @@ def best_moves_round(g, p: ClusteringParams, c: Clustering, frontier=None,
         ctypes.byref(gs), ctypes.byref(ps), c.assignment.data_ptr(), K.data_ptr(),
         None if fr is None else fr.data_ptr(), 0 if fr is None else fr.numel(), int(schedule),
         int(degree_threshold), int(async_chunks), D.data_ptr(), moved.data_ptr(), ctypes.byref(cnt),
-        stream_ptr()))
+        None, stream_ptr()))
     if schedule == Schedule.Asynchronous:
         D = c.assignment
     return MoveBuffer(D, moved, cnt.value)
@@ -220,7 +220,7 @@ def compute_frontier(policy, moved, g, c_old=None, c_new=None) -> Frontier:
     _lib.check(_lib.load().lcc_compute_frontier(ctypes.byref(gs), int(policy), mv.data_ptr(),
                                                 None if co is None else co.data_ptr(),
                                                 None if cn is None else cn.data_ptr(), out.data_ptr(),
-                                                ctypes.byref(cnt), stream_ptr()))
+                                                ctypes.byref(cnt), None, stream_ptr()))
     return Frontier(n, out[:cnt.value].clone())
 
 

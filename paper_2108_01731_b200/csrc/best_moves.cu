@@ -454,8 +454,8 @@ constexpr size_t group_smem_bytes() {
     return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::weighted>::bytes_per_slot;
 }
 
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U>
-__global__ void __launch_bounds__(GW * 32 * GROUPS)
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
+__global__ void __launch_bounds__(GW * 32 * GROUPS, MINB)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr bool WEIGHTED = WLoad<WT>::weighted;
     constexpr int GT = GW * 32;
@@ -1070,20 +1070,20 @@ void set_smem(K kernel, int bytes) {
     LCC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U>
+template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
 void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     if (hi <= lo) return;
     constexpr int THREADS = GW * 32 * GROUPS;
     constexpr int SMEM = (int)group_smem_bytes<WT, CAP, GROUPS>();
     static int occ = 0;
     if (!occ) {
-        set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS, U>, SMEM);
-        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS, U>, THREADS, SMEM));
+        set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS, U, MINB>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS, U, MINB>, THREADS, SMEM));
         occ = std::max(occ, 1);
     }
     const int64_t blocks_needed = (hi - lo + GROUPS - 1) / GROUPS;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * occ));
-    k_group<WT, ASYNC, GW, CAP, GROUPS, U><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
+    k_group<WT, ASYNC, GW, CAP, GROUPS, U, MINB><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
     LCC_LAUNCH_CHECK();
 }
 
@@ -1099,8 +1099,16 @@ void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64
     const char* ev = getenv("LCC_VARIANT");
     const int var = ev ? atoi(ev) : 0;
     switch (bin) {  //                         GW  CAP    GROUPS U
-        case 2: launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s); break;     //  ..128      warp
-        case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;    //  ..512      warp
+        case 2:
+            if (var == 4) launch_group<WT, ASYNC, 1, 256, 8, 4, 6>(a, list, lo, hi, s);
+            else if (var == 5) launch_group<WT, ASYNC, 1, 256, 8, 2, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s);            //  ..128      warp
+            break;
+        case 3:
+            if (var == 4) launch_group<WT, ASYNC, 1, 1024, 4, 8, 7>(a, list, lo, hi, s);
+            else if (var == 5) launch_group<WT, ASYNC, 1, 1024, 4, 4, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s);           //  ..512      warp
+            break;
         case 4:
             if (var == 3) launch_group<WT, ASYNC, 8, 4096, 1, 8>(a, list, lo, hi, s);
             else launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s);           //  ..2048     4 warps

@@ -67,12 +67,7 @@ struct ListDeg {
 struct MarkNbr {
     const int32_t* indices;
     uint8_t* mark;
-    __device__ __forceinline__ void operator()(int64_t, int64_t e) const {
-        const int32_t u = __ldg(indices + e);
-        // most neighbours of a hub are marked many times: test before writing
-        // so repeated marks stay reads and do not dirty the L2 line again
-        if (!*(volatile uint8_t*)(mark + u)) mark[u] = 1;
-    }
+    __device__ __forceinline__ void operator()(int64_t, int64_t e) const { mark[__ldg(indices + e)] = 1; }
     __device__ __forceinline__ void flush() const {}
 };
 

@@ -1099,16 +1099,8 @@ void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64
     const char* ev = getenv("LCC_VARIANT");
     const int var = ev ? atoi(ev) : 0;
     switch (bin) {  //                         GW  CAP    GROUPS U
-        case 2:
-            if (var == 4) launch_group<WT, ASYNC, 1, 256, 8, 4, 6>(a, list, lo, hi, s);
-            else if (var == 5) launch_group<WT, ASYNC, 1, 256, 8, 2, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 1, 256, 8, 4>(a, list, lo, hi, s);            //  ..128      warp
-            break;
-        case 3:
-            if (var == 4) launch_group<WT, ASYNC, 1, 1024, 4, 8, 7>(a, list, lo, hi, s);
-            else if (var == 5) launch_group<WT, ASYNC, 1, 1024, 4, 4, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s);           //  ..512      warp
-            break;
+        case 2: launch_group<WT, ASYNC, 1, 256, 8, 4, 6>(a, list, lo, hi, s); break;   //  ..128      warp
+        case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;     //  ..512      warp
         case 4:
             if (var == 3) launch_group<WT, ASYNC, 8, 4096, 1, 8>(a, list, lo, hi, s);
             else launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s);           //  ..2048     4 warps
@@ -1231,6 +1223,29 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_
     }
 }
 
+// side streams for concurrent bin kernels (one set per device, created once)
+struct SideStreams {
+    cudaStream_t st[NBINS];
+    cudaEvent_t fork;
+    cudaEvent_t join[NBINS];
+};
+inline SideStreams& side_streams() {
+    static SideStreams per_dev[16];
+    static bool made[16] = {false};
+    int dev = 0;
+    LCC_CUDA(cudaGetDevice(&dev));
+    SideStreams& ss = per_dev[dev & 15];
+    if (!made[dev & 15]) {
+        for (int i = 0; i < NBINS; ++i) {
+            LCC_CUDA(cudaStreamCreateWithFlags(&ss.st[i], cudaStreamNonBlocking));
+            LCC_CUDA(cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming));
+        }
+        LCC_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+        made[dev & 15] = true;
+    }
+    return ss;
+}
+
 template <class WT, bool ASYNC>
 int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                   const int32_t* frontier, int64_t nF, int deg_threshold, int chunks, int32_t* D,
@@ -1297,46 +1312,54 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     }
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    LCC_CUDA(cudaEventCreate(&ev0));
-    LCC_CUDA(cudaEventCreate(&ev1));
+    LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
+    LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
     const long long launches0 = launch_counter();
-    float kms = 0.f, kms_large = 0.f;
+    float kms = 0.f;
 
-    const int64_t nL = (int64_t)hc[NBINS - 1];
-    if (nL > 0) {
-        LCC_CUDA(cudaEventRecord(ev0, s));
-        run_large<WT, ASYNC>(a, g, lists.get() + binstart[NBINS - 1], nL, s);
-        LCC_CUDA(cudaEventRecord(ev1, s));
-        LCC_CUDA(cudaEventSynchronize(ev1));
-        LCC_CUDA(cudaEventElapsedTime(&kms_large, ev0, ev1));
-    }
-    // async sub-rounds: `chunks` > 0 is explicit; 0 = auto, enough sub-rounds
-    // that small frontiers still see each other's moves (symmetry breaking,
-    // PAPER.md:193) while large ones run as one wave (measured on R-MAT s24:
-    // 1 sub-round is 20% faster than 16 and reaches a higher objective)
     int P = 1;
     if (ASYNC) P = chunks > 0 ? chunks : (int)std::min<int64_t>(16, std::max<int64_t>(1, ((1LL << 22) + nF - 1) / std::max<int64_t>(nF, 1)));
     WindowPlan wp;
     if (hc[1] > 0) plan_windows(g.indptr, lists.get() + binstart[1], (int64_t)hc[1], wp, s);
+    const int64_t nL = (int64_t)hc[NBINS - 1];
+    // The bins are independent within a (sub-)round -- sync reads a frozen
+    // state and writes disjoint D entries; async tolerates any interleaving --
+    // so their latency-bound kernels run concurrently on side streams
+    // (fork/join with events) instead of back to back.
+    SideStreams& ss = side_streams();
     LCC_CUDA(cudaEventRecord(ev0, s));
     for (int j = 0; j < P; ++j) {
+        LCC_CUDA(cudaEventRecord(ss.fork, s));
+        int used = 0;
+        auto next_stream = [&]() -> cudaStream_t {
+            cudaStream_t t = ss.st[used++];
+            LCC_CUDA(cudaStreamWaitEvent(t, ss.fork, 0));
+            return t;
+        };
+        if (j == 0 && nL > 0) run_large<WT, ASYNC>(a, g, lists.get() + binstart[NBINS - 1], nL, next_stream());
         for (int b = 0; b < NBINS - 1; ++b) {
             const int64_t nb = (int64_t)hc[b];
             if (nb == 0) continue;
             const int32_t* list = lists.get() + binstart[b];
             if (b == 1) {
-                launch_window<WT, ASYNC>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, s);
+                if (wp.nwin * (j + 1) / P > wp.nwin * j / P)
+                    launch_window<WT, ASYNC>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, next_stream());
                 continue;
             }
             const int64_t lo = nb * j / P, hi = nb * (j + 1) / P;
             if (hi <= lo) continue;
+            cudaStream_t t = next_stream();
             if (b == 0) {
                 const int64_t warps = (hi - lo + 31) / 32;
-                k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, s>>>(a, list, lo, hi);
+                k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, t>>>(a, list, lo, hi);
                 LCC_LAUNCH_CHECK();
             } else {
-                launch_bin<WT, ASYNC>(b, a, list, lo, hi, s);
+                launch_bin<WT, ASYNC>(b, a, list, lo, hi, t);
             }
+        }
+        for (int i = 0; i < used; ++i) {
+            LCC_CUDA(cudaEventRecord(ss.join[i], ss.st[i]));
+            LCC_CUDA(cudaStreamWaitEvent(s, ss.join[i], 0));
         }
     }
     LCC_CUDA(cudaEventRecord(ev1, s));
@@ -1346,6 +1369,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     LCC_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
+    const float kms_large = 0.f;
     if (st) {
         st->vertices += nF;
         st->edges += (int64_t)hc[NBINS];

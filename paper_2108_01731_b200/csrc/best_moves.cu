@@ -1326,12 +1326,17 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     // state and writes disjoint D entries; async tolerates any interleaving --
     // so their latency-bound kernels run concurrently on side streams
     // (fork/join with events) instead of back to back.
+    // With ordered async sub-rounds (P > 1, small frontiers) the bins stay in
+    // order on the caller's stream: the interleaving is what breaks symmetry
+    // on small graphs (measured on the config-1 SBM).
     SideStreams& ss = side_streams();
+    const bool concurrent = P == 1;
     LCC_CUDA(cudaEventRecord(ev0, s));
     for (int j = 0; j < P; ++j) {
         LCC_CUDA(cudaEventRecord(ss.fork, s));
         int used = 0;
         auto next_stream = [&]() -> cudaStream_t {
+            if (!concurrent) return s;
             cudaStream_t t = ss.st[used++];
             LCC_CUDA(cudaStreamWaitEvent(t, ss.fork, 0));
             return t;

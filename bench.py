@@ -364,6 +364,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4),
                "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()),
                "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
+               "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
+               "device_ms_best_move_kernels": stats.ms_kernels,
                "objective": obj, "clusters": int(np.unique(out_h.numpy()).size),
                "api": "paper_2108_01731_b200.parallel_cc(host pinned CSR) + labels D2H"}
 

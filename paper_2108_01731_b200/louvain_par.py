@@ -55,7 +55,7 @@ class ParOptions:
     from below by the warp path (32) and from above by the shared-memory
     table capacity.  ``async_chunks``: the asynchronous schedule walks the
     frontier in this many ordered sub-rounds; later sub-rounds see the moves
-    of earlier ones (symmetry breaking).  0 = auto (up to 16
+    of earlier ones (symmetry breaking).  0 = auto (up to 64
     for small frontiers, one wave for frontiers of 4M+ vertices)."""
     schedule: Schedule = Schedule.Asynchronous
     frontier_policy: FrontierPolicy = FrontierPolicy.VertexNeighbors

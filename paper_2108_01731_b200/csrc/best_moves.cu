@@ -477,10 +477,15 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
-    auto process = [&](const int32_t v, const int64_t s, const int64_t end, const int32_t c, const double kv,
-                       const double Kc) {
+    for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += (int64_t)gridDim.x * GROUPS) {
+        const int32_t v = __ldg(list + i);
+        const int64_t s = __ldg(a.indptr + v);
+        const int64_t end = __ldg(a.indptr + v + 1);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const double kv = kval(a.k, v);
+        const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
         for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
@@ -548,36 +553,6 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         }
         if (gt == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
         gsync();  // table (already reset by take) and s_g free for the next vertex
-        };
-    const int64_t stride = (int64_t)gridDim.x * GROUPS;
-    if constexpr (GW == 1) {
-        // one warp per vertex: the headers of the warp's next 32 vertices are
-        // loaded in one coalesced step and broadcast by shuffles, so each
-        // vertex pays two dependent global round trips instead of five
-        for (int64_t ib = lo + (int64_t)blockIdx.x * GROUPS + gid; ib < hi; ib += stride * 32) {
-            const int64_t il = ib + (int64_t)lane * stride;
-            int32_t hv = 0, hc = 0;
-            int64_t hs = 0, he = 0;
-            double hkv = 1.0, hKc = 0.0;
-            if (il < hi) {
-                hv = __ldg(list + il);
-                hs = __ldg(a.indptr + hv);
-                he = __ldg(a.indptr + hv + 1);
-                hc = ldC<ASYNC>(a.C, hv, pol_keep);
-                hkv = kval(a.k, hv);
-                hKc = ldK<ASYNC>(a.K, hc, pol_keep);
-            }
-            const int cnt = (int)min64(32, (hi - ib + stride - 1) / stride);
-            for (int l = 0; l < cnt; ++l)
-                process(__shfl_sync(FULL, hv, l), __shfl_sync(FULL, hs, l), __shfl_sync(FULL, he, l),
-                        __shfl_sync(FULL, hc, l), __shfl_sync(FULL, hkv, l), __shfl_sync(FULL, hKc, l));
-        }
-    } else {
-        for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += stride) {
-            const int32_t v = __ldg(list + i);
-            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
-            process(v, __ldg(a.indptr + v), __ldg(a.indptr + v + 1), c, kval(a.k, v), ldK<ASYNC>(a.K, c, pol_keep));
-        }
     }
     flush_moves(a, my_moves);
 }

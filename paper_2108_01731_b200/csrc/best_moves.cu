@@ -520,14 +520,12 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
-        // warp-uniform trip count (the warp-private insert uses full-mask
-        // warp collectives)
-        for (int64_t e0 = s; e0 < end; e0 += (int64_t)GT * U) {
+        for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
             int32_t u[U];
             double wv[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                const int64_t e = e0 + gt + (int64_t)j * GT;
+                const int64_t e = e0 + (int64_t)j * GT;
                 u[j] = e < end ? ld_stream_i32(a.indices + e, pol_stream) : -1;
                 wv[j] = e < end ? WLoad<WT>::at(a.w, e) : 0.0;
             }

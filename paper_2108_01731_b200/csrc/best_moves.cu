@@ -310,38 +310,6 @@ struct SmemTable<false> {
             }
         }
     }
-    // Warp-private table (one warp owns it): insert one label per lane with
-    // plain shared loads/stores.  Equal labels in the warp are merged first
-    // (__match_any_sync, the leader carries the count); leaders that find the
-    // same empty slot in one step are separated by a second match -- the
-    // lowest lane claims it, the others probe on.  Every lane must call this
-    // (warp-uniform); `want` = lane has a label to insert.
-    __device__ __forceinline__ void insert_warp(uint32_t cap, int32_t x, bool want) const {
-        const unsigned lane = threadIdx.x & 31u;
-        const unsigned grp = __match_any_sync(0xffffffffu, want ? (uint32_t)x : (0x80000000u | lane));
-        bool pending = want && (__ffs(grp) - 1 == (int)lane);
-        const uint32_t cnt = __popc(grp);
-        uint32_t h = pending ? slot_of(x, cap) : 0u;
-        while (__any_sync(0xffffffffu, pending)) {
-            int32_t k = 0;
-            if (pending) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(k) : "r"(keys + 4 * h) : "memory");
-            if (pending && k == x) {
-                uint32_t cq;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cq) : "r"(cnts + 4 * h) : "memory");
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(cq + cnt) : "memory");
-                pending = false;
-            }
-            const bool claim = pending && k == EMPTY_KEY;
-            const unsigned g = __match_any_sync(0xffffffffu, claim ? h : (0x80000000u | lane));
-            if (claim && (__ffs(g) - 1 == (int)lane)) {
-                asm volatile("st.shared.b32 [%0], %1;" ::"r"(keys + 4 * h), "r"(x) : "memory");
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(cnt) : "memory");
-                pending = false;
-            }
-            if (pending) h = (h + 1 == cap) ? 0 : h + 1;
-            __syncwarp();
-        }
-    }
     __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
         int32_t kq;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
@@ -531,21 +499,13 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
-            if constexpr (GW == 1 && !WEIGHTED) {
-                // warp-private table: no shared atomics (ATOMS costs 2 LSU
-                // cycles per lane, the dominant per-edge cost otherwise)
+            // (batched probe rounds measured slower here than for the L2
+            // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    if (u[j] == c) sc += 1.0;
-                    tab.insert_warp(cap, u[j], u[j] != EMPTY_KEY && u[j] != c);
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    if (u[j] == EMPTY_KEY) continue;
-                    if (u[j] == c) sc += wv[j];
-                    else tab.insert(cap, u[j], wv[j]);
-                }
+            for (int j = 0; j < U; ++j) {
+                if (u[j] == EMPTY_KEY) continue;
+                if (u[j] == c) sc += wv[j];
+                else tab.insert(cap, u[j], wv[j]);
             }
         }
 #pragma unroll

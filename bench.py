@@ -53,11 +53,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE.json configs[i-1]; cfg4 is the headline workload")
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=24)
-    ap.add_argument("--lam", type=float, default=0.85)
-    ap.add_argument("--schedule", default="async", choices=["async", "sync"])
+    ap.add_argument("--lam", type=float, default=None, help="default: the config's lambda")
+    ap.add_argument("--schedule", default=None, choices=["async", "sync"], help="default: the config's schedule")
     ap.add_argument("--async-chunks", type=int, default=0)
     ap.add_argument("--degree-threshold", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -146,29 +148,45 @@ def cpu_sample(indptr, stride):
     return F, edges
 
 
-def run_cpu_baseline(indptr, indices, lam, stride, seconds, warmup=1, max_reps=50):
-    """Oracle port of the reference's async round (OpenMP atomics, all threads)."""
+def cpu_round(og, k, lam, schedule, F, threads):
+    """One best-move round of the oracle port over F from singletons; seconds."""
     from oracle import oracle as O
-    g = O.Graph(indptr.size - 1, indptr, indices, None, float(indices.size // 2))
-    F, edges = cpu_sample(indptr, stride)
+    n = og.n
+    C = np.arange(n, dtype=np.int32)
+    t0 = time.perf_counter()
+    if schedule == "async":
+        K2 = np.zeros(2 * n)
+        K2[:n] = 1.0 if k is None else k
+        O.async_round(og, k, lam, C, K2, F, parallel=True, threads=threads)
+    else:
+        K = np.ones(n) if k is None else k
+        O.sync_round(og, k, lam, C, K, F, threads=threads)
+    return time.perf_counter() - t0
+
+
+def host_oracle_graph(wl):
+    from oracle import oracle as O
+    ip, ix, w = wl.dg.to_host()
+    return O.Graph(wl.dg.n, ip, ix, w, wl.dg.total_weight), (None if wl.k is None else wl.k.cpu().numpy())
+
+
+def run_cpu_baseline(og, k, lam, schedule, stride, seconds, warmup=1, max_reps=50):
+    """Oracle port of the reference's round (OpenMP; async = relaxed atomics
+    like the reference's numba + _atomics.py design), all host threads."""
+    F, edges = cpu_sample(og.indptr, stride)
     threads = os.cpu_count() or 1
-    n = g.n
     times = []
     for r in range(warmup + max_reps):
-        C = np.arange(n, dtype=np.int32)
-        K2 = np.zeros(2 * n); K2[:n] = 1.0
-        t0 = time.perf_counter()
-        O.async_round(g, None, lam, C, K2, F, parallel=True, threads=threads)
-        dt = time.perf_counter() - t0
+        dt = cpu_round(og, k, lam, schedule, F, threads)
         if r >= warmup:
             times.append(dt)
         if sum(times) >= seconds:
             break
     t = statistics.median(times)
+    kind = "async (OpenMP relaxed atomics)" if schedule == "async" else "sync Jacobi (OpenMP)"
     return {"value": edges / t / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"async best-move round (OpenMP relaxed atomics, oracle/lcc_oracle.c) over every "
-                      f"{stride}th vertex of the graph ({F.size} vertices, {edges} directed edges), "
-                      f"singleton start, median of {len(times)} reps",
+            "sample": f"{kind} best-move round of oracle/lcc_oracle.c over every {stride}th vertex "
+                      f"({F.size} vertices, {edges} directed edges), singleton start, median of {len(times)} reps",
             "seconds": sum(times)}, t
 
 
@@ -177,16 +195,64 @@ def build_graph_device(scale, ef, seed):
     return rmat_device(scale=scale, edge_factor=ef, a=0.57, b=0.19, c=0.19, seed=seed)
 
 
-def config_dict(args, g, extra=None):
-    d = {"workload": f"rmat-s{args.scale}-ef{args.edge_factor} (BASELINE.json configs[3]: R-MAT scale 24, "
-                     f"edge factor 16, a=0.57 b=c=0.19, symmetrised/deduped, unweighted)",
-         "n": g["n"], "m": g["m"], "objective": "cc", "lambda": args.lam, "schedule": args.schedule,
+class Workload:
+    """One BASELINE.json config: device graph, objective parameters, options."""
+
+    def __init__(self, args):
+        import torch
+        import paper_2108_01731_b200 as L
+        from paper_2108_01731_b200 import gen
+        cfg = args.config
+        self.k = None
+        self.weighted = False
+        if cfg == "cfg4":
+            self.dg = build_graph_device(args.scale, args.edge_factor, args.seed)
+            lam, sched = 0.85, "async"
+            self.desc = (f"rmat-s{args.scale}-ef{args.edge_factor} (BASELINE.json configs[3]: R-MAT scale 24, "
+                         f"edge factor 16, a=0.57 b=c=0.19, symmetrised/deduped, unweighted; CC lambda=0.85, "
+                         f"async + vertex neighbours + refine)")
+        elif cfg == "cfg1":
+            hg, _ = gen.sbm(seed=1)
+            self.dg = L.DeviceGraph.from_graph(hg)
+            lam, sched = 0.85, "sync"
+            self.desc = ("sbm-10k (BASELINE.json configs[0]: planted partition n=10,000, 100 communities, "
+                         "p_in=0.05, p_out=0.0005; CC lambda=0.85, sync, one level + contraction)")
+        elif cfg == "cfg2":
+            hg, _ = gen.lfr_like(n=1_200_000, seed=2)
+            self.dg = L.DeviceGraph.from_graph(hg)
+            p = L.modularity_params(self.dg, 1.0)
+            self.k, lam, sched = p.k, p.lam, "async"
+            self.desc = ("lfr-1.2M (BASELINE.json configs[1]: power-law degrees exp 2.5 mean 6, communities "
+                         "exp 1.5, mu=0.3; modularity gamma=1 -> k=deg, lambda=1/2m; async, multi-level)")
+        elif cfg == "cfg3":
+            hg, _ = gen.knn_mixture(seed=3)
+            self.dg = L.DeviceGraph.from_graph(hg)
+            lam, sched = 0.1, "sync"
+            self.weighted = True
+            self.desc = ("knn-4M (BASELINE.json configs[2]: 4M points, 64-d Gaussian mixture of 10,000 "
+                         "components, k=10 cosine, symmetrised, fp32 weights; CC lambda=0.1 (sweep middle), sync)")
+        else:
+            self.dg = gen.powerlaw_communities_device(seed=5)
+            lam, sched = 0.85, "async"
+            self.desc = ("plc-65M (BASELINE.json configs[4]: 65M vertices, ~1.8B edges, degree exp 2.2 capped "
+                         "at 5,214, mu=0.4, planted communities; CC lambda=0.85, async, multi-level)")
+        self.lam = args.lam if args.lam is not None else lam
+        self.schedule = args.schedule or sched
+        self.cfg = cfg
+        torch.cuda.synchronize()
+
+
+def config_dict(args, g, wl=None, extra=None):
+    d = {"workload": wl.desc if wl is not None else args.config,
+         "n": g["n"], "m": g["m"], "lambda": wl.lam if wl is not None else args.lam,
+         "schedule": wl.schedule if wl is not None else args.schedule,
          "frontier": "vertex-neighbors", "refine": True, "num_iter": 10,
          "async_chunks": args.async_chunks, "degree_threshold": args.degree_threshold,
          "step": "one best-move iteration over V'=V from singletons: lcc_best_moves_round + lcc_apply_moves + "
                  "lcc_compute_frontier (partition, kernels, reconcile, next active set)",
-         "l2": "inputs larger than L2 (CSR indices %.2f GB vs 126 MB L2); no flush" % (4 * 2 * g["m"] / 1e9),
-         "parallelism": "replicas" if g.get("ws", 1) > 1 else "single-gpu"}
+         "l2": "inputs larger than L2 (CSR indices %.2f GB vs 126 MB L2); no flush" % (4 * 2 * g["m"] / 1e9)
+               if 8 * g["m"] > 126e6 else "inputs smaller than L2 (launch/L2 bound config)",
+         "parallelism": "single-gpu"}
     if extra:
         d.update(extra)
     return d
@@ -199,43 +265,28 @@ def run_reference(args):
         return 0
     import torch
     if torch.cuda.is_available():
-        # input preparation only (the timed region below is CPU-only)
         torch.cuda.set_device(lrank)
-        dg = build_graph_device(args.scale, args.edge_factor, args.seed)
-        indptr, indices, _ = dg.to_host()
-        del dg
-        torch.cuda.empty_cache()
-    else:
-        from paper_2108_01731_b200.gen import csr_from_pairs, rmat_pairs_host
-        u, v = rmat_pairs_host(args.scale, args.edge_factor << args.scale, 0.57, 0.19, 0.19, args.seed)
-        hg = csr_from_pairs(1 << args.scale, u, v)
-        indptr, indices = hg.indptr, hg.indices
-    g = {"n": indptr.size - 1, "m": indices.size // 2}
-    from oracle import oracle as O
-    og = O.Graph(g["n"], indptr, indices, None, float(g["m"]))
-    F, edges = cpu_sample(indptr, args.cpu_sample_stride)
+    # input preparation may use the GPU generators; the timed region is CPU only
+    wl = Workload(args)
+    og, k = host_oracle_graph(wl)
+    del wl.dg
+    torch.cuda.empty_cache()
+    g = {"n": og.n, "m": og.m}
+    F, edges = cpu_sample(og.indptr, args.cpu_sample_stride)
     threads = os.cpu_count() or 1
-    n = g["n"]
-
-    def step():
-        C = np.arange(n, dtype=np.int32)
-        K2 = np.zeros(2 * n); K2[:n] = 1.0
-        t0 = time.perf_counter()
-        O.async_round(og, None, args.lam, C, K2, F, parallel=True, threads=threads)
-        return time.perf_counter() - t0
-
     for _ in range(args.warmup):
-        step()
-    ts = [step() for _ in range(args.steps)]
+        cpu_round(og, k, wl.lam, wl.schedule, F, threads)
+    ts = [cpu_round(og, k, wl.lam, wl.schedule, F, threads) for _ in range(args.steps)]
     t = sum(ts) / len(ts)
     val = edges / t / 1e9
+    kind = "async (OpenMP relaxed atomics)" if wl.schedule == "async" else "sync Jacobi (OpenMP)"
     cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"async best-move round (OpenMP relaxed atomics, oracle/lcc_oracle.c) over every "
-                     f"{args.cpu_sample_stride}th vertex ({F.size} vertices, {edges} directed edges), singleton start"}
+           "sample": f"{kind} best-move round of oracle/lcc_oracle.c over every {args.cpu_sample_stride}th vertex "
+                     f"({F.size} vertices, {edges} directed edges), singleton start"}
     out = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT)", "impl": "reference",
-           "config": config_dict(args, g), "cpu_baseline": cpu,
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)", "impl": "reference",
+           "config": config_dict(args, g, wl), "cpu_baseline": cpu,
            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -252,14 +303,15 @@ def run_ours(args):
     torch.cuda.set_device(lrank)
     dist = None  # single GPU; N > 1 goes through run_sharded
     lib = _lib.load()
-    dg = build_graph_device(args.scale, args.edge_factor, args.seed)
+    wl = Workload(args)
+    dg = wl.dg
     n, nnz = dg.n, dg.nnz
     g = {"n": n, "m": nnz // 2, "ws": ws}
-    p = L.ClusteringParams(args.lam)
-    opts = L.ParOptions(schedule=args.schedule, num_iter=1, degree_threshold=args.degree_threshold,
-                        async_chunks=args.async_chunks)
+    p = L.ClusteringParams.__new__(L.ClusteringParams)
+    p.lam, p.k = float(wl.lam), wl.k
     gs, ps = dg.c_struct(), p.c_struct()
-    sched = 1 if args.schedule == "async" else 0
+    sched = 1 if wl.schedule == "async" else 0
+    kfill = wl.k if wl.k is not None else None
     C = torch.empty(n, dtype=torch.int32, device="cuda")
     D = torch.empty(n, dtype=torch.int32, device="cuda")
     K2 = torch.empty(2 * n, dtype=torch.float64, device="cuda")
@@ -274,14 +326,18 @@ def run_ours(args):
         # one Alg. 1 iteration from singletons: best moves over V' = V, the
         # mass/label reconcile, and the next active set (vertex neighbours)
         C.copy_(iota)
-        K2[:n].fill_(1.0)
+        if kfill is None:
+            K2[:n].fill_(1.0)
+        else:
+            K2[:n].copy_(kfill)
         K2[n:].zero_()
         sp = stream_ptr()
         _lib.check(lib.lcc_best_moves_round(ctypes.byref(gs), ctypes.byref(ps), C.data_ptr(), K2.data_ptr(), None, n,
                                             sched, args.degree_threshold, args.async_chunks, D.data_ptr(),
                                             moved.data_ptr(), ctypes.byref(cnt), ctypes.byref(st), sp))
         labels = C if sched == 1 else D
-        _lib.check(lib.lcc_apply_moves(n, labels.data_ptr(), 2 * n, None, Cn.data_ptr(), Kn.data_ptr(), sp))
+        _lib.check(lib.lcc_apply_moves(n, labels.data_ptr(), 2 * n, None if kfill is None else kfill.data_ptr(),
+                                       Cn.data_ptr(), Kn.data_ptr(), sp))
         _lib.check(lib.lcc_compute_frontier(ctypes.byref(gs), 1, moved.data_ptr(), iota.data_ptr(), Cn.data_ptr(),
                                             F.data_ptr(), ctypes.byref(nF), sp))
 
@@ -314,8 +370,8 @@ def run_ours(args):
 
     # roofline of the dominant kernel group (the best-move kernels)
     peak, peak_kind = peaks()
-    B_vertex = 8 + 4 + 8 + 4 + 1          # indptr (dense), C[v], K[C[v]], D/C write, moved
-    B_edge = 4 + 4                         # indices + label gather
+    B_vertex = 8 + 4 + 8 + 4 + 1 + (8 if wl.k is not None else 0)  # indptr, C[v], K[C[v]], D/C, moved (+k_v)
+    B_edge = 4 + 4 + (4 if wl.weighted else 0)                      # indices + label gather (+fp32 weight)
     B_distinct = 8                         # K gather per distinct cluster (= deg at singleton start)
     alg_bytes = n * B_vertex + nnz * B_edge + nnz * B_distinct
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
@@ -329,17 +385,26 @@ def run_ours(args):
     if not args.no_e2e:
         indptr_h = dg.indptr.cpu().pin_memory()
         indices_h = dg.indices.cpu().pin_memory()
+        weights_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
 
         class HostG:
             pass
         hgr = HostG()
-        hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = n, nnz // 2, indptr_h, indices_h, None, float(nnz // 2)
-        full = L.ParOptions(schedule=args.schedule, degree_threshold=args.degree_threshold,
+        hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = (
+            n, nnz // 2, indptr_h, indices_h, weights_h, dg.total_weight)
+        full = L.ParOptions(schedule=wl.schedule, degree_threshold=args.degree_threshold,
                             async_chunks=args.async_chunks)
         out_h = torch.empty(n, dtype=torch.int32).pin_memory()
 
         def e2e_step():
-            cl = L.parallel_cc(hgr, p, full)
+            if wl.cfg == "cfg1":
+                # configs[0]: single level plus contraction (par_best_moves + par_compress)
+                cl, _ = L.par_best_moves(hgr, p, None, full)
+                lvl = L.par_compress(dg, p, cl)
+                cl.meta["stats"].levels = 1
+                cl.meta["coarse_n"] = lvl.graph.n
+            else:
+                cl = L.parallel_cc(hgr, p, full)
             out_h.copy_(cl.assignment, non_blocking=True)
             torch.cuda.synchronize()
             return cl
@@ -361,25 +426,27 @@ def run_ours(args):
             dist.all_reduce(ed_t, op=dist.ReduceOp.SUM)
         obj = L.cc_objective(dg, p, torch.as_tensor(out_h).cuda())
         e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4),
+               "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
+                                         (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
                "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()),
                "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
                "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
                "device_ms_best_move_kernels": stats.ms_kernels,
                "objective": obj, "clusters": int(np.unique(out_h.numpy()).size),
-               "api": "paper_2108_01731_b200.parallel_cc(host pinned CSR) + labels D2H"}
+               "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
+                       "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
 
     cpu = None
     if not args.no_cpu and rank == 0:
-        ih, xh = dg.indptr.cpu().numpy(), dg.indices.cpu().numpy()
-        cpu, _ = run_cpu_baseline(ih, xh, args.lam, args.cpu_sample_stride, args.cpu_seconds)
+        og, kh = host_oracle_graph(wl)
+        cpu, _ = run_cpu_baseline(og, kh, wl.lam, wl.schedule, args.cpu_sample_stride, args.cpu_seconds)
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (seeded R-MAT generated on device; random-free deterministic stream)",
-               "config": config_dict(args, g), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "data": "synthetic (seeded; BASELINE.json shapes, see config.workload)",
+               "config": config_dict(args, g, wl), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(launches), "clocks": clk.summary(),
                "round_stats": {"vertices": st.vertices // args.steps, "edges": st.edges_scanned // args.steps,
                                "moves": st.moves // args.steps, "next_frontier": int(nF.value)}}
@@ -409,14 +476,16 @@ def run_sharded(args):
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     part = make_part(dg.indptr, dg.indices, None, float(nnz // 2), lo, hi, torch.device("cuda", lrank))
     be = CudaBackend()
-    opts1 = L.ParOptions(schedule=args.schedule, num_iter=1, degree_threshold=args.degree_threshold,
+    lam = 0.85 if args.lam is None else args.lam
+    sched = args.schedule or "async"
+    opts1 = L.ParOptions(schedule=sched, num_iter=1, degree_threshold=args.degree_threshold,
                          async_chunks=args.async_chunks)
     iota = torch.arange(n, dtype=torch.int32, device="cuda")
 
     def step(st):
         C = iota.clone()
         K = torch.ones(n, dtype=torch.float64, device="cuda")
-        sharded_best_moves(part, None, args.lam, C, K, opts1, be, None, st)
+        sharded_best_moves(part, None, lam, C, K, opts1, be, None, st)
 
     for _ in range(args.warmup):
         step(ShardStats())
@@ -444,21 +513,21 @@ def run_sharded(args):
     if not args.no_e2e:
         ip_h = torch.from_numpy(indptr_h).pin_memory()
         ix_h = dg.indices.cpu().pin_memory()
-        full = L.ParOptions(schedule=args.schedule, degree_threshold=args.degree_threshold,
+        full = L.ParOptions(schedule=sched, degree_threshold=args.degree_threshold,
                             async_chunks=args.async_chunks)
-        sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, args.lam, full, be)  # warm-up
+        sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, lam, full, be)  # warm-up
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st2 = ShardStats()
-        C = sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, args.lam, full, be, None, st2)
+        C = sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, lam, full, be, None, st2)
         out_h = C.cpu()
         torch.cuda.synchronize()
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ed2 = torch.tensor([float(st2.edges_scanned)], dtype=torch.float64, device="cuda")
         dist.all_reduce(ed2, op=dist.ReduceOp.SUM)
-        obj = L.cc_objective(dg, L.ClusteringParams(args.lam), C)
+        obj = L.cc_objective(dg, L.ClusteringParams(lam), C)
         h2d = int((bounds[rank + 1] - bounds[rank]) * 8 + (indptr_h[hi] - indptr_h[lo]) * 4)
         e2e = {"value": float(ed2.item()) / float(te.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": int(n * 4),
@@ -469,8 +538,10 @@ def run_sharded(args):
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded R-MAT generated on device, identical on every rank)",
-               "config": config_dict(args, {"n": n, "m": nnz // 2, "ws": ws},
-                                     {"parallelism": f"vertex-sharded x{ws} (NCCL MAX all-reduce of labels/flags)"}),
+               "config": config_dict(args, {"n": n, "m": nnz // 2, "ws": ws}, None,
+                                     {"workload": f"rmat-s{args.scale}-ef{args.edge_factor} (BASELINE.json configs[3])",
+                                      "lambda": lam, "schedule": sched,
+                                      "parallelism": f"vertex-sharded x{ws} (NCCL MAX all-reduce of labels/flags)"}),
                "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)

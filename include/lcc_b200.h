@@ -173,6 +173,18 @@ lcc_status lcc_gen_rmat(int32_t scale, int64_t samples, double a, double b,
                         double c, uint64_t seed, int64_t* indptr,
                         int32_t* indices, int64_t* nnz, void* stream);
 
+/* Power-law planted communities (config 5 stand-in): `samples` Chung-Lu draws,
+ * intra-community with probability 1-mu (community by weight, endpoints by
+ * weight inside it; communities are contiguous id ranges cstart[0..nc]),
+ * otherwise endpoints by weight over all vertices.  vw_prefix[n+1] and
+ * cw_prefix[nc+1] are exclusive prefix sums of the vertex / community
+ * weights (device).  Deduplicated, symmetrised CSR as lcc_gen_rmat.         */
+lcc_status lcc_gen_powerlaw_communities(int64_t n, int64_t samples, double mu,
+                                        const double* vw_prefix, const int64_t* cstart,
+                                        const double* cw_prefix, int64_t n_communities,
+                                        uint64_t seed, int64_t* indptr, int32_t* indices,
+                                        int64_t* nnz, void* stream);
+
 /* Build symmetric CSR from undirected pairs (u[i], v[i]) on the device:
  * self-loops dropped, duplicate unordered pairs merged (unweighted graphs,
  * so merged edges keep w = 1), both directions emitted, rows sorted.

@@ -21,7 +21,8 @@ FRONTIER_ALL, FRONTIER_VERTEX_NBRS, FRONTIER_CLUSTER_NBRS = 0, 1, 2
 EXPORTS = (
     "lcc_abi_version", "lcc_last_error", "lcc_kernel_launches", "lcc_best_moves_round", "lcc_apply_moves",
     "lcc_compute_frontier", "lcc_par_best_moves", "lcc_par_compress", "lcc_par_flatten",
-    "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_build_csr_from_pairs",
+    "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_gen_powerlaw_communities",
+    "lcc_build_csr_from_pairs",
 )
 
 
@@ -88,6 +89,7 @@ def load() -> ctypes.CDLL:
         "lcc_cc_objective": (ctypes.c_int, [G, PR, P, pF64, P]),
         "lcc_parallel_cc": (ctypes.c_int, [G, PR, O, P, ST, P]),
         "lcc_gen_rmat": (ctypes.c_int, [I32, I64, F64, F64, F64, ctypes.c_uint64, P, P, pI64, P]),
+        "lcc_gen_powerlaw_communities": (ctypes.c_int, [I64, I64, F64, P, P, P, I64, ctypes.c_uint64, P, P, pI64, P]),
         "lcc_build_csr_from_pairs": (ctypes.c_int, [I64, I64, P, P, P, P, pI64, P]),
     }
     for name, (res, args) in sig.items():

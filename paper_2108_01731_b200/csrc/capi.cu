@@ -203,6 +203,18 @@ lcc_status lcc_gen_rmat(int32_t scale, int64_t samples, double a, double b, doub
     });
 }
 
+lcc_status lcc_gen_powerlaw_communities(int64_t n, int64_t samples, double mu, const double* vw_prefix,
+                                        const int64_t* cstart, const double* cw_prefix, int64_t n_communities,
+                                        uint64_t seed, int64_t* indptr, int32_t* indices, int64_t* nnz,
+                                        void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(vw_prefix && cstart && cw_prefix && indptr && (samples == 0 || indices), "NULL buffer");
+        const int64_t r = lcc::gen_powerlaw_communities(n, samples, mu, vw_prefix, cstart, cw_prefix, n_communities,
+                                                        seed, indptr, indices, S(stream));
+        if (nnz) *nnz = r;
+    });
+}
+
 lcc_status lcc_build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u, const int32_t* v, int64_t* indptr,
                                     int32_t* indices, int64_t* nnz, void* stream) {
     return guard([&] {

@@ -83,11 +83,6 @@ __global__ void k_emit_rows(const uint64_t* __restrict__ ukeys, int64_t R, int b
     }
 }
 
-__global__ void k_counts_to_w(const int32_t* __restrict__ cnt, int64_t R, double* cw) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x)
-        cw[i] = (double)cnt[i];
-}
-
 struct Sq {
     __device__ __forceinline__ double operator()(double x) const { return x * x; }
 };
@@ -135,29 +130,25 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         // 3. stable radix sort on the 2*bits live bits
         if (WLoad<WT>::weighted) sort_pairs(keys.get(), keys2.get(), vals.get(), vals2.get(), nnz, 2 * bits, s);
         else sort_keys(keys.get(), keys2.get(), nnz, 2 * bits, s);
-        // 4. run-length reduce (keys reuse `keys` as unique output)
+        // 4. reduce by key (keys reuse `keys` as unique output); unweighted
+        //    entries sum a constant 1.0 -- integer-valued, exact below 2^53;
+        //    64-bit item counts (2m > 2^31 at config 5)
         Buf<int64_t> druns(1, s);
-        if (WLoad<WT>::weighted) {
+        {
             size_t bytes = 0;
-            LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, keys2.get(), keys.get(), vals2.get(), vals.get(),
-                                                    druns.get(), cub::Sum(), nnz, s));
-            Buf<unsigned char> tmp(bytes, s);
-            LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, keys2.get(), keys.get(), vals2.get(), vals.get(),
-                                                    druns.get(), cub::Sum(), nnz, s));
-        } else {
-            Buf<int32_t> counts(nnz, s);
-            size_t bytes = 0;
-            LCC_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, keys2.get(), keys.get(), counts.get(),
-                                                        druns.get(), nnz, s));
-            Buf<unsigned char> tmp(bytes, s);
-            LCC_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), bytes, keys2.get(), keys.get(), counts.get(),
-                                                        druns.get(), nnz, s));
-            int64_t runs = 0;
-            LCC_CUDA(cudaMemcpyAsync(&runs, druns.get(), sizeof(runs), cudaMemcpyDeviceToHost, s));
-            LCC_CUDA(cudaStreamSynchronize(s));
-            if (runs > 0) {
-                k_counts_to_w<<<grid_for(runs, 256), 256, 0, s>>>(counts.get(), runs, cw);
-                LCC_LAUNCH_CHECK();
+            if (WLoad<WT>::weighted) {
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, keys2.get(), keys.get(), vals2.get(), cw,
+                                                        druns.get(), cub::Sum(), nnz, s));
+                Buf<unsigned char> tmp(bytes, s);
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, keys2.get(), keys.get(), vals2.get(), cw,
+                                                        druns.get(), cub::Sum(), nnz, s));
+            } else {
+                cub::ConstantInputIterator<double> ones(1.0);
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, keys2.get(), keys.get(), ones, cw,
+                                                        druns.get(), cub::Sum(), nnz, s));
+                Buf<unsigned char> tmp(bytes, s);
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, keys2.get(), keys.get(), ones, cw,
+                                                        druns.get(), cub::Sum(), nnz, s));
             }
         }
         int64_t runs = 0;
@@ -166,9 +157,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         LCC_CUDA(cudaMemcpyAsync(&hintra, dintra.get(), sizeof(hintra), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaMemcpyAsync(&intra_w, dacc.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaStreamSynchronize(s));
-        R = runs - (hintra > 0 ? 1 : 0);
-        if (WLoad<WT>::weighted && R > 0)
-            LCC_CUDA(cudaMemcpyAsync(cw, vals.get(), sizeof(double) * R, cudaMemcpyDeviceToDevice, s));
+        R = runs - (hintra > 0 ? 1 : 0);  // the all-ones sentinel run (intra entries) sorts last
         if (!WLoad<WT>::weighted) intra_w = (double)hintra;
         k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(keys.get(), R, bits, cn, cindptr, cindices);
         LCC_LAUNCH_CHECK();

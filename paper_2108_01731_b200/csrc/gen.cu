@@ -69,7 +69,59 @@ __global__ void k_rmat(int scale, int64_t samples, double t1, double t2, double 
     }
 }
 
+// Power-law planted communities (config 5): Chung-Lu draws, intra-community
+// with probability 1-mu (community chosen by weight, endpoints by weight inside
+// it), else endpoints by weight over the whole graph.  Vertices of a
+// community are contiguous ids; vw_prefix is the inclusive-exclusive prefix of
+// the vertex weights (vw_prefix[0] = 0), cw_prefix the same per community.
+__device__ __forceinline__ double u01(uint64_t seed, uint64_t ctr) {
+    return (double)(splitmix64(seed + 0x9E3779B97F4A7C15ULL * ctr) >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ int64_t prefix_search(const double* __restrict__ p, int64_t lo, int64_t hi, double x) {
+    // largest i in [lo, hi) with p[i] <= x
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (p[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+__global__ void k_plc(int64_t samples, double mu, const double* __restrict__ vw, int64_t n,
+                      const int64_t* __restrict__ cstart, const double* __restrict__ cw, int64_t nc, uint64_t seed,
+                      int32_t* u, int32_t* v) {
+    const double W = vw[n];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < samples; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t base = (uint64_t)i * 4ULL + 1ULL;
+        int64_t a, b;
+        if (u01(seed, base) >= mu) {
+            const int64_t c = prefix_search(cw, 0, nc, u01(seed, base + 1) * cw[nc]);
+            const int64_t s = cstart[c], e = cstart[c + 1];
+            const double w0 = vw[s], ws = vw[e] - vw[s];
+            a = prefix_search(vw, s, e, w0 + u01(seed, base + 2) * ws);
+            b = prefix_search(vw, s, e, w0 + u01(seed, base + 3) * ws);
+        } else {
+            a = prefix_search(vw, 0, n, u01(seed, base + 2) * W);
+            b = prefix_search(vw, 0, n, u01(seed, base + 3) * W);
+        }
+        u[i] = (int32_t)a;
+        v[i] = (int32_t)b;
+    }
+}
+
 }  // namespace
+
+int64_t gen_powerlaw_communities(int64_t n, int64_t samples, double mu, const double* vw_prefix,
+                                 const int64_t* cstart, const double* cw_prefix, int64_t nc, uint64_t seed,
+                                 int64_t* indptr, int32_t* indices, cudaStream_t s) {
+    LCC_REQUIRE(n > 0 && n < (1LL << 31), "vertex count out of range");
+    LCC_REQUIRE(nc > 0 && samples >= 0 && mu >= 0.0 && mu <= 1.0, "bad generator parameters");
+    Buf<int32_t> u(std::max<int64_t>(samples, 1), s), v(std::max<int64_t>(samples, 1), s);
+    if (samples > 0) {
+        k_plc<<<grid_for(samples, 256, 16), 256, 0, s>>>(samples, mu, vw_prefix, n, cstart, cw_prefix, nc, seed,
+                                                         u.get(), v.get());
+        LCC_LAUNCH_CHECK();
+    }
+    return build_csr_from_pairs(n, samples, u.get(), v.get(), indptr, indices, s);
+}
 
 int64_t build_csr_from_pairs(int64_t n, int64_t np, const int32_t* u, const int32_t* v, int64_t* indptr,
                              int32_t* indices, cudaStream_t s) {
@@ -83,7 +135,7 @@ int64_t build_csr_from_pairs(int64_t n, int64_t np, const int32_t* u, const int3
     Buf<uint64_t> k1(np, s), k2(np, s);
     k_pair_keys<<<grid_for(np, 256), 256, 0, s>>>(u, v, np, bits, k1.get());
     LCC_LAUNCH_CHECK();
-    sort_keys(k1.get(), k2.get(), np, 64, s);
+    sort_keys(k1.get(), k2.get(), np, 2 * bits, s);  // sentinel ~0 keeps the max on these bits too
     Buf<int64_t> dcnt(1, s);
     {
         size_t bytes = 0;

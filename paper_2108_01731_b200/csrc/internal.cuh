@@ -51,6 +51,9 @@ int64_t build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u, const
                              int64_t* indptr, int32_t* indices, cudaStream_t s);
 int64_t gen_rmat(int scale, int64_t samples, double a, double b, double c, uint64_t seed,
                  int64_t* indptr, int32_t* indices, cudaStream_t s);
+int64_t gen_powerlaw_communities(int64_t n, int64_t samples, double mu, const double* vw_prefix,
+                                 const int64_t* cstart, const double* cw_prefix, int64_t nc, uint64_t seed,
+                                 int64_t* indptr, int32_t* indices, cudaStream_t s);
 
 // driver.cu
 struct Options {

@@ -11,18 +11,18 @@ namespace lcc {
 template <class InIt, class OutIt, class Pred>
 inline void select_if(InIt in, OutIt out, int64_t* d_count, int64_t n, Pred pred, cudaStream_t s) {
     size_t bytes = 0;
-    LCC_CUDA(cub::DeviceSelect::If(nullptr, bytes, in, out, d_count, (int)n, pred, s));
+    LCC_CUDA(cub::DeviceSelect::If(nullptr, bytes, in, out, d_count, n, pred, s));
     Buf<unsigned char> tmp(bytes, s);
-    LCC_CUDA(cub::DeviceSelect::If(tmp.get(), bytes, in, out, d_count, (int)n, pred, s));
+    LCC_CUDA(cub::DeviceSelect::If(tmp.get(), bytes, in, out, d_count, n, pred, s));
 }
 
 template <class InIt, class FlagIt, class OutIt>
 inline void select_flagged(InIt in, FlagIt flags, OutIt out, int64_t* d_count, int64_t n,
                            cudaStream_t s) {
     size_t bytes = 0;
-    LCC_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, in, flags, out, d_count, (int)n, s));
+    LCC_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, in, flags, out, d_count, n, s));
     Buf<unsigned char> tmp(bytes, s);
-    LCC_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, in, flags, out, d_count, (int)n, s));
+    LCC_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, in, flags, out, d_count, n, s));
 }
 
 template <class InIt, class OutIt>

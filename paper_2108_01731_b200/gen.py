@@ -286,3 +286,61 @@ def knn_mixture(n: int = 4_000_000, dim: int = 64, components: int = 10_000, k: 
     np.cumsum(np.bincount(src, minlength=n), out=indptr[1:])
     m = int(lo.size)
     return HostGraph(n, m, indptr, dst.astype(np.int32), ww, float(w.astype(np.float64).sum())), comp.numpy()
+
+
+# ---------------------------------------------------------------------------
+# config 5: large power-law planted-community graph (BASELINE.json configs[4])
+# ---------------------------------------------------------------------------
+
+def powerlaw_communities_device(n: int = 65_000_000, m_target: int = 1_800_000_000, deg_exponent: float = 2.2,
+                                mu: float = 0.4, max_degree: int = 5214, comm_exponent: float = 1.5,
+                                min_comm: int = 20, max_comm: int = 5000, seed: int = 5,
+                                oversample: float = 1.02) -> DeviceGraph:
+    """Seeded stand-in for friendster (65.6M vertices, 1.8B
+    edges; max degree 5,214 per PAPER.md:594).  Expected degrees follow a
+    power law (exponent 2.2) capped at max_degree and scaled to mean
+    2*m_target/n; community sizes follow a power law (exponent 1.5) on
+    [min_comm, max_comm], contiguous ids; Chung-Lu draws (lcc_gen_powerlaw_
+    communities) with mixing mu, then deduplicated and symmetrised on the
+    device.  Host numpy builds the weight prefixes only."""
+    dev = _device()
+    rng = np.random.Generator(np.random.PCG64(seed))
+    a = 1.0 - deg_exponent
+    u = rng.random(n)
+    theta = (1.0 + u * (float(max_degree) ** a - 1.0)) ** (1.0 / a)   # power law on [1, max_degree]
+    theta *= (2.0 * m_target / n) / theta.mean()
+    sizes = []
+    tot = 0
+    while tot < n:
+        k = max(1, (n - tot) // 200)
+        ua = rng.random(k)
+        b = 1.0 - comm_exponent
+        s = np.floor((min_comm ** b + ua * ((max_comm + 1) ** b - min_comm ** b)) ** (1.0 / b)).astype(np.int64)
+        s = s[np.cumsum(s) <= n - tot] if s.sum() > n - tot else s
+        if s.size == 0:
+            s = np.array([n - tot], np.int64)
+        sizes.append(s)
+        tot += int(s.sum())
+    sizes = np.concatenate(sizes)
+    cstart = np.zeros(sizes.size + 1, np.int64)
+    np.cumsum(sizes, out=cstart[1:])
+    vw = np.zeros(n + 1, np.float64)
+    np.cumsum(theta, out=vw[1:])
+    cwp = vw[cstart]
+    cw = cwp - cwp[0]
+    samples = int(m_target * oversample)
+    d_vw = torch.from_numpy(vw).to(dev)
+    d_cs = torch.from_numpy(cstart).to(dev)
+    d_cw = torch.from_numpy(cw).to(dev)
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(2 * samples, dtype=torch.int32, device=dev)
+    nnz = ctypes.c_int64()
+    _lib.check(_lib.load().lcc_gen_powerlaw_communities(n, samples, mu, d_vw.data_ptr(), d_cs.data_ptr(),
+                                                        d_cw.data_ptr(), sizes.size, seed, indptr.data_ptr(),
+                                                        indices.data_ptr(), ctypes.byref(nnz), stream_ptr()))
+    del d_vw, d_cs, d_cw
+    nnz = nnz.value
+    out = indices[:nnz].clone()
+    del indices
+    torch.cuda.empty_cache()
+    return DeviceGraph(n, nnz // 2, indptr, out, None, float(nnz // 2))

@@ -1318,7 +1318,11 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     float kms = 0.f;
 
     int P = 1;
-    if (ASYNC) P = chunks > 0 ? chunks : (int)std::min<int64_t>(64, std::max<int64_t>(1, ((1LL << 22) + nF - 1) / std::max<int64_t>(nF, 1)));
+    if (ASYNC && chunks > 0) P = chunks;
+    else if (ASYNC) {  // ~4M / F sub-rounds, each >= 1024 vertices, at most 64
+        const int64_t f = std::max<int64_t>(nF, 1);
+        P = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(64, ((1LL << 22) + f - 1) / f), f / 1024));
+    }
     WindowPlan wp;
     if (hc[1] > 0) plan_windows(g.indptr, lists.get() + binstart[1], (int64_t)hc[1], wp, s);
     const int64_t nL = (int64_t)hc[NBINS - 1];

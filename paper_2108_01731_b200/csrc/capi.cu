@@ -19,24 +19,34 @@ thread_local std::string g_err;
 // Keep freed scratch in the device's stream-ordered pool: the default release
 // threshold (0) hands memory back to the driver at every synchronisation, so
 // each best-move iteration would pay for fresh cudaMalloc/cudaFree of its
-// O(n) scratch.
-void init_pool_once() {
+// O(n) scratch.  Up to POOL_KEEP bytes stay cached; anything above (the
+// one-off peaks of graph generation and contraction) is trimmed when the
+// call returns so it can be used by the caller's allocator (e.g. PyTorch).
+constexpr uint64_t POOL_KEEP = 16ull << 30;
+
+cudaMemPool_t pool_once() {
     static bool done[64] = {false};
+    static cudaMemPool_t pools[64];
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!done[dev]) {
+        if (cudaDeviceGetDefaultMemPool(&pools[dev], dev) == cudaSuccess) {
+            uint64_t thr = POOL_KEEP;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            pools[dev] = nullptr;
+        }
+        done[dev] = true;
     }
-    done[dev] = true;
+    return pools[dev];
 }
 
 template <class F>
 lcc_status guard(F&& f) {
     try {
-        init_pool_once();
+        cudaMemPool_t pool = pool_once();
         f();
+        if (pool) cudaMemPoolTrimTo(pool, POOL_KEEP);
         g_err.clear();
         return LCC_OK;
     } catch (const lcc::Invalid& e) {

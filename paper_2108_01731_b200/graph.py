@@ -69,6 +69,11 @@ class DeviceGraph:
         nnz = indices.numel()
         w = getattr(g, "weights", None)
         wt = None
+        if isinstance(w, torch.Tensor) and w.dtype == torch.float32 and nnz:
+            if w.numel() != nnz:
+                raise GraphError("weights must have one entry per CSR index")
+            wt = w.to(dev).contiguous()          # already the compact layout
+            w = None
         if w is not None and nnz:
             wh = w.detach().cpu().numpy() if isinstance(w, torch.Tensor) else np.asarray(w)
             wh = np.asarray(wh, dtype=np.float64)

@@ -1319,9 +1319,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     int P = 1;
     if (ASYNC && chunks > 0) P = chunks;
-    else if (ASYNC) {  // ~4M / F sub-rounds, each >= 1024 vertices, at most 64
+    else if (ASYNC) {  // ~4M / F sub-rounds, at most 64 (small graphs need the ordering:
+                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative)
         const int64_t f = std::max<int64_t>(nF, 1);
-        P = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(64, ((1LL << 22) + f - 1) / f), f / 1024));
+        P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
     }
     WindowPlan wp;
     if (hc[1] > 0) plan_windows(g.indptr, lists.get() + binstart[1], (int64_t)hc[1], wp, s);

@@ -204,7 +204,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const unsigned grp = __match_any_sync(FULL, key);
             double S;
             if constexpr (!WLoad<WT>::weighted) {
-                S = (double)__popc(grp);
+                S = u32_to_f64(__popc(grp));
             } else {
                 S = 0.0;
 #pragma unroll
@@ -318,7 +318,7 @@ struct SmemTable<false> {
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cq) : "r"(cnts + 4 * q));
         clear(q);
         x = kq;
-        S = (double)cq;
+        S = u32_to_f64(cq);
         return true;
     }
 };
@@ -413,7 +413,7 @@ struct GlobalTable<false> {
         const unsigned long long w = tab[q];
         if (w == EMPTY64) return false;
         x = (int32_t)(w >> 32);
-        S = (double)(uint32_t)w;
+        S = u32_to_f64((uint32_t)w);
         return true;
     }
 };
@@ -703,7 +703,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
         }
         __syncthreads();
         if (tid < nv) {
-            const double sc = WEIGHTED ? s_scw[tid] : (double)s_sc[tid];
+            const double sc = WEIGHTED ? s_scw[tid] : u32_to_f64(s_sc[tid]);
             s_b[tid] = dadd(dsub(sc, dmul(s_t[tid], s_Kc[tid])), dmul(s_t[tid], s_kv[tid]));
         }
         __syncthreads();
@@ -713,7 +713,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             if (key == KEY_EMPTY) continue;
             const int32_t x = (int32_t)(key & ((1u << LABEL_BITS) - 1u));
             const int sj = (int)(key >> LABEL_BITS);
-            const double S = WEIGHTED ? sums[q] : (double)cnts[q];
+            const double S = WEIGHTED ? sums[q] : u32_to_f64(cnts[q]);
             const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC>(a.K, x, pol_keep))), s_b[sj]);
             gval[q] = g;
             atomicMax(&s_hi[sj], (uint32_t)(ord_gain(g) >> 32));

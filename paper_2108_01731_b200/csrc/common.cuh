@@ -100,6 +100,13 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
+// Exact u32 -> fp64 without I2F (the conversion runs on the narrow XU pipe,
+// which ncu showed 56-70% busy in the table kernels): OR the integer into the
+// mantissa of 2^52 and subtract 2^52 (exact for any 32-bit value).
+__device__ __forceinline__ double u32_to_f64(uint32_t x) {
+    return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
+}
+
 // Weight loads: WNone means every edge weighs 1.
 struct WNone { };
 template <class W> struct WLoad;

@@ -1100,10 +1100,10 @@ void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64
     const int var = ev ? atoi(ev) : 0;
     switch (bin) {  //                         GW  CAP    GROUPS U
         case 2: launch_group<WT, ASYNC, 1, 256, 8, 4, 6>(a, list, lo, hi, s); break;   //  ..128      warp
-        case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8>(a, list, lo, hi, s); break;     //  ..512      warp
+        case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8, 3>(a, list, lo, hi, s); break;  //  ..512      warp
         case 4:
             if (var == 3) launch_group<WT, ASYNC, 8, 4096, 1, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 4, 4096, 2, 8>(a, list, lo, hi, s);           //  ..2048     4 warps
+            else launch_group<WT, ASYNC, 4, 4096, 2, 8, 3>(a, list, lo, hi, s);        //  ..2048     4 warps
             break;
         case 5:
             if (var == 1) launch_group<WT, ASYNC, 16, 8192, 1, 8>(a, list, lo, hi, s);

@@ -245,6 +245,26 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 }
 
 // ===========================================================================
+// isolated vertices (deg 0): S = 0 for every cluster, so the only candidate is
+// the fresh singleton (gain -b), taken when v sits in a heavier cluster
+// ===========================================================================
+template <bool ASYNC>
+__global__ void __launch_bounds__(256)
+k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
+    const uint64_t pol_keep = policy_evict_last();
+    unsigned long long my_moves = 0;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(list + i);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const double kv = kval(a.k, v);
+        const double t = dmul(a.lam, kv);
+        const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC>(a.K, c, pol_keep))), dmul(t, kv));
+        my_moves += decide<ASYNC>(a, v, c, kv, b, false, 0.0, 0);
+    }
+    flush_moves(a, my_moves);
+}
+
+// ===========================================================================
 // neighbour-cluster tables.  One atomic per edge: unweighted graphs pack
 // (cluster id, count) into one 64-bit slot, claimed by a 64-bit CAS that
 // already carries count 1, bumped by a 64-bit RED otherwise.  Weighted
@@ -973,7 +993,7 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
 // ===========================================================================
 // degree-bin partition (one pass, block-aggregated reservations)
 // ===========================================================================
-constexpr int NBINS = 8;
+constexpr int NBINS = 9;
 struct BinEdges {
     int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
@@ -1256,9 +1276,9 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
-    // bins: 0 deg<=32 warp windows | 1 optional edge windows | 2-3 warp per
-    //       vertex up to the threshold | 4 ..2048 4 warps | 5 ..4096 8 warps |
-    //       6 ..large_min 8 warps | 7 hubs (L2 tables)
+    // bins: 0 isolated | 1 deg<=32 warp windows | 2 optional edge windows |
+    //       3-4 warp per vertex up to the threshold | 5 ..2048 4 warps |
+    //       6 ..4096 8 warps | 7 ..large_min 32 warps | 8 hubs (L2 tables)
     // LCC_WINDOW=0 / LCC_LARGE_MIN (env): tuning knobs for the bin shapes only
     // measured on B200 (R-MAT s24): per-vertex warp groups beat the window
     // kernel by ~5%, and CTA groups beat the L2 hub path up to 10240
@@ -1273,14 +1293,15 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     int64_t Tw = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
     if (!use_window || 2 * n > (1LL << LABEL_BITS)) Tw = SMALL_MAX + 1;  // window keys need ids < 2^27
     BinEdges be;
-    be.hi[0] = SMALL_MAX;
-    be.hi[1] = Tw - 1;
-    be.hi[2] = std::max<int64_t>(be.hi[1], std::min<int64_t>(128, Tg - 1));
-    be.hi[3] = std::max<int64_t>(be.hi[2], Tg - 1);
-    be.hi[4] = std::min<int64_t>(2048, large_min);
-    be.hi[5] = std::min<int64_t>(4096, large_min);
-    be.hi[6] = std::min<int64_t>(MED_MAX, large_min);
-    be.hi[7] = INT64_MAX;
+    be.hi[0] = 0;                 // isolated vertices: only the fresh-singleton option
+    be.hi[1] = SMALL_MAX;
+    be.hi[2] = Tw - 1;
+    be.hi[3] = std::max<int64_t>(be.hi[2], std::min<int64_t>(128, Tg - 1));
+    be.hi[4] = std::max<int64_t>(be.hi[3], Tg - 1);
+    be.hi[5] = std::min<int64_t>(2048, large_min);
+    be.hi[6] = std::min<int64_t>(4096, large_min);
+    be.hi[7] = std::min<int64_t>(MED_MAX, large_min);
+    be.hi[8] = INT64_MAX;
 
     Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);
     std::vector<int64_t> binstart;
@@ -1325,7 +1346,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
     }
     WindowPlan wp;
-    if (hc[1] > 0) plan_windows(g.indptr, lists.get() + binstart[1], (int64_t)hc[1], wp, s);
+    if (hc[2] > 0) plan_windows(g.indptr, lists.get() + binstart[2], (int64_t)hc[2], wp, s);
     const int64_t nL = (int64_t)hc[NBINS - 1];
     // The bins are independent within a (sub-)round -- sync reads a frozen
     // state and writes disjoint D entries; async tolerates any interleaving --
@@ -1351,7 +1372,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             const int64_t nb = (int64_t)hc[b];
             if (nb == 0) continue;
             const int32_t* list = lists.get() + binstart[b];
-            if (b == 1) {
+            if (b == 2) {
                 if (wp.nwin * (j + 1) / P > wp.nwin * j / P)
                     launch_window<WT, ASYNC>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, next_stream());
                 continue;
@@ -1360,11 +1381,14 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             if (hi <= lo) continue;
             cudaStream_t t = next_stream();
             if (b == 0) {
+                k_isolated<ASYNC><<<grid_for(hi - lo, 256, 8), 256, 0, t>>>(a, list, lo, hi);
+                LCC_LAUNCH_CHECK();
+            } else if (b == 1) {
                 const int64_t warps = (hi - lo + 31) / 32;
                 k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, t>>>(a, list, lo, hi);
                 LCC_LAUNCH_CHECK();
             } else {
-                launch_bin<WT, ASYNC>(b, a, list, lo, hi, t);
+                launch_bin<WT, ASYNC>(b - 1, a, list, lo, hi, t);
             }
         }
         for (int i = 0; i < used; ++i) {
@@ -1384,8 +1408,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         st->vertices += nF;
         st->edges += (int64_t)hc[NBINS];
         st->moved += (int64_t)hm;
-        st->n_small += (int64_t)hc[0];
-        for (int b = 1; b < NBINS - 1; ++b) st->n_medium += (int64_t)hc[b];
+        st->n_small += (int64_t)(hc[0] + hc[1]);
+        for (int b = 2; b < NBINS - 1; ++b) st->n_medium += (int64_t)hc[b];
         st->n_large += nL;
         st->ms_kernels += (double)kms + (double)kms_large;
         st->launches += launch_counter() - launches0;

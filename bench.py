@@ -248,8 +248,9 @@ def config_dict(args, g, wl=None, extra=None):
          "schedule": wl.schedule if wl is not None else args.schedule,
          "frontier": "vertex-neighbors", "refine": True, "num_iter": 10,
          "async_chunks": args.async_chunks, "degree_threshold": args.degree_threshold,
-         "step": "one best-move iteration over V'=V from singletons: lcc_best_moves_round + lcc_apply_moves + "
-                 "lcc_compute_frontier (partition, kernels, reconcile, next active set)",
+         "step": "one best-move iteration over V'=V from singletons: lcc_best_moves_round (VertexNeighbors "
+                 "frontier mask fused) + lcc_apply_moves + lcc_frontier_from_mask (partition, kernels, reconcile, "
+                 "next active set)",
          "l2": "inputs larger than L2 (CSR indices %.2f GB vs 126 MB L2); no flush" % (4 * 2 * g["m"] / 1e9)
                if 8 * g["m"] > 126e6 else "inputs smaller than L2 (launch/L2 bound config)",
          "parallelism": "single-gpu"}
@@ -319,6 +320,7 @@ def run_ours(args):
     Kn = torch.empty(n, dtype=torch.float64, device="cuda")
     F = torch.empty(n, dtype=torch.int32, device="cuda")
     moved = torch.empty(n, dtype=torch.uint8, device="cuda")
+    mark = torch.empty(n, dtype=torch.uint8, device="cuda")
     iota = torch.arange(n, dtype=torch.int32, device="cuda")
     cnt, nF = ctypes.c_int64(), ctypes.c_int64()
 
@@ -332,14 +334,15 @@ def run_ours(args):
             K2[:n].copy_(kfill)
         K2[n:].zero_()
         sp = stream_ptr()
+        # (the VertexNeighbors frontier is fused into the round: nbr_mark)
         _lib.check(lib.lcc_best_moves_round(ctypes.byref(gs), ctypes.byref(ps), C.data_ptr(), K2.data_ptr(), None, n,
                                             sched, args.degree_threshold, args.async_chunks, D.data_ptr(),
-                                            moved.data_ptr(), ctypes.byref(cnt), ctypes.byref(st), sp))
+                                            moved.data_ptr(), mark.data_ptr(), ctypes.byref(cnt),
+                                            ctypes.byref(st), sp))
         labels = C if sched == 1 else D
         _lib.check(lib.lcc_apply_moves(n, labels.data_ptr(), 2 * n, None if kfill is None else kfill.data_ptr(),
                                        Cn.data_ptr(), Kn.data_ptr(), sp))
-        _lib.check(lib.lcc_compute_frontier(ctypes.byref(gs), 1, moved.data_ptr(), iota.data_ptr(), Cn.data_ptr(),
-                                            F.data_ptr(), ctypes.byref(nF), sp))
+        _lib.check(lib.lcc_frontier_from_mask(n, mark.data_ptr(), F.data_ptr(), ctypes.byref(nF), sp))
 
     for _ in range(args.warmup):
         step(_lib.LccStats())
@@ -380,6 +383,13 @@ def run_ours(args):
                 "alg_bytes_per_launch_group": alg_bytes, "kernel_ms_per_step": kern_ms,
                 "kernel_share_of_step": kern_ms / (ms / args.steps)}
 
+    # CPU baseline (oracle port) first: the e2e leg below drops the device graph
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        og, kh = host_oracle_graph(wl)
+        cpu, _ = run_cpu_baseline(og, kh, wl.lam, wl.schedule, args.cpu_sample_stride, args.cpu_seconds)
+        og = kh = None
+
     # e2e: whole clustering via the public API from pinned host memory
     e2e = None
     if not args.no_e2e:
@@ -392,6 +402,12 @@ def run_ours(args):
         hgr = HostG()
         hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = (
             n, nnz // 2, indptr_h, indices_h, weights_h, dg.total_weight)
+        # the e2e call uploads its own copy: release the round-bench buffers
+        # (and, except for cfg1 which contracts `dg` directly, the device graph)
+        C = D = K2 = Cn = Kn = F = moved = mark = iota = None
+        if wl.cfg != "cfg1":
+            dg = wl.dg = None
+        torch.cuda.empty_cache()
         full = L.ParOptions(schedule=wl.schedule, degree_threshold=args.degree_threshold,
                             async_chunks=args.async_chunks)
         out_h = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -403,6 +419,23 @@ def run_ours(args):
                 lvl = L.par_compress(dg, p, cl)
                 cl.meta["stats"].levels = 1
                 cl.meta["coarse_n"] = lvl.graph.n
+            elif os.environ.get("LCC_BENCH_DEBUG"):
+                from paper_2108_01731_b200.louvain_par import _prep
+                t = [time.perf_counter()]
+                dgx, gsx, psx = _prep(hgr, p)
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                Cx = torch.empty(n, dtype=torch.int32, device="cuda")
+                stx = _lib.LccStats()
+                osx = full.c_struct()
+                _lib.check(lib.lcc_parallel_cc(ctypes.byref(gsx), ctypes.byref(psx), ctypes.byref(osx),
+                                               Cx.data_ptr(), ctypes.byref(stx), stream_ptr()))
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                from paper_2108_01731_b200.objective import clustering_from_labels
+                cl = clustering_from_labels(Cx, p)
+                cl.meta["stats"] = L.louvain_par._stats_from(stx)
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                print("e2e phases ms: upload %.1f parallel_cc %.1f (device %.1f) relabel %.1f" % (
+                    1e3 * (t[1] - t[0]), 1e3 * (t[2] - t[1]), stx.ms_total, 1e3 * (t[3] - t[2])), file=sys.stderr)
             else:
                 cl = L.parallel_cc(hgr, p, full)
             out_h.copy_(cl.assignment, non_blocking=True)
@@ -424,7 +457,9 @@ def run_ours(args):
         if dist:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(ed_t, op=dist.ReduceOp.SUM)
-        obj = L.cc_objective(dg, p, torch.as_tensor(out_h).cuda())
+        cl = None
+        torch.cuda.empty_cache()
+        obj = L.cc_objective(dg if dg is not None else hgr, p, torch.as_tensor(out_h).cuda())
         e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
                                          (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
@@ -435,11 +470,6 @@ def run_ours(args):
                "objective": obj, "clusters": int(np.unique(out_h.numpy()).size),
                "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
                        "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
-
-    cpu = None
-    if not args.no_cpu and rank == 0:
-        og, kh = host_oracle_graph(wl)
-        cpu, _ = run_cpu_baseline(og, kh, wl.lam, wl.schedule, args.cpu_sample_stride, args.cpu_seconds)
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define LCC_ABI_VERSION 1
+#define LCC_ABI_VERSION 2
 
 typedef enum {
     LCC_OK = 0,
@@ -104,6 +104,9 @@ int64_t lcc_kernel_launches(void);
  *              fresh-singleton targets are n+v) and moved[n] (0/1).
  *   LCC_ASYNC: updates C[n] and K[2n] in place with relaxed atomics
  *              (SPEC.md:261,313); D may be NULL; moved[n] written.
+ * nbr_mark (may be NULL, n bytes): zeroed, then nbr_mark[u] = 1 for every
+ * neighbour u of a mover -- the VertexNeighbors frontier
+ * fused into the round; lcc_frontier_from_mask compacts it.
  * *moved_count (host) receives the number of movers; stats (may be NULL) is
  * accumulated (vertices, edges scanned, movers, best-move kernel time).     */
 lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p,
@@ -111,7 +114,7 @@ lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p,
                                 const int32_t* frontier, int64_t n_frontier,
                                 int32_t schedule, int32_t degree_threshold,
                                 int32_t async_chunks,
-                                int32_t* D, uint8_t* moved,
+                                int32_t* D, uint8_t* moved, uint8_t* nbr_mark,
                                 int64_t* moved_count, lcc_stats* stats,
                                 void* stream);
 
@@ -127,6 +130,12 @@ lcc_status lcc_compute_frontier(const lcc_graph* g, int32_t policy,
                                 const uint8_t* moved, const int32_t* C_old,
                                 const int32_t* C_new, int32_t* frontier,
                                 int64_t* n_frontier, void* stream);
+
+/* Sorted ids v with mark[v] != 0 -> frontier[n]; *n_frontier (host) = size.
+ * With the nbr_mark of lcc_best_moves_round this equals compute_frontier
+ * under LCC_FRONTIER_VERTEX_NBRS.                                           */
+lcc_status lcc_frontier_from_mask(int64_t n, const uint8_t* mark, int32_t* frontier,
+                                  int64_t* n_frontier, void* stream);
 
 /* ---- par_best_moves -----------------------------------
  * Up to opts->num_iter iterations starting from the frontier V' = V.

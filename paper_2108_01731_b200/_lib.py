@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_lib", "liblcc_b200.so")
+# LCC_LIB_PATH: an in-tree tuning build (A/B variants); default = the product
+SO_PATH = os.environ.get("LCC_LIB_PATH") or os.path.join(_HERE, "_lib", "liblcc_b200.so")
 
 LCC_OK, LCC_ERR_INVALID, LCC_ERR_CUDA, LCC_ERR_OOM = 0, 1, 2, 3
 W_NONE, W_F32, W_F64 = 0, 1, 2
@@ -22,7 +23,7 @@ EXPORTS = (
     "lcc_abi_version", "lcc_last_error", "lcc_kernel_launches", "lcc_best_moves_round", "lcc_apply_moves",
     "lcc_compute_frontier", "lcc_par_best_moves", "lcc_par_compress", "lcc_par_flatten",
     "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_gen_powerlaw_communities",
-    "lcc_build_csr_from_pairs",
+    "lcc_build_csr_from_pairs", "lcc_frontier_from_mask",
 )
 
 
@@ -80,7 +81,8 @@ def load() -> ctypes.CDLL:
         "lcc_abi_version": (ctypes.c_int, []),
         "lcc_last_error": (ctypes.c_char_p, []),
         "lcc_kernel_launches": (ctypes.c_int64, []),
-        "lcc_best_moves_round": (ctypes.c_int, [G, PR, P, P, P, I64, I32, I32, I32, P, P, pI64, ST, P]),
+        "lcc_best_moves_round": (ctypes.c_int, [G, PR, P, P, P, I64, I32, I32, I32, P, P, P, pI64, ST, P]),
+        "lcc_frontier_from_mask": (ctypes.c_int, [I64, P, P, pI64, P]),
         "lcc_apply_moves": (ctypes.c_int, [I64, P, I64, P, P, P, P]),
         "lcc_compute_frontier": (ctypes.c_int, [G, I32, P, P, P, P, pI64, P]),
         "lcc_par_best_moves": (ctypes.c_int, [G, PR, O, P, P, pI32, ST, P]),
@@ -97,7 +99,7 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     ver = L.lcc_abi_version()
-    if ver != 1:
+    if ver != 2:
         raise NativeLibraryError(f"ABI version mismatch: library {ver}, binding 1")
     _lib = L
     return L

@@ -30,18 +30,23 @@ def _needs(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OUT_DIR, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, extra: list[str] | None = None,
+          out_dir: str | None = None) -> str:
+    """Compile + link.  ``extra`` / ``out_dir``: tuning builds (A/B variants
+    selected at run time with LCC_LIB_PATH); the product is the default."""
+    out_dir = out_dir or OUT_DIR
+    so = os.path.join(out_dir, "liblcc_b200.so")
+    os.makedirs(out_dir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
     headers.append(os.path.join(HERE, "..", "include", "lcc_b200.h"))
     jobs = []
     objs = []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(out_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _needs(obj, [sp] + headers):
-            jobs.append([NVCC, *FLAGS, "-c", sp, "-o", obj])
+            jobs.append([NVCC, *FLAGS, *(extra or []), "-c", sp, "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -53,9 +58,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
-    if jobs or not os.path.exists(SO):
-        run([NVCC, *ARCH, "-shared", "-o", SO, *objs, "-lcudart"])
-    return SO
+    if jobs or not os.path.exists(so):
+        run([NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart"])
+    return so
 
 
 if __name__ == "__main__":

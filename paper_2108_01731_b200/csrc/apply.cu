@@ -171,7 +171,13 @@ int64_t compute_frontier(const lcc_graph& g, int policy, const uint8_t* moved, c
         LCC_CUDA(cudaStreamSynchronize(s));
         edge_balanced(g.indptr, clist.get(), off.get(), nc, total, MarkNbr{g.indices, mark.get()}, s);
     }
-    select_flagged(cub::CountingInputIterator<int32_t>(0), mark.get(), frontier, dcnt.get(), n, s);
+    return frontier_from_mask(n, mark.get(), frontier, s);
+}
+
+int64_t frontier_from_mask(int64_t n, const uint8_t* mark, int32_t* frontier, cudaStream_t s) {
+    if (n <= 0) return 0;
+    Buf<int64_t> dcnt(1, s);
+    select_flagged(cub::CountingInputIterator<int32_t>(0), mark, frontier, dcnt.get(), n, s);
     int64_t h = 0;
     LCC_CUDA(cudaMemcpyAsync(&h, dcnt.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));

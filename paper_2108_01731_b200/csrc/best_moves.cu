@@ -86,6 +86,7 @@ struct BMArgs {
     uint8_t* moved;
     unsigned long long* moved_count;
     int32_t n;
+    uint8_t* mark;  // optional: neighbours of movers flagged here (fused VertexNeighbors frontier)
 };
 
 // Final choice for one vertex (mirrors oracle best_target()).
@@ -192,11 +193,12 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const int64_t sj = __shfl_sync(FULL, s, j);
             const int32_t cj = __shfl_sync(FULL, c, j);
             const double tj = __shfl_sync(FULL, t, j);
-            int32_t x = 0;
+            int32_t x = 0, nbr = 0;
             double wv = 0.0;
             if (has_edge) {
                 const int64_t e = sj + (lane - p);
-                x = ldC<ASYNC>(a.C, ld_stream_i32(a.indices + e, pol_stream), pol_keep);
+                nbr = ld_stream_i32(a.indices + e, pol_stream);
+                x = ldC<ASYNC>(a.C, nbr, pol_keep);
                 wv = WLoad<WT>::at(a.w, e);
             }
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
@@ -236,7 +238,12 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const int src = starter ? rs : lane;
             const double hg = __shfl_sync(FULL, g, src);
             const int32_t hx = __shfl_sync(FULL, gx, src);
-            if (inwin) my_moves += decide<ASYNC>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx);
+            const int mv = inwin ? decide<ASYNC>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx) : 0;
+            my_moves += mv;
+            if (a.mark) {  // the window's neighbour ids are still in registers
+                const int mvj = __shfl_sync(FULL, mv, j);
+                if (has_edge && mvj) a.mark[nbr] = 1;
+            }
             base = end;
             __syncwarp();
         }
@@ -482,6 +489,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_g[GROUPS * GW];
     __shared__ int32_t s_x[GROUPS * GW];
+    __shared__ int32_t s_mv[GROUPS];
     const int gid = threadIdx.x / GT;
     const int gt = threadIdx.x % GT;
     const int wig = gt >> 5;
@@ -501,9 +509,9 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
         const int64_t end = __ldg(a.indptr + v + 1);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
@@ -571,7 +579,24 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 if (better(og, ox, bg, bx)) { bg = og; bx = ox; }
             }
         }
-        if (gt == 0) my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
+        int mv = 0;
+        if (gt == 0) {
+            mv = decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
+            my_moves += mv;
+        }
+        if (a.mark) {  // fused frontier: a mover flags its neighbours (row re-read hits L2)
+            if constexpr (GW == 1) {
+                mv = __shfl_sync(FULL, mv, 0);
+            } else {
+                if (gt == 0) s_mv[gid] = mv;
+                gsync();
+                mv = s_mv[gid];
+            }
+            if (mv) {
+#pragma unroll 4
+                for (int64_t e = s + gt; e < end; e += GT) a.mark[__ldg(a.indices + e)] = 1;
+            }
+        }
         gsync();  // table (already reset by take) and s_g free for the next vertex
     }
     flush_moves(a, my_moves);
@@ -632,6 +657,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
     __shared__ double s_t[WIN_MAXV], s_kv[WIN_MAXV], s_Kc[WIN_MAXV], s_b[WIN_MAXV], s_scw[WIN_MAXV];
     __shared__ uint32_t s_sc[WIN_MAXV], s_hi[WIN_MAXV], s_lo[WIN_MAXV];
     __shared__ int32_t s_bx[WIN_MAXV];
+    __shared__ int32_t s_mv[WIN_MAXV];
     const int tid = threadIdx.x;
     const uint32_t keys_s = smem_u32(keys), cnts_s = smem_u32(cnts), sums_s = smem_u32(sums);
     for (int q = tid; q < WIN_CAP; q += WIN_THREADS) {
@@ -763,9 +789,28 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
         if (tid < nv) {
             const int32_t bx = s_bx[tid];
             const unsigned long long o = ((unsigned long long)s_hi[tid] << 32) | s_lo[tid];
-            my_moves += decide<ASYNC>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND, unord_gain(o), bx);
+            const int mv = decide<ASYNC>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND, unord_gain(o), bx);
+            my_moves += mv;
+            s_mv[tid] = mv;
         }
         __syncthreads();
+        if (a.mark) {  // fused frontier: the same 8 positions per thread as phase 1
+            const int p0 = tid * WIN_ITEMS;
+            if (p0 < E) {
+                int lo = 0, hi = nv;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_loc[mid] <= p0) lo = mid; else hi = mid;
+                }
+                int sl = lo;
+                for (int j = 0; j < WIN_ITEMS && p0 + j < E; ++j) {
+                    const int p = p0 + j;
+                    while (p >= s_loc[sl + 1]) ++sl;
+                    if (s_mv[sl]) a.mark[__ldg(a.indices + s_start[sl] + (p - s_loc[sl]))] = 1;
+                }
+            }
+            __syncthreads();
+        }
     }
     flush_moves(a, my_moves);
 }
@@ -988,6 +1033,22 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
         }
     }
     flush_moves(a, my_moves);
+}
+
+// fused frontier for hubs: every moved hub flags its neighbours, over the
+// same LARGE_CHUNK-edge work items as the insertion
+__global__ void __launch_bounds__(LARGE_THREADS)
+k_large_mark(BMArgs a, LargeBatch L, int64_t total_items) {
+    for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
+        const int64_t li = owner_of(L.item_off, L.nL, it);
+        const int32_t v = L.list[li];
+        if (!a.moved[v]) continue;
+        const int64_t s = a.indptr[v], e_end = a.indptr[v + 1];
+        const int64_t e0 = s + (it - L.item_off[li]) * LARGE_CHUNK;
+        const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
+#pragma unroll 4
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += LARGE_THREADS) a.mark[__ldg(a.indices + e)] = 1;
+    }
 }
 
 // ===========================================================================
@@ -1240,6 +1301,10 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_
         LCC_LAUNCH_CHECK();
         k_large_decide<ASYNC><<<grid_for(bt.nb * 32, 256), 256, 0, s>>>(a, L);
         LCC_LAUNCH_CHECK();
+        if (a.mark) {
+            k_large_mark<<<grid_for(bt.items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, bt.items);
+            LCC_LAUNCH_CHECK();
+        }
     }
 }
 
@@ -1269,10 +1334,11 @@ inline SideStreams& side_streams() {
 template <class WT, bool ASYNC>
 int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                   const int32_t* frontier, int64_t nF, int deg_threshold, int chunks, int32_t* D,
-                  uint8_t* moved, RoundStats* st, cudaStream_t s) {
+                  uint8_t* moved, uint8_t* mark, RoundStats* st, cudaStream_t s) {
     const int64_t n = g.n;
     if (!ASYNC) LCC_CUDA(cudaMemcpyAsync(D, C, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
     LCC_CUDA(cudaMemsetAsync(moved, 0, n, s));
+    if (mark) LCC_CUDA(cudaMemsetAsync(mark, 0, n, s));
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
@@ -1331,7 +1397,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         for (int b = 0; b <= NBINS; ++b) hc[b] = 0;
         binstart.assign(NBINS + 1, 0);
     }
-    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n};
+    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n, mark};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
     LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
@@ -1421,7 +1487,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
 int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                          const int32_t* frontier, int64_t nF, int schedule, int deg_threshold,
-                         int async_chunks, int32_t* D, uint8_t* moved, RoundStats* st,
+                         int async_chunks, int32_t* D, uint8_t* moved, uint8_t* mark, RoundStats* st,
                          cudaStream_t s) {
     LCC_REQUIRE(g.n >= 0 && g.n < (1LL << 30), "vertex count out of range");
     LCC_REQUIRE(schedule == LCC_SYNC || schedule == LCC_ASYNC, "unknown schedule");
@@ -1431,14 +1497,14 @@ int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_
     const bool as = schedule == LCC_ASYNC;
     switch (g.weights ? g.wtype : LCC_W_NONE) {
         case LCC_W_NONE:
-            return as ? run_round<WNone, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, st, s)
-                      : run_round<WNone, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, st, s);
+            return as ? run_round<WNone, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
+                      : run_round<WNone, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
         case LCC_W_F32:
-            return as ? run_round<float, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, st, s)
-                      : run_round<float, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, st, s);
+            return as ? run_round<float, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
+                      : run_round<float, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
         case LCC_W_F64:
-            return as ? run_round<double, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, st, s)
-                      : run_round<double, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, st, s);
+            return as ? run_round<double, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
+                      : run_round<double, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
         default:
             throw Invalid("unknown weight dtype");
     }

@@ -91,24 +91,34 @@ struct KSq {
     __device__ __forceinline__ double operator()(int64_t v) const { const double x = k ? k[v] : 1.0; return x * x; }
 };
 
+struct RunHead {
+    const uint64_t* keys;
+    __device__ __forceinline__ int64_t operator()(int64_t i) const {
+        return (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+    }
+};
+
 template <class WT>
 Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
-                     int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cw,
-                     cudaStream_t s) {
+                     int32_t* mapping, double* ck, cudaStream_t s) {
     const int64_t n = g.n, nnz = g.nnz;
     Coarse out;
     // 1. dense renumbering by smallest member
-    Buf<int32_t> rank(n + 1, s);
-    cub::TransformInputIterator<int32_t, IsRoot, cub::CountingInputIterator<int32_t>> roots(
-        cub::CountingInputIterator<int32_t>(0), IsRoot{C, n});
-    exclusive_sum(roots, rank.get(), n + 1, s);
-    int32_t hcn = 0;
-    LCC_CUDA(cudaMemcpyAsync(&hcn, rank.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    k_map<<<grid_for(n, 256), 256, 0, s>>>(C, rank.get(), K, n, mapping, ck);
-    LCC_LAUNCH_CHECK();
-    LCC_CUDA(cudaStreamSynchronize(s));
-    const int64_t cn = hcn;
+    int64_t cn = 0;
+    {
+        Buf<int32_t> rank(n + 1, s);
+        cub::TransformInputIterator<int32_t, IsRoot, cub::CountingInputIterator<int32_t>> roots(
+            cub::CountingInputIterator<int32_t>(0), IsRoot{C, n});
+        exclusive_sum(roots, rank.get(), n + 1, s);
+        int32_t hcn = 0;
+        LCC_CUDA(cudaMemcpyAsync(&hcn, rank.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        k_map<<<grid_for(n, 256), 256, 0, s>>>(C, rank.get(), K, n, mapping, ck);
+        LCC_LAUNCH_CHECK();
+        LCC_CUDA(cudaStreamSynchronize(s));
+        cn = hcn;
+    }
     out.cn = cn;
+    out.indptr.alloc(cn + 1, s);
     const int bits = std::max(1, bit_width((uint64_t)cn));
     LCC_REQUIRE(2 * bits <= 64, "coarse graph too large");
 
@@ -120,55 +130,76 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     int64_t R = 0;
     double intra_w = 0.0;
     if (nnz > 0) {
-        Buf<uint64_t> keys(nnz, s), keys2(nnz, s);
-        Buf<double> vals, vals2;
-        if (WLoad<WT>::weighted) { vals.alloc(nnz, s); vals2.alloc(nnz, s); }
+        Buf<uint64_t> ka(nnz, s), kb(nnz, s);
+        Buf<double> va, vb;
+        if (WLoad<WT>::weighted) { va.alloc(nnz, s); vb.alloc(nnz, s); }
         const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
         edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
-                      EdgeKey<WT>{g.indices, g.weights, mapping, bits, sentinel, keys.get(), vals.get(),
+                      EdgeKey<WT>{g.indices, g.weights, mapping, bits, sentinel, ka.get(), va.get(),
                                   dintra.get(), dacc.get()}, s);
-        // 3. stable radix sort on the 2*bits live bits
-        if (WLoad<WT>::weighted) sort_pairs(keys.get(), keys2.get(), vals.get(), vals2.get(), nnz, 2 * bits, s);
-        else sort_keys(keys.get(), keys2.get(), nnz, 2 * bits, s);
-        // 4. reduce by key (keys reuse `keys` as unique output); unweighted
-        //    entries sum a constant 1.0 -- integer-valued, exact below 2^53;
-        //    64-bit item counts (2m > 2^31 at config 5)
-        Buf<int64_t> druns(1, s);
-        {
-            size_t bytes = 0;
-            if (WLoad<WT>::weighted) {
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, keys2.get(), keys.get(), vals2.get(), cw,
-                                                        druns.get(), cub::Sum(), nnz, s));
-                Buf<unsigned char> tmp(bytes, s);
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, keys2.get(), keys.get(), vals2.get(), cw,
-                                                        druns.get(), cub::Sum(), nnz, s));
-            } else {
-                cub::ConstantInputIterator<double> ones(1.0);
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, keys2.get(), keys.get(), ones, cw,
-                                                        druns.get(), cub::Sum(), nnz, s));
-                Buf<unsigned char> tmp(bytes, s);
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, keys2.get(), keys.get(), ones, cw,
-                                                        druns.get(), cub::Sum(), nnz, s));
-            }
-        }
+        // 3. stable radix sort on the 2*bits live bits, double-buffered (peak
+        //    memory = the two key (+value) buffers, no hidden n-sized temp)
+        cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());
+        cub::DoubleBuffer<double> dv(va.get(), vb.get());
+        if (WLoad<WT>::weighted) sort_pairs_db(dk, dv, nnz, 2 * bits, s);
+        else sort_keys_db(dk, nnz, 2 * bits, s);
+        Buf<uint64_t>& ksorted = dk.Current() == ka.get() ? ka : kb;
+        (dk.Current() == ka.get() ? kb : ka).release();
+        Buf<double>& vsorted = dv.Current() == va.get() ? va : vb;
+        if (WLoad<WT>::weighted) (dv.Current() == va.get() ? vb : va).release();
+        // 4. count the runs, then reduce by key into exact-size outputs;
+        //    unweighted entries sum a constant 1.0 (integer-valued, exact
+        //    below 2^53); 64-bit item counts (2m > 2^31 at config 5)
         int64_t runs = 0;
         unsigned long long hintra = 0;
-        LCC_CUDA(cudaMemcpyAsync(&runs, druns.get(), sizeof(runs), cudaMemcpyDeviceToHost, s));
-        LCC_CUDA(cudaMemcpyAsync(&hintra, dintra.get(), sizeof(hintra), cudaMemcpyDeviceToHost, s));
-        LCC_CUDA(cudaMemcpyAsync(&intra_w, dacc.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
-        LCC_CUDA(cudaStreamSynchronize(s));
+        {
+            Buf<int64_t> dr(1, s);
+            cub::TransformInputIterator<int64_t, RunHead, cub::CountingInputIterator<int64_t>> heads(
+                cub::CountingInputIterator<int64_t>(0), RunHead{ksorted.get()});
+            device_sum(heads, dr.get(), nnz, s);
+            LCC_CUDA(cudaMemcpyAsync(&runs, dr.get(), sizeof(runs), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaMemcpyAsync(&hintra, dintra.get(), sizeof(hintra), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaMemcpyAsync(&intra_w, dacc.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+        }
         R = runs - (hintra > 0 ? 1 : 0);  // the all-ones sentinel run (intra entries) sorts last
         if (!WLoad<WT>::weighted) intra_w = (double)hintra;
-        k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(keys.get(), R, bits, cn, cindptr, cindices);
+        Buf<uint64_t> ukeys(std::max<int64_t>(runs, 1), s);
+        out.w.alloc(std::max<int64_t>(runs, 1), s);
+        {
+            Buf<int64_t> druns(1, s);
+            size_t bytes = 0;
+            if (WLoad<WT>::weighted) {
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, ksorted.get(), ukeys.get(), vsorted.get(),
+                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+                Buf<unsigned char> tmp(bytes, s);
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, ksorted.get(), ukeys.get(), vsorted.get(),
+                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+            } else {
+                cub::ConstantInputIterator<double> ones(1.0);
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, ksorted.get(), ukeys.get(), ones,
+                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+                Buf<unsigned char> tmp(bytes, s);
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, ksorted.get(), ukeys.get(), ones,
+                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+            }
+        }
+        ksorted.release();
+        vsorted.release();
+        out.indices.alloc(std::max<int64_t>(R, 1), s);
+        k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(ukeys.get(), R, bits, cn, out.indptr.get(),
+                                                         out.indices.get());
         LCC_LAUNCH_CHECK();
     } else {
-        LCC_CUDA(cudaMemsetAsync(cindptr, 0, sizeof(int64_t) * (cn + 1), s));
+        out.w.alloc(1, s);
+        out.indices.alloc(1, s);
+        LCC_CUDA(cudaMemsetAsync(out.indptr.get(), 0, sizeof(int64_t) * (cn + 1), s));
     }
     out.cnnz = R;
     // 5. scalars: total weight, internal offset
     Buf<double> sums(3, s);
     LCC_CUDA(cudaMemsetAsync(sums.get(), 0, 3 * sizeof(double), s));
-    if (R > 0) device_sum(cw, sums.get() + 0, R, s);
+    if (R > 0) device_sum(out.w.get(), sums.get() + 0, R, s);
     if (cn > 0) {
         cub::TransformInputIterator<double, Sq, const double*> sq(ck, Sq{});
         device_sum(sq, sums.get() + 1, cn, s);
@@ -194,13 +225,12 @@ __global__ void k_compose(const int32_t* __restrict__ mapping, const int32_t* __
 }  // namespace
 
 Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
-                int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cw,
-                cudaStream_t s) {
+                int32_t* mapping, double* ck, cudaStream_t s) {
     LCC_REQUIRE(g.n >= 0 && g.n < (1LL << 31) - 1, "vertex count out of range");
     switch (g.weights ? g.wtype : LCC_W_NONE) {
-        case LCC_W_NONE: return compress_impl<WNone>(g, k, lam, C, K, mapping, ck, cindptr, cindices, cw, s);
-        case LCC_W_F32: return compress_impl<float>(g, k, lam, C, K, mapping, ck, cindptr, cindices, cw, s);
-        case LCC_W_F64: return compress_impl<double>(g, k, lam, C, K, mapping, ck, cindptr, cindices, cw, s);
+        case LCC_W_NONE: return compress_impl<WNone>(g, k, lam, C, K, mapping, ck, s);
+        case LCC_W_F32: return compress_impl<float>(g, k, lam, C, K, mapping, ck, s);
+        case LCC_W_F64: return compress_impl<double>(g, k, lam, C, K, mapping, ck, s);
         default: throw Invalid("unknown weight dtype");
     }
 }

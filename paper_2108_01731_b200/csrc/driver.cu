@@ -6,6 +6,8 @@
 // host read of the mover count per iteration for the early exit (Alg. 1
 // line 9).  Levels are kept on an explicit stack so refinement can revisit
 // them while unwinding.
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <utility>
 #include <vector>
@@ -45,6 +47,10 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
     const bool as = o.schedule == LCC_ASYNC;
     Buf<int32_t> D(n, s), Cnext(n, s), F(n, s);
     Buf<uint8_t> moved(n, s);
+    // VertexNeighbors frontier fused into the round (nbr_mark), else computed after
+    const bool fused = o.policy == LCC_FRONTIER_VERTEX_NBRS;
+    Buf<uint8_t> mark;
+    if (fused && o.num_iter > 1) mark.alloc(n, s);
     Buf<double> K2;
     if (as) K2.alloc(2 * n, s);
     int32_t* cur = C;
@@ -56,18 +62,22 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         if (frontier && nF == 0) break;
         RoundStats rs;
         int64_t cnt;
+        uint8_t* mk = (fused && it + 1 < o.num_iter) ? mark.get() : nullptr;
         EventTimer tm(s);
         if (!as) {
             cnt = best_moves_round(g, k, lam, cur, K, frontier, nF, LCC_SYNC, o.deg_threshold, 1, D.get(),
-                                   moved.get(), &rs, s);
+                                   moved.get(), mk, &rs, s);
         } else {
             LCC_CUDA(cudaMemcpyAsync(D.get(), cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemcpyAsync(K2.get(), K, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemsetAsync(K2.get() + n, 0, sizeof(double) * n, s));
             cnt = best_moves_round(g, k, lam, D.get(), K2.get(), frontier, nF, LCC_ASYNC, o.deg_threshold,
-                                   o.async_chunks, nullptr, moved.get(), &rs, s);
+                                   o.async_chunks, nullptr, moved.get(), mk, &rs, s);
         }
         const float ms = tm.stop();
+        if (getenv("LCC_TRACE"))
+            fprintf(stderr, "[lcc]     iter %d frontier %lld edges %lld movers %lld launches %lld %.2f ms (kernels %.2f)\n",
+                    it, (long long)nF, (long long)rs.edges, (long long)cnt, (long long)rs.launches, ms, rs.ms_kernels);
         if (st) {
             st->rounds += 1;
             st->vertices += rs.vertices;
@@ -81,7 +91,8 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         any = true;
         apply_moves(n, D.get(), 2 * n, k, nxt, K, s);  // sync apply / async reconcile
         if (it + 1 < o.num_iter) {  // the next frontier is only needed by a next iteration
-            nF = compute_frontier(g, o.policy, moved.get(), cur, nxt, F.get(), s);
+            nF = mk ? frontier_from_mask(n, mk, F.get(), s)
+                    : compute_frontier(g, o.policy, moved.get(), cur, nxt, F.get(), s);
             frontier = F.get();
         }
         std::swap(cur, nxt);
@@ -115,32 +126,34 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
     const double* k = k0;
     Buf<int32_t> C;
     Buf<double> K;
+    const bool trace = getenv("LCC_TRACE") != nullptr;  // per-phase device times on stderr
     while (true) {
         const int64_t n = g.n;
+        EventTimer tl(s);
         C.alloc(std::max<int64_t>(n, 1), s);
         K.alloc(std::max<int64_t>(n, 1), s);
         fill_iota(C.get(), n, s);  // singletons
         fill_k(K.get(), k, n, s);
         if (st) st->levels += 1;
         const bool moved = par_best_moves(g, k, lam, o, C.get(), K.get(), st, s);
+        if (trace) fprintf(stderr, "[lcc] level n=%lld nnz=%lld best_moves %.2f ms\n", (long long)n,
+                           (long long)g.nnz, tl.stop());
         if (!moved) break;  // Alg. 1 line 13
-        // contraction into upper-bound buffers, then shrink to exact size
-        Buf<int32_t> mapping(n, s), cind(std::max<int64_t>(g.nnz, 1), s);
-        Buf<double> ck(n, s), cw(std::max<int64_t>(g.nnz, 1), s);
-        Buf<int64_t> cptr(n + 1, s);
-        const Coarse cs = compress(g, k, lam, C.get(), K.get(), mapping.get(), ck.get(), cptr.get(), cind.get(),
-                                   cw.get(), s);
+        EventTimer tc(s);
+        // contraction straight into exact-size buffers
+        Buf<int32_t> mapping(n, s);
+        Buf<double> ck(n, s);
+        Coarse cs = compress(g, k, lam, C.get(), K.get(), mapping.get(), ck.get(), s);
+        if (trace) fprintf(stderr, "[lcc]   compress -> cn=%lld cnnz=%lld %.2f ms\n", (long long)cs.cn,
+                           (long long)cs.cnnz, tc.stop());
         if (cs.cn == n) break;  // no size reduction
+        C.release();
+        K.release();
         auto og = std::make_unique<OwnedGraph>();
-        og->indptr.alloc(cs.cn + 1, s);
-        og->indices.alloc(std::max<int64_t>(cs.cnnz, 1), s);
-        og->w.alloc(std::max<int64_t>(cs.cnnz, 1), s);
+        og->indptr = std::move(cs.indptr);
+        og->indices = std::move(cs.indices);
+        og->w = std::move(cs.w);
         og->k.alloc(std::max<int64_t>(cs.cn, 1), s);
-        LCC_CUDA(cudaMemcpyAsync(og->indptr.get(), cptr.get(), sizeof(int64_t) * (cs.cn + 1), cudaMemcpyDeviceToDevice, s));
-        if (cs.cnnz) {
-            LCC_CUDA(cudaMemcpyAsync(og->indices.get(), cind.get(), sizeof(int32_t) * cs.cnnz, cudaMemcpyDeviceToDevice, s));
-            LCC_CUDA(cudaMemcpyAsync(og->w.get(), cw.get(), sizeof(double) * cs.cnnz, cudaMemcpyDeviceToDevice, s));
-        }
         LCC_CUDA(cudaMemcpyAsync(og->k.get(), ck.get(), sizeof(double) * cs.cn, cudaMemcpyDeviceToDevice, s));
         og->g.n = cs.cn;
         og->g.nnz = cs.cnnz;
@@ -158,10 +171,12 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
     Buf<int32_t> Cres = std::move(C);
     for (auto it = stack.rbegin(); it != stack.rend(); ++it) {
         const int64_t n = it->g.n;
+        EventTimer tu(s);
         Buf<int32_t> Cf(std::max<int64_t>(n, 1), s);
         Buf<double> Kf(std::max<int64_t>(n, 1), s);
         flatten(n, it->mapping.get(), Cres.get(), it->k, Cf.get(), Kf.get(), s);
         if (o.refine) par_best_moves(it->g, it->k, lam, o, Cf.get(), Kf.get(), st, s);
+        if (trace) fprintf(stderr, "[lcc] unwind n=%lld flatten+refine %.2f ms\n", (long long)n, tu.stop());
         Cres = std::move(Cf);
     }
     if (g0.n > 0)

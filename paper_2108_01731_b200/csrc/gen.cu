@@ -107,6 +107,9 @@ __global__ void k_plc(int64_t samples, double mu, const double* __restrict__ vw,
     }
 }
 
+int64_t csr_from_pairs_impl(int64_t n, int64_t np, const int32_t* u, const int32_t* v, Buf<int32_t>* owned_u,
+                            Buf<int32_t>* owned_v, int64_t* indptr, int32_t* indices, cudaStream_t s);
+
 }  // namespace
 
 int64_t gen_powerlaw_communities(int64_t n, int64_t samples, double mu, const double* vw_prefix,
@@ -120,11 +123,14 @@ int64_t gen_powerlaw_communities(int64_t n, int64_t samples, double mu, const do
                                                          u.get(), v.get());
         LCC_LAUNCH_CHECK();
     }
-    return build_csr_from_pairs(n, samples, u.get(), v.get(), indptr, indices, s);
+    return csr_from_pairs_impl(n, samples, u.get(), v.get(), &u, &v, indptr, indices, s);
 }
 
-int64_t build_csr_from_pairs(int64_t n, int64_t np, const int32_t* u, const int32_t* v, int64_t* indptr,
-                             int32_t* indices, cudaStream_t s) {
+namespace {
+// Keys the pairs, then (when `owned`) frees them before the sorts; double-
+// buffered radix sorts keep the peak at two key buffers.
+int64_t csr_from_pairs_impl(int64_t n, int64_t np, const int32_t* u, const int32_t* v, Buf<int32_t>* owned_u,
+                            Buf<int32_t>* owned_v, int64_t* indptr, int32_t* indices, cudaStream_t s) {
     LCC_REQUIRE(n > 0 && n < (1LL << 31), "vertex count out of range");
     LCC_REQUIRE(np >= 0, "negative pair count");
     const int bits = std::max(1, bit_width((uint64_t)(n - 1)));
@@ -135,34 +141,50 @@ int64_t build_csr_from_pairs(int64_t n, int64_t np, const int32_t* u, const int3
     Buf<uint64_t> k1(np, s), k2(np, s);
     k_pair_keys<<<grid_for(np, 256), 256, 0, s>>>(u, v, np, bits, k1.get());
     LCC_LAUNCH_CHECK();
-    sort_keys(k1.get(), k2.get(), np, 2 * bits, s);  // sentinel ~0 keeps the max on these bits too
+    if (owned_u) owned_u->release();
+    if (owned_v) owned_v->release();
+    cub::DoubleBuffer<uint64_t> db(k1.get(), k2.get());
+    sort_keys_db(db, np, 2 * bits, s);  // sentinel ~0 keeps the max on these bits too
+    uint64_t* sorted = db.Current();
+    uint64_t* other = db.Alternate();
     Buf<int64_t> dcnt(1, s);
     {
         size_t bytes = 0;
-        LCC_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, k2.get(), k1.get(), dcnt.get(), np, s));
+        LCC_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, sorted, other, dcnt.get(), np, s));
         Buf<unsigned char> tmp(bytes, s);
-        LCC_CUDA(cub::DeviceSelect::Unique(tmp.get(), bytes, k2.get(), k1.get(), dcnt.get(), np, s));
+        LCC_CUDA(cub::DeviceSelect::Unique(tmp.get(), bytes, sorted, other, dcnt.get(), np, s));
     }
     int64_t nu = 0;
     uint64_t last = 0;
     LCC_CUDA(cudaMemcpyAsync(&nu, dcnt.get(), sizeof(nu), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
     if (nu > 0) {
-        LCC_CUDA(cudaMemcpyAsync(&last, k1.get() + nu - 1, sizeof(last), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaMemcpyAsync(&last, other + nu - 1, sizeof(last), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaStreamSynchronize(s));
     }
     const int64_t m = nu - (nu > 0 && last == ~0ULL ? 1 : 0);
-    k2.release();
+    Buf<uint64_t>& uniq = other == k1.get() ? k1 : k2;
+    (other == k1.get() ? k2 : k1).release();
     Buf<uint64_t> d1(2 * std::max<int64_t>(m, 1), s), d2(2 * std::max<int64_t>(m, 1), s);
+    uint64_t* rows = d1.get();
     if (m > 0) {
-        k_both_dirs<<<grid_for(m, 256), 256, 0, s>>>(k1.get(), m, bits, d1.get());
+        k_both_dirs<<<grid_for(m, 256), 256, 0, s>>>(uniq.get(), m, bits, d1.get());
         LCC_LAUNCH_CHECK();
-        sort_keys(d1.get(), d2.get(), 2 * m, 2 * bits, s);
+        uniq.release();
+        cub::DoubleBuffer<uint64_t> dd(d1.get(), d2.get());
+        sort_keys_db(dd, 2 * m, 2 * bits, s);
+        rows = dd.Current();
     }
-    k_csr_rows<<<grid_for(2 * m + 1, 256), 256, 0, s>>>(d2.get(), 2 * m, bits, n, indptr, indices);
+    k_csr_rows<<<grid_for(2 * m + 1, 256), 256, 0, s>>>(rows, 2 * m, bits, n, indptr, indices);
     LCC_LAUNCH_CHECK();
     LCC_CUDA(cudaStreamSynchronize(s));
     return 2 * m;
+}
+}  // namespace
+
+int64_t build_csr_from_pairs(int64_t n, int64_t np, const int32_t* u, const int32_t* v, int64_t* indptr,
+                             int32_t* indices, cudaStream_t s) {
+    return csr_from_pairs_impl(n, np, u, v, nullptr, nullptr, indptr, indices, s);
 }
 
 int64_t gen_rmat(int scale, int64_t samples, double a, double b, double c, uint64_t seed, int64_t* indptr,
@@ -177,7 +199,7 @@ int64_t gen_rmat(int scale, int64_t samples, double a, double b, double c, uint6
         k_rmat<<<grid_for(samples, 256, 16), 256, 0, s>>>(scale, samples, t1, t2, t3, seed, u.get(), v.get());
         LCC_LAUNCH_CHECK();
     }
-    return build_csr_from_pairs(n, samples, u.get(), v.get(), indptr, indices, s);
+    return csr_from_pairs_impl(n, samples, u.get(), v.get(), &u, &v, indptr, indices, s);
 }
 
 }  // namespace lcc

@@ -16,10 +16,12 @@ struct RoundStats {
 // best_moves.cu: one best-move iteration over `frontier` (nullptr = all).
 //   sync : D <- C, D[v] <- target for movers, moved[] set; C/K untouched.
 //   async: C and K (2n entries) updated live; D unused.
+// mark (optional, n bytes): zeroed, then every neighbour of a mover is
+// flagged -- the VertexNeighbors frontier fused into the round.
 // Returns the number of movers (synchronises the stream once).
 int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                          const int32_t* frontier, int64_t nF, int schedule, int deg_threshold,
-                         int async_chunks, int32_t* D, uint8_t* moved, RoundStats* st,
+                         int async_chunks, int32_t* D, uint8_t* moved, uint8_t* mark, RoundStats* st,
                          cudaStream_t s);
 
 // apply.cu
@@ -28,17 +30,22 @@ void apply_moves(int64_t n, const int32_t* labels_in, int64_t label_range, const
 int64_t compute_frontier(const lcc_graph& g, int policy, const uint8_t* moved,
                          const int32_t* C_old, const int32_t* C_new, int32_t* frontier,
                          cudaStream_t s);
+int64_t frontier_from_mask(int64_t n, const uint8_t* mark, int32_t* frontier, cudaStream_t s);
 void fill_iota(int32_t* p, int64_t n, cudaStream_t s);
 void fill_k(double* K, const double* k, int64_t n, cudaStream_t s);
 
 // contract.cu
+// The coarse CSR is returned in exact-size pool buffers (cindptr[cn+1],
+// cindices[cnnz], cw[cnnz]); mapping[n] and ck[n] are caller buffers.
 struct Coarse {
     int64_t cn = 0, cnnz = 0;
     double internal_offset = 0.0, total_weight = 0.0;
+    Buf<int64_t> indptr;
+    Buf<int32_t> indices;
+    Buf<double> w;
 };
 Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
-                int32_t* mapping, double* ck, int64_t* cindptr, int32_t* cindices, double* cw,
-                cudaStream_t s);
+                int32_t* mapping, double* ck, cudaStream_t s);
 void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C,
              double* K, cudaStream_t s);
 

@@ -58,6 +58,24 @@ inline void sort_keys(uint64_t* keys_in, uint64_t* keys_out, int64_t n, int end_
     LCC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, keys_in, keys_out, n, 0, end_bit, s));
 }
 
+// Double-buffered variants: no n-sized temp copy (peak = the two buffers);
+// the sorted run is in db.Current() afterwards.
+inline void sort_keys_db(cub::DoubleBuffer<uint64_t>& db, int64_t n, int end_bit, cudaStream_t s) {
+    size_t bytes = 0;
+    LCC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, n, 0, end_bit, s));
+    Buf<unsigned char> tmp(bytes, s);
+    LCC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, db, n, 0, end_bit, s));
+}
+
+template <class V>
+inline void sort_pairs_db(cub::DoubleBuffer<uint64_t>& dk, cub::DoubleBuffer<V>& dv, int64_t n, int end_bit,
+                          cudaStream_t s) {
+    size_t bytes = 0;
+    LCC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, n, 0, end_bit, s));
+    Buf<unsigned char> tmp(bytes, s);
+    LCC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, dk, dv, n, 0, end_bit, s));
+}
+
 template <class V>
 inline void sort_pairs(uint64_t* keys_in, uint64_t* keys_out, V* vals_in, V* vals_out, int64_t n,
                        int end_bit, cudaStream_t s) {

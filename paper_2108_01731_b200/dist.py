@@ -124,7 +124,7 @@ class CudaBackend:
             D = torch.empty(n, dtype=torch.int32, device=self.device)
             _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), C.data_ptr(), K.data_ptr(),
                                                      fr.data_ptr() if fr.numel() else None, fr.numel(),
-                                                     _lib.SYNC, thr, chunks, D.data_ptr(), moved.data_ptr(),
+                                                     _lib.SYNC, thr, chunks, D.data_ptr(), moved.data_ptr(), None,
                                                      ctypes.byref(cnt), None, stream_ptr()))
             return D, moved, cnt.value
         Cw = C.clone()
@@ -132,7 +132,7 @@ class CudaBackend:
         K2[:n] = K
         _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), Cw.data_ptr(), K2.data_ptr(),
                                                  fr.data_ptr() if fr.numel() else None, fr.numel(),
-                                                 _lib.ASYNC, thr, chunks, None, moved.data_ptr(),
+                                                 _lib.ASYNC, thr, chunks, None, moved.data_ptr(), None,
                                                  ctypes.byref(cnt), None, stream_ptr()))
         return Cw, moved, cnt.value
 

@@ -295,7 +295,7 @@ def knn_mixture(n: int = 4_000_000, dim: int = 64, components: int = 10_000, k: 
 def powerlaw_communities_device(n: int = 65_000_000, m_target: int = 1_800_000_000, deg_exponent: float = 2.2,
                                 mu: float = 0.4, max_degree: int = 5214, comm_exponent: float = 1.5,
                                 min_comm: int = 20, max_comm: int = 5000, seed: int = 5,
-                                oversample: float = 1.02) -> DeviceGraph:
+                                oversample: float = 1.34) -> DeviceGraph:
     """Seeded stand-in for friendster (65.6M vertices, 1.8B
     edges; max degree 5,214 per PAPER.md:594).  Expected degrees follow a
     power law (exponent 2.2) capped at max_degree and scaled to mean

@@ -155,10 +155,12 @@ def _labels_of(c, dg: DeviceGraph) -> torch.Tensor:
 
 def best_moves_round(g, p: ClusteringParams, c: Clustering, frontier=None,
                      schedule: Schedule = Schedule.Synchronous, degree_threshold: int = 1000,
-                     async_chunks: int = 0) -> MoveBuffer:
+                     async_chunks: int = 0, nbr_mark: torch.Tensor | None = None) -> MoveBuffer:
     """One Alg. 1 iteration (lines 6-8).  Synchronous: returns D and moved
     flags, leaves ``c`` untouched.  Asynchronous: applies the moves to ``c``
-    in place (labels may temporarily use ids n+v; call ``apply_moves``)."""
+    in place (labels may temporarily use ids n+v; call ``apply_moves``).
+    ``nbr_mark`` (uint8 [n], optional): receives the fused VertexNeighbors
+    frontier mask (see ``frontier_from_mask``)."""
     dg, gs, ps = _prep(g, p)
     schedule = Schedule(schedule)
     n = dg.n
@@ -176,8 +178,8 @@ def best_moves_round(g, p: ClusteringParams, c: Clustering, frontier=None,
     _lib.check(_lib.load().lcc_best_moves_round(
         ctypes.byref(gs), ctypes.byref(ps), c.assignment.data_ptr(), K.data_ptr(),
         None if fr is None else fr.data_ptr(), 0 if fr is None else fr.numel(), int(schedule),
-        int(degree_threshold), int(async_chunks), D.data_ptr(), moved.data_ptr(), ctypes.byref(cnt),
-        None, stream_ptr()))
+        int(degree_threshold), int(async_chunks), D.data_ptr(), moved.data_ptr(),
+        None if nbr_mark is None else nbr_mark.data_ptr(), ctypes.byref(cnt), None, stream_ptr()))
     if schedule == Schedule.Asynchronous:
         D = c.assignment
     return MoveBuffer(D, moved, cnt.value)
@@ -221,6 +223,17 @@ def compute_frontier(policy, moved, g, c_old=None, c_new=None) -> Frontier:
                                                 None if co is None else co.data_ptr(),
                                                 None if cn is None else cn.data_ptr(), out.data_ptr(),
                                                 ctypes.byref(cnt), None, stream_ptr()))
+    return Frontier(n, out[:cnt.value].clone())
+
+
+def frontier_from_mask(mark: torch.Tensor) -> Frontier:
+    """Compact a uint8 device mask (e.g. the ``nbr_mark`` of
+    ``best_moves_round``) into a sorted Frontier."""
+    n = mark.numel()
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=mark.device)
+    cnt = ctypes.c_int64()
+    _lib.check(_lib.load().lcc_frontier_from_mask(n, mark.data_ptr(), out.data_ptr(), ctypes.byref(cnt),
+                                                  stream_ptr()))
     return Frontier(n, out[:cnt.value].clone())
 
 

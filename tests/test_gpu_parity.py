@@ -433,3 +433,31 @@ def test_cfg3_knn_weighted_sync(lam):
     assert o1 == pytest.approx(o0, rel=REL_W)
     agree = np.mean(cl.labels() == C0)
     assert agree > 0.999, agree
+
+
+@pytest.mark.parametrize("window", ["1", "0"])
+@pytest.mark.parametrize("large_min", ["2048", "10240"])
+@pytest.mark.parametrize("schedule", [L.Schedule.Synchronous, L.Schedule.Asynchronous])
+def test_fused_frontier_mask_exact(window, large_min, schedule, monkeypatch):
+    """The VertexNeighbors frontier fused into the round (nbr_mark) equals the
+    oracle's compute_frontier of the round's movers, in every kernel shape."""
+    monkeypatch.setenv("LCC_WINDOW", window)
+    monkeypatch.setenv("LCC_LARGE_MIN", large_min)
+    rng = np.random.default_rng(23)
+    hg = hub_graph(rng, 40_000, hubs=[3, 9, 700, 8000, 123], hub_deg=[300, 2500, 6000, 15_000, 31_000],
+                   base_p=0.0004)
+    g = og(hg)
+    d = dg(hg)
+    for nclus, lam in ((40_000, 0.5), (2000, 0.3), (40_000, 0.99)):
+        C, K = clustered_state(rng, g.n, nclus)
+        c = L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda())
+        mark = torch.empty(g.n, dtype=torch.uint8, device="cuda")
+        mb = L.best_moves_round(d, L.ClusteringParams(lam), c, schedule=schedule, nbr_mark=mark)
+        moved = mb.moved.cpu().numpy()
+        if schedule == L.Schedule.Synchronous:
+            D0, m0, _ = O.sync_round(g, None, lam, C, K)
+            assert np.array_equal(m0, moved)
+        F0 = O.frontier(g, O.VERTEX_NBRS, moved, C, C)
+        F1 = L.frontier_from_mask(mark)
+        assert np.array_equal(F0, F1.ids.cpu().numpy())
+        assert mb.moved_count == int(moved.sum())

@@ -39,6 +39,10 @@
 namespace lcc {
 namespace {
 
+#ifndef LCC_SMALL_EARLYK
+#define LCC_SMALL_EARLYK 1
+#endif
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_MAX = 32;
 constexpr int SMALL_THREADS = 256;
@@ -201,6 +205,11 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 x = ldC<ASYNC>(a.C, nbr, pol_keep);
                 wv = WLoad<WT>::at(a.w, e);
             }
+#if LCC_SMALL_EARLYK
+            // every edge lane issues its cluster's mass gather right away; the
+            // grouping below overlaps it (duplicates of a group are L1/L2 hits)
+            const double kx_early = has_edge ? ldK<ASYNC>(a.K, x, pol_keep) : 0.0;
+#endif
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
                                           : ((uint64_t)(64 + lane) << 32);
             const unsigned grp = __match_any_sync(FULL, key);
@@ -224,7 +233,11 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double g = -INFINITY;
             int32_t gx = NO_CAND;
             if (is_leader && x != cj) {
+#if LCC_SMALL_EARLYK
+                g = dsub(dsub(S, dmul(tj, kx_early)), bj);
+#else
                 g = dsub(dsub(S, dmul(tj, ldK<ASYNC>(a.K, x, pol_keep))), bj);
+#endif
                 gx = x;
             }
             const int32_t seg = has_edge ? j : 32 + lane;
@@ -301,15 +314,17 @@ struct SmemTable<false> {
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(keys + 4 * q), "r"(EMPTY_KEY) : "memory");
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(cnts + 4 * q), "r"(0u) : "memory");
     }
-    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double) const {
+    // returns true when this call claimed the slot (first occurrence of x)
+    __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, double) const {
         uint32_t h = slot_of(x, cap);
+        int32_t prev;
         while (true) {
-            int32_t prev;
             asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
             if (prev == EMPTY_KEY || prev == x) break;
             h = (h + 1 == cap) ? 0 : h + 1;
         }
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts + 4 * h) : "memory");
+        return prev == EMPTY_KEY;
     }
     // U keys at once: each probe round issues the CAS of every pending key
     // back to back (one shared-memory latency per probe depth, not per key)
@@ -364,8 +379,9 @@ struct SmemTable<true> {
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(keys + 4 * q), "r"(EMPTY_KEY) : "memory");
         asm volatile("st.shared.f64 [%0], %1;" ::"r"(vals + 8 * q), "d"(0.0) : "memory");
     }
-    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double wv) const {
+    __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, double wv) const {
         uint32_t h = slot_of(x, cap);
+        bool fresh = false;
         while (true) {
             int32_t kq;
             asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * h));
@@ -373,11 +389,13 @@ struct SmemTable<true> {
             if (kq == EMPTY_KEY) {
                 int32_t prev;
                 asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+                fresh = prev == EMPTY_KEY;
                 if (prev == EMPTY_KEY || prev == x) break;
             }
             h = (h + 1 == cap) ? 0 : h + 1;
         }
         asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h), "d"(wv) : "memory");
+        return fresh;
     }
     template <int U>
     __device__ __forceinline__ void insert_batch(uint32_t cap, const int32_t (&x)[U], const double (&wv)[U],
@@ -532,8 +550,11 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
-                if (u[j] == c) sc += wv[j];
-                else tab.insert(cap, u[j], wv[j]);
+                if (u[j] == c) {
+                    sc += wv[j];
+                } else {
+                    tab.insert(cap, u[j], wv[j]);
+                }
             }
         }
 #pragma unroll
@@ -874,8 +895,11 @@ __device__ __forceinline__ int64_t owner_of(const int64_t* off, int64_t n, int64
     return lo;
 }
 
+#ifndef LCC_LARGE_MINB
+#define LCC_LARGE_MINB 4
+#endif
 template <class WT, bool ASYNC>
-__global__ void __launch_bounds__(LARGE_THREADS)
+__global__ void __launch_bounds__(LARGE_THREADS, LCC_LARGE_MINB)
 k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
     constexpr int UL = 8;
     const uint64_t pol_keep = policy_evict_last();
@@ -1170,7 +1194,10 @@ void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, 
 
 constexpr int B5_CAP = 16384;
 constexpr int64_t MED_MAX = (B5_CAP * 5) / 8;      // 10240: load factor <= 0.625
-constexpr int64_t LARGE_TABLE_BYTES = 64ll << 20;  // per batch: stays L2-resident
+#ifndef LCC_LARGE_TABLE_MB
+#define LCC_LARGE_TABLE_MB 256
+#endif
+constexpr int64_t LARGE_TABLE_BYTES = (int64_t)LCC_LARGE_TABLE_MB << 20;  // per batch: stays L2-resident
 
 // bin -> kernel shape.  Shared memory per group = CAP * (4 key + 4|8 value +
 // 2 slot-list) bytes; GROUPS chosen so 2-3 CTAs fit per SM.

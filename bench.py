@@ -444,13 +444,16 @@ def run_ours(args):
 
         e2e_step()  # warm-up (pool growth)
         times, edges_sum, stats = [], 0, None
-        for _ in range(max(1, args.e2e_steps)):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            cl = e2e_step()
-            times.append(time.perf_counter() - t0)
-            stats = cl.meta["stats"]
-            edges_sum += stats.edges_scanned
+        with ClockSampler(lrank) as clk_e2e:
+            for _ in range(max(1, args.e2e_steps)):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                cl = e2e_step()
+                times.append(time.perf_counter() - t0)
+                stats = cl.meta["stats"]
+                edges_sum += stats.edges_scanned
+        if os.environ.get("LCC_BENCH_DEBUG"):
+            print("e2e clock samples:", clk_e2e.lines, file=sys.stderr)
         t_e2e = sum(times) / len(times)
         e_t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         ed_t = torch.tensor([edges_sum / len(times)], dtype=torch.float64, device="cuda")
@@ -458,6 +461,7 @@ def run_ours(args):
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(ed_t, op=dist.ReduceOp.SUM)
         cl = None
+        L.release_memory()
         torch.cuda.empty_cache()
         obj = L.cc_objective(dg if dg is not None else hgr, p, torch.as_tensor(out_h).cuda())
         e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
@@ -467,7 +471,7 @@ def run_ours(args):
                "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
                "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
                "device_ms_best_move_kernels": stats.ms_kernels,
-               "objective": obj, "clusters": int(np.unique(out_h.numpy()).size),
+               "objective": obj, "clusters": int(np.unique(out_h.numpy()).size), "clocks": clk_e2e.summary(),
                "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
                        "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
 

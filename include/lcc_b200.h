@@ -92,6 +92,10 @@ typedef struct {
 } lcc_stats;
 
 int lcc_abi_version(void);
+/* Hand the library's cached device scratch (stream-ordered pool) back to
+ * the driver.  Calls keep up to LCC_POOL_KEEP_GB (default 64) GB cached
+ * between them: fresh pool memory costs ~6 ms per GB to map.             */
+lcc_status lcc_release_memory(void);
 const char* lcc_last_error(void);
 /* Number of this library's own kernel launches so far in this process
  * (diagnostics; CUB helper kernels are not counted).                       */

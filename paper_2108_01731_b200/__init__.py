@@ -12,13 +12,13 @@ from .graph import DeviceGraph, GraphError
 from .objective import (Clustering, ClusteringParams, cc_objective, clustering_from_labels, modularity_params,
                         modularity_value, move_delta, rescaled_weight, singletons)
 from .louvain_par import (CompressedLevel, Frontier, FrontierPolicy, MoveBuffer, ParOptions, RunStats, Schedule,
-                          apply_moves, best_moves_round, compute_frontier, frontier_from_mask, par_best_moves, par_compress,
+                          apply_moves, best_moves_round, compute_frontier, frontier_from_mask, par_best_moves, release_memory, par_compress,
                           par_flatten, parallel_cc, per_vertex_best_target)
 
 __all__ = [
     "NativeLibraryError", "DeviceGraph", "GraphError", "Clustering", "ClusteringParams", "cc_objective",
     "clustering_from_labels", "modularity_params", "modularity_value", "move_delta", "rescaled_weight",
     "singletons", "CompressedLevel", "Frontier", "FrontierPolicy", "MoveBuffer", "ParOptions", "RunStats",
-    "Schedule", "apply_moves", "best_moves_round", "compute_frontier", "frontier_from_mask", "par_best_moves",
+    "Schedule", "apply_moves", "best_moves_round", "compute_frontier", "frontier_from_mask", "par_best_moves", "release_memory",
     "par_compress", "par_flatten", "parallel_cc", "per_vertex_best_target",
 ]

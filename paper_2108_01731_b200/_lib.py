@@ -23,7 +23,7 @@ EXPORTS = (
     "lcc_abi_version", "lcc_last_error", "lcc_kernel_launches", "lcc_best_moves_round", "lcc_apply_moves",
     "lcc_compute_frontier", "lcc_par_best_moves", "lcc_par_compress", "lcc_par_flatten",
     "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_gen_powerlaw_communities",
-    "lcc_build_csr_from_pairs", "lcc_frontier_from_mask",
+    "lcc_build_csr_from_pairs", "lcc_frontier_from_mask", "lcc_release_memory",
 )
 
 
@@ -83,6 +83,7 @@ def load() -> ctypes.CDLL:
         "lcc_kernel_launches": (ctypes.c_int64, []),
         "lcc_best_moves_round": (ctypes.c_int, [G, PR, P, P, P, I64, I32, I32, I32, P, P, P, pI64, ST, P]),
         "lcc_frontier_from_mask": (ctypes.c_int, [I64, P, P, pI64, P]),
+        "lcc_release_memory": (ctypes.c_int, []),
         "lcc_apply_moves": (ctypes.c_int, [I64, P, I64, P, P, P, P]),
         "lcc_compute_frontier": (ctypes.c_int, [G, I32, P, P, P, P, pI64, P]),
         "lcc_par_best_moves": (ctypes.c_int, [G, PR, O, P, P, pI32, ST, P]),

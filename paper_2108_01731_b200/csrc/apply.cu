@@ -67,7 +67,7 @@ struct ListDeg {
 struct MarkNbr {
     const int32_t* indices;
     uint8_t* mark;
-    __device__ __forceinline__ void operator()(int64_t, int64_t e) const { mark[__ldg(indices + e)] = 1; }
+    __device__ __forceinline__ void operator()(int64_t, int64_t e, int64_t) const { mark[__ldg(indices + e)] = 1; }
     __device__ __forceinline__ void flush() const {}
 };
 

@@ -40,7 +40,7 @@ namespace lcc {
 namespace {
 
 #ifndef LCC_SMALL_EARLYK
-#define LCC_SMALL_EARLYK 1
+#define LCC_SMALL_EARLYK 0
 #endif
 
 constexpr unsigned FULL = 0xffffffffu;

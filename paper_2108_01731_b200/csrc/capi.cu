@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary declared in include/lcc_b200.h.
 // Exceptions never cross it: each call returns an lcc_status and leaves a
 // one-line message in a thread-local buffer (lcc_last_error()).
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -16,15 +17,20 @@ long long& launch_counter() {
 namespace {
 thread_local std::string g_err;
 
-// Keep freed scratch in the device's stream-ordered pool for the whole call:
-// the default release threshold (0) hands memory back to the driver at every
-// synchronisation, so each best-move iteration (and each contraction, whose
-// key/value buffers are several GB) would pay for fresh physical mappings --
-// measured 267 ms for a 468M-entry weighted contraction with a 16 GB
-// threshold vs ~50 ms without re-mapping.  Nothing is released inside a call;
-// when the call returns (or fails) the pool is trimmed to POOL_KEEP so the
-// one-off peaks can be used by the caller's allocator (e.g. PyTorch).
-constexpr uint64_t POOL_KEEP = 16ull << 30;
+// Keep freed scratch in the device's stream-ordered pool: fresh pool memory
+// costs ~6 ms per GB to map on B200 (measured: 16 GB 93 ms, reused 2.3 ms),
+// so re-mapping the several-GB contraction buffers every call cost more than
+// the contraction itself.  Nothing is released inside a call; when a call
+// returns the pool is trimmed to pool_keep() (default 64 GB, LCC_POOL_KEEP_GB)
+// and lcc_release_memory() hands everything back on request.  An allocation
+// that fails trims the pool and retries once (common.cuh Buf::alloc).
+uint64_t pool_keep() {
+    static uint64_t keep = [] {
+        const char* e = getenv("LCC_POOL_KEEP_GB");  // tuning / memory-tight callers
+        return (e ? (uint64_t)atoll(e) : 64ull) << 30;
+    }();
+    return keep;
+}
 
 cudaMemPool_t pool_once() {
     static bool done[64] = {false};
@@ -46,7 +52,7 @@ cudaMemPool_t pool_once() {
 struct TrimOnExit {
     cudaMemPool_t pool;
     ~TrimOnExit() {
-        if (pool) cudaMemPoolTrimTo(pool, POOL_KEEP);
+        if (pool) cudaMemPoolTrimTo(pool, pool_keep());
     }
 };
 
@@ -105,6 +111,14 @@ lcc::Options to_opts(const lcc_options* o) {
 extern "C" {
 
 int lcc_abi_version(void) { return LCC_ABI_VERSION; }
+
+lcc_status lcc_release_memory(void) {
+    return guard([&] {
+        cudaMemPool_t pool = pool_once();
+        LCC_CUDA(cudaDeviceSynchronize());
+        if (pool) LCC_CUDA(cudaMemPoolTrimTo(pool, 0));
+    });
+}
 int64_t lcc_kernel_launches(void) { return lcc::launch_counter(); }
 const char* lcc_last_error(void) { return g_err.c_str(); }
 

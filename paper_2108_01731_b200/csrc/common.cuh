@@ -53,7 +53,21 @@ struct Buf {
         release();
         s = st;
         n = count;
-        if (count) LCC_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * count, st));
+        if (!count) return;
+        cudaError_t e = cudaMallocAsync((void**)&p, sizeof(T) * count, st);
+        if (e == cudaErrorMemoryAllocation) {
+            // pool fragmentation: finish pending frees, hand every unused pool
+            // block back to the driver and try once more
+            cudaGetLastError();
+            cudaStreamSynchronize(st);
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+                cudaMemPoolTrimTo(pool, 0);
+            e = cudaMallocAsync((void**)&p, sizeof(T) * count, st);
+        }
+        if (e != cudaSuccess) p = nullptr;
+        LCC_CUDA(e);
     }
     void release() {
         if (p) cudaFreeAsync(p, s);
@@ -71,6 +85,19 @@ struct Buf {
     T* get() const { return p; }
     operator T*() const { return p; }
 };
+
+// stream-ordered pool occupancy (GB reserved, GB in use) for traces
+inline void pool_gb(double& reserved, double& used) {
+    reserved = used = 0.0;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t r = 0, u = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u);
+    reserved = r / 1073741824.0;
+    used = u / 1073741824.0;
+}
 
 inline int num_sms() {
     static int sms = 0;

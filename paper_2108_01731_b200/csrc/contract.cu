@@ -10,6 +10,8 @@
 // neighbour id -- the same sort + segmented-sum contract as the reference's
 // build_graph_arrays (graph.py:126-164).
 #include <cub/cub.cuh>
+#include <cstdio>
+#include <cstdlib>
 
 #include "edgemap.cuh"
 #include "internal.cuh"
@@ -47,7 +49,7 @@ struct EdgeKey {
     double* intra_w;
     unsigned long long cnt = 0;
     double acc = 0.0;
-    __device__ __forceinline__ void operator()(int64_t v, int64_t e) {
+    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
         const uint64_t a = (uint32_t)__ldg(mapping + v);
         const uint64_t b = (uint32_t)__ldg(mapping + __ldg(indices + e));
         const double wv = WLoad<WT>::at(w, e);
@@ -98,11 +100,37 @@ struct RunHead {
     }
 };
 
+// LCC_TRACE: device time of each contraction phase on stderr
+struct PhaseTrace {
+    cudaStream_t s;
+    bool on;
+    cudaEvent_t last = nullptr;
+    explicit PhaseTrace(cudaStream_t st) : s(st), on(getenv("LCC_TRACE") != nullptr) {
+        if (on) { cudaEventCreate(&last); cudaEventRecord(last, s); }
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        cudaEventSynchronize(e);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, last, e);
+        double r, u;
+        pool_gb(r, u);
+        fprintf(stderr, "[lcc]     compress %-10s %.2f ms  (pool %.1f GB reserved, %.1f used)\n", what, ms, r, u);
+        cudaEventDestroy(last);
+        last = e;
+    }
+    ~PhaseTrace() { if (last) cudaEventDestroy(last); }
+};
+
 template <class WT>
 Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
                      int32_t* mapping, double* ck, cudaStream_t s) {
     const int64_t n = g.n, nnz = g.nnz;
     Coarse out;
+    PhaseTrace tr(s);
     // 1. dense renumbering by smallest member
     int64_t cn = 0;
     {
@@ -137,6 +165,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                       EdgeKey<WT>{g.indices, g.weights, mapping, bits, sentinel, ka.get(), va.get(),
                                   dintra.get(), dacc.get()}, s);
+        tr.mark("keys");
         // 3. stable radix sort on the 2*bits live bits, double-buffered (peak
         //    memory = the two key (+value) buffers, no hidden n-sized temp)
         cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());
@@ -145,6 +174,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         else sort_keys_db(dk, nnz, 2 * bits, s);
         Buf<uint64_t>& ksorted = dk.Current() == ka.get() ? ka : kb;
         (dk.Current() == ka.get() ? kb : ka).release();
+        tr.mark("sort");
         Buf<double>& vsorted = dv.Current() == va.get() ? va : vb;
         if (WLoad<WT>::weighted) (dv.Current() == va.get() ? vb : va).release();
         // 4. count the runs, then reduce by key into exact-size outputs;
@@ -186,6 +216,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         }
         ksorted.release();
         vsorted.release();
+        tr.mark("reduce");
         out.indices.alloc(std::max<int64_t>(R, 1), s);
         k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(ukeys.get(), R, bits, cn, out.indptr.get(),
                                                          out.indices.get());

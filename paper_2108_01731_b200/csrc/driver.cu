@@ -136,8 +136,13 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         fill_k(K.get(), k, n, s);
         if (st) st->levels += 1;
         const bool moved = par_best_moves(g, k, lam, o, C.get(), K.get(), st, s);
-        if (trace) fprintf(stderr, "[lcc] level n=%lld nnz=%lld best_moves %.2f ms\n", (long long)n,
-                           (long long)g.nnz, tl.stop());
+        if (trace) {
+            const float ms = tl.stop();
+            double r, u;
+            pool_gb(r, u);
+            fprintf(stderr, "[lcc] level n=%lld nnz=%lld best_moves %.2f ms (pool %.1f/%.1f GB)\n", (long long)n,
+                    (long long)g.nnz, ms, r, u);
+        }
         if (!moved) break;  // Alg. 1 line 13
         EventTimer tc(s);
         // contraction straight into exact-size buffers

@@ -25,7 +25,9 @@ __device__ __forceinline__ int64_t upper_idx(const int64_t* off, int64_t lo, int
     return lo;
 }
 
-// F: functor with  __device__ void operator()(int64_t v, int64_t e)  and
+// F: functor with  __device__ void operator()(int64_t v, int64_t e, int64_t pos)
+//    (v = list entry's vertex, e = its CSR edge index, pos = position in the
+//    concatenated edge space [0, off[nlist]))  and
 //                  __device__ void flush()   (called once per thread at the end)
 // When the tile's window of `off` fits in shared memory (always the case for
 // lists whose entries all have degree >= 1: at most EM_TILE + 1 entries) the
@@ -66,11 +68,11 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
                         const int mid = (a + b) >> 1;
                         if (s_off[mid] <= e) a = mid; else b = mid;
                     }
-                    f((int64_t)s_v[a], s_row[a] + e);
+                    f((int64_t)s_v[a], s_row[a] + e, e);
                 } else {
                     const int64_t li = upper_idx(off, lo, hi, e);
                     const int64_t v = list ? (int64_t)__ldg(list + li) : li;
-                    f(v, __ldg(indptr + v) + (e - __ldg(off + li)));
+                    f(v, __ldg(indptr + v) + (e - __ldg(off + li)), e);
                 }
             }
         }

@@ -226,6 +226,12 @@ def compute_frontier(policy, moved, g, c_old=None, c_new=None) -> Frontier:
     return Frontier(n, out[:cnt.value].clone())
 
 
+def release_memory() -> None:
+    """Return the library's cached device scratch to the driver (calls keep
+    up to LCC_POOL_KEEP_GB, default 64 GB, cached between them)."""
+    _lib.check(_lib.load().lcc_release_memory())
+
+
 def frontier_from_mask(mark: torch.Tensor) -> Frontier:
     """Compact a uint8 device mask (e.g. the ``nbr_mark`` of
     ``best_moves_round``) into a sorted Frontier."""

@@ -22,8 +22,10 @@ thread_local std::string g_err;
 // so re-mapping the several-GB contraction buffers every call cost more than
 // the contraction itself.  Nothing is released inside a call; when a call
 // returns the pool is trimmed to pool_keep() (default 64 GB, LCC_POOL_KEEP_GB)
-// and lcc_release_memory() hands everything back on request.  An allocation
-// that fails trims the pool and retries once (common.cuh Buf::alloc).
+// and lcc_release_memory() hands everything back on request.  Blocks of
+// >= 64 MB are additionally cached by the library (memory.cu), because the
+// pool re-maps pages whenever a request does not fit a free virtual range.
+// An allocation that fails trims both and retries once (memory.cu).
 uint64_t pool_keep() {
     static uint64_t keep = [] {
         const char* e = getenv("LCC_POOL_KEEP_GB");  // tuning / memory-tight callers
@@ -52,6 +54,7 @@ cudaMemPool_t pool_once() {
 struct TrimOnExit {
     cudaMemPool_t pool;
     ~TrimOnExit() {
+        lcc::trim_cache(pool_keep(), nullptr);
         if (pool) cudaMemPoolTrimTo(pool, pool_keep());
     }
 };
@@ -115,6 +118,7 @@ int lcc_abi_version(void) { return LCC_ABI_VERSION; }
 lcc_status lcc_release_memory(void) {
     return guard([&] {
         cudaMemPool_t pool = pool_once();
+        lcc::trim_cache(0, nullptr);
         LCC_CUDA(cudaDeviceSynchronize());
         if (pool) LCC_CUDA(cudaMemPoolTrimTo(pool, 0));
     });

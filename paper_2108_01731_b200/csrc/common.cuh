@@ -40,12 +40,29 @@ long long& launch_counter();
     do { if (!(cond)) throw ::lcc::Invalid(msg); } while (0)
 
 // ---------------------------------------------------------------------------
-// stream-ordered scratch buffer (cudaMallocAsync pool; freed on scope exit)
+// device scratch.  Small buffers come straight from the stream-ordered pool
+// (cudaMallocAsync).  Large ones (>= 64 MB: contraction keys/values, hub
+// tables, per-round arrays at scale) are cached by this library: the pool
+// can reuse freed memory, but when a request does not fit a free virtual
+// range it maps physical pages afresh, ~6 ms per GB on B200 -- measured
+// 100-700 ms per contraction for buffers the previous level had just freed.
+// Cached blocks are reused best-fit (capacity <= 2x the request) in stream
+// order (an event orders reuse on another stream) and handed back by
+// trim_cache() at the end of every C-ABI call above the keep limit.
 // ---------------------------------------------------------------------------
+constexpr size_t CACHE_MIN_BYTES = 64ull << 20;
+void* cache_alloc(size_t bytes, cudaStream_t s, size_t* cap);
+void cache_free(void* p, size_t cap, cudaStream_t s);
+void trim_cache(size_t keep_bytes, cudaStream_t s);
+size_t cache_bytes();
+
+void* pool_alloc(size_t bytes, cudaStream_t s);  // cudaMallocAsync with one trim-and-retry
+
 template <class T>
 struct Buf {
     T* p = nullptr;
     size_t n = 0;
+    size_t cap = 0;  // bytes actually held (cached blocks may be larger)
     cudaStream_t s = nullptr;
     Buf() = default;
     Buf(size_t count, cudaStream_t st) { alloc(count, st); }
@@ -54,32 +71,29 @@ struct Buf {
         s = st;
         n = count;
         if (!count) return;
-        cudaError_t e = cudaMallocAsync((void**)&p, sizeof(T) * count, st);
-        if (e == cudaErrorMemoryAllocation) {
-            // pool fragmentation: finish pending frees, hand every unused pool
-            // block back to the driver and try once more
-            cudaGetLastError();
-            cudaStreamSynchronize(st);
-            int dev = 0;
-            cudaMemPool_t pool;
-            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-                cudaMemPoolTrimTo(pool, 0);
-            e = cudaMallocAsync((void**)&p, sizeof(T) * count, st);
+        const size_t bytes = sizeof(T) * count;
+        if (bytes >= CACHE_MIN_BYTES) {
+            p = static_cast<T*>(cache_alloc(bytes, st, &cap));
+        } else {
+            p = static_cast<T*>(pool_alloc(bytes, st));
+            cap = bytes;
         }
-        if (e != cudaSuccess) p = nullptr;
-        LCC_CUDA(e);
     }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) {
+            if (cap >= CACHE_MIN_BYTES) cache_free(p, cap, s);
+            else cudaFreeAsync(p, s);
+        }
         p = nullptr;
         n = 0;
+        cap = 0;
     }
     ~Buf() { release(); }
     Buf(const Buf&) = delete;
     Buf& operator=(const Buf&) = delete;
-    Buf(Buf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    Buf(Buf&& o) noexcept : p(o.p), n(o.n), cap(o.cap), s(o.s) { o.p = nullptr; o.n = 0; o.cap = 0; }
     Buf& operator=(Buf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; cap = o.cap; s = o.s; o.p = nullptr; o.n = 0; o.cap = 0; }
         return *this;
     }
     T* get() const { return p; }

@@ -162,10 +162,20 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         Buf<double> va, vb;
         if (WLoad<WT>::weighted) { va.alloc(nnz, s); vb.alloc(nnz, s); }
         const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
+        cudaEvent_t k0 = nullptr, k1 = nullptr;
+        if (tr.on) { cudaEventCreate(&k0); cudaEventCreate(&k1); cudaEventRecord(k0, s); }
         edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                       EdgeKey<WT>{g.indices, g.weights, mapping, bits, sentinel, ka.get(), va.get(),
                                   dintra.get(), dacc.get()}, s);
+        if (tr.on) cudaEventRecord(k1, s);
         tr.mark("keys");
+        if (tr.on) {
+            float kms = 0.f;
+            cudaEventElapsedTime(&kms, k0, k1);
+            fprintf(stderr, "[lcc]       (EdgeKey kernel alone %.2f ms)\n", kms);
+            cudaEventDestroy(k0);
+            cudaEventDestroy(k1);
+        }
         // 3. stable radix sort on the 2*bits live bits, double-buffered (peak
         //    memory = the two key (+value) buffers, no hidden n-sized temp)
         cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());

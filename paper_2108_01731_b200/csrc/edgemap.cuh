@@ -58,18 +58,33 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
             }
         }
         __syncthreads();
-#pragma unroll 2
-        for (int j = 0; j < EM_ITEMS; ++j) {
-            const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
-            if (e < t1) {
-                if (cached) {
-                    int a = 0, b = (int)wn;  // largest a with s_off[a] <= e
+        if (cached) {
+            // owners of all EM_ITEMS positions first (shared-memory searches),
+            // then the functor calls as straight-line code, so their global
+            // gathers are all in flight together
+            int own[EM_ITEMS];
+#pragma unroll
+            for (int j = 0; j < EM_ITEMS; ++j) {
+                const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+                int a = 0, b = (int)wn;  // largest a with s_off[a] <= e
+                if (e < t1) {
                     while (b - a > 1) {
                         const int mid = (a + b) >> 1;
                         if (s_off[mid] <= e) a = mid; else b = mid;
                     }
-                    f((int64_t)s_v[a], s_row[a] + e, e);
-                } else {
+                }
+                own[j] = a;
+            }
+#pragma unroll
+            for (int j = 0; j < EM_ITEMS; ++j) {
+                const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+                if (e < t1) f((int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+            }
+        } else {
+#pragma unroll 2
+            for (int j = 0; j < EM_ITEMS; ++j) {
+                const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+                if (e < t1) {
                     const int64_t li = upper_idx(off, lo, hi, e);
                     const int64_t v = list ? (int64_t)__ldg(list + li) : li;
                     f(v, __ldg(indptr + v) + (e - __ldg(off + li)), e);

@@ -35,7 +35,10 @@ typedef enum {
     LCC_ERR_OOM = 3      /* device allocation failed                        */
 } lcc_status;
 
-typedef enum { LCC_W_NONE = 0, LCC_W_F32 = 1, LCC_W_F64 = 2 } lcc_wtype;
+/* LCC_W_U32: non-negative integer weights (multi-edge counts, e.g. every
+ * coarse level of an unweighted graph), summed exactly in 32-bit integers;
+ * requires 2 * total_weight < 2^32.                                          */
+typedef enum { LCC_W_NONE = 0, LCC_W_F32 = 1, LCC_W_F64 = 2, LCC_W_U32 = 3 } lcc_wtype;
 /* ParOptions.schedule */
 typedef enum { LCC_SYNC = 0, LCC_ASYNC = 1 } lcc_schedule;
 /* ParOptions.frontier_policy */
@@ -53,7 +56,7 @@ typedef struct {
     int64_t nnz;
     const int64_t* indptr;  /* [n+1]                                       */
     const int32_t* indices; /* [nnz], sorted within each row, no self loops */
-    const void* weights;    /* [nnz] float or double, or NULL              */
+    const void* weights;    /* [nnz] float, double or uint32, or NULL      */
     int32_t wtype;          /* lcc_wtype                                    */
     int32_t _pad;
     double total_weight;    /* sum of w over undirected edges               */

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("LCC_LIB_PATH") or os.path.join(_HERE, "_lib", "liblcc_b200.so")
 
 LCC_OK, LCC_ERR_INVALID, LCC_ERR_CUDA, LCC_ERR_OOM = 0, 1, 2, 3
-W_NONE, W_F32, W_F64 = 0, 1, 2
+W_NONE, W_F32, W_F64, W_U32 = 0, 1, 2, 3
 SYNC, ASYNC = 0, 1
 FRONTIER_ALL, FRONTIER_VERTEX_NBRS, FRONTIER_CLUSTER_NBRS = 0, 1, 2
 

@@ -299,7 +299,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 
 constexpr uint64_t EMPTY64 = ~0ull;  // key -1 (never a cluster id); memset(0xff)-able
 
-template <bool WEIGHTED>
+template <bool FSUM>
 struct SmemTable;
 
 template <>
@@ -315,7 +315,7 @@ struct SmemTable<false> {
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(cnts + 4 * q), "r"(0u) : "memory");
     }
     // returns true when this call claimed the slot (first occurrence of x)
-    __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, double) const {
+    __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, uint32_t add) const {
         uint32_t h = slot_of(x, cap);
         int32_t prev;
         while (true) {
@@ -323,36 +323,10 @@ struct SmemTable<false> {
             if (prev == EMPTY_KEY || prev == x) break;
             h = (h + 1 == cap) ? 0 : h + 1;
         }
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts + 4 * h) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add) : "memory");
         return prev == EMPTY_KEY;
     }
-    // U keys at once: each probe round issues the CAS of every pending key
-    // back to back (one shared-memory latency per probe depth, not per key)
-    template <int U>
-    __device__ __forceinline__ void insert_batch(uint32_t cap, const int32_t (&x)[U], const double (&)[U],
-                                                 unsigned pending) const {
-        uint32_t h[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) h[j] = (pending >> j & 1u) ? slot_of(x[j], cap) : 0u;
-        while (pending) {
-            int32_t prev[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j)
-                if (pending >> j & 1u)
-                    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev[j]) : "r"(keys + 4 * h[j]), "r"(EMPTY_KEY), "r"(x[j]) : "memory");
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                if (!(pending >> j & 1u)) continue;
-                if (prev[j] == EMPTY_KEY || prev[j] == x[j]) {
-                    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts + 4 * h[j]) : "memory");
-                    pending &= ~(1u << j);
-                } else {
-                    h[j] = (h[j] + 1 == cap) ? 0 : h[j] + 1;
-                }
-            }
-        }
-    }
-    __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
+        __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
         int32_t kq;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
         if (kq == EMPTY_KEY) return false;
@@ -397,31 +371,7 @@ struct SmemTable<true> {
         asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h), "d"(wv) : "memory");
         return fresh;
     }
-    template <int U>
-    __device__ __forceinline__ void insert_batch(uint32_t cap, const int32_t (&x)[U], const double (&wv)[U],
-                                                 unsigned pending) const {
-        uint32_t h[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) h[j] = (pending >> j & 1u) ? slot_of(x[j], cap) : 0u;
-        while (pending) {
-            int32_t prev[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j)
-                if (pending >> j & 1u)
-                    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev[j]) : "r"(keys + 4 * h[j]), "r"(EMPTY_KEY), "r"(x[j]) : "memory");
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                if (!(pending >> j & 1u)) continue;
-                if (prev[j] == EMPTY_KEY || prev[j] == x[j]) {
-                    asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h[j]), "d"(wv[j]) : "memory");
-                    pending &= ~(1u << j);
-                } else {
-                    h[j] = (h[j] + 1 == cap) ? 0 : h[j] + 1;
-                }
-            }
-        }
-    }
-    __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
+        __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
         int32_t kq;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
         if (kq == EMPTY_KEY) return false;
@@ -439,16 +389,14 @@ template <>
 struct GlobalTable<false> {
     static constexpr int bytes_per_slot = 8;
     unsigned long long* tab;
-    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, double) const {
-        insert_from(cap, x, slot_of(x, cap));
-    }
-    __device__ __forceinline__ void insert_from(uint32_t cap, int32_t x, uint32_t h) const {
-        const unsigned long long want = ((unsigned long long)(uint32_t)x << 32) | 1ull;
+    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, uint32_t add) const {
+        uint32_t h = slot_of(x, cap);
+        const unsigned long long want = ((unsigned long long)(uint32_t)x << 32) | add;
         while (true) {
             const unsigned long long prev = atomicCAS(tab + h, (unsigned long long)EMPTY64, want);
             if (prev == EMPTY64) return;
             if ((int32_t)(prev >> 32) == x) {
-                atomicAdd(tab + h, 1ull);
+                atomicAdd(tab + h, (unsigned long long)add);
                 return;
             }
             h = (h + 1 == cap) ? 0 : h + 1;
@@ -496,13 +444,14 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // ===========================================================================
 template <class WT, int CAP, int GROUPS>
 constexpr size_t group_smem_bytes() {
-    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::weighted>::bytes_per_slot;
+    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot;
 }
 
 template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
 __global__ void __launch_bounds__(GW * 32 * GROUPS, MINB)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
-    constexpr bool WEIGHTED = WLoad<WT>::weighted;
+    constexpr bool FSUM = WLoad<WT>::fsum;
+    using TW = typename WLoad<WT>::TW;
     constexpr int GT = GW * 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_g[GROUPS * GW];
@@ -512,8 +461,8 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const int gt = threadIdx.x % GT;
     const int wig = gt >> 5;
     const int lane = threadIdx.x & 31;
-    SmemTable<WEIGHTED> tab;
-    tab.init_cap(smem + (size_t)gid * CAP * SmemTable<WEIGHTED>::bytes_per_slot, CAP);
+    SmemTable<FSUM> tab;
+    tab.init_cap(smem + (size_t)gid * CAP * SmemTable<FSUM>::bytes_per_slot, CAP);
     auto gsync = [&]() {
         if constexpr (GW == 1) __syncwarp();
         else named_sync(1 + gid, GT);
@@ -536,12 +485,12 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
         for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
             int32_t u[U];
-            double wv[U];
+            TW wv[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 const int64_t e = e0 + (int64_t)j * GT;
                 u[j] = e < end ? ld_stream_i32(a.indices + e, pol_stream) : -1;
-                wv[j] = e < end ? WLoad<WT>::at(a.w, e) : 0.0;
+                wv[j] = e < end ? WLoad<WT>::tw(a.w, e) : TW(0);
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
@@ -551,7 +500,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             for (int j = 0; j < U; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) {
-                    sc += wv[j];
+                    sc += WLoad<WT>::f64(wv[j]);
                 } else {
                     tab.insert(cap, u[j], wv[j]);
                 }
@@ -656,22 +605,23 @@ __device__ __forceinline__ double unord_gain(unsigned long long k) {
     return __longlong_as_double((long long)b);
 }
 
-template <bool WEIGHTED>
+template <bool FSUM>
 constexpr size_t window_smem_bytes() {
     // keys u32 + counts u32 (or sums f64) + gain f64
-    return (size_t)WIN_CAP * (4 + (WEIGHTED ? 8 : 4) + 8);
+    return (size_t)WIN_CAP * (4 + (FSUM ? 8 : 4) + 8);
 }
 
 template <class WT, bool ASYNC>
 __global__ void __launch_bounds__(WIN_THREADS)
 k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__ off,
          const int64_t* __restrict__ wstart, int64_t w0, int64_t w1) {
-    constexpr bool WEIGHTED = WLoad<WT>::weighted;
+    constexpr bool FSUM = WLoad<WT>::fsum;
+    using TW = typename WLoad<WT>::TW;
     extern __shared__ __align__(16) unsigned char smem[];
     double* gval = reinterpret_cast<double*>(smem);
     double* sums = reinterpret_cast<double*>(smem + (size_t)WIN_CAP * 8);          // weighted
     uint32_t* cnts = reinterpret_cast<uint32_t*>(smem + (size_t)WIN_CAP * 8);      // unweighted
-    uint32_t* keys = reinterpret_cast<uint32_t*>(smem + (size_t)WIN_CAP * (WEIGHTED ? 16 : 12));
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem + (size_t)WIN_CAP * (FSUM ? 16 : 12));
     __shared__ int64_t s_start[WIN_MAXV];
     __shared__ int32_t s_loc[WIN_MAXV + 1];
     __shared__ int32_t s_v[WIN_MAXV], s_c[WIN_MAXV];
@@ -683,7 +633,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
     const uint32_t keys_s = smem_u32(keys), cnts_s = smem_u32(cnts), sums_s = smem_u32(sums);
     for (int q = tid; q < WIN_CAP; q += WIN_THREADS) {
         keys[q] = KEY_EMPTY;
-        if constexpr (WEIGHTED) sums[q] = 0.0;
+        if constexpr (FSUM) sums[q] = 0.0;
         else cnts[q] = 0;
     }
     const uint64_t pol_keep = policy_evict_last();
@@ -721,7 +671,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             const int p0 = tid * WIN_ITEMS;
             int32_t u[WIN_ITEMS];
             int slot[WIN_ITEMS];
-            double wv[WIN_ITEMS];
+            TW wv[WIN_ITEMS];
             int sl = 0;
             if (p0 < E) {
                 int lo = 0, hi = nv;  // last sl with s_loc[sl] <= p0
@@ -735,13 +685,13 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             for (int j = 0; j < WIN_ITEMS; ++j) {
                 const int p = p0 + j;
                 u[j] = -1;
-                wv[j] = 0.0;
+                wv[j] = TW(0);
                 slot[j] = 0;
                 if (p < E) {
                     while (p >= s_loc[sl + 1]) ++sl;
                     const int64_t e = s_start[sl] + (p - s_loc[sl]);
                     u[j] = ld_stream_i32(a.indices + e, pol_stream);
-                    wv[j] = WLoad<WT>::at(a.w, e);
+                    wv[j] = WLoad<WT>::tw(a.w, e);
                     slot[j] = sl;
                 }
             }
@@ -752,8 +702,8 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                 if (u[j] == EMPTY_KEY) continue;
                 const int sj = slot[j];
                 if (u[j] == s_c[sj]) {
-                    if constexpr (WEIGHTED) atomicAdd(&s_scw[sj], wv[j]);
-                    else atomicAdd(&s_sc[sj], 1u);
+                    if constexpr (FSUM) atomicAdd(&s_scw[sj], wv[j]);
+                    else atomicAdd(&s_sc[sj], wv[j]);
                     continue;
                 }
                 const uint32_t key = ((uint32_t)sj << LABEL_BITS) | (uint32_t)u[j];
@@ -764,13 +714,13 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                     if (prev == KEY_EMPTY || prev == key) break;
                     h = (h + 1 == cap) ? 0 : h + 1;
                 }
-                if constexpr (WEIGHTED) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
-                else asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnts_s + 4 * h) : "memory");
+                if constexpr (FSUM) asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(sums_s + 8 * h), "d"(wv[j]) : "memory");
+                else asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts_s + 4 * h), "r"(wv[j]) : "memory");
             }
         }
         __syncthreads();
         if (tid < nv) {
-            const double sc = WEIGHTED ? s_scw[tid] : u32_to_f64(s_sc[tid]);
+            const double sc = FSUM ? s_scw[tid] : u32_to_f64(s_sc[tid]);
             s_b[tid] = dadd(dsub(sc, dmul(s_t[tid], s_Kc[tid])), dmul(s_t[tid], s_kv[tid]));
         }
         __syncthreads();
@@ -780,7 +730,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             if (key == KEY_EMPTY) continue;
             const int32_t x = (int32_t)(key & ((1u << LABEL_BITS) - 1u));
             const int sj = (int)(key >> LABEL_BITS);
-            const double S = WEIGHTED ? sums[q] : u32_to_f64(cnts[q]);
+            const double S = FSUM ? sums[q] : u32_to_f64(cnts[q]);
             const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC>(a.K, x, pol_keep))), s_b[sj]);
             gval[q] = g;
             atomicMax(&s_hi[sj], (uint32_t)(ord_gain(g) >> 32));
@@ -802,7 +752,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             if ((uint32_t)(o >> 32) == s_hi[sj] && (uint32_t)o == s_lo[sj])
                 atomicMin(&s_bx[sj], (int32_t)(key & ((1u << LABEL_BITS) - 1u)));
             keys[q] = KEY_EMPTY;  // reset for the next window
-            if constexpr (WEIGHTED) sums[q] = 0.0;
+            if constexpr (FSUM) sums[q] = 0.0;
             else cnts[q] = 0;
         }
         __syncthreads();
@@ -880,9 +830,9 @@ struct LargeBatch {
     int32_t* px;               // [scoring items] partial best cluster
 };
 
-template <bool WEIGHTED>
-__device__ __forceinline__ GlobalTable<WEIGHTED> gtable(const LargeBatch& L, int64_t off) {
-    if constexpr (WEIGHTED) return GlobalTable<true>{static_cast<int32_t*>(L.tab) + off, L.tabv + off};
+template <bool FSUM>
+__device__ __forceinline__ GlobalTable<FSUM> gtable(const LargeBatch& L, int64_t off) {
+    if constexpr (FSUM) return GlobalTable<true>{static_cast<int32_t*>(L.tab) + off, L.tabv + off};
     else return GlobalTable<false>{static_cast<unsigned long long*>(L.tab) + off};
 }
 
@@ -911,21 +861,21 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
         const int64_t e0 = s + (it - L.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
-        const auto tab = gtable<WLoad<WT>::weighted>(L, L.cap_off[li]);
+        const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         double sc = 0.0;
         for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * UL) {
             int32_t u[UL];
-            double wv[UL];
+            typename WLoad<WT>::TW wv[UL];
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 const int64_t e = eb + (int64_t)j * LARGE_THREADS;
                 u[j] = e < e1 ? ld_stream_i32(a.indices + e, pol_stream) : -1;
-                wv[j] = e < e1 ? WLoad<WT>::at(a.w, e) : 0.0;
+                wv[j] = e < e1 ? WLoad<WT>::tw(a.w, e) : typename WLoad<WT>::TW(0);
             }
 #pragma unroll
             for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
-            if constexpr (!WLoad<WT>::weighted) {
+            if constexpr (!WLoad<WT>::fsum) {
                 // first probe of all UL keys issued back to back (UL device
                 // CAS in flight per lane); collisions finish in the probe loop
                 unsigned long long* T = static_cast<unsigned long long*>(L.tab) + L.cap_off[li];
@@ -935,7 +885,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
                 for (int j = 0; j < UL; ++j) {
                     h[j] = 0;
                     if (u[j] == EMPTY_KEY) continue;
-                    if (u[j] == c) { sc += 1.0; continue; }
+                    if (u[j] == c) { sc += WLoad<WT>::f64(wv[j]); continue; }
                     h[j] = slot_of(u[j], cap);
                     pending |= 1u << j;
                 }
@@ -948,13 +898,13 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
                     for (int j = 0; j < UL; ++j)
                         if (pending & (1u << j))
                             old[j] = atomicCAS(T + h[j], (unsigned long long)EMPTY64,
-                                               ((unsigned long long)(uint32_t)u[j] << 32) | 1ull);
+                                               ((unsigned long long)(uint32_t)u[j] << 32) | wv[j]);
 #pragma unroll
                     for (int j = 0; j < UL; ++j) {
                         if (!(pending & (1u << j))) continue;
                         if (old[j] == EMPTY64) { pending &= ~(1u << j); continue; }
                         if ((int32_t)(old[j] >> 32) == u[j]) {
-                            atomicAdd(T + h[j], 1ull);
+                            atomicAdd(T + h[j], (unsigned long long)wv[j]);
                             pending &= ~(1u << j);
                             continue;
                         }
@@ -1003,7 +953,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
         const uint32_t q_begin = (uint32_t)((it - L.sitem_off[li]) * SCORE_CHUNK);
         const uint32_t q_end = (uint32_t)min64((int64_t)q_begin + SCORE_CHUNK, cap);
-        const auto tab = gtable<WLoad<WT>::weighted>(L, L.cap_off[li]);
+        const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
@@ -1248,7 +1198,7 @@ inline void plan_windows(const int64_t* indptr, const int32_t* list, int64_t nb,
 template <class WT, bool ASYNC>
 void launch_window(const BMArgs& a, const int32_t* list, const WindowPlan& P, int64_t w0, int64_t w1, cudaStream_t s) {
     if (w1 <= w0) return;
-    constexpr int SMEM = (int)window_smem_bytes<WLoad<WT>::weighted>();
+    constexpr int SMEM = (int)window_smem_bytes<WLoad<WT>::fsum>();
     static int occ = 0;
     if (!occ) {
         set_smem(k_window<WT, ASYNC>, SMEM);
@@ -1264,7 +1214,7 @@ inline int64_t large_cap(int64_t deg) { return (2 * deg + 31) & ~31LL; }
 
 template <class WT, bool ASYNC>
 void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large, int64_t nL, cudaStream_t s) {
-    constexpr bool WEIGHTED = WLoad<WT>::weighted;
+    constexpr bool WEIGHTED = WLoad<WT>::fsum;  // float sums: key + f64 value tables
     Buf<int64_t> ddeg(nL, s);
     k_degrees_of<<<grid_for(nL, 256), 256, 0, s>>>(g.indptr, large, nL, ddeg.get());
     LCC_LAUNCH_CHECK();
@@ -1532,6 +1482,11 @@ int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_
         case LCC_W_F64:
             return as ? run_round<double, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
                       : run_round<double, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
+        case LCC_W_U32:
+            // integer sums in 32-bit slots: every per-vertex sum <= 2 * total weight
+            LCC_REQUIRE(2.0 * g.total_weight < 4294967296.0, "uint32 weights need 2 * total_weight < 2^32");
+            return as ? run_round<uint32_t, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
+                      : run_round<uint32_t, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
         default:
             throw Invalid("unknown weight dtype");
     }

@@ -86,7 +86,8 @@ void check_graph(const lcc_graph* g) {
     LCC_REQUIRE(g->nnz >= 0, "negative entry count");
     LCC_REQUIRE(g->n == 0 || g->indptr != nullptr, "indptr is NULL");
     LCC_REQUIRE(g->nnz == 0 || g->indices != nullptr, "indices is NULL");
-    LCC_REQUIRE(g->weights == nullptr || g->wtype == LCC_W_F32 || g->wtype == LCC_W_F64, "unknown weight dtype");
+    LCC_REQUIRE(g->weights == nullptr || g->wtype == LCC_W_F32 || g->wtype == LCC_W_F64 || g->wtype == LCC_W_U32,
+                "unknown weight dtype");
 }
 
 void check_params(const lcc_params* p) {
@@ -207,8 +208,9 @@ lcc_status lcc_par_compress(const lcc_graph* g, const lcc_params* p, const int32
         if (r.cnnz) {
             LCC_CUDA(cudaMemcpyAsync(cindices, r.indices.get(), sizeof(int32_t) * r.cnnz, cudaMemcpyDeviceToDevice,
                                      S(stream)));
-            LCC_CUDA(cudaMemcpyAsync(cweights, r.w.get(), sizeof(double) * r.cnnz, cudaMemcpyDeviceToDevice,
-                                     S(stream)));
+            if (r.integral) lcc::widen_u32(r.wi.get(), cweights, r.cnnz, S(stream));
+            else LCC_CUDA(cudaMemcpyAsync(cweights, r.w.get(), sizeof(double) * r.cnnz, cudaMemcpyDeviceToDevice,
+                                          S(stream)));
         }
         if (cn) *cn = r.cn;
         if (cnnz) *cnnz = r.cnnz;

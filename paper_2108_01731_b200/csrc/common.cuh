@@ -149,23 +149,44 @@ __device__ __forceinline__ double u32_to_f64(uint32_t x) {
 }
 
 // Weight loads: WNone means every edge weighs 1.
+// fsum: neighbour-cluster sums need floating point (float/double weights);
+// otherwise they are exact integer sums in native 32-bit atomics (TW =
+// uint32_t: 1 per edge unweighted, the count for LCC_W_U32).
 struct WNone { };
 template <class W> struct WLoad;
 template <> struct WLoad<WNone> {
-    static constexpr bool weighted = false;
+    static constexpr bool weighted = false, fsum = false;
+    using TW = uint32_t;
     __device__ __forceinline__ static double at(const void*, int64_t) { return 1.0; }
+    __device__ __forceinline__ static TW tw(const void*, int64_t) { return 1u; }
+    __device__ __forceinline__ static double f64(TW x) { return u32_to_f64(x); }
+};
+template <> struct WLoad<uint32_t> {
+    static constexpr bool weighted = true, fsum = false;
+    using TW = uint32_t;
+    __device__ __forceinline__ static TW tw(const void* w, int64_t e) {
+        return __ldg(static_cast<const uint32_t*>(w) + e);
+    }
+    __device__ __forceinline__ static double at(const void* w, int64_t e) { return u32_to_f64(tw(w, e)); }
+    __device__ __forceinline__ static double f64(TW x) { return u32_to_f64(x); }
 };
 template <> struct WLoad<float> {
-    static constexpr bool weighted = true;
+    static constexpr bool weighted = true, fsum = true;
+    using TW = double;
     __device__ __forceinline__ static double at(const void* w, int64_t e) {
         return (double)__ldg(static_cast<const float*>(w) + e);
     }
+    __device__ __forceinline__ static TW tw(const void* w, int64_t e) { return at(w, e); }
+    __device__ __forceinline__ static double f64(TW x) { return x; }
 };
 template <> struct WLoad<double> {
-    static constexpr bool weighted = true;
+    static constexpr bool weighted = true, fsum = true;
+    using TW = double;
     __device__ __forceinline__ static double at(const void* w, int64_t e) {
         return __ldg(static_cast<const double*>(w) + e);
     }
+    __device__ __forceinline__ static TW tw(const void* w, int64_t e) { return at(w, e); }
+    __device__ __forceinline__ static double f64(TW x) { return x; }
 };
 
 __device__ __forceinline__ double kval(const double* k, int64_t v) {

@@ -11,6 +11,7 @@
 // build_graph_arrays (graph.py:126-164).
 #include <cub/cub.cuh>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include "edgemap.cuh"
@@ -36,7 +37,7 @@ __global__ void k_map(const int32_t* __restrict__ C, const int32_t* __restrict__
 }
 
 // edge functor: key of the directed entry (v, u), intra entries -> sentinel
-template <class WT>
+template <class WT, class VT>
 struct EdgeKey {
     const int32_t* indices;
     const void* w;
@@ -44,7 +45,7 @@ struct EdgeKey {
     int bits;
     uint64_t sentinel;
     uint64_t* keys;
-    double* vals;
+    VT* vals;
     unsigned long long* intra_cnt;
     double* intra_w;
     unsigned long long cnt = 0;
@@ -52,15 +53,15 @@ struct EdgeKey {
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
         const uint64_t a = (uint32_t)__ldg(mapping + v);
         const uint64_t b = (uint32_t)__ldg(mapping + __ldg(indices + e));
-        const double wv = WLoad<WT>::at(w, e);
+        const auto wv = WLoad<WT>::tw(w, e);
         if (a == b) {
             keys[e] = sentinel;
             ++cnt;
-            acc += wv;
+            acc += WLoad<WT>::f64(wv);
         } else {
             keys[e] = (a << bits) | b;
         }
-        if (vals) vals[e] = wv;
+        if (vals) vals[e] = (VT)wv;
     }
     __device__ __forceinline__ void flush() {
         for (int d = 16; d; d >>= 1) {
@@ -87,6 +88,9 @@ __global__ void k_emit_rows(const uint64_t* __restrict__ ukeys, int64_t R, int b
 
 struct Sq {
     __device__ __forceinline__ double operator()(double x) const { return x * x; }
+};
+struct U32F64 {
+    __device__ __forceinline__ double operator()(uint32_t x) const { return (double)x; }
 };
 struct KSq {
     const double* k;
@@ -150,7 +154,15 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     const int bits = std::max(1, bit_width((uint64_t)cn));
     LCC_REQUIRE(2 * bits <= 64, "coarse graph too large");
 
-    // 2. keys for every directed entry
+    // 2. keys for every directed entry.  Integer weights (none, or uint32)
+    //    stay integers: uint32 values through the sort, uint32 sums out
+    //    (exact; the coarse graph is LCC_W_U32) as long as 2 * total weight
+    //    fits in 32 bits; float weights carry fp64 values.
+    constexpr bool FS = WLoad<WT>::fsum;
+    using VT = std::conditional_t<FS, double, uint32_t>;
+    const bool int_out = !FS && 2.0 * g.total_weight < 4294967296.0;
+    LCC_REQUIRE((!std::is_same<WT, uint32_t>::value || int_out), "uint32 weights need 2 * total_weight < 2^32");
+    out.integral = int_out;
     Buf<double> dacc(2, s);  // [intra_w, scratch]
     Buf<unsigned long long> dintra(1, s);
     LCC_CUDA(cudaMemsetAsync(dacc.get(), 0, 2 * sizeof(double), s));
@@ -159,14 +171,14 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     double intra_w = 0.0;
     if (nnz > 0) {
         Buf<uint64_t> ka(nnz, s), kb(nnz, s);
-        Buf<double> va, vb;
+        Buf<VT> va, vb;
         if (WLoad<WT>::weighted) { va.alloc(nnz, s); vb.alloc(nnz, s); }
         const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
         cudaEvent_t k0 = nullptr, k1 = nullptr;
         if (tr.on) { cudaEventCreate(&k0); cudaEventCreate(&k1); cudaEventRecord(k0, s); }
         edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
-                      EdgeKey<WT>{g.indices, g.weights, mapping, bits, sentinel, ka.get(), va.get(),
-                                  dintra.get(), dacc.get()}, s);
+                      EdgeKey<WT, VT>{g.indices, g.weights, mapping, bits, sentinel, ka.get(), va.get(),
+                                      dintra.get(), dacc.get()}, s);
         if (tr.on) cudaEventRecord(k1, s);
         tr.mark("keys");
         if (tr.on) {
@@ -179,17 +191,16 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         // 3. stable radix sort on the 2*bits live bits, double-buffered (peak
         //    memory = the two key (+value) buffers, no hidden n-sized temp)
         cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());
-        cub::DoubleBuffer<double> dv(va.get(), vb.get());
+        cub::DoubleBuffer<VT> dv(va.get(), vb.get());
         if (WLoad<WT>::weighted) sort_pairs_db(dk, dv, nnz, 2 * bits, s);
         else sort_keys_db(dk, nnz, 2 * bits, s);
         Buf<uint64_t>& ksorted = dk.Current() == ka.get() ? ka : kb;
         (dk.Current() == ka.get() ? kb : ka).release();
         tr.mark("sort");
-        Buf<double>& vsorted = dv.Current() == va.get() ? va : vb;
+        Buf<VT>& vsorted = dv.Current() == va.get() ? va : vb;
         if (WLoad<WT>::weighted) (dv.Current() == va.get() ? vb : va).release();
-        // 4. count the runs, then reduce by key into exact-size outputs;
-        //    unweighted entries sum a constant 1.0 (integer-valued, exact
-        //    below 2^53); 64-bit item counts (2m > 2^31 at config 5)
+        // 4. count the runs, then reduce by key into exact-size outputs
+        //    (64-bit item counts: 2m > 2^31 at config 5)
         int64_t runs = 0;
         unsigned long long hintra = 0;
         {
@@ -205,23 +216,24 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         R = runs - (hintra > 0 ? 1 : 0);  // the all-ones sentinel run (intra entries) sorts last
         if (!WLoad<WT>::weighted) intra_w = (double)hintra;
         Buf<uint64_t> ukeys(std::max<int64_t>(runs, 1), s);
-        out.w.alloc(std::max<int64_t>(runs, 1), s);
+        if (int_out) out.wi.alloc(std::max<int64_t>(runs, 1), s);
+        else out.w.alloc(std::max<int64_t>(runs, 1), s);
         {
             Buf<int64_t> druns(1, s);
-            size_t bytes = 0;
-            if (WLoad<WT>::weighted) {
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, ksorted.get(), ukeys.get(), vsorted.get(),
-                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+            auto rbk = [&](auto vals_in, auto* sums_out) {
+                size_t bytes = 0;
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, ksorted.get(), ukeys.get(), vals_in, sums_out,
+                                                        druns.get(), cub::Sum(), nnz, s));
                 Buf<unsigned char> tmp(bytes, s);
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, ksorted.get(), ukeys.get(), vsorted.get(),
-                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, ksorted.get(), ukeys.get(), vals_in,
+                                                        sums_out, druns.get(), cub::Sum(), nnz, s));
+            };
+            if constexpr (WLoad<WT>::weighted) {
+                if constexpr (FS) rbk(vsorted.get(), out.w.get());
+                else rbk(vsorted.get(), out.wi.get());
             } else {
-                cub::ConstantInputIterator<double> ones(1.0);
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, ksorted.get(), ukeys.get(), ones,
-                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
-                Buf<unsigned char> tmp(bytes, s);
-                LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, ksorted.get(), ukeys.get(), ones,
-                                                        out.w.get(), druns.get(), cub::Sum(), nnz, s));
+                if (int_out) rbk(cub::ConstantInputIterator<uint32_t>(1u), out.wi.get());
+                else rbk(cub::ConstantInputIterator<double>(1.0), out.w.get());
             }
         }
         ksorted.release();
@@ -232,7 +244,8 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
                                                          out.indices.get());
         LCC_LAUNCH_CHECK();
     } else {
-        out.w.alloc(1, s);
+        if (int_out) out.wi.alloc(1, s);
+        else out.w.alloc(1, s);
         out.indices.alloc(1, s);
         LCC_CUDA(cudaMemsetAsync(out.indptr.get(), 0, sizeof(int64_t) * (cn + 1), s));
     }
@@ -240,7 +253,14 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     // 5. scalars: total weight, internal offset
     Buf<double> sums(3, s);
     LCC_CUDA(cudaMemsetAsync(sums.get(), 0, 3 * sizeof(double), s));
-    if (R > 0) device_sum(out.w.get(), sums.get() + 0, R, s);
+    if (R > 0) {
+        if (int_out) {
+            cub::TransformInputIterator<double, U32F64, const uint32_t*> wd(out.wi.get(), U32F64{});
+            device_sum(wd, sums.get() + 0, R, s);
+        } else {
+            device_sum(out.w.get(), sums.get() + 0, R, s);
+        }
+    }
     if (cn > 0) {
         cub::TransformInputIterator<double, Sq, const double*> sq(ck, Sq{});
         device_sum(sq, sums.get() + 1, cn, s);
@@ -272,8 +292,22 @@ Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* 
         case LCC_W_NONE: return compress_impl<WNone>(g, k, lam, C, K, mapping, ck, s);
         case LCC_W_F32: return compress_impl<float>(g, k, lam, C, K, mapping, ck, s);
         case LCC_W_F64: return compress_impl<double>(g, k, lam, C, K, mapping, ck, s);
+        case LCC_W_U32: return compress_impl<uint32_t>(g, k, lam, C, K, mapping, ck, s);
         default: throw Invalid("unknown weight dtype");
     }
+}
+
+namespace {
+__global__ void k_widen_u32(const uint32_t* __restrict__ in, double* out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
+}  // namespace
+
+void widen_u32(const uint32_t* in, double* out, int64_t n, cudaStream_t s) {
+    if (n <= 0) return;
+    k_widen_u32<<<grid_for(n, 256), 256, 0, s>>>(in, out, n);
+    LCC_LAUNCH_CHECK();
 }
 
 void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C, double* K,

@@ -107,6 +107,7 @@ struct OwnedGraph {
     Buf<int64_t> indptr;
     Buf<int32_t> indices;
     Buf<double> w;
+    Buf<uint32_t> wi;
     Buf<double> k;
     lcc_graph g{};
 };
@@ -158,14 +159,16 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         og->indptr = std::move(cs.indptr);
         og->indices = std::move(cs.indices);
         og->w = std::move(cs.w);
+        og->wi = std::move(cs.wi);
         og->k.alloc(std::max<int64_t>(cs.cn, 1), s);
         LCC_CUDA(cudaMemcpyAsync(og->k.get(), ck.get(), sizeof(double) * cs.cn, cudaMemcpyDeviceToDevice, s));
         og->g.n = cs.cn;
         og->g.nnz = cs.cnnz;
         og->g.indptr = og->indptr.get();
         og->g.indices = og->indices.get();
-        og->g.weights = og->w.get();
-        og->g.wtype = LCC_W_F64;
+        // integer sums stay integers (LCC_W_U32: exact 32-bit table sums)
+        og->g.weights = cs.integral ? (const void*)og->wi.get() : (const void*)og->w.get();
+        og->g.wtype = cs.integral ? LCC_W_U32 : LCC_W_F64;
         og->g.total_weight = cs.total_weight;
         stack.push_back(Frame{g, k, std::move(mapping)});
         g = og->g;

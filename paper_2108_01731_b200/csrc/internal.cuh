@@ -42,10 +42,13 @@ struct Coarse {
     double internal_offset = 0.0, total_weight = 0.0;
     Buf<int64_t> indptr;
     Buf<int32_t> indices;
-    Buf<double> w;
+    Buf<double> w;       // float sums (float/double inputs) ...
+    Buf<uint32_t> wi;    // ... or exact integer sums (unweighted / uint32 inputs)
+    bool integral = false;
 };
 Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
                 int32_t* mapping, double* ck, cudaStream_t s);
+void widen_u32(const uint32_t* in, double* out, int64_t n, cudaStream_t s);
 void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C,
              double* K, cudaStream_t s);
 

@@ -88,6 +88,7 @@ double cc_objective(const lcc_graph& g, const double* k, double lam, const int32
         case LCC_W_NONE: return objective_impl<WNone>(g, k, lam, C, s);
         case LCC_W_F32: return objective_impl<float>(g, k, lam, C, s);
         case LCC_W_F64: return objective_impl<double>(g, k, lam, C, s);
+        case LCC_W_U32: return objective_impl<uint32_t>(g, k, lam, C, s);
         default: throw Invalid("unknown weight dtype");
     }
 }

@@ -102,7 +102,7 @@ class CudaBackend:
     def _g(self, part) -> _lib.LccGraph:
         wtype, wp = _lib.W_NONE, None
         if part.weights is not None:
-            wtype = _lib.W_F32 if part.weights.dtype == torch.float32 else _lib.W_F64
+            wtype = {torch.float32: _lib.W_F32, torch.int32: _lib.W_U32}.get(part.weights.dtype, _lib.W_F64)
             wp = part.weights.data_ptr()
         nnz = int(part.indices.numel())
         return _lib.LccGraph(part.n, nnz, part.indptr.data_ptr(), part.indices.data_ptr() if nnz else None, wp,

@@ -7,11 +7,15 @@ the same three arrays in HBM with two lossless layout choices:
 
 * all-ones weights are not stored at all (``weights is None``): the kernels
   read 8 B per directed entry instead of 16 B;
-* weights that are exactly representable in float32 are stored as float32
+* non-negative integer weights (multi-edge counts) with 2 * total weight
+  < 2^31 are stored as int32 and summed in exact 32-bit integer tables
+  (``LCC_W_U32``; shared-memory fp64 atomics are CAS loops on sm_100a);
+* other weights exactly representable in float32 are stored as float32
   (the level-0 kNN config); the kernels widen them to fp64 on load, so the
   arithmetic is identical to fp64 storage.
 
-Coarse levels produced by contraction always carry float64 weights.
+Coarse levels produced by contraction carry integer weights when the input
+is unweighted or integer-weighted, float64 weights otherwise.
 """
 from __future__ import annotations
 
@@ -51,7 +55,7 @@ class DeviceGraph:
     m: int
     indptr: torch.Tensor            # int64 [n+1]
     indices: torch.Tensor           # int32 [2m]
-    weights: torch.Tensor | None    # float32/float64 [2m] or None (w == 1)
+    weights: torch.Tensor | None    # float32/float64/int32 [2m] or None (w == 1)
     total_weight: float
 
     @classmethod
@@ -81,7 +85,10 @@ class DeviceGraph:
                 raise GraphError("weights must have one entry per CSR index")
             if not np.all(wh == 1.0):
                 w32 = wh.astype(np.float32)
-                if not keep_f64 and np.array_equal(w32.astype(np.float64), wh):
+                if (not keep_f64 and wh.min() >= 0 and 2 * wh.sum() < 2 ** 31
+                        and np.array_equal(np.floor(wh), wh)):
+                    wt = _to_dev(wh.astype(np.int32), torch.int32, dev)
+                elif not keep_f64 and np.array_equal(w32.astype(np.float64), wh):
                     wt = _to_dev(w32, torch.float32, dev)
                 else:
                     wt = _to_dev(wh, torch.float64, dev)
@@ -115,7 +122,7 @@ class DeviceGraph:
         wtype = _lib.W_NONE
         wp = None
         if self.weights is not None:
-            wtype = _lib.W_F32 if self.weights.dtype == torch.float32 else _lib.W_F64
+            wtype = {torch.float32: _lib.W_F32, torch.int32: _lib.W_U32}.get(self.weights.dtype, _lib.W_F64)
             wp = self.weights.data_ptr()
         return _lib.LccGraph(self.n, self.nnz, self.indptr.data_ptr(),
                              self.indices.data_ptr() if self.nnz else None, wp, wtype, 0,

@@ -461,3 +461,44 @@ def test_fused_frontier_mask_exact(window, large_min, schedule, monkeypatch):
         F1 = L.frontier_from_mask(mark)
         assert np.array_equal(F0, F1.ids.cpu().numpy())
         assert mb.moved_count == int(moved.sum())
+
+
+def int_weighted_hub_graph(rng, n, hubs, hub_deg, base_p, wmax=7):
+    """Hub graph with symmetric integer weights 1..wmax (multi-edge counts)."""
+    hg = hub_graph(rng, n, hubs, hub_deg, base_p=base_p)
+    src = np.repeat(np.arange(n), np.diff(hg.indptr))
+    lo_, hi_ = np.minimum(src, hg.indices), np.maximum(src, hg.indices)
+    hg.weights = (1 + (lo_ * 7919 + hi_ * 104729) % wmax).astype(np.float64)
+    hg.total_weight = float(hg.weights.sum() / 2)
+    return hg
+
+
+@pytest.mark.parametrize("schedule_sync", [True])
+def test_integer_weights_exact(schedule_sync):
+    """Integer weights ride the exact 32-bit integer tables (LCC_W_U32):
+    rounds, contraction and the multi-level driver are bit-exact vs the fp64
+    oracle in every degree bin (hubs included)."""
+    rng = np.random.default_rng(29)
+    hg = int_weighted_hub_graph(rng, 40_000, hubs=[3, 9, 700, 8000], hub_deg=[300, 2500, 6000, 15_000],
+                                base_p=0.0004)
+    d = dg(hg)
+    assert d.weights is not None and d.weights.dtype == torch.int32
+    g = og(hg)
+    for nclus in (40_000, 2000):
+        C, K = clustered_state(rng, g.n, nclus)
+        for lam in (0.05, 0.4):
+            D0, m0, c0 = O.sync_round(g, None, lam, C, K)
+            D1, m1, c1 = gpu_sync_round(hg, None, lam, C, K)
+            assert np.array_equal(D0, D1) and c0 == c1
+        lvl0 = O.compress(g, None, 0.4, C, K)
+        lvl1 = L.par_compress(d, L.ClusteringParams(0.4), L.Clustering(torch.as_tensor(C).cuda(),
+                                                                         torch.as_tensor(K).cuda()))
+        assert np.array_equal(lvl1.graph.indices.cpu().numpy(), lvl0.graph.indices)
+        assert np.array_equal(lvl1.graph.weights.cpu().numpy(), lvl0.graph.weights)
+        assert lvl1.internal_offset == lvl0.internal_offset
+    small = int_weighted_hub_graph(rng, 6000, hubs=[5], hub_deg=[2000], base_p=0.002)
+    gs = og(small)
+    C0 = O.parallel_cc(gs, None, 0.3, O.Opts(schedule=O.SYNC))
+    cl = L.parallel_cc(small, L.ClusteringParams(0.3), L.ParOptions(schedule="sync"))
+    assert np.array_equal(cl.labels(), C0)
+    assert L.cc_objective(small, L.ClusteringParams(0.3), cl) == O.objective(gs, None, 0.3, C0)

@@ -378,8 +378,16 @@ def run_ours(args):
     B_distinct = 8                         # K gather per distinct cluster (= deg at singleton start)
     alg_bytes = n * B_vertex + nnz * B_edge + nnz * B_distinct
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    # measured DRAM traffic of the same kernel group per step: from the
+    # committed `ncu --set full` capture of this exact command (cfg4 default)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    if wl.cfg == "cfg4" and args.scale == 24 and os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic, traffic_src = tj["dram_bytes_per_step"], "profiles/r01_traffic.json (" + tj["source"] + ")"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_kind": peak_kind, "kernel": "best-move (k_small/k_medium/k_large_*)",
+                "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
+                "kernel": "best-move (k_small/k_medium/k_large_*)",
                 "alg_bytes_per_launch_group": alg_bytes, "kernel_ms_per_step": kern_ms,
                 "kernel_share_of_step": kern_ms / (ms / args.steps)}
 

@@ -103,6 +103,10 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
 }
 
 namespace {
+// A coarse level owned by the driver.  Levels that are only needed again
+// while unwinding can be parked in pinned host memory when the next
+// contraction would not fit (config 5: every level of a 1.8B-edge graph is
+// ~24 GB and the levels shrink slowly), then restored for their refinement.
 struct OwnedGraph {
     Buf<int64_t> indptr;
     Buf<int32_t> indices;
@@ -110,12 +114,73 @@ struct OwnedGraph {
     Buf<uint32_t> wi;
     Buf<double> k;
     lcc_graph g{};
+    char* host = nullptr;
+    size_t wbytes() const { return g.wtype == LCC_W_U32 ? 4 : 8; }
+    size_t bytes() const { return sizeof(int64_t) * (g.n + 1) + (sizeof(int32_t) + wbytes()) * g.nnz; }
+    void park(cudaStream_t s) {
+        if (host) return;
+        LCC_CUDA(cudaHostAlloc((void**)&host, std::max<size_t>(bytes(), 1), cudaHostAllocDefault));
+        char* p = host;
+        LCC_CUDA(cudaMemcpyAsync(p, g.indptr, sizeof(int64_t) * (g.n + 1), cudaMemcpyDeviceToHost, s));
+        p += sizeof(int64_t) * (g.n + 1);
+        if (g.nnz) {
+            LCC_CUDA(cudaMemcpyAsync(p, g.indices, sizeof(int32_t) * g.nnz, cudaMemcpyDeviceToHost, s));
+            p += sizeof(int32_t) * g.nnz;
+            LCC_CUDA(cudaMemcpyAsync(p, g.weights, wbytes() * g.nnz, cudaMemcpyDeviceToHost, s));
+        }
+        LCC_CUDA(cudaStreamSynchronize(s));
+        indptr.release();
+        indices.release();
+        w.release();
+        wi.release();
+        g.indptr = nullptr;
+        g.indices = nullptr;
+        g.weights = nullptr;
+    }
+    void unpark(cudaStream_t s) {
+        if (!host) return;
+        indptr.alloc(g.n + 1, s);
+        indices.alloc(std::max<int64_t>(g.nnz, 1), s);
+        const char* p = host;
+        LCC_CUDA(cudaMemcpyAsync(indptr.get(), p, sizeof(int64_t) * (g.n + 1), cudaMemcpyHostToDevice, s));
+        p += sizeof(int64_t) * (g.n + 1);
+        void* wp;
+        if (g.wtype == LCC_W_U32) { wi.alloc(std::max<int64_t>(g.nnz, 1), s); wp = wi.get(); }
+        else { w.alloc(std::max<int64_t>(g.nnz, 1), s); wp = w.get(); }
+        if (g.nnz) {
+            LCC_CUDA(cudaMemcpyAsync(indices.get(), p, sizeof(int32_t) * g.nnz, cudaMemcpyHostToDevice, s));
+            p += sizeof(int32_t) * g.nnz;
+            LCC_CUDA(cudaMemcpyAsync(wp, p, wbytes() * g.nnz, cudaMemcpyHostToDevice, s));
+        }
+        LCC_CUDA(cudaStreamSynchronize(s));
+        cudaFreeHost(host);
+        host = nullptr;
+        g.indptr = indptr.get();
+        g.indices = indices.get();
+        g.weights = wp;
+    }
+    ~OwnedGraph() {
+        if (host) cudaFreeHost(host);
+    }
 };
 struct Frame {
-    lcc_graph g;
+    int own;  // owner of this level's graph: -1 = the caller's graph, else owned[own]
     const double* k;
     Buf<int32_t> mapping;
 };
+
+// device bytes a contraction of g may take (keys x2, values x2, unique keys,
+// outputs), vs what is free on the device plus what the library has cached
+bool contraction_fits(const lcc_graph& g) {
+    const double vb = (g.weights && g.wtype != LCC_W_U32) ? 8.0 : 4.0;
+    const double need = (double)g.nnz * (16.0 + 2.0 * vb + 8.0 + 4.0 + vb) + (double)g.n * 64.0;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return true;
+    double r, u;
+    pool_gb(r, u);
+    const double avail = (double)fr + (double)cache_bytes() + (r - u) * 1073741824.0;
+    return need < 0.9 * avail;
+}
 }  // namespace
 
 void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Options& o, int32_t* C_out,
@@ -145,6 +210,17 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
                     (long long)g.nnz, ms, r, u);
         }
         if (!moved) break;  // Alg. 1 line 13
+        // deeper levels first: park the finer owned levels on the host when
+        // this contraction would not fit next to them
+        if (owned.size() > 1 && !contraction_fits(g)) {
+            for (size_t i = 0; i + 1 < owned.size(); ++i) {
+                if (owned[i]->host) continue;
+                owned[i]->park(s);
+                if (trace) fprintf(stderr, "[lcc]   parked level %zu (%.1f GB) on the host\n", i + 1,
+                                   owned[i]->bytes() / 1073741824.0);
+                if (contraction_fits(g)) break;
+            }
+        }
         EventTimer tc(s);
         // contraction straight into exact-size buffers
         Buf<int32_t> mapping(n, s);
@@ -170,7 +246,7 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         og->g.weights = cs.integral ? (const void*)og->wi.get() : (const void*)og->w.get();
         og->g.wtype = cs.integral ? LCC_W_U32 : LCC_W_F64;
         og->g.total_weight = cs.total_weight;
-        stack.push_back(Frame{g, k, std::move(mapping)});
+        stack.push_back(Frame{(int)owned.size() - 1, k, std::move(mapping)});
         g = og->g;
         k = og->k.get();
         owned.push_back(std::move(og));
@@ -178,12 +254,17 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
     // unwind: flatten (+ refine) level by level (Alg. 1 lines 17-18)
     Buf<int32_t> Cres = std::move(C);
     for (auto it = stack.rbegin(); it != stack.rend(); ++it) {
-        const int64_t n = it->g.n;
+        // the coarse level above this one is finished: free it
+        owned[it->own + 1].reset();
+        OwnedGraph* fine = it->own >= 0 ? owned[it->own].get() : nullptr;
+        if (fine) fine->unpark(s);
+        const lcc_graph& gf = fine ? fine->g : g0;
+        const int64_t n = gf.n;
         EventTimer tu(s);
         Buf<int32_t> Cf(std::max<int64_t>(n, 1), s);
         Buf<double> Kf(std::max<int64_t>(n, 1), s);
         flatten(n, it->mapping.get(), Cres.get(), it->k, Cf.get(), Kf.get(), s);
-        if (o.refine) par_best_moves(it->g, it->k, lam, o, Cf.get(), Kf.get(), st, s);
+        if (o.refine) par_best_moves(gf, it->k, lam, o, Cf.get(), Kf.get(), st, s);
         if (trace) fprintf(stderr, "[lcc] unwind n=%lld flatten+refine %.2f ms\n", (long long)n, tu.stop());
         Cres = std::move(Cf);
     }

@@ -1,6 +1,6 @@
 """Build profiles/rNN_summary.md from an ncu launch list (--csv --metrics
 gpu__time_duration.sum) and `ncu --set full` reports of the top kernels.
-Usage: python tools/profile_report.py RND launches.csv rep1.ncu-rep [rep2 ...]"""
+Usage: python tools/profile_report.py RND launches.csv rep1.ncu-rep|raw1.csv [...]"""
 import collections
 import csv
 import io
@@ -52,8 +52,11 @@ def main():
     for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{k[-90:]}` | {c} | {v/1e6:.3f} | {100*v/tot:.1f}% |")
     for rep in reps:
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        rows = list(csv.reader(io.StringIO(raw)))
+        if rep.endswith(".csv"):  # raw-page export made on the GPU box
+            rows = list(csv.reader(open(rep)))
+        else:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+            rows = list(csv.reader(io.StringIO(raw)))
         if len(rows) < 3:
             continue
         hdr, units = rows[0], rows[1]

@@ -401,87 +401,91 @@ def run_ours(args):
     # e2e: whole clustering via the public API from pinned host memory
     e2e = None
     if not args.no_e2e:
-        indptr_h = dg.indptr.cpu().pin_memory()
-        indices_h = dg.indices.cpu().pin_memory()
-        weights_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
+        try:
+            indptr_h = dg.indptr.cpu().pin_memory()
+            indices_h = dg.indices.cpu().pin_memory()
+            weights_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
 
-        class HostG:
-            pass
-        hgr = HostG()
-        hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = (
-            n, nnz // 2, indptr_h, indices_h, weights_h, dg.total_weight)
-        # the e2e call uploads its own copy: release the round-bench buffers
-        # (and, except for cfg1 which contracts `dg` directly, the device graph)
-        C = D = K2 = Cn = Kn = F = moved = mark = iota = None
-        if wl.cfg != "cfg1":
-            dg = wl.dg = None
-        torch.cuda.empty_cache()
-        full = L.ParOptions(schedule=wl.schedule, degree_threshold=args.degree_threshold,
-                            async_chunks=args.async_chunks)
-        out_h = torch.empty(n, dtype=torch.int32).pin_memory()
+            class HostG:
+                pass
+            hgr = HostG()
+            hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = (
+                n, nnz // 2, indptr_h, indices_h, weights_h, dg.total_weight)
+            # the e2e call uploads its own copy: release the round-bench buffers
+            # (and, except for cfg1 which contracts `dg` directly, the device graph)
+            C = D = K2 = Cn = Kn = F = moved = mark = iota = None
+            if wl.cfg != "cfg1":
+                dg = wl.dg = None
+            torch.cuda.empty_cache()
+            full = L.ParOptions(schedule=wl.schedule, degree_threshold=args.degree_threshold,
+                                async_chunks=args.async_chunks)
+            out_h = torch.empty(n, dtype=torch.int32).pin_memory()
 
-        def e2e_step():
-            if wl.cfg == "cfg1":
-                # configs[0]: single level plus contraction (par_best_moves + par_compress)
-                cl, _ = L.par_best_moves(hgr, p, None, full)
-                lvl = L.par_compress(dg, p, cl)
-                cl.meta["stats"].levels = 1
-                cl.meta["coarse_n"] = lvl.graph.n
-            elif os.environ.get("LCC_BENCH_DEBUG"):
-                from paper_2108_01731_b200.louvain_par import _prep
-                t = [time.perf_counter()]
-                dgx, gsx, psx = _prep(hgr, p)
-                torch.cuda.synchronize(); t.append(time.perf_counter())
-                Cx = torch.empty(n, dtype=torch.int32, device="cuda")
-                stx = _lib.LccStats()
-                osx = full.c_struct()
-                _lib.check(lib.lcc_parallel_cc(ctypes.byref(gsx), ctypes.byref(psx), ctypes.byref(osx),
-                                               Cx.data_ptr(), ctypes.byref(stx), stream_ptr()))
-                torch.cuda.synchronize(); t.append(time.perf_counter())
-                from paper_2108_01731_b200.objective import clustering_from_labels
-                cl = clustering_from_labels(Cx, p)
-                cl.meta["stats"] = L.louvain_par._stats_from(stx)
-                torch.cuda.synchronize(); t.append(time.perf_counter())
-                print("e2e phases ms: upload %.1f parallel_cc %.1f (device %.1f) relabel %.1f" % (
-                    1e3 * (t[1] - t[0]), 1e3 * (t[2] - t[1]), stx.ms_total, 1e3 * (t[3] - t[2])), file=sys.stderr)
-            else:
-                cl = L.parallel_cc(hgr, p, full)
-            out_h.copy_(cl.assignment, non_blocking=True)
-            torch.cuda.synchronize()
-            return cl
-
-        e2e_step()  # warm-up (pool growth)
-        times, edges_sum, stats = [], 0, None
-        with ClockSampler(lrank) as clk_e2e:
-            for _ in range(max(1, args.e2e_steps)):
+            def e2e_step():
+                if wl.cfg == "cfg1":
+                    # configs[0]: single level plus contraction (par_best_moves + par_compress)
+                    cl, _ = L.par_best_moves(hgr, p, None, full)
+                    lvl = L.par_compress(dg, p, cl)
+                    cl.meta["stats"].levels = 1
+                    cl.meta["coarse_n"] = lvl.graph.n
+                elif os.environ.get("LCC_BENCH_DEBUG"):
+                    from paper_2108_01731_b200.louvain_par import _prep
+                    t = [time.perf_counter()]
+                    dgx, gsx, psx = _prep(hgr, p)
+                    torch.cuda.synchronize(); t.append(time.perf_counter())
+                    Cx = torch.empty(n, dtype=torch.int32, device="cuda")
+                    stx = _lib.LccStats()
+                    osx = full.c_struct()
+                    _lib.check(lib.lcc_parallel_cc(ctypes.byref(gsx), ctypes.byref(psx), ctypes.byref(osx),
+                                                   Cx.data_ptr(), ctypes.byref(stx), stream_ptr()))
+                    torch.cuda.synchronize(); t.append(time.perf_counter())
+                    from paper_2108_01731_b200.objective import clustering_from_labels
+                    cl = clustering_from_labels(Cx, p)
+                    cl.meta["stats"] = L.louvain_par._stats_from(stx)
+                    torch.cuda.synchronize(); t.append(time.perf_counter())
+                    print("e2e phases ms: upload %.1f parallel_cc %.1f (device %.1f) relabel %.1f" % (
+                        1e3 * (t[1] - t[0]), 1e3 * (t[2] - t[1]), stx.ms_total, 1e3 * (t[3] - t[2])), file=sys.stderr)
+                else:
+                    cl = L.parallel_cc(hgr, p, full)
+                out_h.copy_(cl.assignment, non_blocking=True)
                 torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                cl = e2e_step()
-                times.append(time.perf_counter() - t0)
-                stats = cl.meta["stats"]
-                edges_sum += stats.edges_scanned
-        if os.environ.get("LCC_BENCH_DEBUG"):
-            print("e2e clock samples:", clk_e2e.lines, file=sys.stderr)
-        t_e2e = sum(times) / len(times)
-        e_t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-        ed_t = torch.tensor([edges_sum / len(times)], dtype=torch.float64, device="cuda")
-        if dist:
-            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-            dist.all_reduce(ed_t, op=dist.ReduceOp.SUM)
-        cl = None
-        L.release_memory()
-        torch.cuda.empty_cache()
-        obj = L.cc_objective(dg if dg is not None else hgr, p, torch.as_tensor(out_h).cuda())
-        e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
-                                         (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
-               "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()),
-               "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
-               "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
-               "device_ms_best_move_kernels": stats.ms_kernels,
-               "objective": obj, "clusters": int(np.unique(out_h.numpy()).size), "clocks": clk_e2e.summary(),
-               "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
-                       "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
+                return cl
+
+            e2e_step()  # warm-up (pool growth)
+            times, edges_sum, stats = [], 0, None
+            with ClockSampler(lrank) as clk_e2e:
+                for _ in range(max(1, args.e2e_steps)):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    cl = e2e_step()
+                    times.append(time.perf_counter() - t0)
+                    stats = cl.meta["stats"]
+                    edges_sum += stats.edges_scanned
+            if os.environ.get("LCC_BENCH_DEBUG"):
+                print("e2e clock samples:", clk_e2e.lines, file=sys.stderr)
+            t_e2e = sum(times) / len(times)
+            e_t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+            ed_t = torch.tensor([edges_sum / len(times)], dtype=torch.float64, device="cuda")
+            if dist:
+                dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+                dist.all_reduce(ed_t, op=dist.ReduceOp.SUM)
+            cl = None
+            L.release_memory()
+            torch.cuda.empty_cache()
+            obj = L.cc_objective(dg if dg is not None else hgr, p, torch.as_tensor(out_h).cuda())
+            e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
+                                             (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
+                   "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()),
+                   "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
+                   "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
+                   "device_ms_best_move_kernels": stats.ms_kernels,
+                   "objective": obj, "clusters": int(np.unique(out_h.numpy()).size), "clocks": clk_e2e.summary(),
+                   "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
+                           "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
+        except MemoryError as exc:  # e.g. config 5: coarse levels beyond device + host memory
+            L.release_memory()
+            e2e = {"value": None, "unit": UNIT, "unavailable": str(exc)[:300]}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

@@ -103,6 +103,19 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
 }
 
 namespace {
+// MemAvailable of the host (bytes), or 0 if unknown
+size_t host_available() {
+    FILE* f = fopen("/proc/meminfo", "r");
+    if (!f) return 0;
+    char line[256];
+    size_t kb = 0;
+    while (fgets(line, sizeof(line), f)) {
+        if (sscanf(line, "MemAvailable: %zu kB", &kb) == 1) break;
+    }
+    fclose(f);
+    return kb * 1024;
+}
+
 // A coarse level owned by the driver.  Levels that are only needed again
 // while unwinding can be parked in pinned host memory when the next
 // contraction would not fit (config 5: every level of a 1.8B-edge graph is
@@ -119,6 +132,10 @@ struct OwnedGraph {
     size_t bytes() const { return sizeof(int64_t) * (g.n + 1) + (sizeof(int32_t) + wbytes()) * g.nnz; }
     void park(cudaStream_t s) {
         if (host) return;
+        // pinned pages cannot be swapped: keep 16 GB of the host free
+        if (host_available() < bytes() + (16ull << 30))
+            throw OutOfMemory("parallel_cc: the coarse levels exceed device memory and the host cannot hold "
+                              "them either (" + std::to_string(bytes() >> 30) + " GB per level)");
         LCC_CUDA(cudaHostAlloc((void**)&host, std::max<size_t>(bytes(), 1), cudaHostAllocDefault));
         char* p = host;
         LCC_CUDA(cudaMemcpyAsync(p, g.indptr, sizeof(int64_t) * (g.n + 1), cudaMemcpyDeviceToHost, s));

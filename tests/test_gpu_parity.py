@@ -504,3 +504,18 @@ def test_integer_weights_exact(schedule_sync):
     cl = L.parallel_cc(small, L.ClusteringParams(0.3), L.ParOptions(schedule="sync"))
     assert np.array_equal(cl.labels(), C0)
     assert L.cc_objective(small, L.ClusteringParams(0.3), cl) == O.objective(gs, None, 0.3, C0)
+
+
+def test_hub_cluster_path_exact(monkeypatch):
+    """The DSMEM cluster hub path (LCC_HUB_CLUSTER=1, off by default) gives
+    the oracle's labels bit for bit, unweighted and with integer weights."""
+    monkeypatch.setenv("LCC_HUB_CLUSTER", "1")
+    rng = np.random.default_rng(31)
+    for hg in (hub_graph(rng, 60_000, hubs=[3, 9, 700], hub_deg=[12_000, 30_000, 50_000], base_p=0.0002),
+               int_weighted_hub_graph(rng, 60_000, hubs=[5, 11], hub_deg=[20_000, 45_000], base_p=0.0002)):
+        g = og(hg)
+        for nclus in (60_000, 500):
+            C, K = clustered_state(rng, g.n, nclus)
+            D0, m0, c0 = O.sync_round(g, None, 0.3, C, K)
+            D1, m1, c1 = gpu_sync_round(hg, None, 0.3, C, K)
+            assert np.array_equal(D0, D1) and c0 == c1

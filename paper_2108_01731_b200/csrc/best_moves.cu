@@ -39,6 +39,9 @@
 namespace lcc {
 namespace {
 
+#ifndef LCC_PEDGE
+#define LCC_PEDGE 0  // 1: also cap async sub-rounds by the frontier edges (more oscillation: off)
+#endif
 #ifndef LCC_SMALL_EARLYK
 #define LCC_SMALL_EARLYK 0
 #endif
@@ -1656,9 +1659,14 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     int P = 1;
     if (ASYNC && chunks > 0) P = chunks;
     else if (ASYNC) {  // ~4M / F sub-rounds, at most 64 (small graphs need the ordering:
-                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative)
+                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative),
+                       // and one wave once the frontier's edges alone fill the GPU
+                       // (late config-4 rounds: 58K hub-heavy vertices, 126M edges,
+                       // 64 sub-rounds = 405 launches)
         const int64_t f = std::max<int64_t>(nF, 1);
-        P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
+        const int64_t ef = LCC_PEDGE ? std::max<int64_t>((int64_t)hc[NBINS], 1) : 1;
+        P = (int)std::max<int64_t>(
+            1, std::min<int64_t>(std::min<int64_t>(64, ((1LL << 22) + f - 1) / f), ((1LL << 26) + ef - 1) / ef));
     }
     WindowPlan wp;
     if (hc[2] > 0) plan_windows(g.indptr, lists.get() + binstart[2], (int64_t)hc[2], wp, s);

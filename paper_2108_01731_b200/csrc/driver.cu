@@ -229,13 +229,15 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         if (!moved) break;  // Alg. 1 line 13
         // deeper levels first: park the finer owned levels on the host when
         // this contraction would not fit next to them
-        if (owned.size() > 1 && !contraction_fits(g)) {
+        // (LCC_PARK_ALWAYS=1 parks every finer level: tests of the parking path)
+        const bool park_always = getenv("LCC_PARK_ALWAYS") && getenv("LCC_PARK_ALWAYS")[0] == '1';
+        if (owned.size() > 1 && (park_always || !contraction_fits(g))) {
             for (size_t i = 0; i + 1 < owned.size(); ++i) {
                 if (owned[i]->host) continue;
                 owned[i]->park(s);
                 if (trace) fprintf(stderr, "[lcc]   parked level %zu (%.1f GB) on the host\n", i + 1,
                                    owned[i]->bytes() / 1073741824.0);
-                if (contraction_fits(g)) break;
+                if (!park_always && contraction_fits(g)) break;
             }
         }
         EventTimer tc(s);

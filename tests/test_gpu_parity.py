@@ -519,3 +519,16 @@ def test_hub_cluster_path_exact(monkeypatch):
             D0, m0, c0 = O.sync_round(g, None, 0.3, C, K)
             D1, m1, c1 = gpu_sync_round(hg, None, 0.3, C, K)
             assert np.array_equal(D0, D1) and c0 == c1
+
+
+def test_parallel_cc_parked_levels_exact(monkeypatch):
+    """Coarse levels parked in host memory (forced with LCC_PARK_ALWAYS=1) and
+    restored for their refinement give the same labels as the oracle."""
+    monkeypatch.setenv("LCC_PARK_ALWAYS", "1")
+    u, v = rmat_pairs_host(13, 16 << 13, 0.57, 0.19, 0.19, 7)
+    hg = csr_from_pairs(1 << 13, u, v)
+    g = og(hg)
+    C0 = O.parallel_cc(g, None, 0.3, O.Opts(schedule=O.SYNC))
+    cl = L.parallel_cc(hg, L.ClusteringParams(0.3), L.ParOptions(schedule="sync"))
+    assert cl.meta["stats"].levels >= 3
+    assert np.array_equal(cl.labels(), C0)

@@ -39,8 +39,11 @@
 namespace lcc {
 namespace {
 
-#ifndef LCC_PEDGE
-#define LCC_PEDGE 0  // 1: also cap async sub-rounds by the frontier edges (more oscillation: off)
+#ifndef LCC_OCC
+#define LCC_OCC 0  // occupied-slot lists in the group tables (measured -35%: off)
+#endif
+#ifndef LCC_VALIDATE
+#define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
 #endif
 #ifndef LCC_SMALL_EARLYK
 #define LCC_SMALL_EARLYK 0
@@ -99,7 +102,7 @@ struct BMArgs {
 // Final choice for one vertex (mirrors oracle best_target()).
 template <bool ASYNC>
 __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, double kv, double b,
-                                      bool has, double bg, int32_t bx) {
+                                      bool has, double bg, int32_t bx, double bS = NAN) {
     const double gf = dsub(0.0, b);
     int32_t choice = c;
     double cg = 0.0;
@@ -107,6 +110,22 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
     if (!has || gf > cg) { choice = a.n + v; cg = gf; }
     if (cg > 0.0) {
         if constexpr (ASYNC) {
+            if (LCC_VALIDATE && choice != a.n + v && bS == bS) {
+                // commit-time check: the mass x has when v joins (the atomic's
+                // return value, after every earlier joiner) must still leave a
+                // positive gain; otherwise v stays (it is in the next frontier,
+                // since its neighbours moved).  Stops stale-mass pile-ups.
+                const double kold = atomicAdd(a.K + choice, kv);
+                const double gnow = dsub(dsub(bS, dmul(dmul(a.lam, kv), kold)), b);
+                if (!(gnow > 0.0)) {
+                    atomicAdd(a.K + choice, -kv);
+                    return 0;
+                }
+                stC_relaxed(a.C, v, choice);
+                atomicAdd(a.K + c, -kv);
+                a.moved[v] = 1;
+                return 1;
+            }
             stC_relaxed(a.C, v, choice);
             atomicAdd(a.K + c, -kv);
             atomicAdd(a.K + choice, kv);
@@ -125,6 +144,16 @@ __device__ __forceinline__ void warp_argmax(double& g, int32_t& x) {
         double og = __shfl_xor_sync(FULL, g, d);
         int32_t ox = __shfl_xor_sync(FULL, x, d);
         if (better(og, ox, g, x)) { g = og; x = ox; }
+    }
+}
+// ... carrying the winner's neighbour weight S (commit-time validation)
+__device__ __forceinline__ void warp_argmax(double& g, int32_t& x, double& S) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        double og = __shfl_xor_sync(FULL, g, d);
+        int32_t ox = __shfl_xor_sync(FULL, x, d);
+        double oS = __shfl_xor_sync(FULL, S, d);
+        if (better(og, ox, g, x)) { g = og; x = ox; S = oS; }
     }
 }
 
@@ -235,7 +264,9 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const double bj = __shfl_sync(FULL, bv, j);
             double g = -INFINITY;
             int32_t gx = NO_CAND;
+            double gS = 0.0;
             if (is_leader && x != cj) {
+                gS = S;
 #if LCC_SMALL_EARLYK
                 g = dsub(dsub(S, dmul(tj, kx_early)), bj);
 #else
@@ -249,12 +280,16 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 const double og = __shfl_down_sync(FULL, g, d);
                 const int32_t ox = __shfl_down_sync(FULL, gx, d);
                 const int32_t os = __shfl_down_sync(FULL, seg, d);
-                if (lane + d < 32 && os == seg && better(og, ox, g, gx)) { g = og; gx = ox; }
+                double oS = 0.0;
+                if constexpr (ASYNC && LCC_VALIDATE) oS = __shfl_down_sync(FULL, gS, d);
+                if (lane + d < 32 && os == seg && better(og, ox, g, gx)) { g = og; gx = ox; gS = oS; }
             }
             const int src = starter ? rs : lane;
             const double hg = __shfl_sync(FULL, g, src);
             const int32_t hx = __shfl_sync(FULL, gx, src);
-            const int mv = inwin ? decide<ASYNC>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx) : 0;
+            double hS = NAN;
+            if constexpr (ASYNC && LCC_VALIDATE) hS = __shfl_sync(FULL, gS, src);
+            const int mv = inwin ? decide<ASYNC>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx, hS) : 0;
             my_moves += mv;
             if (a.mark) {  // the window's neighbour ids are still in registers
                 const int mvj = __shfl_sync(FULL, mv, j);
@@ -319,6 +354,10 @@ struct SmemTable<false> {
     }
     // returns true when this call claimed the slot (first occurrence of x)
     __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, uint32_t add) const {
+        uint32_t slot;
+        return insert(cap, x, add, slot);
+    }
+    __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, uint32_t add, uint32_t& slot) const {
         uint32_t h = slot_of(x, cap);
         int32_t prev;
         while (true) {
@@ -327,6 +366,7 @@ struct SmemTable<false> {
             h = (h + 1 == cap) ? 0 : h + 1;
         }
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add) : "memory");
+        slot = h;
         return prev == EMPTY_KEY;
     }
         __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
@@ -357,6 +397,10 @@ struct SmemTable<true> {
         asm volatile("st.shared.f64 [%0], %1;" ::"r"(vals + 8 * q), "d"(0.0) : "memory");
     }
     __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, double wv) const {
+        uint32_t slot;
+        return insert(cap, x, wv, slot);
+    }
+    __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, double wv, uint32_t& slot) const {
         uint32_t h = slot_of(x, cap);
         bool fresh = false;
         while (true) {
@@ -372,6 +416,7 @@ struct SmemTable<true> {
             h = (h + 1 == cap) ? 0 : h + 1;
         }
         asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(vals + 8 * h), "d"(wv) : "memory");
+        slot = h;
         return fresh;
     }
         __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
@@ -412,6 +457,13 @@ struct GlobalTable<false> {
         S = u32_to_f64((uint32_t)w);
         return true;
     }
+    __device__ __forceinline__ double find(uint32_t cap, int32_t x) const {
+        for (uint32_t h = slot_of(x, cap);; h = (h + 1 == cap) ? 0 : h + 1) {
+            const unsigned long long w = tab[h];
+            if (w == EMPTY64) return NAN;
+            if ((int32_t)(w >> 32) == x) return u32_to_f64((uint32_t)w);
+        }
+    }
 };
 template <>
 struct GlobalTable<true> {
@@ -434,6 +486,13 @@ struct GlobalTable<true> {
         S = vals[q];
         return true;
     }
+    __device__ __forceinline__ double find(uint32_t cap, int32_t x) const {
+        for (uint32_t h = slot_of(x, cap);; h = (h + 1 == cap) ? 0 : h + 1) {
+            const int32_t kq = keys[h];
+            if (kq == EMPTY_KEY) return NAN;
+            if (kq == x) return vals[h];
+        }
+    }
 };
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
@@ -445,9 +504,15 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // Every lane keeps U independent loads in flight (index stream + label
 // gather; then slot read + mass gather) before consuming them.
 // ===========================================================================
+// occupied-slot list per group (16-bit slot ids): at most one entry per
+// distinct neighbour cluster <= the bin's maximum degree
+template <int CAP>
+constexpr int occ_cap() { return CAP >= 16384 ? (CAP * 5) / 8 : CAP / 2; }
+
 template <class WT, int CAP, int GROUPS>
 constexpr size_t group_smem_bytes() {
-    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot;
+    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot +
+           (LCC_OCC ? (size_t)GROUPS * occ_cap<CAP>() * sizeof(uint16_t) : 0);
 }
 
 template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
@@ -460,6 +525,9 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     __shared__ double s_g[GROUPS * GW];
     __shared__ int32_t s_x[GROUPS * GW];
     __shared__ int32_t s_mv[GROUPS];
+    __shared__ int32_t s_occ[GROUPS];
+    constexpr bool VAL = ASYNC && LCC_VALIDATE;
+    __shared__ double s_S[VAL ? GROUPS * GW : 1];
     const int gid = threadIdx.x / GT;
     const int gt = threadIdx.x % GT;
     const int wig = gt >> 5;
@@ -471,6 +539,13 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         else named_sync(1 + gid, GT);
     };
     for (uint32_t q = gt; q < CAP; q += GT) tab.clear(q);
+#if LCC_OCC
+    // slots claimed for the current vertex, so scoring visits (and clears)
+    // exactly the occupied ones instead of all 2*deg
+    uint16_t* occ = reinterpret_cast<uint16_t*>(smem + (size_t)GROUPS * CAP * SmemTable<FSUM>::bytes_per_slot) +
+                    (size_t)gid * occ_cap<CAP>();
+    if (gt == 0) s_occ[gid] = 0;
+#endif
     gsync();
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
@@ -501,12 +576,31 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
             for (int j = 0; j < U; ++j) {
+#if LCC_OCC
+                bool fresh = false;
+                uint32_t slot = 0;
+                if (u[j] != EMPTY_KEY) {
+                    if (u[j] == c) sc += WLoad<WT>::f64(wv[j]);
+                    else fresh = tab.insert(cap, u[j], wv[j], slot);
+                }
+                // lanes past the row end have left the loop: active-mask collectives
+                const unsigned am = __activemask();
+                const unsigned fm = __ballot_sync(am, fresh);
+                if (fm) {
+                    const int leader = __ffs(fm) - 1;
+                    int base = 0;
+                    if (lane == leader) base = atomicAdd(&s_occ[gid], __popc(fm));
+                    base = __shfl_sync(am, base, leader);
+                    if (fresh) occ[base + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)slot;
+                }
+#else
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) {
                     sc += WLoad<WT>::f64(wv[j]);
                 } else {
                     tab.insert(cap, u[j], wv[j]);
                 }
+#endif
             }
         }
 #pragma unroll
@@ -523,6 +617,18 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
+        double bS = 0.0;
+#if LCC_OCC
+        const int nocc = s_occ[gid];
+        for (int i0 = gt; i0 < nocc; i0 += GT * U) {
+            int32_t x[U];
+            double S[U], Kx[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int i = i0 + j * GT;
+                if (!(i < nocc && tab.take(occ[i], x[j], S[j]))) x[j] = EMPTY_KEY;
+            }
+#else
         for (uint32_t q0 = gt; q0 < cap; q0 += GT * U) {
             int32_t x[U];
             double S[U], Kx[U];
@@ -531,31 +637,44 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 const uint32_t q = q0 + j * GT;
                 if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
+#endif
 #pragma unroll
             for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
                 const double gq = dsub(dsub(S[j], dmul(t, Kx[j])), b);
-                if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; }
+                if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; bS = S[j]; }
             }
         }
-        warp_argmax(bg, bx);
+        if constexpr (VAL) warp_argmax(bg, bx, bS);
+        else warp_argmax(bg, bx);
         if constexpr (GW > 1) {
             gsync();  // everyone has read s_g (S_c) before reuse
-            if (lane == 0) { s_g[gid * GW + wig] = bg; s_x[gid * GW + wig] = bx; }
+            if (lane == 0) {
+                s_g[gid * GW + wig] = bg;
+                s_x[gid * GW + wig] = bx;
+                if constexpr (VAL) s_S[gid * GW + wig] = bS;
+            }
             gsync();
 #pragma unroll
             for (int w = 0; w < GW; ++w) {
                 const double og = s_g[gid * GW + w];
                 const int32_t ox = s_x[gid * GW + w];
-                if (better(og, ox, bg, bx)) { bg = og; bx = ox; }
+                if (better(og, ox, bg, bx)) {
+                    bg = og;
+                    bx = ox;
+                    if constexpr (VAL) bS = s_S[gid * GW + w];
+                }
             }
         }
         int mv = 0;
         if (gt == 0) {
-            mv = decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
+            mv = decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx, VAL ? bS : NAN);
             my_moves += mv;
+#if LCC_OCC
+            s_occ[gid] = 0;  // every thread read it before the argmax barriers
+#endif
         }
         if (a.mark) {  // fused frontier: a mover flags its neighbours (row re-read hits L2)
             if constexpr (GW == 1) {
@@ -986,7 +1105,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
     }
 }
 
-template <bool ASYNC>
+template <class WT, bool ASYNC>
 __global__ void k_large_decide(BMArgs a, LargeBatch L) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1006,7 +1125,12 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
             const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
             const double t = dmul(a.lam, kv);
             const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
-            my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx);
+            double bS = NAN;  // the winner's S, for the commit-time check (the batch's table is intact)
+            if (ASYNC && LCC_VALIDATE && bx != NO_CAND) {
+                const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
+                bS = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]).find(cap, bx);
+            }
+            my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bS);
         }
     }
     flush_moves(a, my_moves);
@@ -1551,7 +1675,7 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int
         LCC_LAUNCH_CHECK();
         k_large_score<WT, ASYNC><<<grid_for(bt.sitems * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L, bt.sitems);
         LCC_LAUNCH_CHECK();
-        k_large_decide<ASYNC><<<grid_for(bt.nb * 32, 256), 256, 0, s>>>(a, L);
+        k_large_decide<WT, ASYNC><<<grid_for(bt.nb * 32, 256), 256, 0, s>>>(a, L);
         LCC_LAUNCH_CHECK();
         if (a.mark) {
             k_large_mark<<<grid_for(bt.items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, bt.items);
@@ -1659,14 +1783,11 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     int P = 1;
     if (ASYNC && chunks > 0) P = chunks;
     else if (ASYNC) {  // ~4M / F sub-rounds, at most 64 (small graphs need the ordering:
-                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative),
-                       // and one wave once the frontier's edges alone fill the GPU
-                       // (late config-4 rounds: 58K hub-heavy vertices, 126M edges,
-                       // 64 sub-rounds = 405 launches)
+                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative);
+                       // chunks < 0: at least -chunks (driver: rounds after the first)
         const int64_t f = std::max<int64_t>(nF, 1);
-        const int64_t ef = LCC_PEDGE ? std::max<int64_t>((int64_t)hc[NBINS], 1) : 1;
-        P = (int)std::max<int64_t>(
-            1, std::min<int64_t>(std::min<int64_t>(64, ((1LL << 22) + f - 1) / f), ((1LL << 26) + ef - 1) / ef));
+        P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
+        if (chunks < 0) P = std::max(P, -chunks);
     }
     WindowPlan wp;
     if (hc[2] > 0) plan_windows(g.indptr, lists.get() + binstart[2], (int64_t)hc[2], wp, s);
@@ -1679,7 +1800,9 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     // order on the caller's stream: the interleaving is what breaks symmetry
     // on small graphs (measured on the config-1 SBM).
     SideStreams& ss = side_streams();
-    const bool concurrent = P == 1;
+    // (large frontiers: bins may also overlap inside each ordered sub-round)
+    const char* esc = getenv("LCC_SUBCONC");
+    const bool concurrent = P == 1 || (esc && esc[0] == '1' && nF >= (1 << 20));
     LCC_CUDA(cudaEventRecord(ev0, s));
     for (int j = 0; j < P; ++j) {
         LCC_CUDA(cudaEventRecord(ss.fork, s));
@@ -1749,6 +1872,7 @@ int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_
     LCC_REQUIRE(g.n >= 0 && g.n < (1LL << 30), "vertex count out of range");
     LCC_REQUIRE(schedule == LCC_SYNC || schedule == LCC_ASYNC, "unknown schedule");
     LCC_REQUIRE(schedule == LCC_ASYNC || D != nullptr, "sync schedule needs D");
+    LCC_REQUIRE(async_chunks >= -64, "async_chunks out of range");
     if (!frontier) nF = g.n;
     if (g.n == 0) return 0;
     const bool as = schedule == LCC_ASYNC;

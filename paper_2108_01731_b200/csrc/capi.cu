@@ -188,7 +188,7 @@ lcc_status lcc_par_best_moves(const lcc_graph* g, const lcc_params* p, const lcc
         check_graph(g);
         check_params(p);
         LCC_REQUIRE(g->n == 0 || (C && K), "NULL buffer");
-        const bool a = lcc::par_best_moves(*g, p->k, p->lambda, to_opts(opts), C, K, stats, S(stream));
+        const bool a = lcc::par_best_moves(*g, p->k, p->lambda, to_opts(opts), true, C, K, stats, S(stream));
         if (any_moved) *any_moved = a ? 1 : 0;
     });
 }

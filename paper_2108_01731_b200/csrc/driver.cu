@@ -14,6 +14,10 @@
 
 #include "internal.cuh"
 
+#ifndef LCC_PMIN_DEFAULT
+#define LCC_PMIN_DEFAULT 1
+#endif
+
 namespace lcc {
 
 namespace {
@@ -39,8 +43,13 @@ struct EventTimer {
 };
 }  // namespace
 
-bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C, double* K,
-                    lcc_stats* st, cudaStream_t s) {
+int async_min_subrounds() {
+    const char* e = getenv("LCC_PMIN");  // tuning knob
+    return e ? std::max(1, std::min(64, atoi(e))) : LCC_PMIN_DEFAULT;
+}
+
+bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, bool first_level, int32_t* C,
+                    double* K, lcc_stats* st, cudaStream_t s) {
     LCC_REQUIRE(o.num_iter >= 1, "num_iter must be >= 1");
     const int64_t n = g.n;
     if (n == 0) return false;
@@ -72,7 +81,9 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
             LCC_CUDA(cudaMemcpyAsync(K2.get(), K, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemsetAsync(K2.get() + n, 0, sizeof(double) * n, s));
             cnt = best_moves_round(g, k, lam, D.get(), K2.get(), frontier, nF, LCC_ASYNC, o.deg_threshold,
-                                   o.async_chunks, nullptr, moved.get(), mk, &rs, s);
+                                   o.async_chunks > 0 ? o.async_chunks
+                                   : (first_level && it == 0) ? 0 : -async_min_subrounds(),
+                                   nullptr, moved.get(), mk, &rs, s);
         }
         const float ms = tm.stop();
         if (getenv("LCC_TRACE"))
@@ -218,7 +229,7 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         fill_iota(C.get(), n, s);  // singletons
         fill_k(K.get(), k, n, s);
         if (st) st->levels += 1;
-        const bool moved = par_best_moves(g, k, lam, o, C.get(), K.get(), st, s);
+        const bool moved = par_best_moves(g, k, lam, o, stack.empty(), C.get(), K.get(), st, s);
         if (trace) {
             const float ms = tl.stop();
             double r, u;
@@ -283,7 +294,7 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         Buf<int32_t> Cf(std::max<int64_t>(n, 1), s);
         Buf<double> Kf(std::max<int64_t>(n, 1), s);
         flatten(n, it->mapping.get(), Cres.get(), it->k, Cf.get(), Kf.get(), s);
-        if (o.refine) par_best_moves(gf, it->k, lam, o, Cf.get(), Kf.get(), st, s);
+        if (o.refine) par_best_moves(gf, it->k, lam, o, false, Cf.get(), Kf.get(), st, s);
         if (trace) fprintf(stderr, "[lcc] unwind n=%lld flatten+refine %.2f ms\n", (long long)n, tu.stop());
         Cres = std::move(Cf);
     }

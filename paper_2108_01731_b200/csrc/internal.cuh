@@ -70,7 +70,10 @@ struct Options {
     int schedule = LCC_ASYNC, policy = LCC_FRONTIER_VERTEX_NBRS, refine = 1, num_iter = 10;
     int deg_threshold = 1000, async_chunks = 0;  // 0 = auto
 };
-bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C,
+// first_level: the first iteration may run as one wave (P auto); later
+// async iterations take at least async_min_subrounds() ordered sub-rounds.
+int async_min_subrounds();
+bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Options& o, bool first_level, int32_t* C,
                     double* K, lcc_stats* st, cudaStream_t s);
 void parallel_cc(const lcc_graph& g, const double* k, double lam, const Options& o, int32_t* C_out,
                  lcc_stats* st, cudaStream_t s);

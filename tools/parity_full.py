@@ -34,17 +34,26 @@ def main(which):
     out = {}
     if "cfg4" in which:
         dg = rmat_device(24, 16, seed=24)
-        lab, t_gpu = gpu_run(dg, None, 0.85)
         ip, ix, _ = dg.to_host()
         g = O.Graph(dg.n, ip, ix, None, float(dg.m))
-        o_gpu = O.objective(g, None, 0.85, lab)
-        t0 = time.perf_counter()
-        ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.ASYNC, async_parallel=True, threads=threads))
-        t_cpu = time.perf_counter() - t0
-        o_ref = O.objective(g, None, 0.85, ref)
-        out["cfg4"] = {"objective_gpu": o_gpu, "objective_cpu_parallel_async": o_ref,
-                       "rel_diff": (o_gpu - o_ref) / abs(o_ref), "pass_0.5pct": o_gpu >= o_ref - 0.005 * abs(o_ref),
-                       "gpu_s": t_gpu, "cpu_s": t_cpu, "cpu_threads": threads}
+        # async is nondeterministic on both sides: distributions, not single runs
+        o_gpu, t_gpu = [], []
+        for _ in range(5):
+            lab, t = gpu_run(dg, None, 0.85)
+            o_gpu.append(O.objective(g, None, 0.85, lab))
+            t_gpu.append(t)
+        o_ref, t_cpu = [], []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.ASYNC, async_parallel=True, threads=threads))
+            t_cpu.append(time.perf_counter() - t0)
+            o_ref.append(O.objective(g, None, 0.85, ref))
+        mg, mr = float(np.median(o_gpu)), float(np.median(o_ref))
+        out["cfg4"] = {"objective_gpu_runs": o_gpu, "objective_cpu_parallel_async_runs": o_ref,
+                       "median_gpu": mg, "median_cpu": mr, "rel_diff_medians": (mg - mr) / abs(mr),
+                       "pass_0.5pct_medians": mg >= mr - 0.005 * abs(mr),
+                       "gpu_s_median": float(np.median(t_gpu)), "cpu_s_median": float(np.median(t_cpu)),
+                       "cpu_threads": threads}
         print(json.dumps({"cfg4": out["cfg4"]}), flush=True)
     if "cfg2" in which:
         hg, _ = lfr_like(n=1_200_000, seed=2)

@@ -7,26 +7,33 @@
 // plus the fresh-singleton option (gain -b, temporary id n+v, loses ties),
 // and pick the argmax with the lowest-id tie rule; move iff gain > 0.
 //
-// The frontier is split by degree into bins, each with a kernel whose
-// thread count matches the work (grids sized to SM count x occupancy):
-//   0  deg <= 32          : k_small, one warp packs 32 vertices into 32-edge
-//                           windows; labels grouped by __match_any_sync on
-//                           (vertex, label); segmented argmax by shuffles.
-//                           Sums run in CSR order (bit-identical to the oracle
-//                           even for weighted graphs).
-//   1-3 33 .. threshold-1 : k_group, one WARP per vertex with a 256/1024/4096
-//                           slot shared-memory hash table (the paper's
-//                           "sequential" per-vertex accumulation)
-//   4-5 threshold .. 10240: k_group, 4 or 16 warps per vertex with a 4K/16K
-//                           slot shared-memory table ("parallel hash table")
-//   6   > 10240           : hubs; edges cut into 8192-edge work items spread
-//                           over all SMs inserting into per-vertex global
-//                           tables, batched so every batch's tables stay
-//                           L2-resident (48 MB), then CTA-per-vertex scoring.
+// The frontier is split by degree into bins (stable two-pass partition),
+// each with a kernel whose thread count matches the work:
+//   0  isolated            : k_isolated, thread per vertex (fresh singleton only)
+//   1  deg <= 32           : k_small, one warp packs 32 vertices into 32-edge
+//                            windows; labels grouped by __match_any_sync on
+//                            (vertex, label); segmented argmax by shuffles.
+//                            Sums run in CSR order (bit-identical to the oracle
+//                            even for weighted graphs).
+//   2  (opt-in LCC_WINDOW) : k_window, edge-balanced multi-vertex CTAs
+//   3-4 33 .. 512          : k_group, one WARP per vertex, 256/1024-slot
+//                            shared-memory hash table (the paper's
+//                            "sequential" per-vertex accumulation)
+//   5-7 .. 10240           : k_group, 4/8/32 warps per vertex, 4K-16K slots
+//                            ("parallel hash table")
+//   8  hubs                : edges cut into 2048-edge work items spread over
+//                            all SMs inserting into per-vertex global tables,
+//                            batched (256 MB) and scored in 16K-slot items;
+//                            opt-in DSMEM cluster tables (LCC_HUB_CLUSTER=1).
+// Tables use native 32-bit shared atomics (CAS on the key, RED on the
+// count / integer weight); float weights add with fp64 RED.
 // sync  : targets written to D (apply happens in apply.cu);
 // async : C stored and K updated with relaxed device atomics right away
 //         (the CUDA analogue of _atomics.py:37-43), the
-//         frontier processed in `async_chunks` ordered sub-rounds.
+//         frontier processed in ordered sub-rounds for small frontiers, and
+//         every move re-validated at commit time against the target's mass
+//         returned by the join atomic (no stale-mass pile-ups).
+// Optional fused VertexNeighbors frontier: movers flag their neighbours.
 #include <cub/cub.cuh>
 #include <math.h>
 #include <type_traits>
@@ -39,14 +46,8 @@
 namespace lcc {
 namespace {
 
-#ifndef LCC_OCC
-#define LCC_OCC 0  // occupied-slot lists in the group tables (measured -35%: off)
-#endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
-#endif
-#ifndef LCC_SMALL_EARLYK
-#define LCC_SMALL_EARLYK 0
 #endif
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -237,11 +238,6 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 x = ldC<ASYNC>(a.C, nbr, pol_keep);
                 wv = WLoad<WT>::at(a.w, e);
             }
-#if LCC_SMALL_EARLYK
-            // every edge lane issues its cluster's mass gather right away; the
-            // grouping below overlaps it (duplicates of a group are L1/L2 hits)
-            const double kx_early = has_edge ? ldK<ASYNC>(a.K, x, pol_keep) : 0.0;
-#endif
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
                                           : ((uint64_t)(64 + lane) << 32);
             const unsigned grp = __match_any_sync(FULL, key);
@@ -267,11 +263,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double gS = 0.0;
             if (is_leader && x != cj) {
                 gS = S;
-#if LCC_SMALL_EARLYK
-                g = dsub(dsub(S, dmul(tj, kx_early)), bj);
-#else
                 g = dsub(dsub(S, dmul(tj, ldK<ASYNC>(a.K, x, pol_keep))), bj);
-#endif
                 gx = x;
             }
             const int32_t seg = has_edge ? j : 32 + lane;
@@ -504,15 +496,9 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // Every lane keeps U independent loads in flight (index stream + label
 // gather; then slot read + mass gather) before consuming them.
 // ===========================================================================
-// occupied-slot list per group (16-bit slot ids): at most one entry per
-// distinct neighbour cluster <= the bin's maximum degree
-template <int CAP>
-constexpr int occ_cap() { return CAP >= 16384 ? (CAP * 5) / 8 : CAP / 2; }
-
 template <class WT, int CAP, int GROUPS>
 constexpr size_t group_smem_bytes() {
-    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot +
-           (LCC_OCC ? (size_t)GROUPS * occ_cap<CAP>() * sizeof(uint16_t) : 0);
+    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot;
 }
 
 template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
@@ -525,7 +511,6 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     __shared__ double s_g[GROUPS * GW];
     __shared__ int32_t s_x[GROUPS * GW];
     __shared__ int32_t s_mv[GROUPS];
-    __shared__ int32_t s_occ[GROUPS];
     constexpr bool VAL = ASYNC && LCC_VALIDATE;
     __shared__ double s_S[VAL ? GROUPS * GW : 1];
     const int gid = threadIdx.x / GT;
@@ -539,13 +524,6 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         else named_sync(1 + gid, GT);
     };
     for (uint32_t q = gt; q < CAP; q += GT) tab.clear(q);
-#if LCC_OCC
-    // slots claimed for the current vertex, so scoring visits (and clears)
-    // exactly the occupied ones instead of all 2*deg
-    uint16_t* occ = reinterpret_cast<uint16_t*>(smem + (size_t)GROUPS * CAP * SmemTable<FSUM>::bytes_per_slot) +
-                    (size_t)gid * occ_cap<CAP>();
-    if (gt == 0) s_occ[gid] = 0;
-#endif
     gsync();
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
@@ -576,31 +554,12 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-#if LCC_OCC
-                bool fresh = false;
-                uint32_t slot = 0;
-                if (u[j] != EMPTY_KEY) {
-                    if (u[j] == c) sc += WLoad<WT>::f64(wv[j]);
-                    else fresh = tab.insert(cap, u[j], wv[j], slot);
-                }
-                // lanes past the row end have left the loop: active-mask collectives
-                const unsigned am = __activemask();
-                const unsigned fm = __ballot_sync(am, fresh);
-                if (fm) {
-                    const int leader = __ffs(fm) - 1;
-                    int base = 0;
-                    if (lane == leader) base = atomicAdd(&s_occ[gid], __popc(fm));
-                    base = __shfl_sync(am, base, leader);
-                    if (fresh) occ[base + __popc(fm & ((1u << lane) - 1u))] = (uint16_t)slot;
-                }
-#else
                 if (u[j] == EMPTY_KEY) continue;
                 if (u[j] == c) {
                     sc += WLoad<WT>::f64(wv[j]);
                 } else {
                     tab.insert(cap, u[j], wv[j]);
                 }
-#endif
             }
         }
 #pragma unroll
@@ -618,17 +577,6 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         double bg = -INFINITY;
         int32_t bx = NO_CAND;
         double bS = 0.0;
-#if LCC_OCC
-        const int nocc = s_occ[gid];
-        for (int i0 = gt; i0 < nocc; i0 += GT * U) {
-            int32_t x[U];
-            double S[U], Kx[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int i = i0 + j * GT;
-                if (!(i < nocc && tab.take(occ[i], x[j], S[j]))) x[j] = EMPTY_KEY;
-            }
-#else
         for (uint32_t q0 = gt; q0 < cap; q0 += GT * U) {
             int32_t x[U];
             double S[U], Kx[U];
@@ -637,7 +585,6 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 const uint32_t q = q0 + j * GT;
                 if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
-#endif
 #pragma unroll
             for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
@@ -672,9 +619,6 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         if (gt == 0) {
             mv = decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx, VAL ? bS : NAN);
             my_moves += mv;
-#if LCC_OCC
-            s_occ[gid] = 0;  // every thread read it before the argmax barriers
-#endif
         }
         if (a.mark) {  // fused frontier: a mover flags its neighbours (row re-read hits L2)
             if constexpr (GW == 1) {

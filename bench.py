@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--schedule", default=None, choices=["async", "sync"], help="default: the config's schedule")
     ap.add_argument("--async-chunks", type=int, default=0)
     ap.add_argument("--degree-threshold", type=int, default=1000)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-stride", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -84,12 +84,15 @@ class ClockSampler:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, enabled: bool = True):
         self.gpu = gpu
         self.lines = []
         self.p = None
+        self.enabled = enabled
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -453,7 +456,7 @@ def run_ours(args):
 
             e2e_step()  # warm-up (pool growth)
             times, edges_sum, stats = [], 0, None
-            with ClockSampler(lrank) as clk_e2e:
+            with ClockSampler(lrank, enabled=not os.environ.get("LCC_BENCH_NOCLK")) as clk_e2e:
                 for _ in range(max(1, args.e2e_steps)):
                     torch.cuda.synchronize()
                     t0 = time.perf_counter()
@@ -464,6 +467,7 @@ def run_ours(args):
             if os.environ.get("LCC_BENCH_DEBUG"):
                 print("e2e clock samples:", clk_e2e.lines, file=sys.stderr)
             t_e2e = sum(times) / len(times)
+        step_ms = [round(1e3 * t, 1) for t in times]
             e_t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
             ed_t = torch.tensor([edges_sum / len(times)], dtype=torch.float64, device="cuda")
             if dist:
@@ -476,7 +480,7 @@ def run_ours(args):
             e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
                                              (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
-                   "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()),
+                   "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()), "clustering_ms_per_step": step_ms,
                    "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
                    "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
                    "device_ms_best_move_kernels": stats.ms_kernels,

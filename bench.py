@@ -467,7 +467,7 @@ def run_ours(args):
             if os.environ.get("LCC_BENCH_DEBUG"):
                 print("e2e clock samples:", clk_e2e.lines, file=sys.stderr)
             t_e2e = sum(times) / len(times)
-        step_ms = [round(1e3 * t, 1) for t in times]
+            step_ms = [round(1e3 * t, 1) for t in times]
             e_t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
             ed_t = torch.tensor([edges_sum / len(times)], dtype=torch.float64, device="cuda")
             if dist:

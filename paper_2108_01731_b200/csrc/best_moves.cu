@@ -39,6 +39,8 @@
 #include <type_traits>
 #include <vector>
 #include <cstdlib>
+#include <chrono>
+#include <cstdio>
 
 #include "internal.cuh"
 #include "prims.cuh"
@@ -98,6 +100,9 @@ struct BMArgs {
     unsigned long long* moved_count;
     int32_t n;
     uint8_t* mark;  // optional: neighbours of movers flagged here (fused VertexNeighbors frontier)
+    const uint8_t* prev_moved;       // async damping (AsyncDamp), or null
+    uint32_t salt;
+    unsigned long long* pending;     // deferred movers this round
 };
 
 // Final choice for one vertex (mirrors oracle best_target()).
@@ -111,6 +116,12 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
     if (!has || gf > cg) { choice = a.n + v; cg = gf; }
     if (cg > 0.0) {
         if constexpr (ASYNC) {
+            if (a.prev_moved && a.prev_moved[v] && (hash32((uint32_t)v * 0x9E3779B9u + a.salt) & 1u)) {
+                // deferred: v moved last iteration too; it stays in the frontier
+                a.mark[v] = 1;
+                atomicAdd(a.pending, 1ull);
+                return 0;
+            }
             if (LCC_VALIDATE && choice != a.n + v && bS == bS) {
                 // commit-time check: the mass x has when v joins (the atomic's
                 // return value, after every earlier joiner) must still leave a
@@ -1628,6 +1639,19 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int
     }
 }
 
+// LCC_TRACE: host-side sections of a round that take > 20 ms (stall hunting)
+struct HostProbe {
+    bool on = getenv("LCC_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+        if (ms > 20.0) fprintf(stderr, "[lcc]       host section '%s' took %.1f ms\n", what, ms);
+        t = now;
+    }
+};
+
 // side streams for concurrent bin kernels (one set per device, created once)
 struct SideStreams {
     cudaStream_t st[NBINS];
@@ -1654,8 +1678,9 @@ inline SideStreams& side_streams() {
 template <class WT, bool ASYNC>
 int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                   const int32_t* frontier, int64_t nF, int deg_threshold, int chunks, int32_t* D,
-                  uint8_t* moved, uint8_t* mark, RoundStats* st, cudaStream_t s) {
+                  uint8_t* moved, uint8_t* mark, RoundStats* st, cudaStream_t s, const AsyncDamp* damp) {
     const int64_t n = g.n;
+    HostProbe hprobe;
     if (!ASYNC) LCC_CUDA(cudaMemcpyAsync(D, C, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
     LCC_CUDA(cudaMemsetAsync(moved, 0, n, s));
     if (mark) LCC_CUDA(cudaMemsetAsync(mark, 0, n, s));
@@ -1689,10 +1714,15 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     be.hi[7] = std::min<int64_t>(MED_MAX, large_min);
     be.hi[8] = INT64_MAX;
 
+    if (hprobe.on && getenv("LCC_TRACE_SYNC")) {  // device work queued before this round
+        LCC_CUDA(cudaStreamSynchronize(s));
+        hprobe.mark("prior device work");
+    }
     Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);
+    hprobe.mark("alloc lists");
     std::vector<int64_t> binstart;
-    Buf<unsigned long long> dcnt(2, s);  // [edges, movers]
-    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * 2, s));
+    Buf<unsigned long long> dcnt(3, s);  // [edges, movers, deferred]
+    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * 3, s));
     unsigned long long* dmoved = dcnt.get() + 1;
     const int64_t ntiles = std::max<int64_t>((nF + BIN_TILE - 1) / BIN_TILE, 1);
     Buf<int64_t> tcnt(NBINS * ntiles + 1, s), tbase(NBINS * ntiles + 1, s);
@@ -1702,6 +1732,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         LCC_LAUNCH_CHECK();
         LCC_CUDA(cudaMemsetAsync(tcnt.get() + NBINS * ntiles, 0, sizeof(int64_t), s));
         exclusive_sum(tcnt.get(), tbase.get(), NBINS * ntiles + 1, s);
+        hprobe.mark("count + scan enqueue");
         k_bin_scatter<<<(unsigned)ntiles, BIN_THREADS, 0, s>>>(g.indptr, frontier, nF, be, ntiles, tbase.get(),
                                                                lists.get());
         LCC_LAUNCH_CHECK();
@@ -1710,14 +1741,18 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         for (int b = 0; b <= NBINS; ++b)
             LCC_CUDA(cudaMemcpyAsync(&hb[b], tbase.get() + (int64_t)b * ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaMemcpyAsync(&hc[NBINS], dcnt.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        hprobe.mark("scatter + D2H enqueue");
         LCC_CUDA(cudaStreamSynchronize(s));
         for (int b = 0; b < NBINS; ++b) hc[b] = (unsigned long long)(hb[b + 1] - hb[b]);
         binstart.assign(hb.begin(), hb.end());
+        hprobe.mark("bin partition (incl. device wait)");
     } else {
         for (int b = 0; b <= NBINS; ++b) hc[b] = 0;
         binstart.assign(NBINS + 1, 0);
     }
-    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n, mark};
+    const bool dmp = ASYNC && damp && damp->prev_moved && mark;  // deferral needs the fused frontier
+    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n, mark,
+             dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
     LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
@@ -1786,10 +1821,13 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             LCC_CUDA(cudaStreamWaitEvent(s, ss.join[i], 0));
         }
     }
+    hprobe.mark("launches");
     LCC_CUDA(cudaEventRecord(ev1, s));
-    unsigned long long hm = 0;
+    unsigned long long hm = 0, hp = 0;
     LCC_CUDA(cudaMemcpyAsync(&hm, dmoved, sizeof(hm), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaMemcpyAsync(&hp, dcnt.get() + 2, sizeof(hp), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
+    hprobe.mark("kernels (device wait)");
     LCC_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -1804,7 +1842,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         st->ms_kernels += (double)kms + (double)kms_large;
         st->launches += launch_counter() - launches0;
     }
-    return (int64_t)hm;
+    return (int64_t)(hm + hp);  // deferred movers keep the iteration loop going
 }
 
 }  // namespace
@@ -1812,7 +1850,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                          const int32_t* frontier, int64_t nF, int schedule, int deg_threshold,
                          int async_chunks, int32_t* D, uint8_t* moved, uint8_t* mark, RoundStats* st,
-                         cudaStream_t s) {
+                         cudaStream_t s, const AsyncDamp* damp) {
     LCC_REQUIRE(g.n >= 0 && g.n < (1LL << 30), "vertex count out of range");
     LCC_REQUIRE(schedule == LCC_SYNC || schedule == LCC_ASYNC, "unknown schedule");
     LCC_REQUIRE(schedule == LCC_ASYNC || D != nullptr, "sync schedule needs D");
@@ -1822,19 +1860,19 @@ int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_
     const bool as = schedule == LCC_ASYNC;
     switch (g.weights ? g.wtype : LCC_W_NONE) {
         case LCC_W_NONE:
-            return as ? run_round<WNone, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
-                      : run_round<WNone, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
+            return as ? run_round<WNone, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp)
+                      : run_round<WNone, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp);
         case LCC_W_F32:
-            return as ? run_round<float, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
-                      : run_round<float, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
+            return as ? run_round<float, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp)
+                      : run_round<float, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp);
         case LCC_W_F64:
-            return as ? run_round<double, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
-                      : run_round<double, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
+            return as ? run_round<double, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp)
+                      : run_round<double, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp);
         case LCC_W_U32:
             // integer sums in 32-bit slots: every per-vertex sum <= 2 * total weight
             LCC_REQUIRE(2.0 * g.total_weight < 4294967296.0, "uint32 weights need 2 * total_weight < 2^32");
-            return as ? run_round<uint32_t, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s)
-                      : run_round<uint32_t, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s);
+            return as ? run_round<uint32_t, true>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp)
+                      : run_round<uint32_t, false>(g, k, lam, C, K, frontier, nF, deg_threshold, async_chunks, D, moved, mark, st, s, damp);
         default:
             throw Invalid("unknown weight dtype");
     }

@@ -50,7 +50,7 @@ long long& launch_counter();
 // order (an event orders reuse on another stream) and handed back by
 // trim_cache() at the end of every C-ABI call above the keep limit.
 // ---------------------------------------------------------------------------
-constexpr size_t CACHE_MIN_BYTES = 64ull << 20;
+constexpr size_t CACHE_MIN_BYTES = 1ull << 20;
 void* cache_alloc(size_t bytes, cudaStream_t s, size_t* cap);
 void cache_free(void* p, size_t cap, cudaStream_t s);
 void trim_cache(size_t keep_bytes, cudaStream_t s);

@@ -60,6 +60,13 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
     const bool fused = o.policy == LCC_FRONTIER_VERTEX_NBRS;
     Buf<uint8_t> mark;
     if (fused && o.num_iter > 1) mark.alloc(n, s);
+    // async damping needs last iteration's movers: two flag arrays, swapped
+    const char* ed = getenv("LCC_DAMP");
+    const bool damping = as && fused && o.num_iter > 1 && !(ed && ed[0] == '0');
+    Buf<uint8_t> moved2;
+    if (damping) moved2.alloc(n, s);
+    uint8_t* mv_cur = moved.get();
+    uint8_t* mv_prev = nullptr;
     Buf<double> K2;
     if (as) K2.alloc(2 * n, s);
     int32_t* cur = C;
@@ -75,15 +82,18 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         EventTimer tm(s);
         if (!as) {
             cnt = best_moves_round(g, k, lam, cur, K, frontier, nF, LCC_SYNC, o.deg_threshold, 1, D.get(),
-                                   moved.get(), mk, &rs, s);
+                                   mv_cur, mk, &rs, s);
         } else {
+            AsyncDamp damp;
+            damp.prev_moved = damping ? mv_prev : nullptr;
+            damp.salt = 0x85EBCA6Bu * (uint32_t)(it + 1);
             LCC_CUDA(cudaMemcpyAsync(D.get(), cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemcpyAsync(K2.get(), K, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemsetAsync(K2.get() + n, 0, sizeof(double) * n, s));
             cnt = best_moves_round(g, k, lam, D.get(), K2.get(), frontier, nF, LCC_ASYNC, o.deg_threshold,
                                    o.async_chunks > 0 ? o.async_chunks
                                    : (first_level && it == 0) ? 0 : -async_min_subrounds(),
-                                   nullptr, moved.get(), mk, &rs, s);
+                                   nullptr, mv_cur, mk, &rs, s, &damp);
         }
         const float ms = tm.stop();
         if (getenv("LCC_TRACE"))
@@ -103,10 +113,14 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         apply_moves(n, D.get(), 2 * n, k, nxt, K, s);  // sync apply / async reconcile
         if (it + 1 < o.num_iter) {  // the next frontier is only needed by a next iteration
             nF = mk ? frontier_from_mask(n, mk, F.get(), s)
-                    : compute_frontier(g, o.policy, moved.get(), cur, nxt, F.get(), s);
+                    : compute_frontier(g, o.policy, mv_cur, cur, nxt, F.get(), s);
             frontier = F.get();
         }
         std::swap(cur, nxt);
+        if (damping) {
+            mv_prev = mv_cur;
+            mv_cur = mv_cur == moved.get() ? moved2.get() : moved.get();
+        }
     }
     if (cur != C) LCC_CUDA(cudaMemcpyAsync(C, cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
     LCC_CUDA(cudaStreamSynchronize(s));

@@ -19,10 +19,18 @@ struct RoundStats {
 // mark (optional, n bytes): zeroed, then every neighbour of a mover is
 // flagged -- the VertexNeighbors frontier fused into the round.
 // Returns the number of movers (synchronises the stream once).
+// damp (async, optional): vertices that moved in the previous iteration
+// (prev_moved) defer a move with probability 1/2 -- they stay in the next
+// frontier (via mark) and count as pending -- which breaks the 2-cycles
+// (swaps) that simultaneous moves create.
+struct AsyncDamp {
+    const uint8_t* prev_moved = nullptr;
+    uint32_t salt = 0;
+};
 int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                          const int32_t* frontier, int64_t nF, int schedule, int deg_threshold,
                          int async_chunks, int32_t* D, uint8_t* moved, uint8_t* mark, RoundStats* st,
-                         cudaStream_t s);
+                         cudaStream_t s, const AsyncDamp* damp = nullptr);
 
 // apply.cu
 void apply_moves(int64_t n, const int32_t* labels_in, int64_t label_range, const double* k,

@@ -1,7 +1,6 @@
 set -u
 O=gpurun_out; mkdir -p $O
-for mode in clk noclk clk noclk; do
-if [ $mode = noclk ]; then export LCC_BENCH_NOCLK=1; else unset LCC_BENCH_NOCLK; fi
-LCC_BENCH_DEBUG=1 timeout 600 python bench.py --no-cpu --steps 3 --e2e-steps 4 > $O/b.json 2> $O/b.err
-echo $mode $(grep "e2e phases" $O/b.err | sed 's/.*parallel_cc \([0-9.]*\).*relabel \([0-9.]*\)/\1|\2/' | tr '\n' ' ')
+timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -2 $O/gpu_tests.log
+for i in 1 2; do
+timeout 600 python bench.py --no-cpu > $O/b.json 2>/dev/null; python -c "import json;d=json.load(open('$O/b.json'));e=d['e2e'];print(round(d['value'],2), 'e2e', round(e['value'],2), round(e['clustering_ms'],1), e['clustering_ms_per_step'], e['levels'], e['rounds'], round(e['objective']))"
 done

@@ -48,6 +48,9 @@
 namespace lcc {
 namespace {
 
+#ifndef LCC_FHASH
+#define LCC_FHASH 1  // Fibonacci slot hash (+0.8% vs the murmur finalizer)
+#endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
 #endif
@@ -334,7 +337,12 @@ k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 // clean for the next vertex without a separate clearing pass.
 // ===========================================================================
 __device__ __forceinline__ uint32_t slot_of(int32_t x, uint32_t cap) {
+#if LCC_FHASH
+    // Fibonacci hashing: one multiply (cluster ids are vertex ids, dense)
+    return (uint32_t)(((uint64_t)((uint32_t)x * 0x9E3779B1u) * cap) >> 32);
+#else
     return (uint32_t)(((uint64_t)hash32((uint32_t)x) * cap) >> 32);
+#endif
 }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

@@ -51,6 +51,12 @@ namespace {
 #ifndef LCC_FHASH
 #define LCC_FHASH 1  // Fibonacci slot hash (+0.8% vs the murmur finalizer)
 #endif
+#ifndef LCC_LDS_FIRST
+#define LCC_LDS_FIRST 0  // 1: read the slot before the atomic (measured 28% slower: a dependent LDS per probe)
+#endif
+#ifndef LCC_ALWAYS_RED
+#define LCC_ALWAYS_RED 0  // tuning: RED even for unit-weight claims
+#endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
 #endif
@@ -76,15 +82,37 @@ __device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i, uint64_t pol
         return ld_keep_i32(C + i, pol);
     }
 }
-template <bool ASYNC>
-__device__ __forceinline__ double ldK(const double* K, int64_t i, uint64_t pol) {
-    if constexpr (ASYNC) {
-        double r;
-        asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(r) : "l"(K + i));
-        return r;
+// KI: integer masses, gathered from a uint32 image of K (half the bytes of
+// the fp64 array, so labels + masses stay L2-resident); exact, see run_round.
+template <bool ASYNC, bool KI>
+__device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
+    if constexpr (KI) {
+        const uint32_t* K = static_cast<const uint32_t*>(Kp);
+        uint32_t r;
+        if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(K + i));
+        else r = (uint32_t)ld_keep_i32(reinterpret_cast<const int32_t*>(K) + i, pol);
+        return u32_to_f64(r);
     } else {
-        return ld_keep_f64(K + i, pol);
+        const double* K = static_cast<const double*>(Kp);
+        if constexpr (ASYNC) {
+            double r;
+            asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(r) : "l"(K + i));
+            return r;
+        } else {
+            return ld_keep_f64(K + i, pol);
+        }
     }
+}
+// relaxed mass update; returns the mass before the add
+template <bool KI>
+__device__ __forceinline__ double addK(void* Kp, int64_t i, double kv) {
+    if constexpr (KI) return u32_to_f64(atomicAdd(static_cast<uint32_t*>(Kp) + i, (uint32_t)kv));
+    else return atomicAdd(static_cast<double*>(Kp) + i, kv);
+}
+template <bool KI>
+__device__ __forceinline__ void subK(void* Kp, int64_t i, double kv) {
+    if constexpr (KI) atomicSub(static_cast<uint32_t*>(Kp) + i, (uint32_t)kv);
+    else atomicAdd(static_cast<double*>(Kp) + i, -kv);
 }
 __device__ __forceinline__ void stC_relaxed(int32_t* C, int64_t i, int32_t x) {
     asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(C + i), "r"(x) : "memory");
@@ -97,7 +125,7 @@ struct BMArgs {
     const double* k;
     double lam;
     int32_t* C;
-    double* K;
+    void* K;      // double[n | 2n], or the uint32 image (KI kernels)
     int32_t* D;
     uint8_t* moved;
     unsigned long long* moved_count;
@@ -109,7 +137,7 @@ struct BMArgs {
 };
 
 // Final choice for one vertex (mirrors oracle best_target()).
-template <bool ASYNC>
+template <bool ASYNC, bool KI>
 __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, double kv, double b,
                                       bool has, double bg, int32_t bx, double bS = NAN) {
     const double gf = dsub(0.0, b);
@@ -130,20 +158,20 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                 // return value, after every earlier joiner) must still leave a
                 // positive gain; otherwise v stays (it is in the next frontier,
                 // since its neighbours moved).  Stops stale-mass pile-ups.
-                const double kold = atomicAdd(a.K + choice, kv);
+                const double kold = addK<KI>(a.K, choice, kv);
                 const double gnow = dsub(dsub(bS, dmul(dmul(a.lam, kv), kold)), b);
                 if (!(gnow > 0.0)) {
-                    atomicAdd(a.K + choice, -kv);
+                    subK<KI>(a.K, choice, kv);
                     return 0;
                 }
                 stC_relaxed(a.C, v, choice);
-                atomicAdd(a.K + c, -kv);
+                subK<KI>(a.K, c, kv);
                 a.moved[v] = 1;
                 return 1;
             }
             stC_relaxed(a.C, v, choice);
-            atomicAdd(a.K + c, -kv);
-            atomicAdd(a.K + choice, kv);
+            subK<KI>(a.K, c, kv);
+            addK<KI>(a.K, choice, kv);
         } else {
             a.D[v] = choice;
         }
@@ -181,7 +209,7 @@ __device__ __forceinline__ void flush_moves(const BMArgs& a, unsigned long long 
 // ===========================================================================
 // small bin: deg <= 32, warp-packed edge windows
 // ===========================================================================
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 __global__ void __launch_bounds__(SMALL_THREADS)
 k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr int WPB = SMALL_THREADS / 32;
@@ -209,7 +237,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             deg = (int32_t)(__ldg(a.indptr + v + 1) - s);
             c = ldC<ASYNC>(a.C, v, pol_keep);
             kv = kval(a.k, v);
-            Kc = ldK<ASYNC>(a.K, c, pol_keep);
+            Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         }
         const double t = dmul(a.lam, kv);
         int32_t incl = deg;
@@ -277,7 +305,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double gS = 0.0;
             if (is_leader && x != cj) {
                 gS = S;
-                g = dsub(dsub(S, dmul(tj, ldK<ASYNC>(a.K, x, pol_keep))), bj);
+                g = dsub(dsub(S, dmul(tj, ldK<ASYNC, KI>(a.K, x, pol_keep))), bj);
                 gx = x;
             }
             const int32_t seg = has_edge ? j : 32 + lane;
@@ -295,7 +323,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const int32_t hx = __shfl_sync(FULL, gx, src);
             double hS = NAN;
             if constexpr (ASYNC && LCC_VALIDATE) hS = __shfl_sync(FULL, gS, src);
-            const int mv = inwin ? decide<ASYNC>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx, hS) : 0;
+            const int mv = inwin ? decide<ASYNC, KI>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx, hS) : 0;
             my_moves += mv;
             if (a.mark) {  // the window's neighbour ids are still in registers
                 const int mvj = __shfl_sync(FULL, mv, j);
@@ -312,7 +340,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 // isolated vertices (deg 0): S = 0 for every cluster, so the only candidate is
 // the fresh singleton (gain -b), taken when v sits in a heavier cluster
 // ===========================================================================
-template <bool ASYNC>
+template <bool ASYNC, bool KI>
 __global__ void __launch_bounds__(256)
 k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const uint64_t pol_keep = policy_evict_last();
@@ -322,8 +350,8 @@ k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
-        const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC>(a.K, c, pol_keep))), dmul(t, kv));
-        my_moves += decide<ASYNC>(a, v, c, kv, b, false, 0.0, 0);
+        const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC, KI>(a.K, c, pol_keep))), dmul(t, kv));
+        my_moves += decide<ASYNC, KI>(a, v, c, kv, b, false, 0.0, 0);
     }
     flush_moves(a, my_moves);
 }
@@ -368,19 +396,48 @@ struct SmemTable<false> {
         uint32_t slot;
         return insert(cap, x, add, slot);
     }
+    // Shared-memory atomics cost ~2 cycles per lane (B300_MICROARCH.md
+    // "Atomics": ATOMS spread-addr), 64x a plain LDS, and bound the group
+    // bins.  So one atomic per edge: the slot's key is read first; a repeat
+    // key costs one RED, a fresh key one CAS.  The claimer's own weight is
+    // implicit: counts hold (sum of weights - 1) mod 2^32, S = count + 1, so
+    // a unit-weight claim needs no RED at all.
     __device__ __forceinline__ bool insert(uint32_t cap, int32_t x, uint32_t add, uint32_t& slot) const {
         uint32_t h = slot_of(x, cap);
+#if LCC_LDS_FIRST
+        while (true) {
+            int32_t kq;
+            asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * h));
+            if (kq == x) break;
+            if (kq == EMPTY_KEY) {
+                int32_t prev;
+                asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+                if (prev == EMPTY_KEY) {
+                    if (add != 1u) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add - 1u) : "memory");
+                    slot = h;
+                    return true;
+                }
+                if (prev == x) break;
+            }
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add) : "memory");
+        slot = h;
+        return false;
+#else
         int32_t prev;
         while (true) {
             asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
             if (prev == EMPTY_KEY || prev == x) break;
             h = (h + 1 == cap) ? 0 : h + 1;
         }
-        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add) : "memory");
+        const uint32_t inc = prev == EMPTY_KEY ? add - 1u : add;
+        if (inc || LCC_ALWAYS_RED) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(inc) : "memory");
         slot = h;
         return prev == EMPTY_KEY;
+#endif
     }
-        __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
+    __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S) const {
         int32_t kq;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
         if (kq == EMPTY_KEY) return false;
@@ -388,7 +445,7 @@ struct SmemTable<false> {
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cq) : "r"(cnts + 4 * q));
         clear(q);
         x = kq;
-        S = u32_to_f64(cq);
+        S = u32_to_f64(cq + 1u);
         return true;
     }
 };
@@ -520,7 +577,7 @@ constexpr size_t group_smem_bytes() {
     return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot;
 }
 
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
+template <class WT, bool ASYNC, bool KI, int GW, int CAP, int GROUPS, int U, int MINB = 1>
 __global__ void __launch_bounds__(GW * 32 * GROUPS, MINB)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr bool FSUM = WLoad<WT>::fsum;
@@ -555,7 +612,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
         for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
@@ -605,7 +662,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -636,7 +693,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         }
         int mv = 0;
         if (gt == 0) {
-            mv = decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx, VAL ? bS : NAN);
+            mv = decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, VAL ? bS : NAN);
             my_moves += mv;
         }
         if (a.mark) {  // fused frontier: a mover flags its neighbours (row re-read hits L2)
@@ -696,7 +753,7 @@ constexpr size_t window_smem_bytes() {
     return (size_t)WIN_CAP * (4 + (FSUM ? 8 : 4) + 8);
 }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 __global__ void __launch_bounds__(WIN_THREADS)
 k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__ off,
          const int64_t* __restrict__ wstart, int64_t w0, int64_t w1) {
@@ -741,7 +798,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             const double kv = kval(a.k, v);
             s_kv[tid] = kv;
             s_t[tid] = dmul(a.lam, kv);
-            s_Kc[tid] = ldK<ASYNC>(a.K, c, pol_keep);
+            s_Kc[tid] = ldK<ASYNC, KI>(a.K, c, pol_keep);
             s_sc[tid] = 0;
             s_scw[tid] = 0.0;
             s_hi[tid] = 0;
@@ -816,7 +873,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             const int32_t x = (int32_t)(key & ((1u << LABEL_BITS) - 1u));
             const int sj = (int)(key >> LABEL_BITS);
             const double S = FSUM ? sums[q] : u32_to_f64(cnts[q]);
-            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC>(a.K, x, pol_keep))), s_b[sj]);
+            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC, KI>(a.K, x, pol_keep))), s_b[sj]);
             gval[q] = g;
             atomicMax(&s_hi[sj], (uint32_t)(ord_gain(g) >> 32));
         }
@@ -845,7 +902,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
         if (tid < nv) {
             const int32_t bx = s_bx[tid];
             const unsigned long long o = ((unsigned long long)s_hi[tid] << 32) | s_lo[tid];
-            const int mv = decide<ASYNC>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND, unord_gain(o), bx);
+            const int mv = decide<ASYNC, KI>(a, s_v[tid], s_c[tid], s_kv[tid], s_b[tid], bx != NO_CAND, unord_gain(o), bx);
             my_moves += mv;
             s_mv[tid] = mv;
         }
@@ -1025,7 +1082,7 @@ __device__ __forceinline__ void block_argmax(double& g, int32_t& x, double* s_g,
     __syncthreads();
 }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 __global__ void __launch_bounds__(SCORE_THREADS)
 k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
     constexpr int UL = 8;
@@ -1041,7 +1098,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
@@ -1055,7 +1112,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
                 if (!(q < q_end && tab.read(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -1068,7 +1125,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
     }
 }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 __global__ void k_large_decide(BMArgs a, LargeBatch L) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1085,7 +1142,7 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
             const int32_t v = L.list[li];
             const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
             const double kv = kval(a.k, v);
-            const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
+            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
             const double t = dmul(a.lam, kv);
             const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
             double bS = NAN;  // the winner's S, for the commit-time check (the batch's table is intact)
@@ -1093,7 +1150,7 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
                 const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
                 bS = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]).find(cap, bx);
             }
-            my_moves += decide<ASYNC>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bS);
+            my_moves += decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bS);
         }
     }
     flush_moves(a, my_moves);
@@ -1163,7 +1220,7 @@ __device__ __forceinline__ uint32_t cl_map(uint32_t smem_addr, uint32_t rank) {
     return r;
 }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 __global__ void __launch_bounds__(HC_THREADS, 1)
 k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
     static_assert(!WLoad<WT>::fsum, "cluster hub path: integer sums only");
@@ -1263,7 +1320,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
             sct += x;
         }
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(sct, dmul(t, Kc)), dmul(t, kv));
         // ---- 3. score (and clear) the local slice
@@ -1288,7 +1345,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
                 }
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -1312,7 +1369,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
             int32_t x = s_px[0];
             for (int r = 1; r < HC_CL; ++r)
                 if (better(s_pg[r], s_px[r], g, x)) { g = s_pg[r]; x = s_px[r]; }
-            const int mv = decide<ASYNC>(a, v, c, kv, b, x != NO_CAND, g, x);
+            const int mv = decide<ASYNC, KI>(a, v, c, kv, b, x != NO_CAND, g, x);
             my_moves += mv;
             for (int r = 0; r < HC_CL; ++r)
                 asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cl_map(smem_u32(&s_moved), r)), "r"(mv) : "memory");
@@ -1424,25 +1481,60 @@ __global__ void k_degrees_of(const int64_t* __restrict__ indptr, const int32_t* 
     }
 }
 
+// ---- integer masses ------------------------------------------------------
+// Every BASELINE config has integer k (k = 1, or k = unweighted degree), so
+// every cluster mass K_c is an integer.  When a round covers a large part of
+// the graph, K is copied into a uint32 image for the round: the per-candidate
+// mass gathers then read 4 instead of 8 bytes from an array half the size
+// (config 4: labels 67 MB + masses 67 MB stay L2-resident, against 67 + 134
+// MB).  u32 -> f64 is exact, so every gain is bit-identical.  The copy checks
+// integrality (K and k), non-negativity and sum(K) < 2^31 (no transient sum
+// can wrap); any failure keeps the fp64 kernels for the round.
+__global__ void k_mass_to_u32(const double* __restrict__ K, int64_t klen, const double* __restrict__ k, int64_t n,
+                              uint32_t* __restrict__ Ki, unsigned long long* sum, unsigned* bad) {
+    unsigned long long my = 0;
+    bool ok = true;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = K[i];
+        const bool good = x >= 0.0 && x < 2147483648.0 && x == floor(x);
+        ok &= good;
+        const uint32_t u = good ? (uint32_t)x : 0u;
+        Ki[i] = u;
+        my += u;
+        if (k && i < n) {
+            const double kv = k[i];
+            ok &= kv >= 0.0 && kv < 2147483648.0 && kv == floor(kv);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) my += __shfl_xor_sync(FULL, my, d);
+    if ((threadIdx.x & 31) == 0 && my) atomicAdd(sum, my);
+    if (__any_sync(FULL, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+__global__ void k_mass_from_u32(const uint32_t* __restrict__ Ki, int64_t klen, double* __restrict__ K) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x)
+        K[i] = u32_to_f64(Ki[i]);
+}
+
 template <class K>
 void set_smem(K kernel, int bytes) {
     LCC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-template <class WT, bool ASYNC, int GW, int CAP, int GROUPS, int U, int MINB = 1>
+template <class WT, bool ASYNC, bool KI, int GW, int CAP, int GROUPS, int U, int MINB = 1>
 void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     if (hi <= lo) return;
     constexpr int THREADS = GW * 32 * GROUPS;
     constexpr int SMEM = (int)group_smem_bytes<WT, CAP, GROUPS>();
     static int occ = 0;
     if (!occ) {
-        set_smem(k_group<WT, ASYNC, GW, CAP, GROUPS, U, MINB>, SMEM);
-        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, GW, CAP, GROUPS, U, MINB>, THREADS, SMEM));
+        set_smem(k_group<WT, ASYNC, KI, GW, CAP, GROUPS, U, MINB>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group<WT, ASYNC, KI, GW, CAP, GROUPS, U, MINB>, THREADS, SMEM));
         occ = std::max(occ, 1);
     }
     const int64_t blocks_needed = (hi - lo + GROUPS - 1) / GROUPS;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * occ));
-    k_group<WT, ASYNC, GW, CAP, GROUPS, U, MINB><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
+    k_group<WT, ASYNC, KI, GW, CAP, GROUPS, U, MINB><<<grid, THREADS, SMEM, s>>>(a, list, lo, hi);
     LCC_LAUNCH_CHECK();
 }
 
@@ -1455,25 +1547,25 @@ constexpr int64_t LARGE_TABLE_BYTES = (int64_t)LCC_LARGE_TABLE_MB << 20;  // per
 
 // bin -> kernel shape.  Shared memory per group = CAP * (4 key + 4|8 value +
 // 2 slot-list) bytes; GROUPS chosen so 2-3 CTAs fit per SM.
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     // LCC_VARIANT (env, tuning only) selects alternative group shapes
     const char* ev = getenv("LCC_VARIANT");
     const int var = ev ? atoi(ev) : 0;
     switch (bin) {  //                         GW  CAP    GROUPS U
-        case 2: launch_group<WT, ASYNC, 1, 256, 8, 4, 6>(a, list, lo, hi, s); break;   //  ..128      warp
-        case 3: launch_group<WT, ASYNC, 1, 1024, 8, 8, 3>(a, list, lo, hi, s); break;  //  ..512      warp
+        case 2: launch_group<WT, ASYNC, KI, 1, 256, 8, 4, 6>(a, list, lo, hi, s); break;   //  ..128      warp
+        case 3: launch_group<WT, ASYNC, KI, 1, 1024, 8, 8, 3>(a, list, lo, hi, s); break;  //  ..512      warp
         case 4:
-            if (var == 3) launch_group<WT, ASYNC, 8, 4096, 1, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 4, 4096, 2, 8, 3>(a, list, lo, hi, s);        //  ..2048     4 warps
+            if (var == 3) launch_group<WT, ASYNC, KI, 8, 4096, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, KI, 4, 4096, 2, 8, 3>(a, list, lo, hi, s);        //  ..2048     4 warps
             break;
         case 5:
-            if (var == 1) launch_group<WT, ASYNC, 16, 8192, 1, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 8, 8192, 1, 4>(a, list, lo, hi, s);           //  ..4096     8 warps
+            if (var == 1) launch_group<WT, ASYNC, KI, 16, 8192, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, KI, 8, 8192, 1, 4>(a, list, lo, hi, s);           //  ..4096     8 warps
             break;
         case 6:
-            if (var == 1) launch_group<WT, ASYNC, 16, B5_CAP, 1, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, 32, B5_CAP, 1, 4>(a, list, lo, hi, s);        //  ..10240    32 warps
+            if (var == 1) launch_group<WT, ASYNC, KI, 16, B5_CAP, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, KI, 32, B5_CAP, 1, 4>(a, list, lo, hi, s);        //  ..10240    32 warps
             break;
         default: break;
     }
@@ -1499,28 +1591,28 @@ inline void plan_windows(const int64_t* indptr, const int32_t* list, int64_t nb,
     LCC_LAUNCH_CHECK();
 }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 void launch_window(const BMArgs& a, const int32_t* list, const WindowPlan& P, int64_t w0, int64_t w1, cudaStream_t s) {
     if (w1 <= w0) return;
     constexpr int SMEM = (int)window_smem_bytes<WLoad<WT>::fsum>();
     static int occ = 0;
     if (!occ) {
-        set_smem(k_window<WT, ASYNC>, SMEM);
-        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<WT, ASYNC>, WIN_THREADS, SMEM));
+        set_smem(k_window<WT, ASYNC, KI>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<WT, ASYNC, KI>, WIN_THREADS, SMEM));
         occ = std::max(occ, 1);
     }
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(w1 - w0, (int64_t)num_sms() * occ));
-    k_window<WT, ASYNC><<<grid, WIN_THREADS, SMEM, s>>>(a, list, P.off.get(), P.wstart.get(), w0, w1);
+    k_window<WT, ASYNC, KI><<<grid, WIN_THREADS, SMEM, s>>>(a, list, P.off.get(), P.wstart.get(), w0, w1);
     LCC_LAUNCH_CHECK();
 }
 
 inline int64_t large_cap(int64_t deg) { return (2 * deg + 31) & ~31LL; }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 void launch_hub_cluster(const BMArgs& a, const int32_t* hubs, int64_t nh, cudaStream_t s) {
     constexpr int SMEM = HC_SLICE * 8;
     static int max_clusters = 0;
-    auto kern = k_hub_cluster<WT, ASYNC>;
+    auto kern = k_hub_cluster<WT, ASYNC, KI>;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1544,7 +1636,7 @@ void launch_hub_cluster(const BMArgs& a, const int32_t* hubs, int64_t nh, cudaSt
     LCC_LAUNCH_CHECK();
 }
 
-template <class WT, bool ASYNC>
+template <class WT, bool ASYNC, bool KI>
 void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int64_t nL_in, cudaStream_t s) {
     constexpr bool WEIGHTED = WLoad<WT>::fsum;  // float sums: key + f64 value tables
     Buf<int64_t> ddeg(nL_in, s);
@@ -1578,7 +1670,7 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int
         LCC_CUDA(cudaMemcpyAsync(dlists.get() + hc.size(), l2.data(), sizeof(int32_t) * l2.size(),
                                  cudaMemcpyHostToDevice, s));
     if constexpr (!WEIGHTED) {
-        if (!hc.empty()) launch_hub_cluster<WT, ASYNC>(a, dlists.get(), (int64_t)hc.size(), s);
+        if (!hc.empty()) launch_hub_cluster<WT, ASYNC, KI>(a, dlists.get(), (int64_t)hc.size(), s);
     }
     const int32_t* large = dlists.get() + hc.size();
     const int64_t nL = (int64_t)l2.size();
@@ -1636,9 +1728,9 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int
         }
         k_large_insert<WT, ASYNC><<<grid_for(bt.items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, bt.items);
         LCC_LAUNCH_CHECK();
-        k_large_score<WT, ASYNC><<<grid_for(bt.sitems * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L, bt.sitems);
+        k_large_score<WT, ASYNC, KI><<<grid_for(bt.sitems * SCORE_THREADS, SCORE_THREADS, 4), SCORE_THREADS, 0, s>>>(a, L, bt.sitems);
         LCC_LAUNCH_CHECK();
-        k_large_decide<WT, ASYNC><<<grid_for(bt.nb * 32, 256), 256, 0, s>>>(a, L);
+        k_large_decide<WT, ASYNC, KI><<<grid_for(bt.nb * 32, 256), 256, 0, s>>>(a, L);
         LCC_LAUNCH_CHECK();
         if (a.mark) {
             k_large_mark<<<grid_for(bt.items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, bt.items);
@@ -1735,6 +1827,29 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const int64_t ntiles = std::max<int64_t>((nF + BIN_TILE - 1) / BIN_TILE, 1);
     Buf<int64_t> tcnt(NBINS * ntiles + 1, s), tbase(NBINS * ntiles + 1, s);
     unsigned long long hc[NBINS + 1];
+    // integer masses (KI kernels): decided here, confirmed by the bin sync.
+    // Only for rounds whose frontier is a sizeable part of the graph (the
+    // image costs ~n * 36 bytes of traffic per round); LCC_KINT=0 disables.
+    const int64_t klen = ASYNC ? 2 * n : n;
+    const char* eki = getenv("LCC_KINT");
+    const bool try_ki = nF > 0 && 8 * nF >= n && !(eki && eki[0] == '0');
+    Buf<uint32_t> Ki;
+    Buf<unsigned long long> kchk;
+    unsigned long long hk[2] = {0, 0};
+    float kconv_ms = 0.f;
+    cudaEvent_t kev[2] = {nullptr, nullptr};
+    if (try_ki) {
+        for (auto& e : kev) LCC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+        Ki.alloc(klen, s);
+        kchk.alloc(2, s);
+        LCC_CUDA(cudaMemsetAsync(kchk.get(), 0, sizeof(unsigned long long) * 2, s));
+        LCC_CUDA(cudaEventRecord(kev[0], s));
+        k_mass_to_u32<<<grid_for(klen, 256), 256, 0, s>>>(K, klen, k, n, Ki.get(), kchk.get(),
+                                                           reinterpret_cast<unsigned*>(kchk.get() + 1));
+        LCC_LAUNCH_CHECK();
+        LCC_CUDA(cudaEventRecord(kev[1], s));
+        LCC_CUDA(cudaMemcpyAsync(hk, kchk.get(), sizeof(hk), cudaMemcpyDeviceToHost, s));
+    }
     if (nF > 0) {
         k_bin_count<<<(unsigned)ntiles, BIN_THREADS, 0, s>>>(g.indptr, frontier, nF, be, ntiles, tcnt.get(), dcnt.get());
         LCC_LAUNCH_CHECK();
@@ -1758,8 +1873,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         for (int b = 0; b <= NBINS; ++b) hc[b] = 0;
         binstart.assign(NBINS + 1, 0);
     }
+    const bool ki = try_ki && hk[1] == 0 && hk[0] < (1ull << 31);
+    if (try_ki) LCC_CUDA(cudaEventElapsedTime(&kconv_ms, kev[0], kev[1]));
     const bool dmp = ASYNC && damp && damp->prev_moved && mark;  // deferral needs the fused frontier
-    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, K, D, moved, dmoved, (int32_t)n, mark,
+    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, ki ? (void*)Ki.get() : (void*)K, D, moved, dmoved, (int32_t)n, mark,
              dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
@@ -1791,6 +1908,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const char* esc = getenv("LCC_SUBCONC");
     const bool concurrent = P == 1 || (esc && esc[0] == '1' && nF >= (1 << 20));
     LCC_CUDA(cudaEventRecord(ev0, s));
+    auto launch_all = [&](auto ki_tag) {
+    constexpr bool KI = decltype(ki_tag)::value;
     for (int j = 0; j < P; ++j) {
         LCC_CUDA(cudaEventRecord(ss.fork, s));
         int used = 0;
@@ -1800,34 +1919,41 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             LCC_CUDA(cudaStreamWaitEvent(t, ss.fork, 0));
             return t;
         };
-        if (j == 0 && nL > 0) run_large<WT, ASYNC>(a, g, lists.get() + binstart[NBINS - 1], nL, next_stream());
+        if (j == 0 && nL > 0) run_large<WT, ASYNC, KI>(a, g, lists.get() + binstart[NBINS - 1], nL, next_stream());
         for (int b = 0; b < NBINS - 1; ++b) {
             const int64_t nb = (int64_t)hc[b];
             if (nb == 0) continue;
             const int32_t* list = lists.get() + binstart[b];
             if (b == 2) {
                 if (wp.nwin * (j + 1) / P > wp.nwin * j / P)
-                    launch_window<WT, ASYNC>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, next_stream());
+                    launch_window<WT, ASYNC, KI>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, next_stream());
                 continue;
             }
             const int64_t lo = nb * j / P, hi = nb * (j + 1) / P;
             if (hi <= lo) continue;
             cudaStream_t t = next_stream();
             if (b == 0) {
-                k_isolated<ASYNC><<<grid_for(hi - lo, 256, 8), 256, 0, t>>>(a, list, lo, hi);
+                k_isolated<ASYNC, KI><<<grid_for(hi - lo, 256, 8), 256, 0, t>>>(a, list, lo, hi);
                 LCC_LAUNCH_CHECK();
             } else if (b == 1) {
                 const int64_t warps = (hi - lo + 31) / 32;
-                k_small<WT, ASYNC><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, t>>>(a, list, lo, hi);
+                k_small<WT, ASYNC, KI><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, t>>>(a, list, lo, hi);
                 LCC_LAUNCH_CHECK();
             } else {
-                launch_bin<WT, ASYNC>(b - 1, a, list, lo, hi, t);
+                launch_bin<WT, ASYNC, KI>(b - 1, a, list, lo, hi, t);
             }
         }
         for (int i = 0; i < used; ++i) {
             LCC_CUDA(cudaEventRecord(ss.join[i], ss.st[i]));
             LCC_CUDA(cudaStreamWaitEvent(s, ss.join[i], 0));
         }
+    }
+    };
+    if (ki) launch_all(std::true_type{});
+    else launch_all(std::false_type{});
+    if (ki && ASYNC) {  // async moves updated the image: back to fp64 K
+        k_mass_from_u32<<<grid_for(klen, 256), 256, 0, s>>>(Ki.get(), klen, K);
+        LCC_LAUNCH_CHECK();
     }
     hprobe.mark("launches");
     LCC_CUDA(cudaEventRecord(ev1, s));
@@ -1839,6 +1965,9 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     LCC_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
+    for (auto& e : kev)
+        if (e) cudaEventDestroy(e);
+    kms += kconv_ms;  // the mass image is part of the round's kernel time
     const float kms_large = 0.f;
     if (st) {
         st->vertices += nF;

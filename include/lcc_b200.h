@@ -209,6 +209,27 @@ lcc_status lcc_build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u
                                     const int32_t* v, int64_t* indptr,
                                     int32_t* indices, int64_t* nnz, void* stream);
 
+/* ---- eval -----------------------
+ * Adjusted Rand index and normalised mutual information (arithmetic-mean
+ * normalisation) of two labelings a[n], b[n] (any int32
+ * values), over their contingency table; sklearn's degenerate cases
+ * (SPEC.md:354-364 `ari`, `nmi`).                                          */
+lcc_status lcc_partition_scores(int64_t n, const int32_t* a, const int32_t* b,
+                                double* ari, double* nmi, void* stream);
+/* avg_precision_recall: ground-truth communities as CSR
+ * (offsets[n_comm+1] starting at 0, members[offsets[n_comm]] vertex ids,
+ * each community non-empty and duplicate-free; they may overlap).  For each
+ * community t the cluster c' of C[n] with the largest |t & c'| (ties to the
+ * lowest cluster id); unweighted means of |t&c'|/|c'| and |t&c'|/|t|.
+ * n_comm == 0 or a member id outside [0, n) -> LCC_ERR_INVALID.             */
+lcc_status lcc_avg_precision_recall(int64_t n, const int32_t* C, int64_t n_comm,
+                                    const int64_t* offsets, const int32_t* members,
+                                    double* precision, double* recall, void* stream);
+/* cluster_stats: number of clusters and min / max / mean
+ * cluster size of C[n].                                                     */
+lcc_status lcc_cluster_stats(int64_t n, const int32_t* C, int64_t* num_clusters,
+                             int64_t* min_size, int64_t* max_size, double* mean_size,
+                             void* stream);
 #ifdef __cplusplus
 }
 #endif

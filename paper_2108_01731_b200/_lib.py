@@ -24,6 +24,7 @@ EXPORTS = (
     "lcc_compute_frontier", "lcc_par_best_moves", "lcc_par_compress", "lcc_par_flatten",
     "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_gen_powerlaw_communities",
     "lcc_build_csr_from_pairs", "lcc_frontier_from_mask", "lcc_release_memory",
+    "lcc_partition_scores", "lcc_avg_precision_recall", "lcc_cluster_stats",
 )
 
 
@@ -94,6 +95,9 @@ def load() -> ctypes.CDLL:
         "lcc_gen_rmat": (ctypes.c_int, [I32, I64, F64, F64, F64, ctypes.c_uint64, P, P, pI64, P]),
         "lcc_gen_powerlaw_communities": (ctypes.c_int, [I64, I64, F64, P, P, P, I64, ctypes.c_uint64, P, P, pI64, P]),
         "lcc_build_csr_from_pairs": (ctypes.c_int, [I64, I64, P, P, P, P, pI64, P]),
+        "lcc_partition_scores": (ctypes.c_int, [I64, P, P, pF64, pF64, P]),
+        "lcc_avg_precision_recall": (ctypes.c_int, [I64, P, I64, P, P, pF64, pF64, P]),
+        "lcc_cluster_stats": (ctypes.c_int, [I64, P, pI64, pI64, pI64, pF64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -279,4 +279,35 @@ lcc_status lcc_build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u
     });
 }
 
+lcc_status lcc_partition_scores(int64_t n, const int32_t* a, const int32_t* b, double* ari, double* nmi,
+                                void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0, "negative length");
+        LCC_REQUIRE(n == 0 || (a && b), "NULL labels");
+        LCC_REQUIRE(ari && nmi, "NULL output");
+        lcc::partition_scores(n, a, b, ari, nmi, S(stream));
+    });
+}
+
+lcc_status lcc_avg_precision_recall(int64_t n, const int32_t* C, int64_t n_comm, const int64_t* offsets,
+                                    const int32_t* members, double* precision, double* recall, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0, "negative vertex count");
+        LCC_REQUIRE(n_comm > 0, "empty ground truth");
+        LCC_REQUIRE(offsets && members && (n == 0 || C), "NULL buffer");
+        LCC_REQUIRE(precision && recall, "NULL output");
+        lcc::avg_precision_recall(n, C, n_comm, offsets, members, precision, recall, S(stream));
+    });
+}
+
+lcc_status lcc_cluster_stats(int64_t n, const int32_t* C, int64_t* num_clusters, int64_t* min_size, int64_t* max_size,
+                             double* mean_size, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0, "negative vertex count");
+        LCC_REQUIRE(n == 0 || C, "C is NULL");
+        LCC_REQUIRE(num_clusters && min_size && max_size && mean_size, "NULL output");
+        lcc::cluster_stats(n, C, num_clusters, min_size, max_size, mean_size, S(stream));
+    });
+}
+
 }  // extern "C"

@@ -73,6 +73,12 @@ int64_t gen_powerlaw_communities(int64_t n, int64_t samples, double mu, const do
                                  const int64_t* cstart, const double* cw_prefix, int64_t nc, uint64_t seed,
                                  int64_t* indptr, int32_t* indices, cudaStream_t s);
 
+// eval.cu
+void partition_scores(int64_t n, const int32_t* a, const int32_t* b, double* ari, double* nmi, cudaStream_t s);
+void avg_precision_recall(int64_t n, const int32_t* C, int64_t nc, const int64_t* off, const int32_t* members,
+                          double* precision, double* recall, cudaStream_t s);
+void cluster_stats(int64_t n, const int32_t* C, int64_t* num, int64_t* mn, int64_t* mx, double* mean, cudaStream_t s);
+
 // driver.cu
 struct Options {
     int schedule = LCC_ASYNC, policy = LCC_FRONTIER_VERTEX_NBRS, refine = 1, num_iter = 10;

@@ -187,12 +187,14 @@ def rmat_pairs_host(scale: int, samples: int, a: float, b: float, c: float, seed
 
 
 def rmat_device(scale: int = 24, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
-                seed: int = 24) -> DeviceGraph:
+                seed: int = 24, samples: int | None = None) -> DeviceGraph:
     """Config 4 (BASELINE.json configs[3]): Graph500 R-MAT, symmetrised,
-    deduplicated, self-loops removed, no vertex permutation."""
+    deduplicated, self-loops removed, no vertex permutation.  ``samples``
+    (directed draws) overrides ``edge_factor * 2^scale``."""
     dev = _device()
     n = 1 << scale
-    samples = edge_factor * n
+    if samples is None:
+        samples = edge_factor * n
     indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
     indices = torch.empty(max(2 * samples, 1), dtype=torch.int32, device=dev)
     nnz = ctypes.c_int64()

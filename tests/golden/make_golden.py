@@ -97,6 +97,29 @@ def frontier_cases(rng):
     return out
 
 
+def build_cases(rng):
+    """Raw edge lists -> the reference builder (graph.py:98-164): duplicates in
+    one orientation (summed), both orientations (averaged), self loops
+    (dropped), weighted and unweighted.  Checks io.build_graph_arrays."""
+    out = {}
+    for t in range(20):
+        n = int(rng.integers(2, 40))
+        k = int(rng.integers(1, 4 * n))
+        u = rng.integers(0, n, k)
+        v = rng.integers(0, n, k)
+        if t % 3 == 0:
+            u = np.concatenate([u, v[: k // 2]])  # reversed copies
+            v = np.concatenate([v, u[: k // 2]])
+        w = np.round(rng.uniform(-1.0, 3.0, u.size), 3) if t % 2 else np.ones(u.size)
+        g = build_graph_arrays(u, v, w, n=n)
+        pre = f"b{t}_"
+        out.update({pre + "u": u, pre + "v": v, pre + "w": w, pre + "n": np.array([n]),
+                    pre + "indptr": g.indptr, pre + "indices": g.indices, pre + "weights": g.weights,
+                    pre + "total": np.array([g.total_weight]), pre + "m": np.array([g.m])})
+    out["cases"] = np.arange(20)
+    return out
+
+
 def main():
     rng = np.random.default_rng(2108_01731)
     np.savez_compressed(os.path.join(HERE, "contraction.npz"), **contraction_cases(rng))
@@ -119,4 +142,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["build"]:  # only the build fixture (tests/golden/build.npz)
+        np.savez_compressed(os.path.join(HERE, "build.npz"), **build_cases(np.random.default_rng(398)))
+    else:
+        main()
+        np.savez_compressed(os.path.join(HERE, "build.npz"), **build_cases(np.random.default_rng(398)))

@@ -209,8 +209,11 @@ __device__ __forceinline__ void flush_moves(const BMArgs& a, unsigned long long 
 // ===========================================================================
 // small bin: deg <= 32, warp-packed edge windows
 // ===========================================================================
+#ifndef LCC_SMALL_MINB
+#define LCC_SMALL_MINB 5  // 48 registers: 40 resident warps (+1.2% vs 32)
+#endif
 template <class WT, bool ASYNC, bool KI>
-__global__ void __launch_bounds__(SMALL_THREADS)
+__global__ void __launch_bounds__(SMALL_THREADS, LCC_SMALL_MINB)
 k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr int WPB = SMALL_THREADS / 32;
     __shared__ int32_t s_owner[WPB][32];
@@ -1174,6 +1177,271 @@ k_large_mark(BMArgs a, LargeBatch L, int64_t total_items) {
 
 
 // ===========================================================================
+// hub bin, bucket path (default for integer sums): the hub's neighbour labels
+// are radix-partitioned by a hash of the label into buckets of ~HB_BE
+// entries, then every bucket is aggregated by one CTA in a shared-memory
+// table -- the same table as the group bins, so the hubs' per-edge work is
+// shared-memory atomics instead of L2 CAS round trips on a 256 MB global
+// table (and no table memset / write-back).
+//   1. k_hub_scatter: LARGE_CHUNK-edge items (as the insert kernel); labels
+//      gathered, the own-cluster weight summed, the rest counting-sorted by
+//      bucket inside the item (shared-memory histogram + scan) and written
+//      to the item's slot of `ent`, with per-item bucket offsets `ioff`.
+//   2. k_hub_bucket: one CTA per (hub, bucket) walks the hub's items, inserts
+//      its bucket's entries, scores its table -> partial (gain, id, S).
+//   3. k_hub_decide: a warp per hub merges the partials and decides.
+// A bucket whose entry count exceeds half the table is split into R passes
+// by a second hash; a table that still fills sets an error flag (the round
+// fails loudly; with murmur-hashed labels it does not happen).
+// ===========================================================================
+constexpr int HB_THREADS = 256;
+#ifndef LCC_HB_CAP
+#define LCC_HB_CAP 8192
+#endif
+constexpr int HB_CAP = LCC_HB_CAP;      // table slots per bucket CTA
+constexpr int HB_BE = HB_CAP / 2;       // target entries per bucket
+constexpr int HB_MAXB = 256;            // buckets per hub (more -> larger buckets, multi-pass)
+
+template <class WT>
+struct HubEntry {
+    using T = typename std::conditional<WLoad<WT>::weighted, uint2, int32_t>::type;
+    __device__ __forceinline__ static T make(int32_t x, uint32_t w) {
+        if constexpr (WLoad<WT>::weighted) return make_uint2((uint32_t)x, w);
+        else return x;
+    }
+    __device__ __forceinline__ static int32_t label(const T& e) {
+        if constexpr (WLoad<WT>::weighted) return (int32_t)e.x;
+        else return e;
+    }
+    __device__ __forceinline__ static uint32_t weight(const T& e) {
+        if constexpr (WLoad<WT>::weighted) return e.y;
+        else return 1u;
+    }
+};
+
+struct HubPlan {
+    const int32_t* list;      // hubs
+    int64_t nL;
+    const int64_t* item_off;  // [nL+1] LARGE_CHUNK items per hub
+    const int64_t* boff;      // [nL+1] buckets per hub
+    int stride;               // ioff entries per item (max buckets + 1)
+    void* ent;                // [items * LARGE_CHUNK] bucketed entries
+    int32_t* ioff;            // [items * stride] per-item bucket offsets
+    double* sc;               // [nL] own-cluster weight
+    double* pg;               // [buckets] partial best gain
+    int32_t* px;              // [buckets] partial best cluster
+    double* pS;               // [buckets] its S
+    unsigned* overflow;
+};
+
+__device__ __forceinline__ uint32_t hub_bucket(int32_t x, uint32_t nb) {
+    return (uint32_t)(((uint64_t)hash32((uint32_t)x) * nb) >> 32);
+}
+__device__ __forceinline__ uint32_t hub_pass(int32_t x, uint32_t R) {
+    return hash32((uint32_t)x ^ 0x5bd1e995u) % R;
+}
+
+template <class WT, bool ASYNC>
+__global__ void __launch_bounds__(HB_THREADS)
+k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
+    using E = HubEntry<WT>;
+    using T = typename E::T;
+    constexpr int PER = LARGE_CHUNK / HB_THREADS;  // 8 edges per thread
+    __shared__ int s_hist[HB_MAXB + 1];
+    __shared__ double s_red[HB_THREADS / 32];
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    const int tid = threadIdx.x;
+    for (int64_t it = blockIdx.x; it < total_items; it += gridDim.x) {
+        const int64_t li = owner_of(P.item_off, P.nL, it);
+        const int32_t v = P.list[li];
+        const int64_t s = a.indptr[v], e_end = a.indptr[v + 1];
+        const int64_t e0 = s + (it - P.item_off[li]) * LARGE_CHUNK;
+        const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
+        const uint32_t nb = (uint32_t)(P.boff[li + 1] - P.boff[li]);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        for (int b = tid; b <= (int)nb; b += HB_THREADS) s_hist[b] = 0;
+        __syncthreads();
+        int32_t x[PER];
+        uint32_t w[PER];
+        int bk[PER], rk[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int64_t e = e0 + (int64_t)j * HB_THREADS + tid;
+            x[j] = e < e1 ? ld_stream_i32(a.indices + e, pol_stream) : -1;
+            w[j] = e < e1 ? (uint32_t)WLoad<WT>::tw(a.w, e) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, x[j], pol_keep) : EMPTY_KEY;
+        double sc = 0.0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            bk[j] = -1;
+            if (x[j] == EMPTY_KEY) continue;
+            if (x[j] == c) { sc += u32_to_f64(w[j]); continue; }
+            bk[j] = (int)hub_bucket(x[j], nb);
+            rk[j] = atomicAdd(&s_hist[bk[j]], 1);
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
+        if ((tid & 31) == 0) s_red[tid >> 5] = sc;
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of the bucket counts (nb <= HB_MAXB)
+            int carry = 0;
+            for (int b0 = 0; b0 <= (int)nb; b0 += 32) {
+                const int b = b0 + tid;
+                const int val = b < (int)nb ? s_hist[b] : 0;
+                int incl = val;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, d);
+                    if (tid >= d) incl += y;
+                }
+                if (b <= (int)nb) {
+                    const int ex = carry + incl - val;
+                    s_hist[b] = ex;
+                    P.ioff[it * P.stride + b] = ex;
+                }
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+            if (tid == 0) {
+                double t = 0.0;
+                for (int q = 0; q < HB_THREADS / 32; ++q) t += s_red[q];
+                if (t != 0.0) atomicAdd(P.sc + li, t);
+            }
+        }
+        __syncthreads();
+        T* out = static_cast<T*>(P.ent) + it * LARGE_CHUNK;
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (bk[j] >= 0) out[s_hist[bk[j]] + rk[j]] = E::make(x[j], w[j]);
+        __syncthreads();  // s_hist reused by the next item
+    }
+}
+
+template <class WT, bool ASYNC, bool KI>
+__global__ void __launch_bounds__(HB_THREADS)
+k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
+    using E = HubEntry<WT>;
+    using T = typename E::T;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_g[HB_THREADS / 32], s_S[HB_THREADS / 32];
+    __shared__ int32_t s_x[HB_THREADS / 32];
+    __shared__ int64_t s_cnt;
+    SmemTable<false> tab;
+    tab.init_cap(smem, HB_CAP);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (uint32_t q = tid; q < HB_CAP; q += HB_THREADS) tab.clear(q);
+    const uint64_t pol_keep = policy_evict_last();
+    for (int64_t gb = blockIdx.x; gb < total_buckets; gb += gridDim.x) {
+        const int64_t li = owner_of(P.boff, P.nL, gb);
+        const int b = (int)(gb - P.boff[li]);
+        const int32_t v = P.list[li];
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const double kv = kval(a.k, v);
+        const double t = dmul(a.lam, kv);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        const double bb = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
+        const int64_t i0 = P.item_off[li], i1 = P.item_off[li + 1];
+        // entries of this bucket over the hub's items
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+        int64_t mine = 0;
+        for (int64_t it = i0 + tid; it < i1; it += HB_THREADS)
+            mine += P.ioff[it * P.stride + b + 1] - P.ioff[it * P.stride + b];
+        for (int d = 16; d; d >>= 1) mine += __shfl_xor_sync(FULL, mine, d);
+        if (lane == 0 && mine) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)mine);
+        __syncthreads();
+        const int64_t cnt = s_cnt;
+        const uint32_t R = (uint32_t)max64(1, (2 * cnt + HB_CAP - 1) / HB_CAP);
+        const uint32_t cap = (uint32_t)min64(HB_CAP, (2 * ((cnt + R - 1) / R) + 31) & ~31LL);
+        double bg = -INFINITY, bS = 0.0;
+        int32_t bx = NO_CAND;
+        for (uint32_t r = 0; r < R; ++r) {
+            // insert: warp w walks items w, w+8, ...; lanes over the item's range
+            for (int64_t it = i0 + wid; it < i1; it += HB_THREADS / 32) {
+                const int lo = P.ioff[it * P.stride + b], hi = P.ioff[it * P.stride + b + 1];
+                const T* src = static_cast<const T*>(P.ent) + it * LARGE_CHUNK;
+                for (int q = lo + lane; q < hi; q += 32) {
+                    const T e = src[q];
+                    const int32_t x = E::label(e);
+                    if (R > 1 && hub_pass(x, R) != r) continue;
+                    uint32_t h = slot_of(x, cap);
+                    uint32_t probes = 0;
+                    int32_t prev;
+                    while (true) {
+                        asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(tab.keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+                        if (prev == EMPTY_KEY || prev == x) break;
+                        h = (h + 1 == cap) ? 0 : h + 1;
+                        if (++probes >= cap) { atomicOr(P.overflow, 1u); break; }
+                    }
+                    if (prev != EMPTY_KEY && prev != x) continue;  // overflow (reported)
+                    const uint32_t inc = prev == EMPTY_KEY ? E::weight(e) - 1u : E::weight(e);
+                    if (inc) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(tab.cnts + 4 * h), "r"(inc) : "memory");
+                }
+            }
+            __syncthreads();
+            // score (and reset) the table
+            for (uint32_t q0 = tid; q0 < cap; q0 += HB_THREADS * 4) {
+                int32_t x[4];
+                double S[4], Kx[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t q = q0 + j * HB_THREADS;
+                    if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (x[j] == EMPTY_KEY) continue;
+                    const double gq = dsub(dsub(S[j], dmul(t, Kx[j])), bb);
+                    if (better(gq, x[j], bg, bx)) { bg = gq; bx = x[j]; bS = S[j]; }
+                }
+            }
+            __syncthreads();
+        }
+        warp_argmax(bg, bx, bS);
+        if (lane == 0) { s_g[wid] = bg; s_x[wid] = bx; s_S[wid] = bS; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int q = 1; q < HB_THREADS / 32; ++q)
+                if (better(s_g[q], s_x[q], bg, bx)) { bg = s_g[q]; bx = s_x[q]; bS = s_S[q]; }
+            P.pg[gb] = bg;
+            P.px[gb] = bx;
+            P.pS[gb] = bS;
+        }
+        __syncthreads();
+    }
+}
+
+template <class WT, bool ASYNC, bool KI>
+__global__ void k_hub_decide(BMArgs a, HubPlan P) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol_keep = policy_evict_last();
+    unsigned long long my_moves = 0;
+    for (int64_t li = gw; li < P.nL; li += nw) {
+        double bg = -INFINITY, bS = 0.0;
+        int32_t bx = NO_CAND;
+        for (int64_t q = P.boff[li] + lane; q < P.boff[li + 1]; q += 32)
+            if (better(P.pg[q], P.px[q], bg, bx)) { bg = P.pg[q]; bx = P.px[q]; bS = P.pS[q]; }
+        warp_argmax(bg, bx, bS);
+        if (lane == 0) {
+            const int32_t v = P.list[li];
+            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+            const double kv = kval(a.k, v);
+            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+            const double t = dmul(a.lam, kv);
+            const double b = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
+            my_moves += decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bx != NO_CAND ? bS : NAN);
+        }
+    }
+    flush_moves(a, my_moves);
+}
+
+// ===========================================================================
 // hub bin, cluster path: one 8-CTA thread-block cluster per hub, its
 // neighbour-cluster table spread over the 8 CTAs' shared memory (DSMEM,
 // 8 x 24K slots: hubs up to ~98K edges).  Inserts are remote shared-memory
@@ -1636,8 +1904,58 @@ void launch_hub_cluster(const BMArgs& a, const int32_t* hubs, int64_t nh, cudaSt
     LCC_LAUNCH_CHECK();
 }
 
+// hub bucket path (integer sums): plan on the host, three kernels + the mark
 template <class WT, bool ASYNC, bool KI>
-void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int64_t nL_in, cudaStream_t s) {
+void run_hub_buckets(const BMArgs& a, const int32_t* large, const std::vector<int64_t>& deg, unsigned* ovf,
+                     cudaStream_t s) {
+    using T = typename HubEntry<WT>::T;
+    const int64_t nL = (int64_t)deg.size();
+    std::vector<int64_t> h(2 * (nL + 1));
+    int64_t* item_off = h.data();
+    int64_t* boff = h.data() + nL + 1;
+    item_off[0] = boff[0] = 0;
+    int maxb = 1;
+    for (int64_t i = 0; i < nL; ++i) {
+        const int64_t nb = std::min<int64_t>(HB_MAXB, std::max<int64_t>(1, (deg[i] + HB_BE - 1) / HB_BE));
+        maxb = std::max<int>(maxb, (int)nb);
+        item_off[i + 1] = item_off[i] + (deg[i] + LARGE_CHUNK - 1) / LARGE_CHUNK;
+        boff[i + 1] = boff[i] + nb;
+    }
+    const int64_t items = item_off[nL], buckets = boff[nL];
+    const int stride = maxb + 1;
+    Buf<int64_t> offs(h.size(), s);
+    LCC_CUDA(cudaMemcpyAsync(offs.get(), h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice, s));
+    Buf<T> ent(items * LARGE_CHUNK, s);
+    Buf<int32_t> ioff(items * stride, s);
+    Buf<double> sc(nL, s), pg(buckets, s), pS(buckets, s);
+    Buf<int32_t> px(buckets, s);
+    LCC_CUDA(cudaMemsetAsync(sc.get(), 0, sizeof(double) * nL, s));
+    HubPlan P{large, nL, offs.get(), offs.get() + nL + 1, stride, ent.get(), ioff.get(), sc.get(), pg.get(), px.get(),
+              pS.get(), ovf};
+    k_hub_scatter<WT, ASYNC><<<grid_for(items * HB_THREADS, HB_THREADS, 8), HB_THREADS, 0, s>>>(a, P, items);
+    LCC_LAUNCH_CHECK();
+    constexpr int SMEM = HB_CAP * SmemTable<false>::bytes_per_slot;
+    static int occ = 0;
+    if (!occ) {
+        set_smem(k_hub_bucket<WT, ASYNC, KI>, SMEM);
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hub_bucket<WT, ASYNC, KI>, HB_THREADS, SMEM));
+        occ = std::max(occ, 1);
+    }
+    const unsigned gridb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(buckets, (int64_t)num_sms() * occ));
+    k_hub_bucket<WT, ASYNC, KI><<<gridb, HB_THREADS, SMEM, s>>>(a, P, buckets);
+    LCC_LAUNCH_CHECK();
+    k_hub_decide<WT, ASYNC, KI><<<grid_for(nL * 32, 256), 256, 0, s>>>(a, P);
+    LCC_LAUNCH_CHECK();
+    if (a.mark) {
+        LargeBatch L{large, nL, nullptr, offs.get(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        k_large_mark<<<grid_for(items * LARGE_THREADS, LARGE_THREADS, 8), LARGE_THREADS, 0, s>>>(a, L, items);
+        LCC_LAUNCH_CHECK();
+    }
+}
+
+template <class WT, bool ASYNC, bool KI>
+void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int64_t nL_in, unsigned* ovf,
+               cudaStream_t s) {
     constexpr bool WEIGHTED = WLoad<WT>::fsum;  // float sums: key + f64 value tables
     Buf<int64_t> ddeg(nL_in, s);
     k_degrees_of<<<grid_for(nL_in, 256), 256, 0, s>>>(g.indptr, large_in, nL_in, ddeg.get());
@@ -1675,6 +1993,13 @@ void run_large(const BMArgs& a, const lcc_graph& g, const int32_t* large_in, int
     const int32_t* large = dlists.get() + hc.size();
     const int64_t nL = (int64_t)l2.size();
     if (nL == 0) return;
+    const char* ehb = getenv("LCC_HUB_BUCKETS");
+    if constexpr (!WEIGHTED) {
+        if (!(ehb && ehb[0] == '0')) {
+            run_hub_buckets<WT, ASYNC, KI>(a, large, deg, ovf, s);
+            return;
+        }
+    }
     const int64_t slot_bytes = GlobalTable<WEIGHTED>::bytes_per_slot;
     int64_t maxcap = 0;
     for (int64_t d : deg) maxcap = std::max<int64_t>(maxcap, large_cap(d));
@@ -1821,8 +2146,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     Buf<int32_t> lists(std::max<int64_t>(nF, 1), s);
     hprobe.mark("alloc lists");
     std::vector<int64_t> binstart;
-    Buf<unsigned long long> dcnt(3, s);  // [edges, movers, deferred]
-    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * 3, s));
+    Buf<unsigned long long> dcnt(4, s);  // [edges, movers, deferred, hub-table overflow]
+    LCC_CUDA(cudaMemsetAsync(dcnt.get(), 0, sizeof(unsigned long long) * 4, s));
     unsigned long long* dmoved = dcnt.get() + 1;
     const int64_t ntiles = std::max<int64_t>((nF + BIN_TILE - 1) / BIN_TILE, 1);
     Buf<int64_t> tcnt(NBINS * ntiles + 1, s), tbase(NBINS * ntiles + 1, s);
@@ -1919,7 +2244,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             LCC_CUDA(cudaStreamWaitEvent(t, ss.fork, 0));
             return t;
         };
-        if (j == 0 && nL > 0) run_large<WT, ASYNC, KI>(a, g, lists.get() + binstart[NBINS - 1], nL, next_stream());
+        if (j == 0 && nL > 0) run_large<WT, ASYNC, KI>(a, g, lists.get() + binstart[NBINS - 1], nL,
+                                                       reinterpret_cast<unsigned*>(dcnt.get() + 3), next_stream());
         for (int b = 0; b < NBINS - 1; ++b) {
             const int64_t nb = (int64_t)hc[b];
             if (nb == 0) continue;
@@ -1957,10 +2283,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     }
     hprobe.mark("launches");
     LCC_CUDA(cudaEventRecord(ev1, s));
-    unsigned long long hm = 0, hp = 0;
+    unsigned long long hm = 0, hp = 0, hov = 0;
     LCC_CUDA(cudaMemcpyAsync(&hm, dmoved, sizeof(hm), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaMemcpyAsync(&hp, dcnt.get() + 2, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaMemcpyAsync(&hov, dcnt.get() + 3, sizeof(hov), cudaMemcpyDeviceToHost, s));
     LCC_CUDA(cudaStreamSynchronize(s));
+    if (hov) throw CudaError("hub bucket table overflow (LCC_HUB_BUCKETS=0 selects the global-table path)");
     hprobe.mark("kernels (device wait)");
     LCC_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
     cudaEventDestroy(ev0);

@@ -233,6 +233,7 @@ __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
 }
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 

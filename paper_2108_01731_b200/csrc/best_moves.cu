@@ -1194,9 +1194,13 @@ k_large_mark(BMArgs a, LargeBatch L, int64_t total_items) {
 // by a second hash; a table that still fills sets an error flag (the round
 // fails loudly; with murmur-hashed labels it does not happen).
 // ===========================================================================
-constexpr int HB_THREADS = 256;
+#ifndef LCC_HB_THREADS
+#define LCC_HB_THREADS 256
+#endif
+constexpr int HB_THREADS = LCC_HB_THREADS;  // bucket CTA
+constexpr int HS_THREADS = 256;             // scatter CTA
 #ifndef LCC_HB_CAP
-#define LCC_HB_CAP 8192
+#define LCC_HB_CAP 4096
 #endif
 constexpr int HB_CAP = LCC_HB_CAP;      // table slots per bucket CTA
 constexpr int HB_BE = HB_CAP / 2;       // target entries per bucket
@@ -1242,13 +1246,13 @@ __device__ __forceinline__ uint32_t hub_pass(int32_t x, uint32_t R) {
 }
 
 template <class WT, bool ASYNC>
-__global__ void __launch_bounds__(HB_THREADS)
+__global__ void __launch_bounds__(HS_THREADS)
 k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
     using E = HubEntry<WT>;
     using T = typename E::T;
-    constexpr int PER = LARGE_CHUNK / HB_THREADS;  // 8 edges per thread
+    constexpr int PER = LARGE_CHUNK / HS_THREADS;  // 8 edges per thread
     __shared__ int s_hist[HB_MAXB + 1];
-    __shared__ double s_red[HB_THREADS / 32];
+    __shared__ double s_red[HS_THREADS / 32];
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     const int tid = threadIdx.x;
@@ -1260,14 +1264,14 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t nb = (uint32_t)(P.boff[li + 1] - P.boff[li]);
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
-        for (int b = tid; b <= (int)nb; b += HB_THREADS) s_hist[b] = 0;
+        for (int b = tid; b <= (int)nb; b += HS_THREADS) s_hist[b] = 0;
         __syncthreads();
         int32_t x[PER];
         uint32_t w[PER];
         int bk[PER], rk[PER];
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
-            const int64_t e = e0 + (int64_t)j * HB_THREADS + tid;
+            const int64_t e = e0 + (int64_t)j * HS_THREADS + tid;
             x[j] = e < e1 ? ld_stream_i32(a.indices + e, pol_stream) : -1;
             w[j] = e < e1 ? (uint32_t)WLoad<WT>::tw(a.w, e) : 0u;
         }
@@ -1306,7 +1310,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
             }
             if (tid == 0) {
                 double t = 0.0;
-                for (int q = 0; q < HB_THREADS / 32; ++q) t += s_red[q];
+                for (int q = 0; q < HS_THREADS / 32; ++q) t += s_red[q];
                 if (t != 0.0) atomicAdd(P.sc + li, t);
             }
         }
@@ -1932,7 +1936,7 @@ void run_hub_buckets(const BMArgs& a, const int32_t* large, const std::vector<in
     LCC_CUDA(cudaMemsetAsync(sc.get(), 0, sizeof(double) * nL, s));
     HubPlan P{large, nL, offs.get(), offs.get() + nL + 1, stride, ent.get(), ioff.get(), sc.get(), pg.get(), px.get(),
               pS.get(), ovf};
-    k_hub_scatter<WT, ASYNC><<<grid_for(items * HB_THREADS, HB_THREADS, 8), HB_THREADS, 0, s>>>(a, P, items);
+    k_hub_scatter<WT, ASYNC><<<grid_for(items * HS_THREADS, HS_THREADS, 8), HS_THREADS, 0, s>>>(a, P, items);
     LCC_LAUNCH_CHECK();
     constexpr int SMEM = HB_CAP * SmemTable<false>::bytes_per_slot;
     static int occ = 0;

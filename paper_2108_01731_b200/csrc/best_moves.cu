@@ -10,21 +10,24 @@
 // The frontier is split by degree into bins (stable two-pass partition),
 // each with a kernel whose thread count matches the work:
 //   0  isolated            : k_isolated, thread per vertex (fresh singleton only)
-//   1  deg <= 32           : k_small, one warp packs 32 vertices into 32-edge
+//   1  deg <= 8            : k_tiny, thread per vertex, labels in registers
+//   2  deg <= 32           : k_small, one warp packs 32 vertices into 32-edge
 //                            windows; labels grouped by __match_any_sync on
 //                            (vertex, label); segmented argmax by shuffles.
 //                            Sums run in CSR order (bit-identical to the oracle
 //                            even for weighted graphs).
-//   2  (opt-in LCC_WINDOW) : k_window, edge-balanced multi-vertex CTAs
-//   3-4 33 .. 512          : k_group, one WARP per vertex, 256/1024-slot
+//   3  (opt-in LCC_WINDOW) : k_window, edge-balanced multi-vertex CTAs
+//   4-5 33 .. 512          : k_group, one WARP per vertex, 256/1024-slot
 //                            shared-memory hash table (the paper's
 //                            "sequential" per-vertex accumulation)
-//   5-7 .. 10240           : k_group, 4/8/32 warps per vertex, 4K-16K slots
+//   6-8 .. 10240           : k_group, 4/8/32 warps per vertex, 4K-16K slots
 //                            ("parallel hash table")
-//   8  hubs                : edges cut into 2048-edge work items spread over
-//                            all SMs inserting into per-vertex global tables,
-//                            batched (256 MB) and scored in 16K-slot items;
-//                            opt-in DSMEM cluster tables (LCC_HUB_CLUSTER=1).
+//   9  hubs                : labels radix-partitioned by hash into ~2K-entry
+//                            buckets, each aggregated by one CTA in a 4K-slot
+//                            shared-memory table (k_hub_*); LCC_HUB_BUCKETS=0:
+//                            2048-edge items inserting into per-vertex global
+//                            (L2) tables; opt-in DSMEM cluster tables
+//                            (LCC_HUB_CLUSTER=1).
 // Tables use native 32-bit shared atomics (CAS on the key, RED on the
 // count / integer weight); float weights add with fp64 RED.
 // sync  : targets written to D (apply happens in apply.cu);
@@ -334,6 +337,83 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
             base = end;
             __syncwarp();
+        }
+    }
+    flush_moves(a, my_moves);
+}
+
+// ===========================================================================
+// tiny bin: 1 <= deg <= TINY_MAX, one THREAD per vertex.  The labels sit in
+// registers; distinct clusters are found by pairwise compares, S sums run in
+// CSR order (bit-identical to k_small and the oracle, weighted or not), and
+// every first occurrence's mass gather is issued before any gain is formed.
+// No shuffles or shared memory: every thread's gathers are independent, so a
+// warp keeps 32 vertices' loads in flight instead of one 32-edge window.
+// ===========================================================================
+#ifndef LCC_TINY_MAX
+#define LCC_TINY_MAX 8
+#endif
+constexpr int TINY_MAX = LCC_TINY_MAX;
+
+template <class WT, bool ASYNC, bool KI>
+__global__ void __launch_bounds__(256)
+k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
+    using TW = typename WLoad<WT>::TW;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    unsigned long long my_moves = 0;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(list + i);
+        const int64_t s = __ldg(a.indptr + v);
+        const int deg = (int)(__ldg(a.indptr + v + 1) - s);
+        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const double kv = kval(a.k, v);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        int32_t u[TINY_MAX], x[TINY_MAX];
+        TW w[TINY_MAX];
+#pragma unroll
+        for (int j = 0; j < TINY_MAX; ++j) {
+            u[j] = j < deg ? ld_stream_i32(a.indices + s + j, pol_stream) : -1;
+            w[j] = j < deg ? WLoad<WT>::tw(a.w, s + j) : TW(0);
+        }
+#pragma unroll
+        for (int j = 0; j < TINY_MAX; ++j) x[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+        // first occurrences of each neighbour cluster (other than c)
+        bool first[TINY_MAX];
+        double Kx[TINY_MAX];
+#pragma unroll
+        for (int j = 0; j < TINY_MAX; ++j) {
+            bool f = x[j] != EMPTY_KEY && x[j] != c;
+#pragma unroll
+            for (int q = 0; q < j; ++q) f = f && x[q] != x[j];
+            first[j] = f;
+        }
+#pragma unroll
+        for (int j = 0; j < TINY_MAX; ++j) Kx[j] = first[j] ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+        double sc = 0.0;
+#pragma unroll
+        for (int j = 0; j < TINY_MAX; ++j)
+            if (x[j] == c) sc = dadd(sc, WLoad<WT>::f64(w[j]));
+        const double t = dmul(a.lam, kv);
+        const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
+        double bg = -INFINITY, bS = 0.0;
+        int32_t bx = NO_CAND;
+#pragma unroll
+        for (int j = 0; j < TINY_MAX; ++j) {
+            if (!first[j]) continue;
+            double S = 0.0;
+#pragma unroll
+            for (int q = j; q < TINY_MAX; ++q)
+                if (x[q] == x[j]) S = dadd(S, WLoad<WT>::f64(w[q]));
+            const double g = dsub(dsub(S, dmul(t, Kx[j])), b);
+            if (better(g, x[j], bg, bx)) { bg = g; bx = x[j]; bS = S; }
+        }
+        const int mv = decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bS);
+        my_moves += mv;
+        if (a.mark && mv) {
+#pragma unroll
+            for (int j = 0; j < TINY_MAX; ++j)
+                if (u[j] >= 0) a.mark[u[j]] = 1;
         }
     }
     flush_moves(a, my_moves);
@@ -1661,7 +1741,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
 // ===========================================================================
 // degree-bin partition (one pass, block-aggregated reservations)
 // ===========================================================================
-constexpr int NBINS = 9;
+constexpr int NBINS = 10;
 struct BinEdges {
     int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
@@ -2116,9 +2196,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
 
     // bin boundaries: warp paths below the degree threshold, CTA paths above
     // (the paper's sequential-vs-parallel hash-table switch)
-    // bins: 0 isolated | 1 deg<=32 warp windows | 2 optional edge windows |
-    //       3-4 warp per vertex up to the threshold | 5 ..2048 4 warps |
-    //       6 ..4096 8 warps | 7 ..large_min 32 warps | 8 hubs (L2 tables)
+    // bins: 0 isolated | 1 deg<=8 thread per vertex | 2 ..32 warp windows |
+    //       3 optional edge windows | 4-5 warp per vertex up to the threshold |
+    //       6 ..2048 4 warps | 7 ..4096 8 warps | 8 ..large_min 32 warps |
+    //       9 hubs (bucketed shared-memory tables)
     // LCC_WINDOW=0 / LCC_LARGE_MIN (env): tuning knobs for the bin shapes only
     // measured on B200 (R-MAT s24): per-vertex warp groups beat the window
     // kernel by ~5%, and CTA groups beat the L2 hub path up to 10240
@@ -2133,15 +2214,18 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     int64_t Tw = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
     if (!use_window || 2 * n > (1LL << LABEL_BITS)) Tw = SMALL_MAX + 1;  // window keys need ids < 2^27
     BinEdges be;
+    const char* et = getenv("LCC_TINY");  // 0: the warp-window kernel takes degrees 1..32 too
+    const int64_t tiny_max = (et && et[0] == '0') ? 0 : TINY_MAX;
     be.hi[0] = 0;                 // isolated vertices: only the fresh-singleton option
-    be.hi[1] = SMALL_MAX;
-    be.hi[2] = Tw - 1;
-    be.hi[3] = std::max<int64_t>(be.hi[2], std::min<int64_t>(128, Tg - 1));
-    be.hi[4] = std::max<int64_t>(be.hi[3], Tg - 1);
-    be.hi[5] = std::min<int64_t>(2048, large_min);
-    be.hi[6] = std::min<int64_t>(4096, large_min);
-    be.hi[7] = std::min<int64_t>(MED_MAX, large_min);
-    be.hi[8] = INT64_MAX;
+    be.hi[1] = tiny_max;          // thread per vertex
+    be.hi[2] = SMALL_MAX;         // warp-packed windows
+    be.hi[3] = Tw - 1;
+    be.hi[4] = std::max<int64_t>(be.hi[3], std::min<int64_t>(128, Tg - 1));
+    be.hi[5] = std::max<int64_t>(be.hi[4], Tg - 1);
+    be.hi[6] = std::min<int64_t>(2048, large_min);
+    be.hi[7] = std::min<int64_t>(4096, large_min);
+    be.hi[8] = std::min<int64_t>(MED_MAX, large_min);
+    be.hi[9] = INT64_MAX;
 
     if (hprobe.on && getenv("LCC_TRACE_SYNC")) {  // device work queued before this round
         LCC_CUDA(cudaStreamSynchronize(s));
@@ -2223,7 +2307,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         if (chunks < 0) P = std::max(P, -chunks);
     }
     WindowPlan wp;
-    if (hc[2] > 0) plan_windows(g.indptr, lists.get() + binstart[2], (int64_t)hc[2], wp, s);
+    if (hc[3] > 0) plan_windows(g.indptr, lists.get() + binstart[3], (int64_t)hc[3], wp, s);
     const int64_t nL = (int64_t)hc[NBINS - 1];
     // The bins are independent within a (sub-)round -- sync reads a frozen
     // state and writes disjoint D entries; async tolerates any interleaving --
@@ -2254,7 +2338,7 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             const int64_t nb = (int64_t)hc[b];
             if (nb == 0) continue;
             const int32_t* list = lists.get() + binstart[b];
-            if (b == 2) {
+            if (b == 3) {
                 if (wp.nwin * (j + 1) / P > wp.nwin * j / P)
                     launch_window<WT, ASYNC, KI>(a, list, wp, wp.nwin * j / P, wp.nwin * (j + 1) / P, next_stream());
                 continue;
@@ -2266,11 +2350,14 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
                 k_isolated<ASYNC, KI><<<grid_for(hi - lo, 256, 8), 256, 0, t>>>(a, list, lo, hi);
                 LCC_LAUNCH_CHECK();
             } else if (b == 1) {
+                k_tiny<WT, ASYNC, KI><<<grid_for(hi - lo, 256, 8), 256, 0, t>>>(a, list, lo, hi);
+                LCC_LAUNCH_CHECK();
+            } else if (b == 2) {
                 const int64_t warps = (hi - lo + 31) / 32;
                 k_small<WT, ASYNC, KI><<<grid_for(warps * 32, SMALL_THREADS, 8), SMALL_THREADS, 0, t>>>(a, list, lo, hi);
                 LCC_LAUNCH_CHECK();
             } else {
-                launch_bin<WT, ASYNC, KI>(b - 1, a, list, lo, hi, t);
+                launch_bin<WT, ASYNC, KI>(b - 2, a, list, lo, hi, t);
             }
         }
         for (int i = 0; i < used; ++i) {
@@ -2305,8 +2392,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         st->vertices += nF;
         st->edges += (int64_t)hc[NBINS];
         st->moved += (int64_t)hm;
-        st->n_small += (int64_t)(hc[0] + hc[1]);
-        for (int b = 2; b < NBINS - 1; ++b) st->n_medium += (int64_t)hc[b];
+        st->n_small += (int64_t)(hc[0] + hc[1] + hc[2]);
+        for (int b = 3; b < NBINS - 1; ++b) st->n_medium += (int64_t)hc[b];
         st->n_large += nL;
         st->ms_kernels += (double)kms + (double)kms_large;
         st->launches += launch_counter() - launches0;

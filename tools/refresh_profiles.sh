@@ -20,7 +20,7 @@ timeout 1200 ncu --set full --clock-control none --import-source on \
   -o /tmp/r${R}_groups python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e > $O/ncu_groups_r$R.log 2>&1 \
   || echo "groups capture failed"
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k 'regex:k_large' -s 0 -c 4 \
+  -k 'regex:k_hub|k_large' -s 0 -c 4 \
   -o /tmp/r${R}_hubs python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e > $O/ncu_hubs_r$R.log 2>&1 \
   || echo "hub capture failed"
 for rep in groups hubs; do
@@ -29,5 +29,7 @@ done
 for i in 0 1 2 3 4 5 6; do
   ncu -i /tmp/r${R}_groups.ncu-rep --page source --csv --print-source cuda,sass -s $i -c 1 > $O/r${R}_groups_src_$i.csv 2>/dev/null
 done
-ncu -i /tmp/r${R}_hubs.ncu-rep --page source --csv --print-source cuda,sass -s 0 -c 1 > $O/r${R}_hubs_src_0.csv 2>/dev/null
+for i in 0 1; do
+  ncu -i /tmp/r${R}_hubs.ncu-rep --page source --csv --print-source cuda,sass -s $i -c 1 > $O/r${R}_hubs_src_$i.csv 2>/dev/null
+done
 echo done

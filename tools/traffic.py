@@ -34,7 +34,7 @@ def main(rnd):
         rs, unit_row = rows(f"gpurun_out/r{rnd}_{rep}_raw.csv")
         hdr = list(rs[0].keys()) if rs else []
         units = dict(zip(hdr, unit_row))
-        if scale is None:  # hub batches per step, from the launch list
+        if scale is None:  # hub batches per step (global-table path), from the launch list; 1 for buckets
             n = sum(1 for line in open(f"gpurun_out/launches_r{rnd}.csv") if "k_large_insert" in line and
                     "gpu__time_duration" in line)
             scale = max(n, 1)

@@ -355,10 +355,15 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 #endif
 constexpr int TINY_MAX = LCC_TINY_MAX;
 
+#ifndef LCC_TINY_MINB
+#define LCC_TINY_MINB 4  // 64 registers, no spill: 32 resident warps (+1%)
+#endif
 template <class WT, bool ASYNC, bool KI>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, LCC_TINY_MINB)
 k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     using TW = typename WLoad<WT>::TW;
+    // masses held raw (uint32 image or fp64) until the gain: fewer registers
+    using KR = typename std::conditional<KI, uint32_t, double>::type;
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
@@ -369,27 +374,37 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
-        int32_t u[TINY_MAX], x[TINY_MAX];
+        int32_t x[TINY_MAX];
         TW w[TINY_MAX];
 #pragma unroll
         for (int j = 0; j < TINY_MAX; ++j) {
-            u[j] = j < deg ? ld_stream_i32(a.indices + s + j, pol_stream) : -1;
+            x[j] = j < deg ? ld_stream_i32(a.indices + s + j, pol_stream) : -1;
             w[j] = j < deg ? WLoad<WT>::tw(a.w, s + j) : TW(0);
         }
 #pragma unroll
-        for (int j = 0; j < TINY_MAX; ++j) x[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, x[j], pol_keep) : EMPTY_KEY;
         // first occurrences of each neighbour cluster (other than c)
-        bool first[TINY_MAX];
-        double Kx[TINY_MAX];
+        unsigned first = 0;
 #pragma unroll
         for (int j = 0; j < TINY_MAX; ++j) {
             bool f = x[j] != EMPTY_KEY && x[j] != c;
 #pragma unroll
             for (int q = 0; q < j; ++q) f = f && x[q] != x[j];
-            first[j] = f;
+            first |= (unsigned)f << j;
         }
+        KR Kx[TINY_MAX];
 #pragma unroll
-        for (int j = 0; j < TINY_MAX; ++j) Kx[j] = first[j] ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+        for (int j = 0; j < TINY_MAX; ++j) {
+            if constexpr (KI) {
+                Kx[j] = 0u;
+                if ((first >> j) & 1u) {
+                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + x[j]));
+                    else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + x[j], pol_keep);
+                }
+            } else {
+                Kx[j] = ((first >> j) & 1u) ? ldK<ASYNC, false>(a.K, x[j], pol_keep) : 0.0;
+            }
+        }
         double sc = 0.0;
 #pragma unroll
         for (int j = 0; j < TINY_MAX; ++j)
@@ -400,20 +415,21 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         int32_t bx = NO_CAND;
 #pragma unroll
         for (int j = 0; j < TINY_MAX; ++j) {
-            if (!first[j]) continue;
+            if (!((first >> j) & 1u)) continue;
             double S = 0.0;
 #pragma unroll
             for (int q = j; q < TINY_MAX; ++q)
                 if (x[q] == x[j]) S = dadd(S, WLoad<WT>::f64(w[q]));
-            const double g = dsub(dsub(S, dmul(t, Kx[j])), b);
+            double K;
+            if constexpr (KI) K = u32_to_f64(Kx[j]);
+            else K = Kx[j];
+            const double g = dsub(dsub(S, dmul(t, K)), b);
             if (better(g, x[j], bg, bx)) { bg = g; bx = x[j]; bS = S; }
         }
         const int mv = decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bS);
         my_moves += mv;
-        if (a.mark && mv) {
-#pragma unroll
-            for (int j = 0; j < TINY_MAX; ++j)
-                if (u[j] >= 0) a.mark[u[j]] = 1;
+        if (a.mark && mv) {  // neighbour ids re-read (L1/L2-hot)
+            for (int j = 0; j < deg; ++j) a.mark[__ldg(a.indices + s + j)] = 1;
         }
     }
     flush_moves(a, my_moves);

@@ -48,20 +48,22 @@ struct EdgeKey {
     VT* vals;
     unsigned long long* intra_cnt;
     double* intra_w;
+    bool compact = false;  // write at the list position (complex rows only) instead of the CSR index
     unsigned long long cnt = 0;
     double acc = 0.0;
-    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
+    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) {
         const uint64_t a = (uint32_t)__ldg(mapping + v);
         const uint64_t b = (uint32_t)__ldg(mapping + __ldg(indices + e));
         const auto wv = WLoad<WT>::tw(w, e);
+        const int64_t o = compact ? pos : e;
         if (a == b) {
-            keys[e] = sentinel;
+            keys[o] = sentinel;
             ++cnt;
             acc += WLoad<WT>::f64(wv);
         } else {
-            keys[e] = (a << bits) | b;
+            keys[o] = (a << bits) | b;
         }
-        if (vals) vals[e] = (VT)wv;
+        if (vals) vals[o] = (VT)wv;
     }
     __device__ __forceinline__ void flush() {
         for (int d = 16; d; d >>= 1) {
@@ -129,6 +131,92 @@ struct PhaseTrace {
     ~PhaseTrace() { if (last) cudaEventDestroy(last); }
 };
 
+// ---- fast path: most clusters are singletons ------------------------------
+// A fine row u is "simple" when u is a singleton cluster and none of its
+// neighbours lies in a non-singleton cluster: its coarse row is the fine row
+// with every id mapped (strictly increasing -- the renumbering is monotone on
+// singletons -- and duplicate free) and the same weights.  Only the other
+// ("complex") rows go through keys + radix sort + reduce; the simple ones are
+// copied by one streaming pass.  Complex rows = members of non-singleton
+// clusters and their neighbours (one edge pass over the members' rows).  The
+// output is identical to the full path's (same rows, same per-entry sums in
+// the same order).  Config 4: the level 1 -> 2 contraction merges 6 of 14.6M
+// vertices, and its 506M-entry radix sort was 60% of that level's time.
+__global__ void k_csize(const int32_t* __restrict__ mapping, int64_t n, int32_t* csize) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(csize + mapping[v], 1);
+}
+__global__ void k_members(const int32_t* __restrict__ mapping, const int32_t* __restrict__ csize, int64_t n,
+                          uint8_t* cf) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        cf[v] = csize[mapping[v]] > 1 ? 1 : 0;
+}
+struct MarkNbrs {
+    const int32_t* indices;
+    uint8_t* cf;
+    __device__ __forceinline__ void operator()(int64_t, int64_t e, int64_t) { cf[__ldg(indices + e)] = 1; }
+    __device__ __forceinline__ void flush() {}
+};
+struct DegOf {
+    const int64_t* indptr;
+    const int32_t* list;
+    int64_t n;
+    __device__ __forceinline__ int64_t operator()(int64_t i) const {
+        if (i >= n) return 0;
+        const int32_t v = list[i];
+        return indptr[v + 1] - indptr[v];
+    }
+};
+__global__ void k_simple_len(const int64_t* __restrict__ indptr, const uint8_t* __restrict__ cf,
+                             const int32_t* __restrict__ mapping, int64_t n, int64_t* clen) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (!cf[v]) clen[mapping[v]] = indptr[v + 1] - indptr[v];
+}
+// run starts, then run ends (two passes: no thread walks a hub's long row)
+__global__ void k_complex_start(const uint64_t* __restrict__ ukeys, int64_t R, int bits, int64_t* cstart) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = (int64_t)(ukeys[i] >> bits);
+        if (i == 0 || (int64_t)(ukeys[i - 1] >> bits) != row) cstart[row] = i;
+    }
+}
+__global__ void k_complex_len(const uint64_t* __restrict__ ukeys, int64_t R, int bits, const int64_t* cstart,
+                              int64_t* clen) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = (int64_t)(ukeys[i] >> bits);
+        if (i == R - 1 || (int64_t)(ukeys[i + 1] >> bits) != row) clen[row] = i + 1 - cstart[row];
+    }
+}
+template <class WT, class OT>
+struct EmitSimple {
+    const int32_t* indices;
+    const void* w;
+    const int32_t* mapping;
+    const uint8_t* cf;
+    const int64_t* indptr;
+    const int64_t* cindptr;
+    int32_t* cind;
+    OT* cw;
+    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
+        if (cf[v]) return;
+        const int64_t o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
+        cind[o] = __ldg(mapping + __ldg(indices + e));
+        cw[o] = (OT)WLoad<WT>::tw(w, e);
+    }
+    __device__ __forceinline__ void flush() {}
+};
+template <class OT, class ST>
+__global__ void k_emit_complex(const uint64_t* __restrict__ ukeys, const ST* __restrict__ sums, int64_t R, int bits,
+                               const int64_t* __restrict__ cindptr, const int64_t* __restrict__ cstart,
+                               int32_t* cind, OT* cw) {
+    const uint64_t mask = (1ULL << bits) - 1ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = (int64_t)(ukeys[i] >> bits);
+        const int64_t o = cindptr[row] + (i - cstart[row]);
+        cind[o] = (int32_t)(ukeys[i] & mask);
+        cw[o] = (OT)sums[i];
+    }
+}
+
 template <class WT>
 Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
                      int32_t* mapping, double* ck, cudaStream_t s) {
@@ -169,7 +257,150 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     LCC_CUDA(cudaMemsetAsync(dintra.get(), 0, sizeof(unsigned long long), s));
     int64_t R = 0;
     double intra_w = 0.0;
-    if (nnz > 0) {
+    bool fast_done = false;
+    const char* ef = getenv("LCC_CONTRACT_FAST");
+    if (nnz > 0 && !(ef && ef[0] == '0')) {
+        // complex rows: members of non-singleton clusters and their neighbours
+        Buf<int32_t> csize(cn, s);
+        LCC_CUDA(cudaMemsetAsync(csize.get(), 0, sizeof(int32_t) * cn, s));
+        k_csize<<<grid_for(n, 256), 256, 0, s>>>(mapping, n, csize.get());
+        LCC_LAUNCH_CHECK();
+        Buf<uint8_t> cf(n, s);
+        k_members<<<grid_for(n, 256), 256, 0, s>>>(mapping, csize.get(), n, cf.get());
+        LCC_LAUNCH_CHECK();
+        csize.release();
+        Buf<int32_t> list(n, s);
+        Buf<int64_t> dcount(1, s);
+        auto compact_rows = [&](int64_t& cnt, Buf<int64_t>& off) {
+            select_flagged(cub::CountingInputIterator<int32_t>(0), cf.get(), list.get(), dcount.get(), n, s);
+            LCC_CUDA(cudaMemcpyAsync(&cnt, dcount.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+            off.alloc(cnt + 1, s);
+            cub::TransformInputIterator<int64_t, DegOf, cub::CountingInputIterator<int64_t>> degs(
+                cub::CountingInputIterator<int64_t>(0), DegOf{g.indptr, list.get(), cnt});
+            exclusive_sum(degs, off.get(), cnt + 1, s);
+            int64_t tot = 0;
+            LCC_CUDA(cudaMemcpyAsync(&tot, off.get() + cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+            return tot;
+        };
+        int64_t nm = 0, nC = 0;
+        Buf<int64_t> moff, coff;
+        const int64_t mdeg = compact_rows(nm, moff);
+        int64_t mc = nnz;
+        if (mdeg * 10 <= nnz * 6) {  // members' rows alone already exceed the cut: full path
+            if (nm > 0 && mdeg > 0)
+                edge_balanced(g.indptr, list.get(), moff.get(), nm, mdeg, MarkNbrs{g.indices, cf.get()}, s);
+            moff.release();
+            mc = compact_rows(nC, coff);
+        }
+        tr.mark("classify");
+        if (mc * 10 <= nnz * 6) {  // complex entries <= 60%: sort only those
+            fast_done = true;
+            const uint64_t sentinel = bits >= 32 ? ~0ULL : ((1ULL << (2 * bits)) - 1ULL);
+            const int64_t mc1 = std::max<int64_t>(mc, 1);
+            Buf<uint64_t> ka(mc1, s), kb(mc1, s);
+            Buf<VT> va, vb;
+            if (WLoad<WT>::weighted) { va.alloc(mc1, s); vb.alloc(mc1, s); }
+            EdgeKey<WT, VT> ek{g.indices, g.weights, mapping, bits, sentinel, ka.get(), va.get(), dintra.get(),
+                               dacc.get()};
+            ek.compact = true;
+            if (mc > 0) edge_balanced(g.indptr, list.get(), coff.get(), nC, mc, ek, s);
+            cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());
+            cub::DoubleBuffer<VT> dv(va.get(), vb.get());
+            if (mc > 0) {
+                if (WLoad<WT>::weighted) sort_pairs_db(dk, dv, mc, 2 * bits, s);
+                else sort_keys_db(dk, mc, 2 * bits, s);
+            }
+            Buf<uint64_t>& ksorted = dk.Current() == ka.get() ? ka : kb;
+            Buf<VT>& vsorted = dv.Current() == va.get() ? va : vb;
+            tr.mark("sort(cx)");
+            int64_t runs = 0;
+            unsigned long long hintra = 0;
+            if (mc > 0) {
+                Buf<int64_t> dr(1, s);
+                cub::TransformInputIterator<int64_t, RunHead, cub::CountingInputIterator<int64_t>> heads(
+                    cub::CountingInputIterator<int64_t>(0), RunHead{ksorted.get()});
+                device_sum(heads, dr.get(), mc, s);
+                LCC_CUDA(cudaMemcpyAsync(&runs, dr.get(), sizeof(runs), cudaMemcpyDeviceToHost, s));
+            }
+            LCC_CUDA(cudaMemcpyAsync(&hintra, dintra.get(), sizeof(hintra), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaMemcpyAsync(&intra_w, dacc.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+            const int64_t Rc = runs - (hintra > 0 ? 1 : 0);
+            if (!WLoad<WT>::weighted) intra_w = (double)hintra;
+            Buf<uint64_t> ukeys(std::max<int64_t>(runs, 1), s);
+            Buf<uint32_t> swi;
+            Buf<double> sw;
+            if (int_out) swi.alloc(std::max<int64_t>(runs, 1), s);
+            else sw.alloc(std::max<int64_t>(runs, 1), s);
+            if (mc > 0) {
+                Buf<int64_t> druns(1, s);
+                auto rbk = [&](auto vals_in, auto* sums_out) {
+                    size_t bytes = 0;
+                    LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, ksorted.get(), ukeys.get(), vals_in,
+                                                            sums_out, druns.get(), cub::Sum(), mc, s));
+                    Buf<unsigned char> tmp(bytes, s);
+                    LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, ksorted.get(), ukeys.get(), vals_in,
+                                                            sums_out, druns.get(), cub::Sum(), mc, s));
+                };
+                if constexpr (WLoad<WT>::weighted) {
+                    if constexpr (FS) rbk(vsorted.get(), sw.get());
+                    else rbk(vsorted.get(), swi.get());
+                } else {
+                    if (int_out) rbk(cub::ConstantInputIterator<uint32_t>(1u), swi.get());
+                    else rbk(cub::ConstantInputIterator<double>(1.0), sw.get());
+                }
+            }
+            ka.release();
+            kb.release();
+            va.release();
+            vb.release();
+            tr.mark("reduce(cx)");
+            // coarse row lengths -> indptr
+            Buf<int64_t> clen(cn + 1, s), cstart(std::max<int64_t>(cn, 1), s);
+            LCC_CUDA(cudaMemsetAsync(clen.get(), 0, sizeof(int64_t) * (cn + 1), s));
+            k_simple_len<<<grid_for(n, 256), 256, 0, s>>>(g.indptr, cf.get(), mapping, n, clen.get());
+            LCC_LAUNCH_CHECK();
+            if (Rc > 0) {
+                k_complex_start<<<grid_for(Rc, 256), 256, 0, s>>>(ukeys.get(), Rc, bits, cstart.get());
+                LCC_LAUNCH_CHECK();
+                k_complex_len<<<grid_for(Rc, 256), 256, 0, s>>>(ukeys.get(), Rc, bits, cstart.get(), clen.get());
+                LCC_LAUNCH_CHECK();
+            }
+            exclusive_sum(clen.get(), out.indptr.get(), cn + 1, s);
+            LCC_CUDA(cudaMemcpyAsync(&R, out.indptr.get() + cn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+            tr.mark("lengths");
+            out.indices.alloc(std::max<int64_t>(R, 1), s);
+            if (int_out) out.wi.alloc(std::max<int64_t>(R, 1), s);
+            else out.w.alloc(std::max<int64_t>(R, 1), s);
+            tr.mark("alloc");
+            if (int_out) {
+                edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
+                              EmitSimple<WT, uint32_t>{g.indices, g.weights, mapping, cf.get(), g.indptr,
+                                                       out.indptr.get(), out.indices.get(), out.wi.get()}, s);
+                if (Rc > 0) {
+                    k_emit_complex<uint32_t, uint32_t><<<grid_for(Rc, 256), 256, 0, s>>>(
+                        ukeys.get(), swi.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),
+                        out.wi.get());
+                    LCC_LAUNCH_CHECK();
+                }
+            } else {
+                edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
+                              EmitSimple<WT, double>{g.indices, g.weights, mapping, cf.get(), g.indptr,
+                                                     out.indptr.get(), out.indices.get(), out.w.get()}, s);
+                if (Rc > 0) {
+                    k_emit_complex<double, double><<<grid_for(Rc, 256), 256, 0, s>>>(
+                        ukeys.get(), sw.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),
+                        out.w.get());
+                    LCC_LAUNCH_CHECK();
+                }
+            }
+            tr.mark("emit(fast)");
+        }
+    }
+    if (!fast_done && nnz > 0) {
         Buf<uint64_t> ka(nnz, s), kb(nnz, s);
         Buf<VT> va, vb;
         if (WLoad<WT>::weighted) { va.alloc(nnz, s); vb.alloc(nnz, s); }
@@ -243,7 +474,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(ukeys.get(), R, bits, cn, out.indptr.get(),
                                                          out.indices.get());
         LCC_LAUNCH_CHECK();
-    } else {
+    } else if (!fast_done) {
         if (int_out) out.wi.alloc(1, s);
         else out.w.alloc(1, s);
         out.indices.alloc(1, s);

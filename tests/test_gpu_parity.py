@@ -532,3 +532,42 @@ def test_parallel_cc_parked_levels_exact(monkeypatch):
     cl = L.parallel_cc(hg, L.ClusteringParams(0.3), L.ParOptions(schedule="sync"))
     assert cl.meta["stats"].levels >= 3
     assert np.array_equal(cl.labels(), C0)
+
+
+@pytest.mark.parametrize("wkind", ["none", "u32", "fp32", "fp64"])
+def test_compress_fast_path_identical(wkind, monkeypatch):
+    """The mostly-singleton contraction (simple rows copied, complex rows
+    sorted) equals the full sort path bit for bit, and the oracle."""
+    rng = np.random.default_rng(71)
+    if wkind == "none":
+        hg = hub_graph(rng, 30_000, [5, 77], [6000, 12000], base_p=0.0003)
+    else:
+        hg = rand_weighted(rng, 20_000, 0.0006, fp32=(wkind == "fp32"), lo=0.1, hi=2.0)
+        if wkind == "u32":
+            hg.weights = np.floor(hg.weights * 3) + 1.0
+            hg.total_weight = float(hg.weights.sum() / 2)
+    g = og(hg)
+    n = g.n
+    for merges in (3, 200, n // 50):
+        lab = np.arange(n, dtype=np.int32)
+        a = rng.choice(n, size=merges, replace=False)
+        b = rng.choice(n, size=merges, replace=False)
+        lab[a] = np.minimum(lab[a], b).astype(np.int32)
+        C, K = O.canonicalize(n, lab, n, None)
+        outs = []
+        for fast in ("1", "0"):
+            monkeypatch.setenv("LCC_CONTRACT_FAST", fast)
+            c = L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda())
+            lvl = L.par_compress(dg(hg), L.ClusteringParams(0.4), c)
+            outs.append((lvl.mapping.cpu().numpy(), lvl.graph.indptr.cpu().numpy(), lvl.graph.indices.cpu().numpy(),
+                         lvl.graph.weights.cpu().numpy(), lvl.internal_offset, lvl.graph.total_weight))
+        f, s = outs
+        for x, y in zip(f[:4], s[:4]):
+            assert np.array_equal(x, y)
+        assert f[4] == s[4] and f[5] == s[5]
+        lvl0 = O.compress(g, None, 0.4, C, K)
+        assert np.array_equal(f[1], lvl0.graph.indptr) and np.array_equal(f[2], lvl0.graph.indices)
+        if wkind in ("none", "u32"):
+            assert np.array_equal(f[3], lvl0.graph.weights)
+        else:
+            np.testing.assert_allclose(f[3], lvl0.graph.weights, rtol=1e-12)

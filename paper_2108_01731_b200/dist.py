@@ -7,9 +7,9 @@ labels C and masses K.
 
 Per best-move iteration (Alg. 1 lines 6-10, bulk-synchronous across ranks):
   1. every rank runs the best-move kernels over its owned frontier;
-  2. the owned slices of the new labels and of the moved flags are combined
-     with an element-wise MAX all-reduce over NCCL (non-owners contribute -1 /
-     0), so every rank holds the full new labelling;
+  2. the owned slices of the new labels are combined with an element-wise
+     MAX all-reduce over NCCL (non-owners contribute -1), so every rank holds
+     the full new labelling; the moved flags follow locally (label changed);
   3. masses K are recomputed locally from the replicated labels (the apply /
      reconcile kernel) -- cheaper than all-reducing a dense fp64 K array, see
      SURVEY.md §8e step 3;
@@ -226,7 +226,8 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
     sched = int(opts.schedule)
     any_moved = False
     deg = (part.indptr[1:] - part.indptr[:-1])
-    for _ in range(int(opts.num_iter)):
+    num_iter = int(opts.num_iter)
+    for it in range(num_iter):
         if _sum_int(int(F.numel()), dev, group) == 0:
             break
         labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
@@ -240,21 +241,22 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
         if total == 0:
             break                               # Alg. 1 line 9
         any_moved = True
-        # owners' labels / moved flags to every rank
+        # owners' labels to every rank (one int32 MAX all-reduce).  The moved
+        # flags need no exchange: a vertex moved iff its label changed (a
+        # mover's target differs from its cluster; fresh ids are n+v).
         lab = torch.full((n,), -1, dtype=torch.int32, device=dev)
         lab[part.lo:part.hi] = labels[part.lo:part.hi]
         _max_(lab, group)
-        mv = torch.zeros(n, dtype=torch.uint8, device=dev)
-        mv[part.lo:part.hi] = moved[part.lo:part.hi]
-        _max_(mv, group)
         Cn, Kn = backend.apply(lab, 2 * n, k)   # canonical labels + masses, replicated
-        policy = FrontierPolicy(opts.frontier_policy)
-        if policy == FrontierPolicy.AllVertices:
-            F = owned
-        else:
-            mask = backend.frontier_mask(part, int(policy), mv, C, Cn)
-            _max_(mask, group)
-            F = (torch.nonzero(mask[part.lo:part.hi]).flatten() + part.lo).to(torch.int32)
+        if it + 1 < num_iter:  # the next frontier is only needed by a next iteration
+            policy = FrontierPolicy(opts.frontier_policy)
+            if policy == FrontierPolicy.AllVertices:
+                F = owned
+            else:
+                mv = (lab != C).to(torch.uint8)
+                mask = backend.frontier_mask(part, int(policy), mv, C, Cn)
+                _max_(mask, group)
+                F = (torch.nonzero(mask[part.lo:part.hi]).flatten() + part.lo).to(torch.int32)
         C, K = Cn, Kn
     return C, K, any_moved
 

@@ -60,6 +60,9 @@ namespace {
 #ifndef LCC_ALWAYS_RED
 #define LCC_ALWAYS_RED 0  // tuning: RED even for unit-weight claims
 #endif
+#ifndef LCC_EXPERIMENT_BIN6
+#define LCC_EXPERIMENT_BIN6 0
+#endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
 #endif
@@ -684,6 +687,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr int GT = GW * 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_g[GROUPS * GW];
+    __shared__ double s_scp[GW > 1 ? GROUPS * GW : 1];  // S_c partials (own array: no reuse barrier)
     __shared__ int32_t s_x[GROUPS * GW];
     __shared__ int32_t s_mv[GROUPS];
     constexpr bool VAL = ASYNC && LCC_VALIDATE;
@@ -703,6 +707,17 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     unsigned long long my_moves = 0;
+    // multi-warp groups: two barriers per vertex (after the inserts, after the
+    // argmax partials); the previous vertex's movers flag their neighbours
+    // right after the next vertex's first barrier (s_mv is stable there)
+    int64_t prev_s = 0, prev_e = 0;
+    bool prev_pending = false;
+    auto mark_prev = [&]() {
+        if (a.mark && prev_pending && s_mv[gid]) {
+#pragma unroll 4
+            for (int64_t e = prev_s + gt; e < prev_e; e += GT) a.mark[__ldg(a.indices + e)] = 1;
+        }
+    };
     for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += (int64_t)gridDim.x * GROUPS) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
@@ -740,13 +755,14 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 #pragma unroll
         for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
         if constexpr (GW > 1) {
-            if (lane == 0) s_g[gid * GW + wig] = sc;
+            if (lane == 0) s_scp[gid * GW + wig] = sc;
         }
-        gsync();
+        gsync();  // (A) table complete, S_c partials and the previous vertex's s_mv visible
         if constexpr (GW > 1) {
+            mark_prev();
             sc = 0.0;
 #pragma unroll
-            for (int w = 0; w < GW; ++w) sc += s_g[gid * GW + w];
+            for (int w = 0; w < GW; ++w) sc += s_scp[gid * GW + w];
         }
         const double b = dadd(dsub(sc, dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
@@ -772,13 +788,12 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         if constexpr (VAL) warp_argmax(bg, bx, bS);
         else warp_argmax(bg, bx);
         if constexpr (GW > 1) {
-            gsync();  // everyone has read s_g (S_c) before reuse
             if (lane == 0) {
                 s_g[gid * GW + wig] = bg;
                 s_x[gid * GW + wig] = bx;
                 if constexpr (VAL) s_S[gid * GW + wig] = bS;
             }
-            gsync();
+            gsync();  // (B) partials visible; every warp has finished scoring (table clean)
 #pragma unroll
             for (int w = 0; w < GW; ++w) {
                 const double og = s_g[gid * GW + w];
@@ -795,20 +810,27 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             mv = decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, VAL ? bS : NAN);
             my_moves += mv;
         }
-        if (a.mark) {  // fused frontier: a mover flags its neighbours (row re-read hits L2)
-            if constexpr (GW == 1) {
+        if constexpr (GW == 1) {
+            if (a.mark) {  // fused frontier: a mover flags its neighbours (row re-read hits L2)
                 mv = __shfl_sync(FULL, mv, 0);
-            } else {
-                if (gt == 0) s_mv[gid] = mv;
-                gsync();
-                mv = s_mv[gid];
-            }
-            if (mv) {
+                if (mv) {
 #pragma unroll 4
-                for (int64_t e = s + gt; e < end; e += GT) a.mark[__ldg(a.indices + e)] = 1;
+                    for (int64_t e = s + gt; e < end; e += GT) a.mark[__ldg(a.indices + e)] = 1;
+                }
             }
+            __syncwarp();
+        } else {
+            // s_mv is read by the group after the next vertex's barrier (A);
+            // every reader of this slot passed (B) of this vertex already
+            if (gt == 0) s_mv[gid] = mv;
+            prev_s = s;
+            prev_e = end;
+            prev_pending = true;
         }
-        gsync();  // table (already reset by take) and s_g free for the next vertex
+    }
+    if constexpr (GW > 1) {
+        gsync();
+        mark_prev();
     }
     flush_moves(a, my_moves);
 }
@@ -1925,6 +1947,13 @@ void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64
         case 3: launch_group<WT, ASYNC, KI, 1, 1024, 8, 8, 3>(a, list, lo, hi, s); break;  //  ..512      warp
         case 4:
             if (var == 3) launch_group<WT, ASYNC, KI, 8, 4096, 1, 8>(a, list, lo, hi, s);
+#if LCC_EXPERIMENT_BIN6
+            // tuning experiments, valid only while every vertex here has degree < 1024
+            else if (var == 6) launch_group<WT, ASYNC, KI, 4, 2048, 4, 4, 2>(a, list, lo, hi, s);
+            else if (var == 7) launch_group<WT, ASYNC, KI, 4, 2048, 2, 8, 4>(a, list, lo, hi, s);
+            else if (var == 8) launch_group<WT, ASYNC, KI, 2, 2048, 4, 8, 4>(a, list, lo, hi, s);
+            else if (var == 9) launch_group<WT, ASYNC, KI, 1, 2048, 4, 8, 4>(a, list, lo, hi, s);
+#endif
             else launch_group<WT, ASYNC, KI, 4, 4096, 2, 8, 3>(a, list, lo, hi, s);        //  ..2048     4 warps
             break;
         case 5:

@@ -92,6 +92,29 @@ def main(which):
                    "rel_diff": (o_gpu - o_ref) / max(abs(o_ref), 1e-300),
                    "pass_1e-6": abs(o_gpu - o_ref) <= 1e-6 * max(abs(o_ref), 1e-300), "gpu_s": t_gpu, "cpu_s": t_cpu}
             print(json.dumps({"cfg3": res}), flush=True)
+    if "cfg5" in which:
+        # configs[4]: 65M vertices, ~1.8B edges, CC lambda 0.85, async default.
+        # The CPU oracle does not finish within the budget here (one async
+        # round over 3.6B entries is ~15 s on 16 cores and a clustering runs
+        # ~25 rounds over 3+ levels), so this line is GPU-only: time,
+        # objective (exact integer edge sums) and the level structure.
+        from paper_2108_01731_b200.gen import powerlaw_communities_device
+        dg = powerlaw_communities_device()
+        p = L.ClusteringParams(0.85)
+        res = {"n": dg.n, "m": dg.m}
+        for rep in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cl = L.parallel_cc(dg, p, L.ParOptions())
+            torch.cuda.synchronize()
+            t = time.perf_counter() - t0
+            st = cl.meta["stats"]
+            res[f"run{rep}"] = {"gpu_s": t, "objective": L.cc_objective(dg, p, cl), "levels": st.levels,
+                                "rounds": st.rounds, "edges_scanned": st.edges_scanned,
+                                "gedges_per_s": st.edges_scanned / t / 1e9, "clusters": cl.num_clusters}
+            del cl
+        res["cpu"] = "DNF within the budget (see comment); parity for this config rests on cfg2/cfg4 and the unit suite"
+        print(json.dumps({"cfg5": res}), flush=True)
 
 
 if __name__ == "__main__":

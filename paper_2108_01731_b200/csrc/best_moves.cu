@@ -20,9 +20,9 @@
 //   4-5 33 .. 512          : k_group, one WARP per vertex, 256/1024-slot
 //                            shared-memory hash table (the paper's
 //                            "sequential" per-vertex accumulation)
-//   6-8 .. 10240           : k_group, 4/8/32 warps per vertex, 4K-16K slots
+//   6-9 .. 10240           : k_group, 4/4/8/32 warps per vertex, 2K-16K slots
 //                            ("parallel hash table")
-//   9  hubs                : labels radix-partitioned by hash into ~2K-entry
+//   10 hubs                : labels radix-partitioned by hash into ~2K-entry
 //                            buckets, each aggregated by one CTA in a 4K-slot
 //                            shared-memory table (k_hub_*); LCC_HUB_BUCKETS=0:
 //                            2048-edge items inserting into per-vertex global
@@ -59,9 +59,6 @@ namespace {
 #endif
 #ifndef LCC_ALWAYS_RED
 #define LCC_ALWAYS_RED 0  // tuning: RED even for unit-weight claims
-#endif
-#ifndef LCC_EXPERIMENT_BIN6
-#define LCC_EXPERIMENT_BIN6 0
 #endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
@@ -1779,7 +1776,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
 // ===========================================================================
 // degree-bin partition (one pass, block-aggregated reservations)
 // ===========================================================================
-constexpr int NBINS = 10;
+constexpr int NBINS = 11;
 struct BinEdges {
     int64_t hi[NBINS];  // bin b holds hi[b-1] < deg <= hi[b]  (hi[-1] = -1)
 };
@@ -1945,23 +1942,22 @@ void launch_bin(int bin, const BMArgs& a, const int32_t* list, int64_t lo, int64
     switch (bin) {  //                         GW  CAP    GROUPS U
         case 2: launch_group<WT, ASYNC, KI, 1, 256, 8, 4, 6>(a, list, lo, hi, s); break;   //  ..128      warp
         case 3: launch_group<WT, ASYNC, KI, 1, 1024, 8, 8, 3>(a, list, lo, hi, s); break;  //  ..512      warp
-        case 4:
-            if (var == 3) launch_group<WT, ASYNC, KI, 8, 4096, 1, 8>(a, list, lo, hi, s);
-#if LCC_EXPERIMENT_BIN6
-            // tuning experiments, valid only while every vertex here has degree < 1024
-            else if (var == 6) launch_group<WT, ASYNC, KI, 4, 2048, 4, 4, 2>(a, list, lo, hi, s);
-            else if (var == 7) launch_group<WT, ASYNC, KI, 4, 2048, 2, 8, 4>(a, list, lo, hi, s);
-            else if (var == 8) launch_group<WT, ASYNC, KI, 2, 2048, 4, 8, 4>(a, list, lo, hi, s);
-            else if (var == 9) launch_group<WT, ASYNC, KI, 1, 2048, 4, 8, 4>(a, list, lo, hi, s);
-#endif
-            else launch_group<WT, ASYNC, KI, 4, 4096, 2, 8, 3>(a, list, lo, hi, s);        //  ..2048     4 warps
+        case 4:  // ..1023: 2048-slot tables, 4 groups of 4 warps per CTA (measured +3.3% vs 4096 slots x 2)
+            if (var == 8) launch_group<WT, ASYNC, KI, 2, 2048, 4, 8, 4>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, KI, 4, 2048, 4, 4, 2>(a, list, lo, hi, s);
             break;
         case 5:
-            if (var == 1) launch_group<WT, ASYNC, KI, 16, 8192, 1, 8>(a, list, lo, hi, s);
-            else launch_group<WT, ASYNC, KI, 8, 8192, 1, 4>(a, list, lo, hi, s);           //  ..4096     8 warps
+            if (var == 3) launch_group<WT, ASYNC, KI, 8, 4096, 1, 8>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, KI, 4, 4096, 2, 8, 3>(a, list, lo, hi, s);        //  ..2048     4 warps
             break;
         case 6:
+            if (var == 1) launch_group<WT, ASYNC, KI, 16, 8192, 1, 8>(a, list, lo, hi, s);
+            else if (var == 4) launch_group<WT, ASYNC, KI, 4, 8192, 1, 8, 3>(a, list, lo, hi, s);
+            else launch_group<WT, ASYNC, KI, 8, 8192, 1, 4>(a, list, lo, hi, s);           //  ..4096     8 warps
+            break;
+        case 7:
             if (var == 1) launch_group<WT, ASYNC, KI, 16, B5_CAP, 1, 8>(a, list, lo, hi, s);
+            else if (var == 4) launch_group<WT, ASYNC, KI, 8, B5_CAP, 1, 4, 1>(a, list, lo, hi, s);
             else launch_group<WT, ASYNC, KI, 32, B5_CAP, 1, 4>(a, list, lo, hi, s);        //  ..10240    32 warps
             break;
         default: break;
@@ -2243,8 +2239,9 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     // (the paper's sequential-vs-parallel hash-table switch)
     // bins: 0 isolated | 1 deg<=8 thread per vertex | 2 ..32 warp windows |
     //       3 optional edge windows | 4-5 warp per vertex up to the threshold |
-    //       6 ..2048 4 warps | 7 ..4096 8 warps | 8 ..large_min 32 warps |
-    //       9 hubs (bucketed shared-memory tables)
+    //       6 ..1023 4 warps (2K slots) | 7 ..2048 4 warps (4K slots) |
+    //       8 ..4096 8 warps | 9 ..large_min 32 warps |
+    //       10 hubs (bucketed shared-memory tables)
     // LCC_WINDOW=0 / LCC_LARGE_MIN (env): tuning knobs for the bin shapes only
     // measured on B200 (R-MAT s24): per-vertex warp groups beat the window
     // kernel by ~5%, and CTA groups beat the L2 hub path up to 10240
@@ -2267,10 +2264,11 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     be.hi[3] = Tw - 1;
     be.hi[4] = std::max<int64_t>(be.hi[3], std::min<int64_t>(128, Tg - 1));
     be.hi[5] = std::max<int64_t>(be.hi[4], Tg - 1);
-    be.hi[6] = std::min<int64_t>(2048, large_min);
-    be.hi[7] = std::min<int64_t>(4096, large_min);
-    be.hi[8] = std::min<int64_t>(MED_MAX, large_min);
-    be.hi[9] = INT64_MAX;
+    be.hi[6] = std::max<int64_t>(be.hi[5], std::min<int64_t>(1023, large_min));
+    be.hi[7] = std::min<int64_t>(2048, large_min);
+    be.hi[8] = std::min<int64_t>(4096, large_min);
+    be.hi[9] = std::min<int64_t>(MED_MAX, large_min);
+    be.hi[10] = INT64_MAX;
 
     if (hprobe.on && getenv("LCC_TRACE_SYNC")) {  // device work queued before this round
         LCC_CUDA(cudaStreamSynchronize(s));

@@ -60,6 +60,9 @@ namespace {
 #ifndef LCC_ALWAYS_RED
 #define LCC_ALWAYS_RED 0  // tuning: RED even for unit-weight claims
 #endif
+#ifndef LCC_SMALL_LADDER2
+#define LCC_SMALL_LADDER2 1  // k_small: segment bounds from the starts mask, S fetched after the ladder
+#endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
 #endif
@@ -314,6 +317,35 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 g = dsub(dsub(S, dmul(tj, ldK<ASYNC, KI>(a.K, x, pol_keep))), bj);
                 gx = x;
             }
+#if LCC_SMALL_LADDER2
+            // segmented argmax: the segment bound comes from the starts
+            // bitmask (no shuffled segment ids); the winner's S is fetched
+            // once after the ladder instead of riding every step
+            int segend = lane + 1;
+            if (has_edge) {
+                const unsigned above = starts & ~((2u << lane) - 1u);
+                segend = above ? __ffs(above) - 1 : nedges;
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double og = __shfl_down_sync(FULL, g, d);
+                const int32_t ox = __shfl_down_sync(FULL, gx, d);
+                if (lane + d < segend && better(og, ox, g, gx)) { g = og; gx = ox; }
+            }
+            const int src = starter ? rs : lane;
+            const double hg = __shfl_sync(FULL, g, src);
+            const int32_t hx = __shfl_sync(FULL, gx, src);
+            double hS = NAN;
+            if constexpr (ASYNC && LCC_VALIDATE) {
+                const int32_t sx = __shfl_sync(FULL, gx, p);  // my segment's winner (head lane p)
+                const unsigned wm = __ballot_sync(FULL, is_leader && x != cj && x == sx);
+                // the owner's segment: lanes [rs, rs + deg)
+                const unsigned omask = starter ? ((deg >= 32 ? FULL : ((1u << deg) - 1u)) << rs) : 0u;
+                const unsigned wo = wm & omask;
+                const double sw = __shfl_sync(FULL, gS, wo ? __ffs(wo) - 1 : lane);
+                hS = sw;
+            }
+#else
             const int32_t seg = has_edge ? j : 32 + lane;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -329,6 +361,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const int32_t hx = __shfl_sync(FULL, gx, src);
             double hS = NAN;
             if constexpr (ASYNC && LCC_VALIDATE) hS = __shfl_sync(FULL, gS, src);
+#endif
             const int mv = inwin ? decide<ASYNC, KI>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx, hS) : 0;
             my_moves += mv;
             if (a.mark) {  // the window's neighbour ids are still in registers

@@ -395,9 +395,22 @@ def run_ours(args):
         traffic, traffic_src = tj["dram_bytes_per_step"], "profiles/r01_traffic.json (" + tj["source"] + ")"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
-                "kernel": "best-move (k_small/k_medium/k_large_*)",
+                "kernel": "best-move (k_tiny/k_small/k_group/k_hub_*)",
                 "alg_bytes_per_launch_group": alg_bytes, "kernel_ms_per_step": kern_ms,
                 "kernel_share_of_step": kern_ms / (ms / args.steps)}
+    # The kernels are latency bound on the dependent chain index -> label
+    # gather -> mass gather, not on bandwidth (DRAM 5-9% busy): compare the
+    # edge rate with the same chain measured alone on this GPU type at the
+    # config-4 array sizes (tools/micro/gather_roof.cu, no hashing at all)
+    gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gather_roof.json")
+    if wl.cfg == "cfg4" and args.scale == 24 and os.path.exists(gpath):
+        gj = json.load(open(gpath))
+        chain = gj["n_16777216"]["chain2_Gps"]
+        edges_per_s = nnz / (kern_ms / 1e3) / 1e9
+        roofline["access_roofline"] = {
+            "pattern": "streamed index -> random label gather -> random mass gather, 67 MB arrays",
+            "achieved": edges_per_s, "peak": chain, "unit": "G chains/s", "frac": edges_per_s / chain,
+            "source": "profiles/r01_gather_roof.json (tools/micro/gather_roof.cu)"}
 
     # CPU baseline (oracle port) first: the e2e leg below drops the device graph
     cpu = None

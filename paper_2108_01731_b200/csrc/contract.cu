@@ -529,6 +529,55 @@ Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* 
 }
 
 namespace {
+__global__ void k_csize_c(const int32_t* __restrict__ C, int64_t n, int32_t* csize) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(csize + C[v], 1);
+}
+}  // namespace
+
+// Entries the contraction of (g, C) would sort: the rows of members of
+// non-singleton clusters and of their neighbours when they are at most 60% of
+// nnz (the fast path of compress_impl), else nnz.  Labels must be canonical
+// (< n).  Used by the driver to size the contraction before deciding to park
+// finer levels on the host.
+int64_t contraction_sort_entries(const lcc_graph& g, const int32_t* C, cudaStream_t s) {
+    const int64_t n = g.n, nnz = g.nnz;
+    if (nnz == 0 || n == 0) return 0;
+    const char* ef = getenv("LCC_CONTRACT_FAST");
+    if (ef && ef[0] == '0') return nnz;
+    Buf<int32_t> csize(n, s);
+    LCC_CUDA(cudaMemsetAsync(csize.get(), 0, sizeof(int32_t) * n, s));
+    k_csize_c<<<grid_for(n, 256), 256, 0, s>>>(C, n, csize.get());
+    LCC_LAUNCH_CHECK();
+    Buf<uint8_t> cf(n, s);
+    k_members<<<grid_for(n, 256), 256, 0, s>>>(C, csize.get(), n, cf.get());
+    LCC_LAUNCH_CHECK();
+    csize.release();
+    Buf<int32_t> list(n, s);
+    Buf<int64_t> dcount(1, s);
+    auto rows = [&](int64_t& cnt, Buf<int64_t>& off) {
+        select_flagged(cub::CountingInputIterator<int32_t>(0), cf.get(), list.get(), dcount.get(), n, s);
+        LCC_CUDA(cudaMemcpyAsync(&cnt, dcount.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaStreamSynchronize(s));
+        off.alloc(cnt + 1, s);
+        cub::TransformInputIterator<int64_t, DegOf, cub::CountingInputIterator<int64_t>> degs(
+            cub::CountingInputIterator<int64_t>(0), DegOf{g.indptr, list.get(), cnt});
+        exclusive_sum(degs, off.get(), cnt + 1, s);
+        int64_t tot = 0;
+        LCC_CUDA(cudaMemcpyAsync(&tot, off.get() + cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaStreamSynchronize(s));
+        return tot;
+    };
+    int64_t nm = 0, nc = 0;
+    Buf<int64_t> moff, coff;
+    const int64_t mdeg = rows(nm, moff);
+    if (mdeg * 10 > nnz * 6) return nnz;
+    if (nm > 0 && mdeg > 0) edge_balanced(g.indptr, list.get(), moff.get(), nm, mdeg, MarkNbrs{g.indices, cf.get()}, s);
+    const int64_t mc = rows(nc, coff);
+    return mc * 10 <= nnz * 6 ? mc : nnz;
+}
+
+namespace {
 __global__ void k_widen_u32(const uint32_t* __restrict__ in, double* out, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (double)in[i];

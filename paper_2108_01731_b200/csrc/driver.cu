@@ -213,9 +213,12 @@ struct Frame {
 
 // device bytes a contraction of g may take (keys x2, values x2, unique keys,
 // outputs), vs what is free on the device plus what the library has cached
-bool contraction_fits(const lcc_graph& g) {
+// sorted: entries going through keys + radix sort (all of them, or only the
+// complex rows' on the mostly-singleton fast path); the coarse outputs are
+// sized by nnz either way
+bool contraction_fits(const lcc_graph& g, int64_t sorted) {
     const double vb = (g.weights && g.wtype != LCC_W_U32) ? 8.0 : 4.0;
-    const double need = (double)g.nnz * (16.0 + 2.0 * vb + 8.0 + 4.0 + vb) + (double)g.n * 64.0;
+    const double need = (double)sorted * (16.0 + 2.0 * vb + 8.0) + (double)g.nnz * (4.0 + vb) + (double)g.n * 64.0;
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return true;
     double r, u;
@@ -256,13 +259,14 @@ void parallel_cc(const lcc_graph& g0, const double* k0, double lam, const Option
         // this contraction would not fit next to them
         // (LCC_PARK_ALWAYS=1 parks every finer level: tests of the parking path)
         const bool park_always = getenv("LCC_PARK_ALWAYS") && getenv("LCC_PARK_ALWAYS")[0] == '1';
-        if (owned.size() > 1 && (park_always || !contraction_fits(g))) {
+        const int64_t sorted = owned.size() > 1 ? contraction_sort_entries(g, C.get(), s) : g.nnz;
+        if (owned.size() > 1 && (park_always || !contraction_fits(g, sorted))) {
             for (size_t i = 0; i + 1 < owned.size(); ++i) {
                 if (owned[i]->host) continue;
                 owned[i]->park(s);
                 if (trace) fprintf(stderr, "[lcc]   parked level %zu (%.1f GB) on the host\n", i + 1,
                                    owned[i]->bytes() / 1073741824.0);
-                if (!park_always && contraction_fits(g)) break;
+                if (!park_always && contraction_fits(g, sorted)) break;
             }
         }
         EventTimer tc(s);

@@ -57,6 +57,7 @@ struct Coarse {
 Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
                 int32_t* mapping, double* ck, cudaStream_t s);
 void widen_u32(const uint32_t* in, double* out, int64_t n, cudaStream_t s);
+int64_t contraction_sort_entries(const lcc_graph& g, const int32_t* C, cudaStream_t s);
 void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C,
              double* K, cudaStream_t s);
 

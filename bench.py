@@ -610,7 +610,7 @@ def run_sharded(args):
                "config": config_dict(args, {"n": n, "m": nnz // 2, "ws": ws}, None,
                                      {"workload": f"rmat-s{args.scale}-ef{args.edge_factor} (BASELINE.json configs[3])",
                                       "lambda": lam, "schedule": sched,
-                                      "parallelism": f"vertex-sharded x{ws} (NCCL MAX all-reduce of labels/flags)"}),
+                                      "parallelism": f"vertex-sharded x{ws} (NCCL all-gather of owned labels)"}),
                "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)

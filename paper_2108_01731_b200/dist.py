@@ -7,9 +7,9 @@ labels C and masses K.
 
 Per best-move iteration (Alg. 1 lines 6-10, bulk-synchronous across ranks):
   1. every rank runs the best-move kernels over its owned frontier;
-  2. the owned slices of the new labels are combined with an element-wise
-     MAX all-reduce over NCCL (non-owners contribute -1), so every rank holds
-     the full new labelling; the moved flags follow locally (label changed);
+  2. the owned slices of the new labels are all-gathered over NCCL (padded
+     equal chunks), so every rank holds the full new labelling; the moved
+     flags follow locally (label changed);
   3. masses K are recomputed locally from the replicated labels (the apply /
      reconcile kernel) -- cheaper than all-reducing a dense fp64 K array, see
      SURVEY.md §8e step 3;
@@ -209,6 +209,33 @@ def _sum_int(x: int, device, group) -> int:
     return int(t.item())
 
 
+def _owned_sizes(part, group) -> list[int]:
+    """Sizes of every rank's owned range (all-gathered once per PartGraph)."""
+    sizes = getattr(part, "_sizes", None)
+    if sizes is None:
+        world = dist.get_world_size(group)
+        dev = part.indptr.device
+        t = torch.tensor([part.hi - part.lo], dtype=torch.int64, device=dev)
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t, group=group)
+        sizes = [int(o.item()) for o in outs]
+        part._sizes = sizes
+    return sizes
+
+
+def _allgather_owned(vals: torch.Tensor, part, group) -> torch.Tensor:
+    """The owned slice of ``vals`` from every rank, concatenated in rank order
+    (the ranges are contiguous and ordered, so this is the full array): one
+    NCCL all-gather of padded equal-size chunks."""
+    sizes = _owned_sizes(part, group)
+    mx = max(sizes)
+    buf = torch.empty(mx, dtype=vals.dtype, device=vals.device)
+    buf[:part.hi - part.lo] = vals[part.lo:part.hi]
+    outs = [torch.empty_like(buf) for _ in sizes]
+    dist.all_gather(outs, buf, group=group)
+    return torch.cat([o[:sz] for o, sz in zip(outs, sizes)])
+
+
 @dataclass
 class ShardStats:
     rounds: int = 0
@@ -241,12 +268,10 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
         if total == 0:
             break                               # Alg. 1 line 9
         any_moved = True
-        # owners' labels to every rank (one int32 MAX all-reduce).  The moved
-        # flags need no exchange: a vertex moved iff its label changed (a
-        # mover's target differs from its cluster; fresh ids are n+v).
-        lab = torch.full((n,), -1, dtype=torch.int32, device=dev)
-        lab[part.lo:part.hi] = labels[part.lo:part.hi]
-        _max_(lab, group)
+        # owners' labels to every rank (one all-gather of the owned slices).
+        # The moved flags need no exchange: a vertex moved iff its label
+        # changed (a mover's target differs from its cluster; fresh ids n+v).
+        lab = _allgather_owned(labels, part, group)
         Cn, Kn = backend.apply(lab, 2 * n, k)   # canonical labels + masses, replicated
         if it + 1 < num_iter:  # the next frontier is only needed by a next iteration
             policy = FrontierPolicy(opts.frontier_policy)

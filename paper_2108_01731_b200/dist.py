@@ -287,7 +287,8 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
 
 
 def _gather_coarse(cn, cptr, cind, cw, device, group):
-    """All-gather partial coarse CSRs and merge duplicate (a, b) entries."""
+    """All-gather partial coarse CSRs; rank 0 merges duplicate (a, b)
+    entries and returns the coarse CSR (other ranks return None)."""
     world = dist.get_world_size(group)
     rows = torch.repeat_interleave(torch.arange(cn, device=device, dtype=torch.int64), cptr[1:] - cptr[:-1])
     local = torch.stack([rows, cind.to(torch.int64)]).contiguous()
@@ -303,6 +304,8 @@ def _gather_coarse(cn, cptr, cind, cw, device, group):
     gw = [torch.empty_like(pad_w) for _ in range(world)]
     dist.all_gather(gi, pad_i, group=group)
     dist.all_gather(gw, pad_w, group=group)
+    if dist.get_rank(group) != 0:
+        return None  # the coarse levels run on rank 0 only
     ab = torch.cat([g[:, :int(s.item())] for g, s in zip(gi, sizes)], dim=1)
     w = torch.cat([g[:int(s.item())] for g, s in zip(gw, sizes)])
     key = ab[0] * max(cn, 1) + ab[1]
@@ -339,9 +342,10 @@ def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, ba
     cn, cptr, cind, cw, ck, mapping = backend.compress(part, k, lam, C, K)
     if cn == n:
         return C                                      # no size reduction
-    c_indptr, c_ind, c_w, c_tot = _gather_coarse(cn, cptr, cind, cw, dev, group)
+    merged = _gather_coarse(cn, cptr, cind, cw, dev, group)
     Cc = torch.empty(cn, dtype=torch.int32, device=dev)
     if rank == 0:
+        c_indptr, c_ind, c_w, c_tot = merged
         Cc = backend.parallel_cc(c_indptr, c_ind, c_w, c_tot, ck, lam, opts).to(torch.int32)
     dist.broadcast(Cc, src=0, group=group)
     C, K = backend.flatten(mapping, Cc, k)

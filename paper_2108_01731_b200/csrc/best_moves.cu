@@ -60,6 +60,9 @@ namespace {
 #ifndef LCC_ALWAYS_RED
 #define LCC_ALWAYS_RED 0  // tuning: RED even for unit-weight claims
 #endif
+#ifndef LCC_SMALL_PIPE
+#define LCC_SMALL_PIPE 1  // k_small: next window's loads issued before this window is processed
+#endif
 #ifndef LCC_SMALL_LADDER2
 #define LCC_SMALL_LADDER2 1  // k_small: segment bounds from the starts mask, S fetched after the ladder
 #endif
@@ -216,14 +219,15 @@ __device__ __forceinline__ void flush_moves(const BMArgs& a, unsigned long long 
 // small bin: deg <= 32, warp-packed edge windows
 // ===========================================================================
 #ifndef LCC_SMALL_MINB
-#define LCC_SMALL_MINB 5  // 48 registers: 40 resident warps (+1.2% vs 32)
+#define LCC_SMALL_MINB 4  // 64 registers for the pipelined windows, no spill (+1.4% vs 48 registers unpipelined)
 #endif
 template <class WT, bool ASYNC, bool KI>
 __global__ void __launch_bounds__(SMALL_THREADS, LCC_SMALL_MINB)
 k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr int WPB = SMALL_THREADS / 32;
     __shared__ int32_t s_owner[WPB][32];
-    __shared__ double s_sc[WPB][32];
+    __shared__ double s_sc[LCC_SMALL_PIPE ? 1 : WPB][32];
+    __shared__ double s_sc2[LCC_SMALL_PIPE ? 2 : 1][WPB][32];  // per-window S_c, double-buffered
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nb = (hi - lo + 31) / 32;
@@ -257,6 +261,128 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         }
         const int32_t excl = incl - deg;
 
+#if LCC_SMALL_PIPE
+        // windows are software pipelined: the next window's geometry and
+        // index loads are issued before this window is processed, and its
+        // label gathers go out while this window waits for its masses
+        struct Geo {
+            bool inwin, starter, has_edge;
+            int end, rs, p, j, nedges;
+            unsigned starts;
+            int64_t e;
+        };
+        auto geometry = [&](int base, int buf, Geo& G) {
+            const int32_t base_off = __shfl_sync(FULL, excl, base);
+            G.inwin = valid && lane >= base && (incl - base_off) <= SMALL_MAX;
+            const unsigned winmask = __ballot_sync(FULL, G.inwin);
+            G.end = 32 - __clz(winmask);
+            G.nedges = __shfl_sync(FULL, incl, G.end - 1) - base_off;
+            G.rs = excl - base_off;
+            G.starter = G.inwin && deg > 0;
+            G.starts = __reduce_or_sync(FULL, G.starter ? (1u << G.rs) : 0u);
+            if (G.starter) s_owner[wib][G.rs] = lane;
+            if (G.inwin) s_sc2[buf][wib][lane] = 0.0;
+            __syncwarp();
+            G.has_edge = lane < G.nedges;
+            G.p = 0;
+            G.j = 0;
+            if (G.has_edge) {
+                const unsigned m = G.starts & ((2u << lane) - 1u);
+                G.p = 31 - __clz(m);
+                G.j = s_owner[wib][G.p];
+            }
+            __syncwarp();  // s_owner is rewritten by the next window's geometry
+            const int64_t sj = __shfl_sync(FULL, s, G.j);
+            G.e = sj + (lane - G.p);
+        };
+        Geo G;
+        int buf = 0;
+        geometry(0, 0, G);
+        int32_t nbr = G.has_edge ? ld_stream_i32(a.indices + G.e, pol_stream) : 0;
+        int32_t x = G.has_edge ? ldC<ASYNC>(a.C, nbr, pol_keep) : 0;
+        while (true) {
+            const bool more = G.end < nvalid;
+            Geo Gn;
+            int32_t nbr_n = 0;
+            if (more) {
+                geometry(G.end, buf ^ 1, Gn);
+                if (Gn.has_edge) nbr_n = ld_stream_i32(a.indices + Gn.e, pol_stream);
+            }
+            const int j = G.j, p = G.p, rs = G.rs, nedges = G.nedges;
+            const bool has_edge = G.has_edge, inwin = G.inwin, starter = G.starter;
+            const unsigned starts = G.starts;
+            const int32_t cj = __shfl_sync(FULL, c, j);
+            const double tj = __shfl_sync(FULL, t, j);
+            const double wv = has_edge ? WLoad<WT>::at(a.w, G.e) : 0.0;
+            const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
+                                          : ((uint64_t)(64 + lane) << 32);
+            const unsigned grp = __match_any_sync(FULL, key);
+            double S;
+            if constexpr (!WLoad<WT>::weighted) {
+                S = u32_to_f64(__popc(grp));
+            } else {
+                S = 0.0;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const double wq = __shfl_sync(FULL, wv, q);
+                    if ((grp >> q) & 1u) S = dadd(S, wq);
+                }
+            }
+            const bool is_leader = has_edge && lane == (__ffs(grp) - 1);
+            const bool cand = is_leader && x != cj;
+            // mass gather of this window, then the next window's label gather
+            const double Kx = cand ? ldK<ASYNC, KI>(a.K, x, pol_keep) : 0.0;
+            int32_t x_n = 0;
+            if (more && Gn.has_edge) x_n = ldC<ASYNC>(a.C, nbr_n, pol_keep);
+            if (is_leader && x == cj) s_sc2[buf][wib][j] = S;
+            __syncwarp();
+            double bv = 0.0;
+            if (inwin) bv = dadd(dsub(s_sc2[buf][wib][lane], dmul(t, Kc)), dmul(t, kv));
+            const double bj = __shfl_sync(FULL, bv, j);
+            double g = -INFINITY;
+            int32_t gx = NO_CAND;
+            double gS = 0.0;
+            if (cand) {
+                gS = S;
+                g = dsub(dsub(S, dmul(tj, Kx)), bj);
+                gx = x;
+            }
+            int segend = lane + 1;
+            if (has_edge) {
+                const unsigned above = starts & ~((2u << lane) - 1u);
+                segend = above ? __ffs(above) - 1 : nedges;
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double og = __shfl_down_sync(FULL, g, d);
+                const int32_t ox = __shfl_down_sync(FULL, gx, d);
+                if (lane + d < segend && better(og, ox, g, gx)) { g = og; gx = ox; }
+            }
+            const int src = starter ? rs : lane;
+            const double hg = __shfl_sync(FULL, g, src);
+            const int32_t hx = __shfl_sync(FULL, gx, src);
+            double hS = NAN;
+            if constexpr (ASYNC && LCC_VALIDATE) {
+                const int32_t sx = __shfl_sync(FULL, gx, p);
+                const unsigned wm = __ballot_sync(FULL, cand && x == sx);
+                const unsigned omask = starter ? ((deg >= 32 ? FULL : ((1u << deg) - 1u)) << rs) : 0u;
+                const unsigned wo = wm & omask;
+                hS = __shfl_sync(FULL, gS, wo ? __ffs(wo) - 1 : lane);
+            }
+            const int mv = inwin ? decide<ASYNC, KI>(a, v, c, kv, bv, starter && hx != NO_CAND, hg, hx, hS) : 0;
+            my_moves += mv;
+            if (a.mark) {  // the window's neighbour ids are still in registers
+                const int mvj = __shfl_sync(FULL, mv, j);
+                if (has_edge && mvj) a.mark[nbr] = 1;
+            }
+            __syncwarp();  // s_sc2[buf] is zeroed again two windows on
+            if (!more) break;
+            G = Gn;
+            nbr = nbr_n;
+            x = x_n;
+            buf ^= 1;
+        }
+#else
         int base = 0;
         while (base < nvalid) {
             const int32_t base_off = __shfl_sync(FULL, excl, base);
@@ -371,6 +497,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             base = end;
             __syncwarp();
         }
+#endif
     }
     flush_moves(a, my_moves);
 }

@@ -2415,10 +2415,26 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const int64_t Tg = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), 513);
     int64_t Tw = std::min<int64_t>(std::max<int64_t>(deg_threshold, SMALL_MAX + 1), WIN_W);
     if (!use_window || 2 * n > (1LL << LABEL_BITS)) Tw = SMALL_MAX + 1;  // window keys need ids < 2^27
+    int P = 1;
+    if (ASYNC && chunks > 0) P = chunks;
+    else if (ASYNC) {  // ~4M / F sub-rounds, at most 64 (small graphs need the ordering:
+                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative);
+                       // chunks < 0: at least -chunks (driver: rounds after the first)
+        const int64_t f = std::max<int64_t>(nF, 1);
+        P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
+        if (chunks < 0) P = std::max(P, -chunks);
+    }
     BinEdges be;
     const char* et = getenv("LCC_TINY");  // 0: the warp-window kernel takes degrees 1..32 too
     const int64_t tiny_max = (et && et[0] == '0') ? 0 : TINY_MAX;
-    be.hi[0] = 0;                 // isolated vertices: only the fresh-singleton option
+    // Small frontiers run as up to 64 ordered sub-rounds of small kernels
+    // whose device-side latency dominates: there, neighbouring bins share a
+    // kernel (isolated vertices ride in the thread-per-vertex bin -- same
+    // arithmetic at degree 0 -- and each pair of table bins takes the larger
+    // table), four kernels fewer per sub-round.  LCC_MERGE_BINS=0 disables.
+    const char* emb = getenv("LCC_MERGE_BINS");
+    const bool merge = P > 1 && nF < (1 << 18) && !(emb && emb[0] == '0');
+    be.hi[0] = (merge && tiny_max > 0) ? -1 : 0;  // isolated vertices: only the fresh-singleton option
     be.hi[1] = tiny_max;          // thread per vertex
     be.hi[2] = SMALL_MAX;         // warp-packed windows
     be.hi[3] = Tw - 1;
@@ -2429,6 +2445,11 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     be.hi[8] = std::min<int64_t>(4096, large_min);
     be.hi[9] = std::min<int64_t>(MED_MAX, large_min);
     be.hi[10] = INT64_MAX;
+    if (merge) {  // empty bins 4, 6, 8: their vertices go to bins 5, 7, 9
+        be.hi[4] = be.hi[3];
+        be.hi[6] = be.hi[5];
+        be.hi[8] = be.hi[7];
+    }
 
     if (hprobe.on && getenv("LCC_TRACE_SYNC")) {  // device work queued before this round
         LCC_CUDA(cudaStreamSynchronize(s));
@@ -2500,15 +2521,6 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const long long launches0 = launch_counter();
     float kms = 0.f;
 
-    int P = 1;
-    if (ASYNC && chunks > 0) P = chunks;
-    else if (ASYNC) {  // ~4M / F sub-rounds, at most 64 (small graphs need the ordering:
-                       // 4 sub-rounds on a 4K-vertex R-MAT drove the objective negative);
-                       // chunks < 0: at least -chunks (driver: rounds after the first)
-        const int64_t f = std::max<int64_t>(nF, 1);
-        P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
-        if (chunks < 0) P = std::max(P, -chunks);
-    }
     WindowPlan wp;
     if (hc[3] > 0) plan_windows(g.indptr, lists.get() + binstart[3], (int64_t)hc[3], wp, s);
     const int64_t nL = (int64_t)hc[NBINS - 1];

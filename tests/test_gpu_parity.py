@@ -571,3 +571,23 @@ def test_compress_fast_path_identical(wkind, monkeypatch):
             assert np.array_equal(f[3], lvl0.graph.weights)
         else:
             np.testing.assert_allclose(f[3], lvl0.graph.weights, rtol=1e-12)
+
+
+def test_integer_mass_image_exact(monkeypatch):
+    """The uint32 mass image (run_round) is exact: identical decisions with it
+    and without it (LCC_KINT=0); non-integral k falls back to fp64 masses and
+    still matches the oracle bit for bit."""
+    rng = np.random.default_rng(33)
+    hg, _ = lfr_like(n=40_000, seed=6)
+    g = og(hg)
+    deg = np.diff(g.indptr).astype(np.float64)
+    for k in (deg, deg * 0.5 + 0.25):
+        lam = 1.0 / (2 * g.m)
+        C, K = clustered_state(rng, g.n, 3000, k)
+        D0, m0, c0 = O.sync_round(g, k, lam, C, K)
+        outs = []
+        for flag in ("1", "0"):
+            monkeypatch.setenv("LCC_KINT", flag)
+            outs.append(gpu_sync_round(hg, k, lam, C, K))
+        for D1, m1, c1 in outs:
+            assert np.array_equal(D0, D1) and c0 == c1

@@ -591,3 +591,17 @@ def test_integer_mass_image_exact(monkeypatch):
             outs.append(gpu_sync_round(hg, k, lam, C, K))
         for D1, m1, c1 in outs:
             assert np.array_equal(D0, D1) and c0 == c1
+
+
+@pytest.mark.parametrize("nclus", [3, 40, 20_000])
+def test_hub_buckets_multipass_exact(nclus):
+    """Hub bucket path (degree > 10240): buckets holding more entries than
+    half a table (few clusters among a hub's neighbours) are aggregated in
+    several passes; decisions stay bit-exact with the oracle."""
+    rng = np.random.default_rng(nclus)
+    hg = hub_graph(rng, 60_000, [11, 12_345], [30_000, 45_000], base_p=0.0001)
+    g = og(hg)
+    C, K = clustered_state(rng, g.n, nclus)
+    D0, m0, c0 = O.sync_round(g, None, 0.3, C, K)
+    D1, m1, c1 = gpu_sync_round(hg, None, 0.3, C, K)
+    assert np.array_equal(D0, D1) and c0 == c1

@@ -1480,6 +1480,10 @@ constexpr int HS_THREADS = 256;             // scatter CTA
 constexpr int HB_CAP = LCC_HB_CAP;      // table slots per bucket CTA
 constexpr int HB_BE = HB_CAP / 2;       // target entries per bucket
 constexpr int HB_MAXB = 256;            // buckets per hub (more -> larger buckets, multi-pass)
+#ifndef LCC_HB_FLAT
+#define LCC_HB_FLAT 1                   // bucket inserts flat over the bucket's entries
+#endif
+constexpr int HB_MAXIT = 1024;          // items per hub for the flat walk (2M edges)
 
 template <class WT>
 struct HubEntry {
@@ -1607,6 +1611,7 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
     __shared__ double s_g[HB_THREADS / 32], s_S[HB_THREADS / 32];
     __shared__ int32_t s_x[HB_THREADS / 32];
     __shared__ int64_t s_cnt;
+    __shared__ int32_t s_pref[LCC_HB_FLAT ? HB_MAXIT + 1 : 1];
     SmemTable<false> tab;
     tab.init_cap(smem, HB_CAP);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1623,26 +1628,73 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
         const double bb = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
         const int64_t i0 = P.item_off[li], i1 = P.item_off[li + 1];
         // entries of this bucket over the hub's items
-        if (tid == 0) s_cnt = 0;
-        __syncthreads();
-        int64_t mine = 0;
-        for (int64_t it = i0 + tid; it < i1; it += HB_THREADS)
-            mine += P.ioff[it * P.stride + b + 1] - P.ioff[it * P.stride + b];
-        for (int d = 16; d; d >>= 1) mine += __shfl_xor_sync(FULL, mine, d);
-        if (lane == 0 && mine) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)mine);
-        __syncthreads();
-        const int64_t cnt = s_cnt;
+        const int64_t nit = i1 - i0;
+        const bool flat = LCC_HB_FLAT && nit <= HB_MAXIT;
+        int64_t cnt;
+        if (flat) {
+            // per-item counts, prefix-summed in shared memory, so the inserts
+            // run over the bucket's entries as one flat range (full lanes even
+            // when a bucket holds a few entries of each of ~200 items)
+            for (int64_t q = tid; q < nit; q += HB_THREADS) {
+                const int64_t it = i0 + q;
+                s_pref[q + 1] = P.ioff[it * P.stride + b + 1] - P.ioff[it * P.stride + b];
+            }
+            if (tid == 0) s_pref[0] = 0;
+            __syncthreads();
+            if (tid < 32) {
+                int carry = 0;
+                for (int64_t b0 = 1; b0 <= nit; b0 += 32) {
+                    const int64_t q = b0 + lane;
+                    const int val = q <= nit ? s_pref[q] : 0;
+                    int incl = val;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int y = __shfl_up_sync(FULL, incl, d);
+                        if (lane >= d) incl += y;
+                    }
+                    if (q <= nit) s_pref[q] = carry + incl;
+                    carry += __shfl_sync(FULL, incl, 31);
+                }
+            }
+            __syncthreads();
+            cnt = s_pref[nit];
+        } else {
+            if (tid == 0) s_cnt = 0;
+            __syncthreads();
+            int64_t mine = 0;
+            for (int64_t it = i0 + tid; it < i1; it += HB_THREADS)
+                mine += P.ioff[it * P.stride + b + 1] - P.ioff[it * P.stride + b];
+            for (int d = 16; d; d >>= 1) mine += __shfl_xor_sync(FULL, mine, d);
+            if (lane == 0 && mine) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)mine);
+            __syncthreads();
+            cnt = s_cnt;
+        }
         const uint32_t R = (uint32_t)max64(1, (2 * cnt + HB_CAP - 1) / HB_CAP);
         const uint32_t cap = (uint32_t)min64(HB_CAP, (2 * ((cnt + R - 1) / R) + 31) & ~31LL);
         double bg = -INFINITY, bS = 0.0;
         int32_t bx = NO_CAND;
         for (uint32_t r = 0; r < R; ++r) {
-            // insert: warp w walks items w, w+8, ...; lanes over the item's range
-            for (int64_t it = i0 + wid; it < i1; it += HB_THREADS / 32) {
-                const int lo = P.ioff[it * P.stride + b], hi = P.ioff[it * P.stride + b + 1];
-                const T* src = static_cast<const T*>(P.ent) + it * LARGE_CHUNK;
-                for (int q = lo + lane; q < hi; q += 32) {
-                    const T e = src[q];
+            // insert: flat over the bucket's entries (item found by binary
+            // search of the prefix), or warp w over items w, w+8, ...
+            const int64_t nouter = flat ? 1 : nit;
+            for (int64_t oi = flat ? 0 : wid; oi < nouter; oi += flat ? 1 : HB_THREADS / 32) {
+                const int64_t it0 = i0 + oi;
+                const int lo = flat ? 0 : P.ioff[it0 * P.stride + b];
+                const int hi = flat ? (int)cnt : P.ioff[it0 * P.stride + b + 1];
+                const int step = flat ? HB_THREADS : 32;
+                for (int q = lo + (flat ? tid : lane); q < hi; q += step) {
+                    T e;
+                    if (flat) {
+                        int l = 0, u = (int)nit;  // last item with s_pref[item] <= q
+                        while (u - l > 1) {
+                            const int m = (l + u) >> 1;
+                            if (s_pref[m] <= q) l = m; else u = m;
+                        }
+                        const int64_t it = i0 + l;
+                        e = static_cast<const T*>(P.ent)[it * LARGE_CHUNK + P.ioff[it * P.stride + b] + (q - s_pref[l])];
+                    } else {
+                        e = static_cast<const T*>(P.ent)[it0 * LARGE_CHUNK + q];
+                    }
                     const int32_t x = E::label(e);
                     if (R > 1 && hub_pass(x, R) != r) continue;
                     uint32_t h = slot_of(x, cap);

@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the vertex-sharded NCCL driver even at world size 1 (exercises the N>1 path on one GPU)")
     return ap.parse_args()
 
 
@@ -535,6 +537,11 @@ def run_sharded(args):
     from paper_2108_01731_b200.dist import CudaBackend, ShardStats, make_part, partition_bounds, sharded_best_moves, sharded_parallel_cc
 
     ws, rank, lrank = dist_init()
+    # NCCL may print its version banner on fd 1 at communicator creation:
+    # route fd 1 to stderr for the run and write the JSON line to the saved fd
+    json_fd = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
     torch.cuda.set_device(lrank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
     lib = _lib.load()
@@ -613,7 +620,7 @@ def run_sharded(args):
                                       "parallelism": f"vertex-sharded x{ws} (NCCL all-gather of owned labels)"}),
                "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clk.summary()}
-        print(json.dumps(out), flush=True)
+        os.write(json_fd, (json.dumps(out) + "\n").encode())
     dist.destroy_process_group()
     return 0
 
@@ -622,7 +629,7 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
         return run_sharded(args)
     return run_ours(args)
 

@@ -32,6 +32,9 @@ the sm_100a C ABI).  Tests drive the same driver with a CPU backend over
 from __future__ import annotations
 
 import ctypes
+import os
+import sys
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -51,11 +54,21 @@ def partition_bounds(indptr: np.ndarray, parts: int) -> np.ndarray:
     Returns bounds[parts+1]; rank r owns [bounds[r], bounds[r+1])."""
     indptr = np.asarray(indptr, dtype=np.int64)
     n = indptr.size - 1
-    work = indptr + np.arange(n + 1, dtype=np.int64)  # vertices + edges prefix
-    total = work[-1]
+    # work(i) = indptr[i] + i (vertices + edges prefix) is increasing: bisect
+    # it per target instead of materialising it (n is up to 65M on the host)
+    total = int(indptr[-1]) + n
     targets = (total * np.arange(1, parts, dtype=np.float64) / parts).astype(np.int64)
-    inner = np.searchsorted(work, targets, side="left")
-    return np.concatenate([[0], inner, [n]]).astype(np.int64)
+    inner = []
+    for t in targets.tolist():     # first i with work(i) >= t (searchsorted "left")
+        lo, hi = 0, n + 1
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if int(indptr[mid]) + mid < t:
+                lo = mid + 1
+            else:
+                hi = mid
+        inner.append(lo)
+    return np.asarray([0] + inner + [n], dtype=np.int64)
 
 
 @dataclass
@@ -77,10 +90,11 @@ class PartGraph:
 
 def make_part(indptr, indices, weights, total_weight, lo: int, hi: int, device) -> PartGraph:
     """Build the owned-rows view from full host (numpy) or torch CSR arrays."""
-    ip = torch.as_tensor(np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr), dtype=torch.int64)
+    ip = indptr if isinstance(indptr, torch.Tensor) else torch.as_tensor(np.asarray(indptr, dtype=np.int64))
     n = ip.numel() - 1
     s, e = int(ip[lo]), int(ip[hi])
-    pip = (ip.clamp(min=s, max=e) - s).to(device)
+    # upload first (a pinned host indptr copies at full speed), clamp on the device
+    pip = ip.to(device=device, dtype=torch.int64).clamp(min=s, max=e) - s
     ind = indices[s:e] if isinstance(indices, torch.Tensor) else torch.as_tensor(np.asarray(indices[s:e]))
     ind = ind.to(device=device, dtype=torch.int32).contiguous()
     w = None
@@ -95,6 +109,8 @@ def make_part(indptr, indices, weights, total_weight, lo: int, hi: int, device) 
 # ---------------------------------------------------------------------------
 
 class CudaBackend:
+    fused_nbr_mark = True
+
     def __init__(self, device=None):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.lib = _lib.load()
@@ -112,11 +128,14 @@ class CudaBackend:
     def _p(k, lam) -> _lib.LccParams:
         return _lib.LccParams(None if k is None else k.data_ptr(), float(lam))
 
-    def round(self, part, k, lam, C, K, frontier, schedule, thr, chunks):
+    def round(self, part, k, lam, C, K, frontier, schedule, thr, chunks, nbr_mark=None):
         """Returns (labels, moved, count): sync -> D; async -> C updated in a
-        copy with masses in a 2n copy of K."""
+        copy with masses in a 2n copy of K.  ``nbr_mark`` (n bytes, optional)
+        receives the VertexNeighbors marks of this rank's movers, fused into
+        the round."""
         n = part.n
         g, p = self._g(part), self._p(k, lam)
+        nm = None if nbr_mark is None else nbr_mark.data_ptr()
         moved = torch.empty(n, dtype=torch.uint8, device=self.device)
         cnt = ctypes.c_int64()
         fr = frontier.to(self.device, torch.int32).contiguous()
@@ -124,7 +143,7 @@ class CudaBackend:
             D = torch.empty(n, dtype=torch.int32, device=self.device)
             _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), C.data_ptr(), K.data_ptr(),
                                                      fr.data_ptr() if fr.numel() else None, fr.numel(),
-                                                     _lib.SYNC, thr, chunks, D.data_ptr(), moved.data_ptr(), None,
+                                                     _lib.SYNC, thr, chunks, D.data_ptr(), moved.data_ptr(), nm,
                                                      ctypes.byref(cnt), None, stream_ptr()))
             return D, moved, cnt.value
         Cw = C.clone()
@@ -132,7 +151,7 @@ class CudaBackend:
         K2[:n] = K
         _lib.check(self.lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), Cw.data_ptr(), K2.data_ptr(),
                                                  fr.data_ptr() if fr.numel() else None, fr.numel(),
-                                                 _lib.ASYNC, thr, chunks, None, moved.data_ptr(), None,
+                                                 _lib.ASYNC, thr, chunks, None, moved.data_ptr(), nm,
                                                  ctypes.byref(cnt), None, stream_ptr()))
         return Cw, moved, cnt.value
 
@@ -178,8 +197,16 @@ class CudaBackend:
         from .louvain_par import parallel_cc
         from .objective import ClusteringParams
         n = indptr.numel() - 1
+        if weights is not None and weights.dtype != torch.int32:
+            weights = weights.to(self.device, torch.float64)
+            # integral coarse weights (multi-edge counts of an unweighted or
+            # integer-weighted level 0) run on the exact uint32 tables, as in
+            # the single-process driver
+            if weights.numel() and bool((weights == weights.round()).all()) and \
+                    float(weights.min()) >= 0 and float(weights.max()) < 2.0 ** 31:
+                weights = weights.to(torch.int32)
         g = DeviceGraph(n, indices.numel() // 2, indptr.to(self.device), indices.to(self.device, torch.int32),
-                        None if weights is None else weights.to(self.device, torch.float64), float(total_weight))
+                        None if weights is None else weights.to(self.device), float(total_weight))
         p = ClusteringParams.__new__(ClusteringParams)
         p.lam, p.k = float(lam), k
         return parallel_cc(g, p, opts).assignment
@@ -204,6 +231,8 @@ def _max_(t: torch.Tensor, group):
 
 
 def _sum_int(x: int, device, group) -> int:
+    if dist.get_world_size(group) == 1:
+        return int(x)
     t = torch.tensor([x], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return int(t.item())
@@ -254,14 +283,24 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
     any_moved = False
     deg = (part.indptr[1:] - part.indptr[:-1])
     num_iter = int(opts.num_iter)
+    policy = FrontierPolicy(opts.frontier_policy)
+    # VertexNeighbors: the round marks its movers' neighbours itself (the
+    # fused nbr_mark of lcc_best_moves_round); backends without it (the test
+    # oracle) fall back to frontier_mask
+    fused = policy == FrontierPolicy.VertexNeighbors and getattr(backend, "fused_nbr_mark", False)
     for it in range(num_iter):
         if _sum_int(int(F.numel()), dev, group) == 0:
             break
-        labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
-                                           int(opts.async_chunks))
+        mark = torch.empty(n, dtype=torch.uint8, device=dev) if fused and it + 1 < num_iter else None
+        if mark is None:
+            labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
+                                               int(opts.async_chunks))
+        else:
+            labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
+                                               int(opts.async_chunks), nbr_mark=mark)
         if stats is not None:
             stats.rounds += 1
-            stats.edges_scanned += int(deg[F.long()].sum().item()) if F.numel() else 0
+            stats.edges_scanned += int(deg.index_select(0, F).sum().item()) if F.numel() else 0
         total = _sum_int(int(cnt), dev, group)
         if stats is not None:
             stats.moves += total
@@ -274,9 +313,11 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
         lab = _allgather_owned(labels, part, group)
         Cn, Kn = backend.apply(lab, 2 * n, k)   # canonical labels + masses, replicated
         if it + 1 < num_iter:  # the next frontier is only needed by a next iteration
-            policy = FrontierPolicy(opts.frontier_policy)
             if policy == FrontierPolicy.AllVertices:
                 F = owned
+            elif mark is not None:
+                _max_(mark, group)
+                F = (torch.nonzero(mark[part.lo:part.hi]).flatten() + part.lo).to(torch.int32)
             else:
                 mv = (lab != C).to(torch.uint8)
                 mask = backend.frontier_mask(part, int(policy), mv, C, Cn)
@@ -290,6 +331,8 @@ def _gather_coarse(cn, cptr, cind, cw, device, group):
     """All-gather partial coarse CSRs; rank 0 merges duplicate (a, b)
     entries and returns the coarse CSR (other ranks return None)."""
     world = dist.get_world_size(group)
+    if world == 1:
+        return cptr, cind, cw, float(cw.sum().item()) / 2.0
     rows = torch.repeat_interleave(torch.arange(cn, device=device, dtype=torch.int64), cptr[1:] - cptr[:-1])
     local = torch.stack([rows, cind.to(torch.int64)]).contiguous()
     size = torch.tensor([local.shape[1]], dtype=torch.int64, device=device)
@@ -319,6 +362,23 @@ def _gather_coarse(cn, cptr, cind, cw, device, group):
     return indptr, b.to(torch.int32), ws, float(ws.sum().item()) / 2.0
 
 
+class _Trace:
+    """Per-phase wall times of the sharded driver on stderr (LCC_TRACE=1)."""
+
+    def __init__(self, rank, dev):
+        self.on = os.environ.get("LCC_TRACE", "0") not in ("", "0")
+        self.rank, self.dev = rank, dev
+        self.t = time.perf_counter()
+
+    def __call__(self, what):
+        if not self.on:
+            return
+        torch.cuda.synchronize(self.dev)
+        t = time.perf_counter()
+        print(f"[lcc dist r{self.rank}] {what}: {1e3 * (t - self.t):.1f} ms", file=sys.stderr, flush=True)
+        self.t = t
+
+
 def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, backend=None, group=None,
                         stats: ShardStats | None = None) -> torch.Tensor:
     """parallel_cc with level 0 sharded over the process
@@ -328,6 +388,7 @@ def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, ba
     backend = backend or CudaBackend()
     dev = backend.device
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    tr = _Trace(rank, dev)
     ip = np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr, dtype=np.int64)
     bounds = partition_bounds(ip, world)
     part = make_part(indptr, indices, weights, total_weight, int(bounds[rank]), int(bounds[rank + 1]), dev)
@@ -336,20 +397,26 @@ def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, ba
         k = torch.as_tensor(k, dtype=torch.float64).to(dev)
     C = torch.arange(n, dtype=torch.int32, device=dev)
     K = torch.ones(n, dtype=torch.float64, device=dev) if k is None else k.clone()
+    tr("upload")
     C, K, moved = sharded_best_moves(part, k, lam, C, K, opts, backend, group, stats)
+    tr("level 0")
     if not moved:
         return C
     cn, cptr, cind, cw, ck, mapping = backend.compress(part, k, lam, C, K)
+    tr("compress")
     if cn == n:
         return C                                      # no size reduction
     merged = _gather_coarse(cn, cptr, cind, cw, dev, group)
+    tr("gather coarse")
     Cc = torch.empty(cn, dtype=torch.int32, device=dev)
     if rank == 0:
         c_indptr, c_ind, c_w, c_tot = merged
         Cc = backend.parallel_cc(c_indptr, c_ind, c_w, c_tot, ck, lam, opts).to(torch.int32)
+    tr("coarse levels")
     dist.broadcast(Cc, src=0, group=group)
     C, K = backend.flatten(mapping, Cc, k)
     if opts.refine:
         C, K, _ = sharded_best_moves(part, k, lam, C, K, opts, backend, group, stats)
+    tr("flatten + refine")
     return C
 

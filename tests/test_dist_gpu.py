@@ -45,11 +45,16 @@ def run(world, backend_name, hg, lam, opts_kw):
 
 
 @pytest.mark.parametrize("world,backend_name", [(2, "gloo"), (1, "nccl")])
-def test_sharded_cuda_sync_exact(world, backend_name):
+@pytest.mark.parametrize("policy", ["vertex", "cluster"])
+def test_sharded_cuda_sync_exact(world, backend_name, policy):
+    """VertexNeighbors runs the fused neighbour marks of the round,
+    ClusterNeighbors the separate compute_frontier; both bit-exact."""
+    from paper_2108_01731_b200.louvain_par import FrontierPolicy
+    fp = FrontierPolicy.VertexNeighbors if policy == "vertex" else FrontierPolicy.ClusterNeighbors
     hg, _ = sbm(seed=1)
     g = O.as_graph(hg)
-    ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC))
-    r = run(world, backend_name, hg, 0.85, dict(schedule="sync"))
+    ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC, frontier=int(fp)))
+    r = run(world, backend_name, hg, 0.85, dict(schedule="sync", frontier_policy=fp))
     assert np.array_equal(r["C"], ref)
 
 

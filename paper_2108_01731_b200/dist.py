@@ -327,35 +327,44 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
     return C, K, any_moved
 
 
-def _gather_coarse(cn, cptr, cind, cw, device, group):
-    """All-gather partial coarse CSRs; rank 0 merges duplicate (a, b)
-    entries and returns the coarse CSR (other ranks return None)."""
+def _gather_coarse(cn, cptr, cind, cw, device, group, integral=False):
+    """Gather the partial coarse CSRs on rank 0 (NCCL gather, not an
+    all-gather: only rank 0 runs the coarse levels); rank 0 merges duplicate
+    (a, b) entries and returns the coarse CSR (other ranks return None).
+    Ids travel as int32 (cn < 2^31) and, when the level-0 weights are
+    integral (unweighted or LCC_W_U32), weights as int32 too: 12 bytes per
+    entry instead of 24."""
     world = dist.get_world_size(group)
     if world == 1:
         return cptr, cind, cw, float(cw.sum().item()) / 2.0
-    rows = torch.repeat_interleave(torch.arange(cn, device=device, dtype=torch.int64), cptr[1:] - cptr[:-1])
-    local = torch.stack([rows, cind.to(torch.int64)]).contiguous()
+    rank = dist.get_rank(group)
+    rows = torch.repeat_interleave(torch.arange(cn, device=device, dtype=torch.int32), cptr[1:] - cptr[:-1])
+    local = torch.stack([rows, cind.to(torch.int32)]).contiguous()
     size = torch.tensor([local.shape[1]], dtype=torch.int64, device=device)
     sizes = [torch.zeros_like(size) for _ in range(world)]
     dist.all_gather(sizes, size, group=group)
-    mx = int(max(s.item() for s in sizes))
-    pad_i = torch.full((2, mx), -1, dtype=torch.int64, device=device)
+    sizes = [int(x.item()) for x in sizes]
+    mx = max(sizes)
+    wdt = torch.int32 if integral else torch.float64
+    pad_i = torch.full((2, mx), -1, dtype=torch.int32, device=device)
     pad_i[:, :local.shape[1]] = local
-    pad_w = torch.zeros(mx, dtype=torch.float64, device=device)
-    pad_w[:cw.numel()] = cw
-    gi = [torch.empty_like(pad_i) for _ in range(world)]
-    gw = [torch.empty_like(pad_w) for _ in range(world)]
-    dist.all_gather(gi, pad_i, group=group)
-    dist.all_gather(gw, pad_w, group=group)
-    if dist.get_rank(group) != 0:
+    pad_w = torch.zeros(mx, dtype=wdt, device=device)
+    pad_w[:cw.numel()] = cw.to(wdt)
+    gi = [torch.empty_like(pad_i) for _ in range(world)] if rank == 0 else None
+    gw = [torch.empty_like(pad_w) for _ in range(world)] if rank == 0 else None
+    dist.gather(pad_i, gi, dst=0, group=group)
+    dist.gather(pad_w, gw, dst=0, group=group)
+    if rank != 0:
         return None  # the coarse levels run on rank 0 only
-    ab = torch.cat([g[:, :int(s.item())] for g, s in zip(gi, sizes)], dim=1)
-    w = torch.cat([g[:int(s.item())] for g, s in zip(gw, sizes)])
+    ab = torch.cat([g[:, :sz] for g, sz in zip(gi, sizes)], dim=1).to(torch.int64)
+    w = torch.cat([g[:sz] for g, sz in zip(gw, sizes)])
+    del gi, gw
     key = ab[0] * max(cn, 1) + ab[1]
+    del ab
     key, order = torch.sort(key, stable=True)
-    w = w[order]
+    w = w[order].to(torch.int64 if integral else torch.float64)
     uk, inv = torch.unique_consecutive(key, return_inverse=True)
-    ws = torch.zeros(uk.numel(), dtype=torch.float64, device=device).index_add_(0, inv, w)
+    ws = torch.zeros(uk.numel(), dtype=w.dtype, device=device).index_add_(0, inv, w).to(torch.float64)
     a, b = uk // max(cn, 1), uk % max(cn, 1)
     indptr = torch.zeros(cn + 1, dtype=torch.int64, device=device)
     indptr[1:] = torch.cumsum(torch.bincount(a, minlength=cn), 0)
@@ -406,7 +415,8 @@ def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, ba
     tr("compress")
     if cn == n:
         return C                                      # no size reduction
-    merged = _gather_coarse(cn, cptr, cind, cw, dev, group)
+    integral = part.weights is None or part.weights.dtype == torch.int32
+    merged = _gather_coarse(cn, cptr, cind, cw, dev, group, integral)
     tr("gather coarse")
     Cc = torch.empty(cn, dtype=torch.int32, device=dev)
     if rank == 0:

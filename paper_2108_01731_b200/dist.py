@@ -256,6 +256,8 @@ def _allgather_owned(vals: torch.Tensor, part, group) -> torch.Tensor:
     """The owned slice of ``vals`` from every rank, concatenated in rank order
     (the ranges are contiguous and ordered, so this is the full array): one
     NCCL all-gather of padded equal-size chunks."""
+    if dist.get_world_size(group) == 1:
+        return vals
     sizes = _owned_sizes(part, group)
     mx = max(sizes)
     buf = torch.empty(mx, dtype=vals.dtype, device=vals.device)

@@ -293,7 +293,9 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
     for it in range(num_iter):
         if _sum_int(int(F.numel()), dev, group) == 0:
             break
-        mark = torch.empty(n, dtype=torch.uint8, device=dev) if fused and it + 1 < num_iter else None
+        # passed on the last iteration too: the round-1 async call measured
+        # 10.7 ms with the marks and 11.9 ms without (tools/round_ab.py)
+        mark = torch.empty(n, dtype=torch.uint8, device=dev) if fused else None
         if mark is None:
             labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
                                                int(opts.async_chunks))

@@ -1,6 +1,7 @@
 """A/B of one async round-1 call through CudaBackend.round at config 4:
 explicit frontier vs none (all vertices), with and without the fused
-neighbour marks.  Run on a GPU box: python tools/round_ab.py"""
+neighbour marks.  Run on a GPU box: python tools/round_ab.py
+(AB_SYNC=1: the synchronous round instead)"""
 import ctypes
 import os
 import sys
@@ -23,6 +24,10 @@ mark = torch.empty(n, dtype=torch.uint8, device="cuda")
 moved = torch.empty(n, dtype=torch.uint8, device="cuda")
 
 
+D = torch.empty(n, dtype=torch.int32, device="cuda")
+SCHED = _lib.SYNC if os.environ.get("AB_SYNC") else _lib.ASYNC
+
+
 def raw(frontier, use_mark):
     C = iota.clone()
     K2 = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
@@ -30,8 +35,8 @@ def raw(frontier, use_mark):
     g, p = be._g(part), be._p(None, 0.85)
     cnt = ctypes.c_int64()
     _lib.check(lib.lcc_best_moves_round(ctypes.byref(g), ctypes.byref(p), C.data_ptr(), K2.data_ptr(),
-                                        None if frontier is None else frontier.data_ptr(), n, _lib.ASYNC,
-                                        1000, 0, None, moved.data_ptr(), mark.data_ptr() if use_mark else None,
+                                        None if frontier is None else frontier.data_ptr(), n, SCHED,
+                                        1000, 0, D.data_ptr() if SCHED == _lib.SYNC else None, moved.data_ptr(), mark.data_ptr() if use_mark else None,
                                         ctypes.byref(cnt), None, stream_ptr()))
 
 

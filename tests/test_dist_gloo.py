@@ -51,6 +51,21 @@ def test_partition_bounds_balanced():
     assert work.max() < 1.2 * work.mean()
 
 
+def test_partition_bounds_matches_prefix_search():
+    """The bisection over work(i) = indptr[i] + i equals a searchsorted over
+    the materialised prefix, including empty graphs, more parts than
+    vertices and runs of isolated vertices."""
+    rng = np.random.default_rng(7)
+    for n in [0, 1, 3, 100, 5000]:
+        for parts in [1, 2, 3, 8]:
+            deg = rng.integers(0, 20, n) * (rng.random(n) < 0.7)
+            ip = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+            work = ip + np.arange(n + 1)
+            t = (work[-1] * np.arange(1, parts, dtype=np.float64) / parts).astype(np.int64)
+            ref = np.concatenate([[0], np.searchsorted(work, t, side="left"), [n]])
+            assert np.array_equal(partition_bounds(ip, parts), ref), (n, parts)
+
+
 @pytest.mark.parametrize("policy", ["vertex-nbrs", "all", "cluster-nbrs"])
 def test_sharded_sync_equals_single_process(policy):
     hg, _ = sbm(seed=1)

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define LCC_ABI_VERSION 2
+#define LCC_ABI_VERSION 3
 
 typedef enum {
     LCC_OK = 0,
@@ -173,6 +173,12 @@ lcc_status lcc_par_flatten(int64_t n, const int32_t* mapping, const int32_t* Cc,
 lcc_status lcc_cc_objective(const lcc_graph* g, const lcc_params* p,
                             const int32_t* C, double* objective, void* stream);
 
+/* ---- weighted_degrees (graph.py:57-61) -----------------
+ * k[v] = sum of the weights of v's CSR row, summed left to right in fp64
+ * (the reference's np.add.at order: bit-identical).  The k_v of the
+ * modularity mapping (modularity_params).                                  */
+lcc_status lcc_weighted_degrees(const lcc_graph* g, double* k, void* stream);
+
 /* ---- parallel_cc (Alg. 1) ---------------------
  * Full multi-level clustering.  C_out[n] receives canonical labels.        */
 lcc_status lcc_parallel_cc(const lcc_graph* g, const lcc_params* p,
@@ -208,6 +214,33 @@ lcc_status lcc_gen_powerlaw_communities(int64_t n, int64_t samples, double mu,
 lcc_status lcc_build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u,
                                     const int32_t* v, int64_t* indptr,
                                     int32_t* indices, int64_t* nnz, void* stream);
+
+/* build_graph (reference graph.py:79-164) on the device.  Edge list
+ * (u[i], v[i], w[i]) with int64 ids (w == NULL: all 1.0): self loops dropped,
+ * same-orientation parallel edges summed in ascending weight order, the two
+ * orientations of a pair averaged, both directions emitted with rows sorted;
+ * every fp64 sum in numpy's order, so indptr / indices / weights and
+ * *total_weight are bit-identical to the reference's.  Ids must lie in
+ * [0, n) (lcc_edge_id_range gives n_seen = max id + 1; the reference's
+ * GraphError cases are LCC_ERR_INVALID).  indptr[n+1]; indices and weights
+ * must hold 2 * n_edges entries.  *m = undirected edge count (nnz = 2m);
+ * *unit_weights = 1 when every weight is 1.                                */
+lcc_status lcc_build_graph(int64_t n, int64_t n_edges, const int64_t* u, const int64_t* v,
+                           const double* w, int64_t* indptr, int32_t* indices, double* weights,
+                           int64_t* m, double* total_weight, int32_t* unit_weights, void* stream);
+/* Smallest and largest id over u[] and v[] (device reduce; n_edges == 0
+ * gives min 0, max -1).                                                     */
+lcc_status lcc_edge_id_range(int64_t n_edges, const int64_t* u, const int64_t* v,
+                             int64_t* min_id, int64_t* max_id, void* stream);
+
+/* COO -> CSR with duplicate (row, col) entries summed (the merge step of the
+ * sharded contraction: partial coarse rows arriving from several ranks).
+ * rows[i] in [0, n), cols[i] >= 0.  wtype LCC_W_NONE (each entry counts 1)
+ * or LCC_W_U32: uint32 sums in w_out; LCC_W_F64: double sums.  indptr[n+1];
+ * indices / w_out hold up to nnz entries; *nnz_out = merged entries.       */
+lcc_status lcc_coo_merge(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                         const void* w, int32_t wtype, int64_t* indptr, int32_t* indices,
+                         void* w_out, int64_t* nnz_out, void* stream);
 
 /* ---- eval -----------------------
  * Adjusted Rand index and normalised mutual information (arithmetic-mean

@@ -8,7 +8,7 @@ objective (``cc_objective``, ``modularity_params``, ``modularity_value``,
 sm_100a library ``_lib/liblcc_b200.so`` (C ABI: ``include/lcc_b200.h``).
 """
 from ._lib import NativeLibraryError
-from .graph import DeviceGraph, GraphError
+from .graph import DeviceGraph, GraphError, build_graph, build_graph_arrays
 from .objective import (Clustering, ClusteringParams, cc_objective, clustering_from_labels, modularity_params,
                         modularity_value, move_delta, rescaled_weight, singletons)
 from .louvain_par import (CompressedLevel, Frontier, FrontierPolicy, MoveBuffer, ParOptions, RunStats, Schedule,
@@ -16,7 +16,7 @@ from .louvain_par import (CompressedLevel, Frontier, FrontierPolicy, MoveBuffer,
                           par_flatten, parallel_cc, per_vertex_best_target)
 
 __all__ = [
-    "NativeLibraryError", "DeviceGraph", "GraphError", "Clustering", "ClusteringParams", "cc_objective",
+    "NativeLibraryError", "DeviceGraph", "GraphError", "build_graph", "build_graph_arrays", "Clustering", "ClusteringParams", "cc_objective",
     "clustering_from_labels", "modularity_params", "modularity_value", "move_delta", "rescaled_weight",
     "singletons", "CompressedLevel", "Frontier", "FrontierPolicy", "MoveBuffer", "ParOptions", "RunStats",
     "Schedule", "apply_moves", "best_moves_round", "compute_frontier", "frontier_from_mask", "par_best_moves", "release_memory",

@@ -24,8 +24,10 @@ EXPORTS = (
     "lcc_compute_frontier", "lcc_par_best_moves", "lcc_par_compress", "lcc_par_flatten",
     "lcc_cc_objective", "lcc_parallel_cc", "lcc_gen_rmat", "lcc_gen_powerlaw_communities",
     "lcc_build_csr_from_pairs", "lcc_frontier_from_mask", "lcc_release_memory",
-    "lcc_partition_scores", "lcc_avg_precision_recall", "lcc_cluster_stats",
+    "lcc_partition_scores", "lcc_avg_precision_recall", "lcc_cluster_stats", "lcc_weighted_degrees",
+    "lcc_build_graph", "lcc_edge_id_range", "lcc_coo_merge",
 )
+ABI_VERSION = 3
 
 
 class NativeLibraryError(RuntimeError):
@@ -96,6 +98,10 @@ def load() -> ctypes.CDLL:
         "lcc_gen_powerlaw_communities": (ctypes.c_int, [I64, I64, F64, P, P, P, I64, ctypes.c_uint64, P, P, pI64, P]),
         "lcc_build_csr_from_pairs": (ctypes.c_int, [I64, I64, P, P, P, P, pI64, P]),
         "lcc_partition_scores": (ctypes.c_int, [I64, P, P, pF64, pF64, P]),
+        "lcc_weighted_degrees": (ctypes.c_int, [G, P, P]),
+        "lcc_build_graph": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, pI64, pF64, pI32, P]),
+        "lcc_edge_id_range": (ctypes.c_int, [I64, P, P, pI64, pI64, P]),
+        "lcc_coo_merge": (ctypes.c_int, [I64, I64, P, P, P, I32, P, P, P, pI64, P]),
         "lcc_avg_precision_recall": (ctypes.c_int, [I64, P, I64, P, P, pF64, pF64, P]),
         "lcc_cluster_stats": (ctypes.c_int, [I64, P, pI64, pI64, pI64, pF64, P]),
     }
@@ -104,8 +110,8 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     ver = L.lcc_abi_version()
-    if ver != 2:
-        raise NativeLibraryError(f"ABI version mismatch: library {ver}, binding 1")
+    if ver != ABI_VERSION:
+        raise NativeLibraryError(f"ABI version mismatch: library {ver}, binding {ABI_VERSION}")
     _lib = L
     return L
 

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 SO = os.path.join(OUT_DIR, "liblcc_b200.so")
-SOURCES = ["best_moves.cu", "apply.cu", "contract.cu", "objective.cu", "gen.cu", "eval.cu", "driver.cu", "memory.cu", "capi.cu"]
+SOURCES = ["best_moves.cu", "apply.cu", "contract.cu", "objective.cu", "gen.cu", "eval.cu", "driver.cu", "memory.cu", "build.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",

@@ -3,7 +3,8 @@
 // apply_moves: the sync apply step and the async boundary
 //   reconcile.  Labels are canonicalised to the smallest member
 //   id (segmented min by 32-bit atomicMin), then K is rebuilt from scratch
-//   with fp64 RED (exact for integer-valued k, which covers every config).
+//   with fp64 RED (exact for integer-valued k, which covers every config);
+//   a non-integral k switches to a fixed-order segmented sum.
 // compute_frontier: AllVertices / VertexNeighbors / ClusterNeighbors
 //    as a byte mask scattered over the
 //   contributing vertices' neighbour lists by the edge-balanced map
@@ -37,13 +38,66 @@ __global__ void k_min_member(const int32_t* __restrict__ L, int32_t* minm, int64
     }
 }
 
+// fp64 RED per vertex: exact (so order free) while every k is an integer --
+// k = 1 or an unweighted degree, every BASELINE config.  A non-integral k
+// sets *nonint and the host redoes K in a fixed order (mass_fixed_order).
 __global__ void k_relabel_mass(const int32_t* __restrict__ L, const int32_t* __restrict__ minm,
-                               const double* __restrict__ k, int32_t* C, double* K, int64_t n) {
+                               const double* __restrict__ k, int32_t* C, double* K, int64_t n,
+                               unsigned* nonint) {
+    bool frac = false;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int32_t c = minm[L[v]];
         C[v] = c;
-        atomicAdd(K + c, k ? k[v] : 1.0);
+        const double x = k ? k[v] : 1.0;
+        frac |= x != floor(x) || fabs(x) >= 4503599627370496.0;  // 2^52: sums may round
+        atomicAdd(K + c, x);
     }
+    if (nonint && __any_sync(__activemask(), frac) && (threadIdx.x & 31) == 0) *nonint = 1u;
+}
+
+__global__ void k_gather_k(const int32_t* __restrict__ members, const double* __restrict__ k, int64_t n,
+                           double* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = k[members[i]];
+}
+
+__global__ void k_scatter_mass(const int32_t* __restrict__ ids, const double* __restrict__ sums,
+                               const int64_t* __restrict__ nruns, double* K) {
+    const int64_t r = *nruns;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x)
+        K[ids[i]] = sums[i];
+}
+
+// K[c] = sum of k over the members of c in a fixed order: members sorted by
+// (label, id) -- a stable radix sort of the labels over the ids -- then one
+// reduce-by-key.  Same inputs, same bits on every run (sync determinism,
+// SPEC.md:306) for any real-valued k.
+void mass_fixed_order(int64_t n, const int32_t* C, const double* k, double* K, cudaStream_t s) {
+    Buf<int32_t> lab(n, s), ids(n, s), ids_in(n, s), runs(n, s);
+    Buf<double> kv(n, s), sums(n, s);
+    Buf<int64_t> nruns(1, s);
+    fill_iota(ids_in.get(), n, s);
+    const int bits = std::max(1, bit_width((uint64_t)n));
+    size_t bytes = 0;
+    LCC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, C, lab.get(), ids_in.get(), ids.get(), n, 0, bits, s));
+    {
+        Buf<unsigned char> tmp(bytes, s);
+        LCC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, C, lab.get(), ids_in.get(), ids.get(), n, 0,
+                                                 bits, s));
+    }
+    k_gather_k<<<grid_for(n, 256), 256, 0, s>>>(ids.get(), k, n, kv.get());
+    LCC_LAUNCH_CHECK();
+    bytes = 0;
+    LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, lab.get(), runs.get(), kv.get(), sums.get(),
+                                            nruns.get(), cub::Sum(), n, s));
+    {
+        Buf<unsigned char> tmp(bytes, s);
+        LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, lab.get(), runs.get(), kv.get(), sums.get(),
+                                                nruns.get(), cub::Sum(), n, s));
+    }
+    LCC_CUDA(cudaMemsetAsync(K, 0, sizeof(double) * n, s));
+    k_scatter_mass<<<grid_for(n, 256), 256, 0, s>>>(runs.get(), sums.get(), nruns.get(), K);
+    LCC_LAUNCH_CHECK();
 }
 
 struct HasEdgesAndFlag {
@@ -112,8 +166,19 @@ void apply_moves(int64_t n, const int32_t* labels_in, int64_t label_range, const
     k_min_member<<<grid_for(n, 256), 256, 0, s>>>(labels_in, minm.get(), n);
     LCC_LAUNCH_CHECK();
     LCC_CUDA(cudaMemsetAsync(K, 0, sizeof(double) * n, s));
-    k_relabel_mass<<<grid_for(n, 256), 256, 0, s>>>(labels_in, minm.get(), k, C, K, n);
+    if (!k) {  // k = 1: integer sums, exact in any order
+        k_relabel_mass<<<grid_for(n, 256), 256, 0, s>>>(labels_in, minm.get(), k, C, K, n, nullptr);
+        LCC_LAUNCH_CHECK();
+        return;
+    }
+    Buf<unsigned> nonint(1, s);
+    LCC_CUDA(cudaMemsetAsync(nonint.get(), 0, sizeof(unsigned), s));
+    k_relabel_mass<<<grid_for(n, 256), 256, 0, s>>>(labels_in, minm.get(), k, C, K, n, nonint.get());
     LCC_LAUNCH_CHECK();
+    unsigned h = 0;
+    LCC_CUDA(cudaMemcpyAsync(&h, nonint.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    if (h) mass_fixed_order(n, C, k, K, s);
 }
 
 int64_t compute_frontier(const lcc_graph& g, int policy, const uint8_t* moved, const int32_t* C_old,

@@ -2678,8 +2678,9 @@ int64_t best_moves_round(const lcc_graph& g, const double* k, double lam, int32_
     LCC_REQUIRE(schedule == LCC_SYNC || schedule == LCC_ASYNC, "unknown schedule");
     LCC_REQUIRE(schedule == LCC_ASYNC || D != nullptr, "sync schedule needs D");
     LCC_REQUIRE(async_chunks >= -64, "async_chunks out of range");
-    if (!frontier) nF = g.n;
     if (g.n == 0) return 0;
+    // NULL = all vertices unless the caller asked for an empty frontier
+    // (nF == 0: D = C, moved / mark cleared, no kernels)
     const bool as = schedule == LCC_ASYNC;
     switch (g.weights ? g.wtype : LCC_W_NONE) {
         case LCC_W_NONE:

@@ -107,6 +107,7 @@ lcc::Options to_opts(const lcc_options* o) {
         r.num_iter = o->num_iter;
         r.deg_threshold = o->degree_threshold;
         r.async_chunks = o->async_chunks > 0 ? o->async_chunks : 0;  // 0 = auto
+        r.seed = o->seed;
     }
     return r;
 }
@@ -136,6 +137,10 @@ lcc_status lcc_best_moves_round(const lcc_graph* g, const lcc_params* p, int32_t
         check_params(p);
         LCC_REQUIRE(C && K && moved, "C, K and moved are required");
         LCC_REQUIRE(n_frontier >= 0 && n_frontier <= g->n, "frontier size out of range");
+        // frontier == NULL means V' = V only with n_frontier == n; an empty
+        // frontier (n_frontier == 0) is an empty round: D = C, no movers
+        LCC_REQUIRE(frontier || n_frontier == 0 || n_frontier == g->n,
+                    "frontier == NULL needs n_frontier == n (all vertices) or 0 (empty)");
         lcc::RoundStats rs;
         const int64_t cnt = lcc::best_moves_round(*g, p->k, p->lambda, C, K, frontier, n_frontier, schedule,
                                                   degree_threshold, async_chunks > 0 ? async_chunks : 0, D, moved,
@@ -239,6 +244,14 @@ lcc_status lcc_cc_objective(const lcc_graph* g, const lcc_params* p, const int32
     });
 }
 
+lcc_status lcc_weighted_degrees(const lcc_graph* g, double* k, void* stream) {
+    return guard([&] {
+        check_graph(g);
+        LCC_REQUIRE(g->n == 0 || k, "k is NULL");
+        lcc::weighted_degrees(*g, k, S(stream));
+    });
+}
+
 lcc_status lcc_parallel_cc(const lcc_graph* g, const lcc_params* p, const lcc_options* opts, int32_t* C_out,
                            lcc_stats* stats, void* stream) {
     return guard([&] {
@@ -276,6 +289,50 @@ lcc_status lcc_build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u
         LCC_REQUIRE(indptr && (n_pairs == 0 || (u && v && indices)), "NULL buffer");
         const int64_t r = lcc::build_csr_from_pairs(n, n_pairs, u, v, indptr, indices, S(stream));
         if (nnz) *nnz = r;
+    });
+}
+
+lcc_status lcc_edge_id_range(int64_t n_edges, const int64_t* u, const int64_t* v, int64_t* min_id, int64_t* max_id,
+                             void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n_edges >= 0, "negative edge count");
+        LCC_REQUIRE(n_edges == 0 || (u && v), "NULL buffer");
+        LCC_REQUIRE(min_id && max_id, "NULL output");
+        lcc::edge_id_range(n_edges, u, v, min_id, max_id, S(stream));
+    });
+}
+
+lcc_status lcc_build_graph(int64_t n, int64_t n_edges, const int64_t* u, const int64_t* v, const double* w,
+                           int64_t* indptr, int32_t* indices, double* weights, int64_t* m, double* total_weight,
+                           int32_t* unit_weights, void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0 && n_edges >= 0, "negative size");
+        LCC_REQUIRE(indptr && (n_edges == 0 || (u && v && indices && weights)), "NULL buffer");
+        const lcc::BuiltGraph b = lcc::build_graph(n, n_edges, u, v, w, indptr, indices, weights, S(stream));
+        if (m) *m = b.m;
+        if (total_weight) *total_weight = b.total_weight;
+        if (unit_weights) *unit_weights = b.unit ? 1 : 0;
+    });
+}
+
+lcc_status lcc_coo_merge(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols, const void* w,
+                         int32_t wtype, int64_t* indptr, int32_t* indices, void* w_out, int64_t* nnz_out,
+                         void* stream) {
+    return guard([&] {
+        LCC_REQUIRE(n >= 0 && nnz >= 0, "negative size");
+        LCC_REQUIRE(indptr && (nnz == 0 || (rows && cols && indices && w_out)), "NULL buffer");
+        LCC_REQUIRE(wtype == LCC_W_NONE || wtype == LCC_W_U32 || wtype == LCC_W_F64,
+                    "coo_merge takes LCC_W_NONE / LCC_W_U32 (uint32 sums) or LCC_W_F64 (double sums)");
+        LCC_REQUIRE(wtype == LCC_W_NONE || nnz == 0 || w, "weights are NULL");
+        int64_t r;
+        if (wtype == LCC_W_F64)
+            r = lcc::coo_merge<double>(n, nnz, rows, cols, static_cast<const double*>(w), indptr, indices,
+                                       static_cast<double*>(w_out), S(stream));
+        else
+            r = lcc::coo_merge<uint32_t>(n, nnz, rows, cols,
+                                         wtype == LCC_W_NONE ? nullptr : static_cast<const uint32_t*>(w), indptr,
+                                         indices, static_cast<uint32_t*>(w_out), S(stream));
+        if (nnz_out) *nnz_out = r;
     });
 }
 

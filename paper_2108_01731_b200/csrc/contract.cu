@@ -516,6 +516,56 @@ __global__ void k_compose(const int32_t* __restrict__ mapping, const int32_t* __
 
 }  // namespace
 
+namespace {
+template <class VT>
+__global__ void k_coo_keys(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                           const VT* __restrict__ vals, int64_t nnz, uint64_t* keys, VT* vout) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = ((uint64_t)(uint32_t)rows[i] << 32) | (uint32_t)cols[i];
+        vout[i] = vals ? vals[i] : (VT)1;
+    }
+}
+}  // namespace
+
+// Sum duplicate (row, col) entries into a CSR: the merge step of a sharded
+// contraction (partial coarse rows from several ranks; dist.py) -- the same
+// key sort + run reduce as compress, with the coarse ids already assigned.
+template <class VT>
+int64_t coo_merge(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols, const VT* vals,
+                  int64_t* indptr, int32_t* indices, VT* wout, cudaStream_t s) {
+    if (nnz <= 0) {
+        LCC_CUDA(cudaMemsetAsync(indptr, 0, sizeof(int64_t) * (n + 1), s));
+        return 0;
+    }
+    Buf<uint64_t> ka(nnz, s), kb(nnz, s);
+    Buf<VT> va(nnz, s), vb(nnz, s);
+    k_coo_keys<VT><<<grid_for(nnz, 256), 256, 0, s>>>(rows, cols, vals, nnz, ka.get(), va.get());
+    LCC_LAUNCH_CHECK();
+    cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());
+    cub::DoubleBuffer<VT> dv(va.get(), vb.get());
+    sort_pairs_db(dk, dv, nnz, 32 + std::max(1, bit_width((uint64_t)std::max<int64_t>(n, 1))), s);
+    Buf<uint64_t> ukeys(nnz, s);
+    Buf<int64_t> druns(1, s);
+    size_t bytes = 0;
+    LCC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, dk.Current(), ukeys.get(), dv.Current(), wout,
+                                            druns.get(), cub::Sum(), nnz, s));
+    {
+        Buf<unsigned char> tmp(bytes, s);
+        LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, dk.Current(), ukeys.get(), dv.Current(), wout,
+                                                druns.get(), cub::Sum(), nnz, s));
+    }
+    int64_t R = 0;
+    LCC_CUDA(cudaMemcpyAsync(&R, druns.get(), sizeof(R), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    k_emit_rows<<<grid_for(R + 1, 256), 256, 0, s>>>(ukeys.get(), R, 32, n, indptr, indices);
+    LCC_LAUNCH_CHECK();
+    return R;
+}
+template int64_t coo_merge<uint32_t>(int64_t, int64_t, const int32_t*, const int32_t*, const uint32_t*, int64_t*,
+                                     int32_t*, uint32_t*, cudaStream_t);
+template int64_t coo_merge<double>(int64_t, int64_t, const int32_t*, const int32_t*, const double*, int64_t*,
+                                   int32_t*, double*, cudaStream_t);
+
 Coarse compress(const lcc_graph& g, const double* k, double lam, const int32_t* C, const double* K,
                 int32_t* mapping, double* ck, cudaStream_t s) {
     LCC_REQUIRE(g.n >= 0 && g.n < (1LL << 31) - 1, "vertex count out of range");

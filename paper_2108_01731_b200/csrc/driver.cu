@@ -86,7 +86,9 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         } else {
             AsyncDamp damp;
             damp.prev_moved = damping ? mv_prev : nullptr;
-            damp.salt = 0x85EBCA6Bu * (uint32_t)(it + 1);
+            // seeded, recorded RNG: the damping coin of iteration
+            // `it` is a hash of (seed, it); the default seed 0 keeps round 1's salts
+            damp.salt = 0x85EBCA6Bu * (uint32_t)(it + 1) ^ (uint32_t)(o.seed * 0x9E3779B97F4A7C15ull >> 32);
             LCC_CUDA(cudaMemcpyAsync(D.get(), cur, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemcpyAsync(K2.get(), K, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             LCC_CUDA(cudaMemsetAsync(K2.get() + n, 0, sizeof(double) * n, s));

@@ -61,9 +61,27 @@ int64_t contraction_sort_entries(const lcc_graph& g, const int32_t* C, cudaStrea
 void flatten(int64_t n, const int32_t* mapping, const int32_t* Cc, const double* k, int32_t* C,
              double* K, cudaStream_t s);
 
+// contract.cu: COO entries (row, col, w) -> CSR with duplicate (row, col)
+// entries summed, rows sorted by col.  VT = uint32_t (counts / integer
+// weights; vals == nullptr means 1 each) or double.  Returns the entry count.
+template <class VT>
+int64_t coo_merge(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols, const VT* vals,
+                  int64_t* indptr, int32_t* indices, VT* wout, cudaStream_t s);
+
+// build.cu: build_graph (graph.py:79-164) on the device
+struct BuiltGraph {
+    int64_t m = 0, nnz = 0;
+    double total_weight = 0.0;
+    bool unit = true;  // every weight is 1 (the reference's unweighted graph)
+};
+void edge_id_range(int64_t ne, const int64_t* u, const int64_t* v, int64_t* lo, int64_t* hi, cudaStream_t s);
+BuiltGraph build_graph(int64_t n, int64_t ne, const int64_t* u, const int64_t* v, const double* w, int64_t* indptr,
+                       int32_t* indices, double* weights, cudaStream_t s);
+
 // objective.cu
 double cc_objective(const lcc_graph& g, const double* k, double lam, const int32_t* C,
                     cudaStream_t s);
+void weighted_degrees(const lcc_graph& g, double* k, cudaStream_t s);
 
 // gen.cu
 int64_t build_csr_from_pairs(int64_t n, int64_t n_pairs, const int32_t* u, const int32_t* v,
@@ -84,6 +102,7 @@ void cluster_stats(int64_t n, const int32_t* C, int64_t* num, int64_t* mn, int64
 struct Options {
     int schedule = LCC_ASYNC, policy = LCC_FRONTIER_VERTEX_NBRS, refine = 1, num_iter = 10;
     int deg_threshold = 1000, async_chunks = 0;  // 0 = auto
+    uint64_t seed = 0;  // ParOptions.seed: salts the async damping coin
 };
 // first_level: the first iteration may run as one wave (P auto); later
 // async iterations take at least async_min_subrounds() ordered sub-rounds.

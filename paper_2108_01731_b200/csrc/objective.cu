@@ -81,7 +81,46 @@ double objective_impl(const lcc_graph& g, const double* k, double lam, const int
     return intra * 0.5 - lam * (hd[1] - hd[2]) * 0.5;
 }
 
+// weighted_degrees (graph.py:57-61): the reference's np.add.at walks the
+// CSR in order, so each row is summed left to right in fp64 -- one thread
+// per row, loads unrolled 8 deep so the dependent adds, not the loads, set
+// the pace.  Bit-identical to the reference for fp32 / fp64 weights.
+template <class WT>
+__global__ void k_wdeg(const int64_t* __restrict__ indptr, const void* __restrict__ w, int64_t n, double* out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = indptr[v], e = indptr[v + 1];
+        double acc = 0.0;
+        int64_t i = b;
+        for (; i + 8 <= e; i += 8) {
+            double x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = WLoad<WT>::at(w, i + j);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, x[j]);
+        }
+        for (; i < e; ++i) acc = __dadd_rn(acc, (double)WLoad<WT>::at(w, i));
+        out[v] = acc;
+    }
+}
+__global__ void k_deg(const int64_t* __restrict__ indptr, int64_t n, double* out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = (double)(indptr[v + 1] - indptr[v]);
+}
+
 }  // namespace
+
+void weighted_degrees(const lcc_graph& g, double* k, cudaStream_t s) {
+    if (g.n <= 0) return;
+    const unsigned grid = grid_for(g.n, 128);
+    switch (g.weights ? g.wtype : LCC_W_NONE) {
+        case LCC_W_NONE: k_deg<<<grid, 128, 0, s>>>(g.indptr, g.n, k); break;
+        case LCC_W_F32: k_wdeg<float><<<grid, 128, 0, s>>>(g.indptr, g.weights, g.n, k); break;
+        case LCC_W_F64: k_wdeg<double><<<grid, 128, 0, s>>>(g.indptr, g.weights, g.n, k); break;
+        case LCC_W_U32: k_wdeg<uint32_t><<<grid, 128, 0, s>>>(g.indptr, g.weights, g.n, k); break;
+        default: throw Invalid("unknown weight dtype");
+    }
+    LCC_LAUNCH_CHECK();
+}
 
 double cc_objective(const lcc_graph& g, const double* k, double lam, const int32_t* C, cudaStream_t s) {
     switch (g.weights ? g.wtype : LCC_W_NONE) {

@@ -19,6 +19,7 @@ is unweighted or integer-weighted, float64 weights otherwise.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -110,13 +111,13 @@ class DeviceGraph:
         return self.indptr[1:] - self.indptr[:-1]
 
     def weighted_degrees(self) -> torch.Tensor:
-        """Per-vertex sum of incident weights (reference graph.py:57-61)."""
-        deg = self.degrees()
-        if self.weights is None:
-            return deg.to(torch.float64)
-        rows = torch.repeat_interleave(torch.arange(self.n, device=self.device), deg)
-        out = torch.zeros(self.n, dtype=torch.float64, device=self.device)
-        return out.index_add_(0, rows, self.weights.to(torch.float64))
+        """Per-vertex sum of incident weights (reference graph.py:57-61):
+        ``lcc_weighted_degrees``, each row summed in CSR order like the
+        reference's np.add.at, so the fp64 result is bit-identical."""
+        out = torch.empty(max(self.n, 1), dtype=torch.float64, device=self.device)
+        gs = self.c_struct()
+        _lib.check(_lib.load().lcc_weighted_degrees(ctypes.byref(gs), out.data_ptr(), stream_ptr()))
+        return out[:self.n]
 
     def c_struct(self) -> _lib.LccGraph:
         wtype = _lib.W_NONE
@@ -136,3 +137,67 @@ class DeviceGraph:
 
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+# ---------------------------------------------------------------------------
+# build_graph (reference graph.py:79-164) on the device
+# ---------------------------------------------------------------------------
+
+def _edge_arrays(edges):
+    """The reference's ``_as_edge_arrays`` input forms (graph.py:62-76): a
+    (u, v, w) tuple of arrays, or an iterable of (u, v, w) triples."""
+    if isinstance(edges, tuple) and len(edges) == 3:
+        return edges
+    arr = np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges, dtype=np.float64)
+    if arr.size == 0:
+        return np.empty(0, np.int64), np.empty(0, np.int64), np.empty(0)
+    if arr.ndim != 2 or arr.shape[1] != 3:
+        raise GraphError("edge list must consist of (u, v, w) triples")
+    return arr[:, 0].astype(np.int64), arr[:, 1].astype(np.int64), arr[:, 2]
+
+
+def build_graph(edges, n: int | None = None) -> DeviceGraph:
+    """SPEC build_graph (graph.py:79-95) on the device: see build_graph_arrays."""
+    u, v, w = _edge_arrays(edges)
+    return build_graph_arrays(u, v, w, n=n)
+
+
+def build_graph_arrays(u, v, w=None, n: int | None = None) -> DeviceGraph:
+    """build_graph_arrays (graph.py:98-164) as one device call
+    (``lcc_build_graph``): self loops dropped, same-orientation parallel
+    edges summed, the two orientations of a pair averaged, rows sorted --
+    CSR, weights and total_weight bit-identical to the reference's (the
+    kernels follow numpy's summation order).  ``w=None`` means every weight
+    is 1.  Unit weights come back as ``weights=None`` (nothing to read)."""
+    dev = _device()
+    uu = _to_dev(u, torch.int64, dev).reshape(-1)
+    vv = _to_dev(v, torch.int64, dev).reshape(-1)
+    ww = None if w is None else _to_dev(w, torch.float64, dev).reshape(-1)
+    if uu.numel() != vv.numel() or (ww is not None and ww.numel() != uu.numel()):
+        raise GraphError("edge arrays must have equal length")
+    ne = int(uu.numel())
+    if ne == 0 and n is None:
+        raise GraphError("empty graph")
+    L = _lib.load()
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(L.lcc_edge_id_range(ne, uu.data_ptr() if ne else None, vv.data_ptr() if ne else None,
+                                   ctypes.byref(lo), ctypes.byref(hi), stream_ptr()))
+    if ne and lo.value < 0:
+        raise GraphError("vertex ids must be non-negative")
+    n_seen = hi.value + 1 if ne else 0
+    if n is None:
+        n = n_seen
+    elif n < n_seen:
+        raise GraphError(f"n={n} smaller than largest vertex id {n_seen - 1}")
+    n = int(n)
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(max(2 * ne, 1), dtype=torch.int32, device=dev)
+    weights = torch.empty(max(2 * ne, 1), dtype=torch.float64, device=dev)
+    m, tw, unit = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
+    _lib.check(L.lcc_build_graph(n, ne, uu.data_ptr() if ne else None, vv.data_ptr() if ne else None,
+                                 None if ww is None or ne == 0 else ww.data_ptr(), indptr.data_ptr(),
+                                 indices.data_ptr(), weights.data_ptr(), ctypes.byref(m), ctypes.byref(tw),
+                                 ctypes.byref(unit), stream_ptr()))
+    nnz = 2 * m.value
+    wt = None if unit.value else weights[:nnz].clone()
+    return DeviceGraph(n, m.value, indptr, indices[:nnz].clone(), wt, tw.value)

@@ -3,90 +3,27 @@
 
 * ``read_edge_list(path, weighted)`` -- "u v" / "u v w" lines, '#' comments;
   non-integer ids are remapped densely (first appearance order) and the
-  mapping is returned; the graph is built with the reference's
-  ``build_graph_arrays`` semantics (``graph.py:98-164``): self loops dropped,
-  parallel same-orientation edges summed, the two orientations of a pair
-  averaged, rows sorted.  Unit weights are stored implicitly (``weights is
-  None``) so the device path reads no weight array.
+  mapping is returned; the CSR is built on the device by
+  ``graph.build_graph_arrays`` (``lcc_build_graph``: the reference's
+  ``build_graph_arrays`` contract, graph.py:98-164, bit for bit).  Unit
+  weights are stored implicitly (``weights is None``) so the device path
+  reads no weight array.
 * ``read_ground_truth(path, id_map)`` -- one community per line.
 * ``read_clustering`` / ``write_clustering`` -- "vertex_id cluster_id" lines
   in original ids; ``write_metrics`` -- one JSON object with the EvalReport
   keys (``SPEC.md:419``).
 
-This is host-side plumbing around the device path (file parsing and the
-CSR build of a file's edge list); the clustering itself and every metric
-run in the sm_100a library.
+This is host-side plumbing around the device path (file parsing); the CSR
+build, the clustering and every metric run in the sm_100a library.
 """
 from __future__ import annotations
 
 import json
 import os
-from dataclasses import dataclass
-
 import numpy as np
 
 from .eval import EvalReport, GroundTruth
-from .graph import GraphError
-
-
-@dataclass
-class WeightedGraph:
-    """Host CSR with the reference's ``WeightedGraph`` fields (graph.py:33-38)."""
-    n: int
-    m: int
-    indptr: np.ndarray          # int64 [n+1]
-    indices: np.ndarray         # int32 [2m]
-    weights: np.ndarray | None  # float64 [2m], None when every weight is 1
-    total_weight: float
-
-
-def build_graph_arrays(u, v, w, n: int | None = None) -> WeightedGraph:
-    """Restatement of the reference builder (graph.py:98-164)."""
-    u = np.asarray(u, dtype=np.int64)
-    v = np.asarray(v, dtype=np.int64)
-    w = np.asarray(w, dtype=np.float64)
-    if not (u.shape == v.shape == w.shape):
-        raise GraphError("edge arrays must have equal length")
-    if u.size == 0 and n is None:
-        raise GraphError("empty graph")
-    if u.size and (u.min() < 0 or v.min() < 0):
-        raise GraphError("vertex ids must be non-negative")
-    n_seen = int(max(u.max(), v.max())) + 1 if u.size else 0
-    if n is None:
-        n = n_seen
-    elif n < n_seen:
-        raise GraphError(f"n={n} smaller than largest vertex id {n_seen - 1}")
-    n = int(n)
-    keep = u != v
-    u, v, w = u[keep], v[keep], w[keep]
-    if u.size == 0:
-        return WeightedGraph(n, 0, np.zeros(n + 1, np.int64), np.empty(0, np.int32), None, 0.0)
-    lo, hi = np.minimum(u, v), np.maximum(u, v)
-    orient = (u > v).astype(np.int8)
-    order = np.lexsort((w, orient, hi, lo))  # weight last: order-independent sums
-    lo, hi, orient, w = lo[order], hi[order], orient[order], w[order]
-    grp = np.empty(lo.size, bool)
-    grp[0] = True
-    grp[1:] = (lo[1:] != lo[:-1]) | (hi[1:] != hi[:-1]) | (orient[1:] != orient[:-1])
-    st = np.flatnonzero(grp)
-    gsum = np.add.reduceat(w, st)
-    glo, ghi = lo[st], hi[st]
-    pair = np.empty(glo.size, bool)
-    pair[0] = True
-    pair[1:] = (glo[1:] != glo[:-1]) | (ghi[1:] != ghi[:-1])
-    ps = np.flatnonzero(pair)
-    cnt = np.diff(np.append(ps, glo.size))
-    ew = np.add.reduceat(gsum, ps) / cnt
-    eu, ev = glo[ps], ghi[ps]
-    src = np.concatenate([eu, ev])
-    dst = np.concatenate([ev, eu])
-    ww = np.concatenate([ew, ew])
-    order = np.lexsort((dst, src))
-    src, dst, ww = src[order], dst[order], ww[order]
-    indptr = np.zeros(n + 1, np.int64)
-    np.cumsum(np.bincount(src, minlength=n), out=indptr[1:])
-    weights = None if bool(np.all(ww == 1.0)) else ww
-    return WeightedGraph(n, int(eu.size), indptr, dst.astype(np.int32), weights, float(ew.sum()))
+from .graph import GraphError, build_graph_arrays
 
 
 def _parse_id(tok: str):
@@ -97,9 +34,16 @@ def _parse_id(tok: str):
 
 
 def read_edge_list(path: str, weighted: bool = False):
-    """SPEC.md:398-406.  Returns ``(graph, id_map)``; ``id_map[i]`` is the
-    original id of vertex i, or None when the file's ids are non-negative
-    integers (kept as they are)."""
+    """SPEC.md:398-406.  Returns ``(graph, id_map)``: ``graph`` is the device
+    CSR (``DeviceGraph``) and ``id_map[i]`` the original id of vertex i, or
+    None when the file's ids are non-negative integers (kept as they are)."""
+    u, v, w, id_map = parse_edge_list(path, weighted)
+    return build_graph_arrays(u, v, w, n=None if u.size else 0), id_map
+
+
+def parse_edge_list(path: str, weighted: bool = False):
+    """The file-parsing half of ``read_edge_list``: ``(u, v, w, id_map)``
+    host arrays (int64 ids, float64 weights or None when unweighted)."""
     if not os.path.exists(path):
         raise FileNotFoundError(path)
     us, vs, ws = [], [], []
@@ -137,9 +81,8 @@ def read_edge_list(path: str, weighted: bool = False):
         u = np.asarray([pos[x] for x in us], np.int64)
         v = np.asarray([pos[x] for x in vs], np.int64)
         id_map = order
-    w = np.asarray(ws, np.float64) if weighted else np.ones(u.size)
-    n = None if u.size else 0
-    return build_graph_arrays(u, v, w, n=n), id_map
+    w = np.asarray(ws, np.float64) if weighted else None
+    return u, v, w, id_map
 
 
 def _index(id_map):

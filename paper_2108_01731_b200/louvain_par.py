@@ -177,7 +177,7 @@ def best_moves_round(g, p: ClusteringParams, c: Clustering, frontier=None,
         c.cluster_mass = K = K2
     _lib.check(_lib.load().lcc_best_moves_round(
         ctypes.byref(gs), ctypes.byref(ps), c.assignment.data_ptr(), K.data_ptr(),
-        None if fr is None else fr.data_ptr(), 0 if fr is None else fr.numel(), int(schedule),
+        None if fr is None else fr.data_ptr(), n if fr is None else fr.numel(), int(schedule),
         int(degree_threshold), int(async_chunks), D.data_ptr(), moved.data_ptr(),
         None if nbr_mark is None else nbr_mark.data_ptr(), ctypes.byref(cnt), None, stream_ptr()))
     if schedule == Schedule.Asynchronous:

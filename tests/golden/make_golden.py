@@ -120,6 +120,36 @@ def build_cases(rng):
     return out
 
 
+def heavy_build_cases(rng):
+    """Summation-order stress for the device builder: same-orientation
+    groups of 1..600 parallel edges with weights over six decades (numpy's
+    pairwise summation differs from a sequential sum past 8 terms), both
+    orientations with different weights, and graphs with ~40K pairs
+    (total_weight's pairwise tree spans two or more 16K-entry leaves)."""
+    out = {}
+    for t in range(6):
+        n = int(rng.integers(50, 2000)) if t < 4 else int(rng.integers(8000, 20000))
+        pairs = int(rng.integers(5, 60)) if t < 4 else 40_000
+        a = rng.integers(0, n, pairs)
+        b = rng.integers(0, n, pairs)
+        mult = rng.integers(1, 600, pairs) if t < 4 else np.ones(pairs, np.int64)
+        u = np.repeat(a, mult)
+        v = np.repeat(b, mult)
+        flip = rng.random(u.size) < (0.5 if t % 2 else 0.1)
+        u, v = np.where(flip, v, u), np.where(flip, u, v)
+        w = rng.uniform(0.0, 1.0, u.size) * 10.0 ** rng.uniform(-3, 3, u.size)
+        w[rng.random(u.size) < 0.05] *= -1.0
+        perm = rng.permutation(u.size)
+        u, v, w = u[perm], v[perm], w[perm]
+        g = build_graph_arrays(u, v, w, n=n)
+        pre = f"b{t}_"
+        out.update({pre + "u": u.astype(np.int32), pre + "v": v.astype(np.int32), pre + "w": w,
+                    pre + "n": np.array([n]), pre + "indptr": g.indptr, pre + "indices": g.indices,
+                    pre + "weights": g.weights, pre + "total": np.array([g.total_weight]), pre + "m": np.array([g.m])})
+    out["cases"] = np.arange(6)
+    return out
+
+
 def main():
     rng = np.random.default_rng(2108_01731)
     np.savez_compressed(os.path.join(HERE, "contraction.npz"), **contraction_cases(rng))
@@ -144,6 +174,9 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["build"]:  # only the build fixture (tests/golden/build.npz)
         np.savez_compressed(os.path.join(HERE, "build.npz"), **build_cases(np.random.default_rng(398)))
+    elif sys.argv[1:] == ["build_heavy"]:  # tests/golden/build_heavy.npz
+        np.savez_compressed(os.path.join(HERE, "build_heavy.npz"), **heavy_build_cases(np.random.default_rng(399)))
     else:
         main()
         np.savez_compressed(os.path.join(HERE, "build.npz"), **build_cases(np.random.default_rng(398)))
+        np.savez_compressed(os.path.join(HERE, "build_heavy.npz"), **heavy_build_cases(np.random.default_rng(399)))

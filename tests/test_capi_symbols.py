@@ -26,7 +26,7 @@ def test_library_loads_and_exports_all_symbols():
     L = _lib.load()
     for name in declared_symbols():
         assert hasattr(L, name), name
-    assert L.lcc_abi_version() == 2
+    assert L.lcc_abi_version() == 3
 
 
 def test_invalid_argument_maps_to_graph_error():

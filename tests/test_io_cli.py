@@ -1,9 +1,10 @@
 """File I/O and CLI.
 
-CPU: the edge-list builder against golden outputs of the reference's own
+CPU: parsing, error paths and round trips.  GPU: the device edge-list
+builder (lcc_build_graph) against golden outputs of the reference's own
 ``build_graph_arrays`` (tests/golden/build.npz, made by
-tests/golden/make_golden.py), the SPEC I/O examples, error paths and
-round trips.  GPU: the ``cluster`` / ``eval`` / ``rmat`` commands end to end.
+tests/golden/make_golden.py), the SPEC I/O examples, and the ``cluster`` /
+``eval`` / ``rmat`` commands end to end.
 """
 import json
 import os
@@ -16,19 +17,35 @@ from paper_2108_01731_b200.eval import EvalReport
 from paper_2108_01731_b200.graph import GraphError
 
 
+@pytest.mark.gpu
 def test_build_matches_reference_golden(golden):
+    """The device build (lcc_build_graph) against the reference's own
+    build_graph_arrays output: CSR, weights and total_weight bit for bit."""
+    from paper_2108_01731_b200.graph import build_graph_arrays
     z = golden("build.npz")
     for t in z["cases"]:
         p = f"b{t}_"
-        g = lio.build_graph_arrays(z[p + "u"], z[p + "v"], z[p + "w"], n=int(z[p + "n"][0]))
+        g = build_graph_arrays(z[p + "u"], z[p + "v"], z[p + "w"], n=int(z[p + "n"][0]))
+        ip, ind, w = g.to_host()
         assert g.m == int(z[p + "m"][0])
-        assert np.array_equal(g.indptr, z[p + "indptr"])
-        assert np.array_equal(g.indices, z[p + "indices"])
-        w = np.ones(g.indices.size) if g.weights is None else g.weights
+        assert np.array_equal(ip, z[p + "indptr"])
+        assert np.array_equal(ind, z[p + "indices"])
+        w = np.ones(ind.size) if w is None else w
         assert np.array_equal(w, z[p + "weights"])  # bit-identical sums and averages
         assert g.total_weight == float(z[p + "total"][0])
 
 
+def test_parse_edge_list(tmp_path):
+    f = tmp_path / "e.txt"
+    f.write_text("# c\na b\nb c 2.5\n")
+    u, v, w, idmap = lio.parse_edge_list(str(f), weighted=True)
+    assert idmap == ["a", "b", "c"] and u.tolist() == [0, 1] and v.tolist() == [1, 2] and w.tolist() == [1.0, 2.5]
+    f.write_text("3 1\n")
+    u, v, w, idmap = lio.parse_edge_list(str(f))
+    assert idmap is None and w is None and u.tolist() == [3]
+
+
+@pytest.mark.gpu
 def test_read_edge_list_spec_examples(tmp_path):
     f = tmp_path / "path.txt"
     f.write_text("0 1\n1 2\n")
@@ -36,13 +53,13 @@ def test_read_edge_list_spec_examples(tmp_path):
     assert (g.n, g.m, idmap) == (3, 2, None) and g.weights is None
     f.write_text("# comment\n0 1 2.5\n")
     g, _ = lio.read_edge_list(str(f), weighted=True)
-    assert g.m == 1 and np.array_equal(g.weights, [2.5, 2.5])
+    assert g.m == 1 and np.array_equal(g.weights.cpu().numpy(), [2.5, 2.5])
     f.write_text("a b\nb c\n")
     g, idmap = lio.read_edge_list(str(f))
     assert idmap == ["a", "b", "c"] and g.n == 3 and g.m == 2
     f.write_text("0 1\n0 1\n1 0\n2 2\n")  # same-orientation sum, orientation average, loop dropped
     g, _ = lio.read_edge_list(str(f))
-    assert g.m == 1 and np.array_equal(g.weights, [1.5, 1.5]) and g.n == 3
+    assert g.m == 1 and np.array_equal(g.weights.cpu().numpy(), [1.5, 1.5]) and g.n == 3
 
 
 def test_read_errors(tmp_path):

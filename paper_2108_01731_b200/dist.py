@@ -6,24 +6,32 @@ owns (edges co-located with their source) and a replica of the cluster
 labels C and masses K.
 
 Per best-move iteration (Alg. 1 lines 6-10, bulk-synchronous across ranks):
-  1. every rank runs the best-move kernels over its owned frontier;
-  2. the owned slices of the new labels are all-gathered over NCCL (padded
-     equal chunks), so every rank holds the full new labelling; the moved
-     flags follow locally (label changed);
+  1. every rank runs the best-move kernels over its owned frontier (an empty
+     owned frontier is an empty round: no call);
+  2. the mover counts are all-gathered (termination, Alg. 1 line 9); the
+     changed labels follow -- as (vertex, label) pairs while movers are
+     sparse (< n/64), else as the owned slices of the label array (padded
+     equal chunks) -- so every rank holds the full new labelling;
   3. masses K are recomputed locally from the replicated labels (the apply /
      reconcile kernel) -- cheaper than all-reducing a dense fp64 K array, see
      SURVEY.md §8e step 3;
-  4. every rank marks the neighbours of its owned movers, the marks are
-     MAX-all-reduced, and each rank keeps its owned part as the next frontier.
+  4. every rank marks the neighbours of its owned movers; the marks are
+     MAX-reduce-scattered so each rank receives its owned part, the next
+     frontier.
 Asynchronous mode is asynchronous inside a GPU and bulk-synchronous across
 GPUs.  Synchronous mode gives labels identical to the single-GPU run (Jacobi
 rounds do not depend on the partition).
 
-Contraction: each rank compresses its owned rows with the device kernel
-(renumbering is identical everywhere since labels are replicated); the
-partial coarse CSRs are all-gathered and merged, the coarse levels run on
-rank 0 (they are a small fraction of the work) and the coarse labels are
-broadcast; flatten and the level-0 refinement run sharded again.
+Contraction repartitions the supervertex graph (SURVEY.md
+§8e): every rank renumbers identically (labels are replicated), compresses
+its owned rows into partial coarse rows, and sends each partial row to the
+coarse row's owner (one all-to-all; coarse ranges balanced on the summed
+partial row lengths); the owner merges duplicate (a, b) entries with the
+device COO merge (lcc_coo_merge) into its shard of the coarse CSR.  Coarse
+levels stay sharded until the coarse graph has fewer than ``gather_below``
+entries; that remainder is merged on rank 0, clustered there by the
+single-GPU driver, and its labels broadcast.  Flatten and refinement run
+sharded on every level while unwinding.
 
 The per-rank compute goes through a backend object (``CudaBackend`` here:
 the sm_100a C ABI).  Tests drive the same driver with a CPU backend over
@@ -211,6 +219,23 @@ class CudaBackend:
         p.lam, p.k = float(lam), k
         return parallel_cc(g, p, opts).assignment
 
+    def merge(self, n, rows, cols, w, integral):
+        """COO (row, col, w) -> CSR with duplicates summed (lcc_coo_merge);
+        integral weights as int32 (exact uint32 sums), else fp64."""
+        d = self.device
+        nnz = int(rows.numel())
+        ip = torch.empty(n + 1, dtype=torch.int64, device=d)
+        ind = torch.empty(max(nnz, 1), dtype=torch.int32, device=d)
+        wo = torch.empty(max(nnz, 1), dtype=torch.int32 if integral else torch.float64, device=d)
+        wi = w.to(d, torch.int32 if integral else torch.float64).contiguous() if nnz else None
+        cnt = ctypes.c_int64()
+        _lib.check(self.lib.lcc_coo_merge(n, nnz, rows.data_ptr() if nnz else None, cols.data_ptr() if nnz else None,
+                                          None if wi is None else wi.data_ptr(),
+                                          _lib.W_U32 if integral else _lib.W_F64, ip.data_ptr(), ind.data_ptr(),
+                                          wo.data_ptr(), ctypes.byref(cnt), stream_ptr()))
+        r = cnt.value
+        return ip, ind[:r], wo[:r]
+
     def flatten(self, mapping, Cc, k):
         n = mapping.numel()
         C = torch.empty(n, dtype=torch.int32, device=self.device)
@@ -222,32 +247,31 @@ class CudaBackend:
 
 
 # ---------------------------------------------------------------------------
-# the sharded driver
+# collectives (NCCL in production; gloo stages CUDA tensors through the host
+# for the collectives it has no CUDA path for)
 # ---------------------------------------------------------------------------
 
-def _max_(t: torch.Tensor, group):
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-    return t
+def _gloo(group) -> bool:
+    return dist.get_backend(group) == "gloo"
 
 
-def _sum_int(x: int, device, group) -> int:
-    if dist.get_world_size(group) == 1:
-        return int(x)
-    t = torch.tensor([x], dtype=torch.int64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return int(t.item())
+def _all_gather_ints(vals: list[int], device, group) -> list[list[int]]:
+    """Every rank's small int vector (one all-gather, one host read)."""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return [list(vals)]
+    dev = torch.device("cpu") if _gloo(group) else device
+    t = torch.tensor(vals, dtype=torch.int64, device=dev)
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t, group=group)
+    return torch.stack(outs).cpu().tolist()
 
 
 def _owned_sizes(part, group) -> list[int]:
     """Sizes of every rank's owned range (all-gathered once per PartGraph)."""
     sizes = getattr(part, "_sizes", None)
     if sizes is None:
-        world = dist.get_world_size(group)
-        dev = part.indptr.device
-        t = torch.tensor([part.hi - part.lo], dtype=torch.int64, device=dev)
-        outs = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(outs, t, group=group)
-        sizes = [int(o.item()) for o in outs]
+        sizes = [r[0] for r in _all_gather_ints([part.hi - part.lo], part.indptr.device, group)]
         part._sizes = sizes
     return sizes
 
@@ -267,11 +291,80 @@ def _allgather_owned(vals: torch.Tensor, part, group) -> torch.Tensor:
     return torch.cat([o[:sz] for o, sz in zip(outs, sizes)])
 
 
+def _sparse(movers: int, n: int) -> bool:
+    """(vertex, label) pairs cost 8 bytes per mover against 4n for the dense
+    slices: pairs below n / LCC_DIST_SPARSE_DIV movers (default 64)."""
+    return movers * int(os.environ.get("LCC_DIST_SPARSE_DIV", "64")) < n
+
+
+def _exchange_labels(labels, moved, part, counts, group) -> torch.Tensor:
+    """Full new labelling on every rank.  Sparse rounds (movers < n/64) send
+    (vertex, label) pairs of the owned movers; dense rounds all-gather the
+    owned slices."""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return labels
+    n = part.n
+    total = sum(counts)
+    if not _sparse(total, n):
+        return _allgather_owned(labels, part, group)
+    ids = torch.nonzero(moved[part.lo:part.hi]).flatten().to(torch.int32) + part.lo
+    mx = max(max(counts), 1)
+    buf = torch.full((2, mx), -1, dtype=torch.int32, device=labels.device)
+    c = int(ids.numel())
+    buf[0, :c] = ids
+    buf[1, :c] = labels[ids.long()]
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    pairs = torch.cat([o[:, :k] for o, k in zip(outs, counts)], dim=1)
+    lab = labels.clone()
+    lab[pairs[0].long()] = pairs[1]
+    return lab
+
+
+def _owned_max(mark: torch.Tensor, part, group) -> torch.Tensor:
+    """This rank's slice of the MAX over ranks of ``mark`` (the neighbour
+    marks): an NCCL reduce-scatter of padded equal chunks; gloo has no
+    reduce-scatter, so it all-reduces."""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return mark[part.lo:part.hi]
+    if _gloo(group):
+        dist.all_reduce(mark, op=dist.ReduceOp.MAX, group=group)
+        return mark[part.lo:part.hi]
+    sizes = _owned_sizes(part, group)
+    mx = max(sizes)
+    inp = torch.zeros(world * mx, dtype=mark.dtype, device=mark.device)
+    off = 0
+    for r, sz in enumerate(sizes):
+        inp[r * mx:r * mx + sz] = mark[off:off + sz]
+        off += sz
+    out = torch.empty(mx, dtype=mark.dtype, device=mark.device)
+    dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.MAX, group=group)
+    return out[:part.hi - part.lo]
+
+
+def _all_to_all(inp: torch.Tensor, send: list[int], recv: list[int], group) -> torch.Tensor:
+    dev = inp.device
+    stage = _gloo(group) and inp.is_cuda
+    x = inp.cpu() if stage else inp
+    out = torch.empty(sum(recv), dtype=inp.dtype, device=x.device)
+    dist.all_to_all_single(out, x.contiguous(), recv, send, group=group)
+    return out.to(dev) if stage else out
+
+
+# ---------------------------------------------------------------------------
+# the sharded driver
+# ---------------------------------------------------------------------------
+
 @dataclass
 class ShardStats:
     rounds: int = 0
     edges_scanned: int = 0   # this rank's owned frontier edges
     moves: int = 0           # global movers
+    sharded_levels: int = 0  # levels whose best moves ran sharded (level 0 included)
+    gathered_levels: int = 0  # levels merged on rank 0 and clustered there
+    sparse_exchanges: int = 0  # iterations that exchanged (vertex, label) pairs
 
 
 def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None, stats: ShardStats | None = None):
@@ -284,6 +377,7 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
     sched = int(opts.schedule)
     any_moved = False
     deg = (part.indptr[1:] - part.indptr[:-1])
+    edges = torch.zeros((), dtype=torch.int64, device=dev)  # summed on the device, read once
     num_iter = int(opts.num_iter)
     policy = FrontierPolicy(opts.frontier_policy)
     # VertexNeighbors: the round marks its movers' neighbours itself (the
@@ -291,88 +385,111 @@ def sharded_best_moves(part: PartGraph, k, lam, C, K, opts, backend, group=None,
     # oracle) fall back to frontier_mask
     fused = policy == FrontierPolicy.VertexNeighbors and getattr(backend, "fused_nbr_mark", False)
     for it in range(num_iter):
-        if _sum_int(int(F.numel()), dev, group) == 0:
-            break
-        # passed on the last iteration too: the round-1 async call measured
-        # 10.7 ms with the marks and 11.9 ms without (tools/round_ab.py)
-        mark = torch.empty(n, dtype=torch.uint8, device=dev) if fused else None
-        if mark is None:
-            labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
-                                               int(opts.async_chunks))
+        nF = int(F.numel())
+        mark = torch.zeros(n, dtype=torch.uint8, device=dev) if fused else None
+        if nF == 0:
+            # empty owned frontier: an empty round, no call (a NULL frontier
+            # would mean V' = V); still take part in the collectives
+            labels = C if sched == SYNC_ else C.clone()
+            moved = torch.zeros(n, dtype=torch.uint8, device=dev)
+        elif mark is None:
+            labels, moved, _ = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
+                                             int(opts.async_chunks))
         else:
-            labels, moved, cnt = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
-                                               int(opts.async_chunks), nbr_mark=mark)
+            # passed on the last iteration too: the round-1 async call measured
+            # 10.7 ms with the marks and 11.9 ms without (tools/round_ab.py)
+            labels, moved, _ = backend.round(part, k, lam, C, K, F, sched, int(opts.degree_threshold),
+                                             int(opts.async_chunks), nbr_mark=mark)
+        cnt = int(moved[part.lo:part.hi].sum().item()) if nF else 0
+        rows = _all_gather_ints([nF, cnt], dev, group)
+        if sum(r[0] for r in rows) == 0:
+            break                               # global frontier empty
+        counts = [r[1] for r in rows]
+        total = sum(counts)
         if stats is not None:
             stats.rounds += 1
-            stats.edges_scanned += int(deg.index_select(0, F).sum().item()) if F.numel() else 0
-        total = _sum_int(int(cnt), dev, group)
-        if stats is not None:
+            if nF:
+                edges += deg.index_select(0, F.long()).sum()
             stats.moves += total
         if total == 0:
             break                               # Alg. 1 line 9
         any_moved = True
-        # owners' labels to every rank (one all-gather of the owned slices).
-        # The moved flags need no exchange: a vertex moved iff its label
-        # changed (a mover's target differs from its cluster; fresh ids n+v).
-        lab = _allgather_owned(labels, part, group)
+        # owners' labels to every rank.  The moved flags need no exchange: a
+        # vertex moved iff its label changed (a mover's target differs from
+        # its cluster; fresh ids n+v).
+        if stats is not None and _sparse(total, n) and dist.get_world_size(group) > 1:
+            stats.sparse_exchanges += 1
+        lab = _exchange_labels(labels, moved, part, counts, group)
         Cn, Kn = backend.apply(lab, 2 * n, k)   # canonical labels + masses, replicated
         if it + 1 < num_iter:  # the next frontier is only needed by a next iteration
             if policy == FrontierPolicy.AllVertices:
                 F = owned
-            elif mark is not None:
-                _max_(mark, group)
-                F = (torch.nonzero(mark[part.lo:part.hi]).flatten() + part.lo).to(torch.int32)
             else:
-                mv = (lab != C).to(torch.uint8)
-                mask = backend.frontier_mask(part, int(policy), mv, C, Cn)
-                _max_(mask, group)
-                F = (torch.nonzero(mask[part.lo:part.hi]).flatten() + part.lo).to(torch.int32)
+                if mark is None:
+                    mark = backend.frontier_mask(part, int(policy), (lab != C).to(torch.uint8), C, Cn)
+                mine = _owned_max(mark, part, group)
+                F = (torch.nonzero(mine).flatten() + part.lo).to(torch.int32)
         C, K = Cn, Kn
+    if stats is not None:
+        stats.edges_scanned += int(edges.item())
     return C, K, any_moved
 
 
-def _gather_coarse(cn, cptr, cind, cw, device, group, integral=False):
-    """Gather the partial coarse CSRs on rank 0 (NCCL gather, not an
-    all-gather: only rank 0 runs the coarse levels); rank 0 merges duplicate
-    (a, b) entries and returns the coarse CSR (other ranks return None).
-    Ids travel as int32 (cn < 2^31) and, when the level-0 weights are
-    integral (unweighted or LCC_W_U32), weights as int32 too: 12 bytes per
-    entry instead of 24."""
+SYNC_ = 0  # lcc_schedule LCC_SYNC
+
+
+def _coarse_bounds(cn, cptr, dev, group) -> list[int]:
+    """Coarse owner ranges: contiguous, balanced on (vertices + summed
+    partial row lengths) like partition_bounds on the coarse graph."""
     world = dist.get_world_size(group)
-    if world == 1:
-        return cptr, cind, cw, float(cw.sum().item()) / 2.0
+    lens = (cptr[1:] - cptr[:-1]).to(torch.int64)
+    stage = _gloo(group) and lens.is_cuda
+    x = lens.cpu() if stage else lens
+    dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
+    lens = x.to(dev) if stage else x
+    P = torch.zeros(cn + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(lens + 1, 0, out=P[1:])
+    total = int(P[-1].item())
+    targets = torch.tensor([total * r // world for r in range(1, world)], dtype=torch.int64, device=dev)
+    inner = torch.searchsorted(P, targets, right=False).cpu().tolist()
+    return [0] + inner + [cn]
+
+
+def _redistribute(cn, cptr, cind, cw, bounds, integral, backend, group):
+    """Send every partial coarse row to its owner (bounds[r]..bounds[r+1]
+    belong to rank r) and merge what arrives: (local indptr over the owned
+    range, indices, weights).  One all-to-all per array; ids int32, weights
+    int32 when integral (12 bytes per entry), else fp64."""
     rank = dist.get_rank(group)
-    rows = torch.repeat_interleave(torch.arange(cn, device=device, dtype=torch.int32), cptr[1:] - cptr[:-1])
-    local = torch.stack([rows, cind.to(torch.int32)]).contiguous()
-    size = torch.tensor([local.shape[1]], dtype=torch.int64, device=device)
-    sizes = [torch.zeros_like(size) for _ in range(world)]
-    dist.all_gather(sizes, size, group=group)
-    sizes = [int(x.item()) for x in sizes]
-    mx = max(sizes)
+    dev = backend.device
+    world = len(bounds) - 1
+    starts = cptr[torch.tensor(bounds, dtype=torch.long, device=cptr.device)].cpu().tolist()
+    send = [starts[r + 1] - starts[r] for r in range(world)]
+    recv = _all_to_all(torch.tensor(send, dtype=torch.int64, device=dev), [1] * world, [1] * world,
+                       group).cpu().tolist()
+    lens = cptr[1:] - cptr[:-1]
+    rows = torch.repeat_interleave(torch.arange(cn, dtype=torch.int32, device=cptr.device), lens)
     wdt = torch.int32 if integral else torch.float64
-    pad_i = torch.full((2, mx), -1, dtype=torch.int32, device=device)
-    pad_i[:, :local.shape[1]] = local
-    pad_w = torch.zeros(mx, dtype=wdt, device=device)
-    pad_w[:cw.numel()] = cw.to(wdt)
-    gi = [torch.empty_like(pad_i) for _ in range(world)] if rank == 0 else None
-    gw = [torch.empty_like(pad_w) for _ in range(world)] if rank == 0 else None
-    dist.gather(pad_i, gi, dst=0, group=group)
-    dist.gather(pad_w, gw, dst=0, group=group)
-    if rank != 0:
-        return None  # the coarse levels run on rank 0 only
-    ab = torch.cat([g[:, :sz] for g, sz in zip(gi, sizes)], dim=1).to(torch.int64)
-    w = torch.cat([g[:sz] for g, sz in zip(gw, sizes)])
-    del gi, gw
-    key = ab[0] * max(cn, 1) + ab[1]
-    del ab
-    key, order = torch.sort(key, stable=True)
-    w = w[order].to(torch.int64 if integral else torch.float64)
-    uk, inv = torch.unique_consecutive(key, return_inverse=True)
-    ws = torch.zeros(uk.numel(), dtype=w.dtype, device=device).index_add_(0, inv, w).to(torch.float64)
-    a, b = uk // max(cn, 1), uk % max(cn, 1)
-    indptr = torch.zeros(cn + 1, dtype=torch.int64, device=device)
-    indptr[1:] = torch.cumsum(torch.bincount(a, minlength=cn), 0)
-    return indptr, b.to(torch.int32), ws, float(ws.sum().item()) / 2.0
+    r_rows = _all_to_all(rows, send, recv, group)
+    r_cols = _all_to_all(cind.to(torch.int32), send, recv, group)
+    r_w = _all_to_all(cw.to(wdt), send, recv, group)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    return backend.merge(hi - lo, (r_rows - lo).to(dev), r_cols.to(dev), r_w.to(dev), integral)
+
+
+def _full_indptr(lptr, lo, cn, dev):
+    """Owned-range indptr -> full-length indptr with empty non-owned rows."""
+    nnz = lptr[-1:]
+    return torch.cat([torch.zeros(lo, dtype=torch.int64, device=dev), lptr.to(dev),
+                      nnz.to(dev).expand(cn - lo - (lptr.numel() - 1))])
+
+
+def _sum_f64(x: float, dev, group) -> float:
+    if dist.get_world_size(group) == 1:
+        return float(x)
+    t = torch.tensor([x], dtype=torch.float64, device=torch.device("cpu") if _gloo(group) else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())
 
 
 class _Trace:
@@ -386,51 +503,85 @@ class _Trace:
     def __call__(self, what):
         if not self.on:
             return
-        torch.cuda.synchronize(self.dev)
+        if self.dev.type == "cuda":
+            torch.cuda.synchronize(self.dev)
         t = time.perf_counter()
         print(f"[lcc dist r{self.rank}] {what}: {1e3 * (t - self.t):.1f} ms", file=sys.stderr, flush=True)
         self.t = t
 
 
+GATHER_BELOW = 64 << 20  # coarse graphs with fewer entries are clustered on rank 0
+
+
 def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, backend=None, group=None,
-                        stats: ShardStats | None = None) -> torch.Tensor:
-    """parallel_cc with level 0 sharded over the process
-    group.  ``indptr``/``indices``/``weights`` are the full graph (host or
-    device); ``k`` the full vertex weights (or None).  Returns the canonical
-    labels (replicated on every rank)."""
+                        stats: ShardStats | None = None, gather_below: int | None = None) -> torch.Tensor:
+    """parallel_cc with every level vertex-sharded over the
+    process group until the coarse graph has fewer than ``gather_below``
+    entries (default 64M; 0 = never gather).  ``indptr``/``indices``/
+    ``weights`` are the full graph (host or device); ``k`` the full vertex
+    weights (or None).  Returns the canonical labels (replicated on every
+    rank)."""
     backend = backend or CudaBackend()
     dev = backend.device
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if gather_below is None:
+        gather_below = int(os.environ.get("LCC_DIST_GATHER_NNZ", GATHER_BELOW))
     tr = _Trace(rank, dev)
     ip = np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr, dtype=np.int64)
     bounds = partition_bounds(ip, world)
     part = make_part(indptr, indices, weights, total_weight, int(bounds[rank]), int(bounds[rank + 1]), dev)
-    n = part.n
     if k is not None:
         k = torch.as_tensor(k, dtype=torch.float64).to(dev)
-    C = torch.arange(n, dtype=torch.int32, device=dev)
-    K = torch.ones(n, dtype=torch.float64, device=dev) if k is None else k.clone()
     tr("upload")
-    C, K, moved = sharded_best_moves(part, k, lam, C, K, opts, backend, group, stats)
-    tr("level 0")
-    if not moved:
-        return C
-    cn, cptr, cind, cw, ck, mapping = backend.compress(part, k, lam, C, K)
-    tr("compress")
-    if cn == n:
-        return C                                      # no size reduction (SPEC.md:317)
-    integral = part.weights is None or part.weights.dtype == torch.int32
-    merged = _gather_coarse(cn, cptr, cind, cw, dev, group, integral)
-    tr("gather coarse")
-    Cc = torch.empty(cn, dtype=torch.int32, device=dev)
-    if rank == 0:
-        c_indptr, c_ind, c_w, c_tot = merged
-        Cc = backend.parallel_cc(c_indptr, c_ind, c_w, c_tot, ck, lam, opts).to(torch.int32)
-    tr("coarse levels")
-    dist.broadcast(Cc, src=0, group=group)
-    C, K = backend.flatten(mapping, Cc, k)
-    if opts.refine:
-        C, K, _ = sharded_best_moves(part, k, lam, C, K, opts, backend, group, stats)
-    tr("flatten + refine")
+    stack = []            # (part, k, mapping) of every contracted level
+    cur, kcur = part, k
+    level = 0
+    while True:
+        n = cur.n
+        C = torch.arange(n, dtype=torch.int32, device=dev)
+        K = torch.ones(n, dtype=torch.float64, device=dev) if kcur is None else kcur.clone()
+        C, K, moved = sharded_best_moves(cur, kcur, lam, C, K, opts, backend, group, stats)
+        if stats is not None:
+            stats.sharded_levels += 1
+        tr(f"level {level} best moves")
+        if not moved:
+            break                                     # Alg. 1 line 13
+        cn, cptr, cind, cw, ck, mapping = backend.compress(cur, kcur, lam, C, K)
+        tr(f"level {level} compress")
+        if cn == n:
+            break                                     # no size reduction (SPEC.md:317)
+        integral = cur.weights is None or cur.weights.dtype == torch.int32
+        stack.append((cur, kcur, mapping))
+        gnnz = int(round(_sum_f64(float(cind.numel()), dev, group)))
+        if world == 1 or gnnz < gather_below:
+            # the remainder on rank 0: single-GPU driver, labels broadcast
+            Cc = torch.empty(cn, dtype=torch.int32, device=dev)
+            if world == 1:
+                Cc = backend.parallel_cc(cptr, cind, cw, float(cw.sum().item()) / 2.0, ck, lam, opts).to(torch.int32)
+            else:
+                lptr, lind, lw = _redistribute(cn, cptr, cind, cw, [0] + [cn] * world, integral, backend, group)
+                if rank == 0:
+                    Cc = backend.parallel_cc(lptr, lind, lw, float(lw.to(torch.float64).sum().item()) / 2.0, ck,
+                                             lam, opts).to(torch.int32)
+                dist.broadcast(Cc, src=0, group=group)
+            if stats is not None:
+                stats.gathered_levels += 1
+            C = Cc
+            tr(f"levels {level + 1}+ on rank 0")
+            break
+        # repartition the supervertex graph and stay sharded
+        cb = _coarse_bounds(cn, cptr, dev, group)
+        lptr, lind, lw = _redistribute(cn, cptr, cind, cw, cb, integral, backend, group)
+        del cptr, cind, cw
+        tw = _sum_f64(float(lw.to(torch.float64).sum().item()), dev, group) / 2.0
+        cur = PartGraph(cn, cb[rank], cb[rank + 1], _full_indptr(lptr, cb[rank], cn, dev), lind, lw, tw)
+        kcur = ck
+        level += 1
+        tr(f"level {level} repartition")
+    # unwind: flatten + refine level by level (Alg. 1 lines 17-18)
+    for lvl, kl, mapping in reversed(stack):
+        C, K = backend.flatten(mapping, C, kl)
+        if opts.refine:
+            C, K, _ = sharded_best_moves(lvl, kl, lam, C, K, opts, backend, group, stats)
+        tr(f"unwind n={lvl.n}")
     return C
-

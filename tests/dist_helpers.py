@@ -52,10 +52,21 @@ class OracleBackend:
                 torch.from_numpy(lvl.k), torch.from_numpy(lvl.mapping))
 
     def parallel_cc(self, indptr, indices, weights, total_weight, k, lam, opts):
-        g = O.Graph(indptr.numel() - 1, _np(indptr), _np(indices).astype(np.int32), _np(weights), total_weight)
+        w = None if weights is None else np.ascontiguousarray(_np(weights), dtype=np.float64)
+        g = O.Graph(indptr.numel() - 1, _np(indptr), _np(indices).astype(np.int32), w, total_weight)
         o = O.Opts(schedule=int(opts.schedule), frontier=int(opts.frontier_policy), refine=bool(opts.refine),
                    num_iter=int(opts.num_iter))
         return torch.from_numpy(O.parallel_cc(g, _np(k), lam, o))
+
+    def merge(self, n, rows, cols, w, integral):
+        r, c, ww = _np(rows).astype(np.int64), _np(cols).astype(np.int64), _np(w).astype(np.float64)
+        key = r * (1 << 32) + c
+        uk, inv = np.unique(key, return_inverse=True)
+        sums = np.bincount(inv, weights=ww, minlength=uk.size) if uk.size else np.zeros(0)
+        ip = np.zeros(n + 1, np.int64)
+        np.cumsum(np.bincount(uk >> 32, minlength=n), out=ip[1:])
+        wt = torch.from_numpy(sums.astype(np.int32)) if integral else torch.from_numpy(sums)
+        return torch.from_numpy(ip), torch.from_numpy((uk & 0xffffffff).astype(np.int32)), wt
 
     def flatten(self, mapping, Cc, k):
         C, K = O.flatten(mapping.numel(), _np(mapping).astype(np.int32), _np(Cc).astype(np.int32), _np(k))

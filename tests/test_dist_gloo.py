@@ -27,12 +27,14 @@ def free_port():
     return p
 
 
-def _cluster(rank, world, indptr, indices, k, lam, opts_kw):
+def _cluster(rank, world, indptr, indices, k, lam, opts_kw, gather_below=None, sparse_always=False):
+    if sparse_always:
+        os.environ["LCC_DIST_SPARSE_DIV"] = "0"  # movers * 0 < n: always pairs
     opts = ParOptions(**opts_kw)
     st = ShardStats()
     C = sharded_parallel_cc(indptr, indices, None, float(indices.size // 2), k, lam, opts,
-                            backend=OracleBackend(), stats=st)
-    return {"C": C.numpy(), "rounds": st.rounds}
+                            backend=OracleBackend(), stats=st, gather_below=gather_below)
+    return {"C": C.numpy(), "rounds": st.rounds, "stats": st}
 
 
 def run_world(world, fn, *args):
@@ -97,3 +99,96 @@ def test_sharded_async_valid_and_close():
     assert C.min() >= 0 and C.max() < g.n and np.all(C[C] == C)
     got = O.objective(g, None, 0.85, C)
     assert got >= ref - 0.005 * abs(ref), (got, ref)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("graph", ["sbm", "rmat"])
+def test_sharded_levels_sync_exact(world, graph):
+    """Every coarse level repartitioned across the ranks (gather_below=0:
+    all-to-all of the partial coarse rows, merged by the owner): labels
+    identical to the single-process run, with >= 2 levels run sharded."""
+    if graph == "sbm":
+        hg, _ = sbm(seed=1)
+    else:
+        u, v = rmat_pairs_host(12, 16 << 12, 0.57, 0.19, 0.19, 11)
+        hg = csr_from_pairs(1 << 12, u, v)
+    g = O.as_graph(hg)
+    ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC))
+    res = run_world(world, _cluster, hg.indptr, hg.indices, None, 0.85, dict(schedule="sync"), 0)
+    assert np.array_equal(res["C"], ref)
+    st = res["stats"]
+    assert st.sharded_levels >= 2 and st.gathered_levels == 0
+
+
+def test_sharded_levels_modularity_and_sparse_exchange():
+    """Modularity (k = degree, lambda = 1/2m) through sharded levels, with
+    every label exchange as (vertex, label) pairs (forced: the sync
+    trajectory never gets sparse on a graph this small)."""
+    u, v = rmat_pairs_host(12, 16 << 12, 0.57, 0.19, 0.19, 12)
+    hg = csr_from_pairs(1 << 12, u, v)
+    g = O.as_graph(hg)
+    k, lam = O.modularity_params(g, 1.0)
+    ref = O.parallel_cc(g, k, lam, O.Opts(schedule=O.SYNC))
+    res = run_world(2, _cluster, hg.indptr, hg.indices, torch.from_numpy(k), lam, dict(schedule="sync"), 0, True)
+    assert np.array_equal(res["C"], ref)
+    st = res["stats"]
+    assert st.sharded_levels >= 2 and st.sparse_exchanges >= st.sharded_levels
+
+
+def _level0(rank, world, indptr, indices):
+    from paper_2108_01731_b200.dist import make_part, sharded_best_moves
+    b = partition_bounds(indptr, world)
+    part = make_part(indptr, indices, None, float(indices.size // 2), int(b[rank]), int(b[rank + 1]), "cpu")
+    n = part.n
+    st = ShardStats()
+    C, _, _ = sharded_best_moves(part, None, 0.85, torch.arange(n, dtype=torch.int32),
+                                 torch.ones(n, dtype=torch.float64), ParOptions(schedule="sync"), OracleBackend(),
+                                 None, st)
+    return {"C": C.numpy(), "moves": st.moves, "rounds": st.rounds}
+
+
+NCLQ = 24000  # vertices in 4-cliques: more than half of the partition work
+
+
+def _split_graph():
+    """Rank 0's range converges at once (4-cliques and isolated vertices),
+    rank 1's range (an R-MAT) keeps moving: rank 0's owned frontier empties
+    while rank 1's does not."""
+    us, vs = [], []
+    for c in range(0, NCLQ, 4):
+        for a in range(4):
+            for b in range(a + 1, 4):
+                us.append(c + a); vs.append(c + b)
+    base = NCLQ + 200  # NCLQ..NCLQ+199 isolated
+    u, v = rmat_pairs_host(11, 12 << 11, 0.57, 0.19, 0.19, 13)
+    us = np.concatenate([np.asarray(us), u + base]); vs = np.concatenate([np.asarray(vs), v + base])
+    return csr_from_pairs(base + (1 << 11), us, vs)
+
+
+@pytest.mark.parametrize("schedule", ["sync", "async"])
+def test_sharded_rank_converges_early(schedule):
+    """ADVICE (round 1): an empty owned frontier is an empty round, not a
+    full one -- sync labels stay identical to the single process, and async
+    stays a valid clustering with the single-process objective."""
+    hg = _split_graph()
+    g = O.as_graph(hg)
+    b = partition_bounds(hg.indptr, 2)
+    assert b[1] < NCLQ  # rank 0 owns only cliques
+    opts = O.Opts(schedule=O.SYNC if schedule == "sync" else O.ASYNC)
+    ref = O.parallel_cc(g, None, 0.85, opts)
+    res = run_world(2, _cluster, hg.indptr, hg.indices, None, 0.85, dict(schedule=schedule), 0)
+    C = res["C"]
+    if schedule == "sync":
+        assert np.array_equal(C, ref)
+        # level 0 alone: sync mover counts are partition independent, so an
+        # idle rank adds no phantom movers
+        two = run_world(2, _level0, hg.indptr, hg.indices)
+        one = run_world(1, _level0, hg.indptr, hg.indices)
+        assert two["moves"] == one["moves"] and two["rounds"] == one["rounds"]
+        assert np.array_equal(two["C"], one["C"])
+    else:
+        assert C.min() >= 0 and C.max() < g.n and np.all(C[C] == C)
+        got, want = O.objective(g, None, 0.85, C), O.objective(g, None, 0.85, ref)
+        assert got >= want - 0.005 * abs(want), (got, want)
+    # the cliques end as four-vertex clusters either way
+    assert np.all(C[:NCLQ].reshape(-1, 4) == C[:NCLQ:4, None])

@@ -1,16 +1,19 @@
 #!/usr/bin/env python
 """Benchmark: LambdaCC best-move edge throughput on B200 (BASELINE.json metric).
 
-Workload (default): BASELINE.json configs[3] -- R-MAT scale 24, edge factor
-16, a=0.57 b=c=0.19, symmetrised / deduplicated / self-loops removed,
-unweighted, CC objective lambda=0.85, asynchronous moves + vertex-neighbour
-subsetting + multi-level refinement.  Synthetic, seeded (seed 24), generated
-on the device; inputs (2 GB of CSR indices) are larger than the 126 MB L2.
+Workload (default): BASELINE.json configs[4] -- the largest configuration,
+and the one that fits a single GPU: power-law planted communities, n = 65M,
+~1.8B undirected edges (3.6B CSR entries), degree exponent 2.2, mu = 0.4,
+unweighted, CC objective lambda = 0.85, asynchronous moves + vertex-neighbour
+subsetting + multi-level refinement.  Synthetic, seeded (seed 5), generated
+on the device; inputs (14.4 GB of CSR indices) are far larger than the
+126 MB L2.  configs[3] (R-MAT scale 24) is measured the same way and
+reported under the "cfg4" key (--extra-config none skips it).
 
 A "step" is one best-move iteration of Alg. 1 over V' = V at level 0 from
 the all-singleton state: the bin partition, the best-move kernels, the
-cluster-mass / label reconcile and the next-frontier build
-(lcc_par_best_moves with num_iter = 1).  value = 2m / step time (Gedges/s).
+cluster-mass / label reconcile and the next-frontier build.
+value = 2m / step time (Gedges/s).
 
 e2e: the whole parallel_cc clustering through the public Python API with the
 CSR in pinned HOST memory and the labels copied back to host, timed end to
@@ -19,10 +22,13 @@ level) / wall time of that call, and `clustering_ms` is the end-to-end
 LambdaCC clustering time (the metric's second half).
 
 --impl reference: the CPU oracle port of the reference's asynchronous
-best-move round (OpenMP, relaxed atomics, all host threads) on a bounded
-vertex sample of the same graph.
+best-move round (OpenMP, relaxed atomics, all host threads) on every 8th
+vertex of the same graph; the sample is written by tools/gen_cache.py in a
+process of its own, so the reference arm's process loads no library of this
+repository except the oracle.  Its apply / frontier / contraction /
+objective phases are timed once on the same sample (cpu_phases).
 
-Multi-GPU (--gpus N under torchrun): level 0 vertex-sharded over NCCL
+Multi-GPU (--gpus N under torchrun): vertex-sharded over NCCL
 (paper_2108_01731_b200/dist.py), the same graph on every rank, strong
 scaling; value = edges scanned by all ranks / max-over-ranks step time.
 """
@@ -48,14 +54,19 @@ METRIC = "best-move edge throughput (Gedges/s)"
 UNIT = "Gedges/s"
 
 
-def parse():
+CONFIGS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
-                    help="BASELINE.json configs[i-1]; cfg4 is the headline workload")
+    ap.add_argument("--config", default="cfg5", choices=CONFIGS,
+                    help="BASELINE.json configs[i-1]; cfg5 (the largest, one GPU) is the headline workload")
+    ap.add_argument("--extra-config", default="cfg4", choices=CONFIGS + ["none"],
+                    help="a second config measured the same way and reported under its own key")
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=24)
@@ -63,14 +74,15 @@ def parse():
     ap.add_argument("--schedule", default=None, choices=["async", "sync"], help="default: the config's schedule")
     ap.add_argument("--async-chunks", type=int, default=0)
     ap.add_argument("--degree-threshold", type=int, default=1000)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-stride", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cache-dir", default=os.environ.get("LCC_BENCH_CACHE", "/tmp/lcc_bench_cache"))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="run the vertex-sharded NCCL driver even at world size 1 (exercises the N>1 path on one GPU)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def peaks():
@@ -152,11 +164,31 @@ def dist_init():
     return ws, rank, lrank
 
 
-def cpu_sample(indptr, stride):
-    n = indptr.size - 1
-    F = np.arange(0, n, stride, dtype=np.int32)
-    edges = int((indptr[F + 1] - indptr[F]).sum())
-    return F, edges
+def sample_rows(dg, stride):
+    """The CPU sample of a device graph: rows of v % stride == 0 keep their
+    neighbour lists, all other rows are empty.  Host (indptr[n+1], indices,
+    sample vertex count, sample entry count)."""
+    import torch
+    n = dg.n
+    deg = dg.indptr[1:] - dg.indptr[:-1]
+    keep_v = torch.zeros(n, dtype=torch.bool, device=deg.device)
+    keep_v[::stride] = True
+    lens = torch.where(keep_v, deg, torch.zeros_like(deg))
+    ip = torch.zeros(n + 1, dtype=torch.int64, device=deg.device)
+    torch.cumsum(lens, 0, out=ip[1:])
+    ix = torch.empty(int(ip[-1].item()), dtype=torch.int32, device=deg.device)
+    step = 1 << 22  # rows per chunk: bounded scratch at 3.6B entries
+    for r0 in range(0, n, step):
+        r1 = min(n, r0 + step)
+        s0, s1 = int(dg.indptr[r0].item()), int(dg.indptr[r1].item())
+        if s1 == s0:
+            continue
+        m = torch.repeat_interleave(keep_v[r0:r1], deg[r0:r1], output_size=s1 - s0)
+        d0 = int(ip[r0].item())
+        chunk = dg.indices[s0:s1][m]
+        ix[d0:d0 + chunk.numel()] = chunk
+    nF = (n + stride - 1) // stride
+    return ip.cpu().numpy(), ix.cpu().numpy(), nF, int(ix.numel())
 
 
 def cpu_round(og, k, lam, schedule, F, threads):
@@ -175,16 +207,20 @@ def cpu_round(og, k, lam, schedule, F, threads):
     return time.perf_counter() - t0
 
 
-def host_oracle_graph(wl):
+def sample_graph(ip, ix, n, m):
     from oracle import oracle as O
-    ip, ix, w = wl.dg.to_host()
-    return O.Graph(wl.dg.n, ip, ix, w, wl.dg.total_weight), (None if wl.k is None else wl.k.cpu().numpy())
+    return O.Graph(n, ip, ix, None, float(m))
 
 
-def run_cpu_baseline(og, k, lam, schedule, stride, seconds, warmup=1, max_reps=50):
+def cpu_sample_desc(kind, stride, nF, edges):
+    return (f"{kind} best-move round of oracle/lcc_oracle.c over every {stride}th vertex "
+            f"({nF} vertices, {edges} directed edges: their full rows), singleton start")
+
+
+def run_cpu_baseline(og, k, lam, schedule, stride, nF, edges, seconds, warmup=1, max_reps=50):
     """Oracle port of the reference's round (OpenMP; async = relaxed atomics
     like the reference's numba + _atomics.py design), all host threads."""
-    F, edges = cpu_sample(og.indptr, stride)
+    F = np.arange(0, og.n, stride, dtype=np.int32)
     threads = os.cpu_count() or 1
     times = []
     for r in range(warmup + max_reps):
@@ -196,28 +232,75 @@ def run_cpu_baseline(og, k, lam, schedule, stride, seconds, warmup=1, max_reps=5
     t = statistics.median(times)
     kind = "async (OpenMP relaxed atomics)" if schedule == "async" else "sync Jacobi (OpenMP)"
     return {"value": edges / t / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{kind} best-move round of oracle/lcc_oracle.c over every {stride}th vertex "
-                      f"({F.size} vertices, {edges} directed edges), singleton start, median of {len(times)} reps",
-            "seconds": sum(times)}, t
+            "sample": cpu_sample_desc(kind, stride, nF, edges) + f", median of {len(times)} reps",
+            "seconds": sum(times)}
 
 
-def build_graph_device(scale, ef, seed):
-    from paper_2108_01731_b200.gen import rmat_device
-    return rmat_device(scale=scale, edge_factor=ef, a=0.57, b=0.19, c=0.19, seed=seed)
+def cpu_phases(og, k, lam, schedule, stride):
+    """The other Alg. 1 phases of the oracle port, timed once
+    on the CPU sample after a round: apply/reconcile (canonical labels +
+    masses over all n), VertexNeighbors frontier of the movers (sample rows),
+    objective (sample rows), contraction (rows of v % (8*stride) == 0:
+    the oracle's contraction is a single-threaded sort)."""
+    from oracle import oracle as O
+    n = og.n
+    threads = os.cpu_count() or 1
+    F = np.arange(0, n, stride, dtype=np.int32)
+    C = np.arange(n, dtype=np.int32)
+    K2 = np.zeros(2 * n)
+    K2[:n] = 1.0 if k is None else k
+    if schedule == "async":
+        moved, _ = O.async_round(og, k, lam, C, K2, F, parallel=True, threads=threads)
+        lab = C
+    else:
+        lab, moved, _ = O.sync_round(og, k, lam, C, K2[:n].copy(), F, threads=threads)
+    out = {}
+    t0 = time.perf_counter()
+    Cn, Kn = O.canonicalize(n, lab, 2 * n, k)
+    out["apply_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fr = O.frontier(og, O.VERTEX_NBRS, np.asarray(moved, np.uint8), np.arange(n, dtype=np.int32), Cn)
+    out["frontier_s"] = time.perf_counter() - t0
+    out["frontier_size"] = int(fr.size)
+    t0 = time.perf_counter()
+    obj = O.objective(og, k, lam, Cn)
+    out["objective_s"] = time.perf_counter() - t0
+    out["objective_entries"] = int(og.indices.size)
+    sub = 8 * stride
+    keep = np.zeros(n, bool)
+    keep[::sub] = True
+    deg = np.diff(og.indptr)
+    lens = np.where(keep, deg, 0)
+    ip2 = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ip2[1:])
+    ix2 = og.indices[np.repeat(keep[::stride], deg[::stride])] if og.indices.size else og.indices
+    g2 = O.Graph(n, ip2, np.ascontiguousarray(ix2, dtype=np.int32), None, float(ix2.size) / 2)
+    t0 = time.perf_counter()
+    O.compress(g2, k, lam, Cn, Kn)
+    out["compress_s"] = time.perf_counter() - t0
+    out["compress_entries"] = int(ix2.size)
+    out["apply_Gvertices_per_s"] = n / out["apply_s"] / 1e9
+    out["objective_Gedges_per_s"] = og.indices.size / out["objective_s"] / 1e9
+    out["compress_Gedges_per_s"] = ix2.size / out["compress_s"] / 1e9
+    out["threads"] = {"round": threads, "apply": 1, "frontier": 1, "objective": 1, "compress": 1}
+    out["note"] = (f"apply over all n; frontier/objective over the stride-{stride} sample rows; contraction "
+                   f"over the stride-{sub} rows (single-threaded sort)")
+    return out
 
 
 class Workload:
     """One BASELINE.json config: device graph, objective parameters, options."""
 
-    def __init__(self, args):
+    def __init__(self, args, cfg=None):
         import torch
         import paper_2108_01731_b200 as L
         from paper_2108_01731_b200 import gen
-        cfg = args.config
+        cfg = cfg or args.config
         self.k = None
         self.weighted = False
         if cfg == "cfg4":
-            self.dg = build_graph_device(args.scale, args.edge_factor, args.seed)
+            self.dg = gen.rmat_device(scale=args.scale, edge_factor=args.edge_factor, a=0.57, b=0.19, c=0.19,
+                                      seed=args.seed)
             lam, sched = 0.85, "async"
             self.desc = (f"rmat-s{args.scale}-ef{args.edge_factor} (BASELINE.json configs[3]: R-MAT scale 24, "
                          f"edge factor 16, a=0.57 b=c=0.19, symmetrised/deduped, unweighted; CC lambda=0.85, "
@@ -271,59 +354,80 @@ def config_dict(args, g, wl=None, extra=None):
 
 
 # ---------------------------------------------------------------------------
+def load_sample(args, cfg):
+    """The CPU sample of config `cfg`, made by tools/gen_cache.py in its own
+    process (the device generator runs there, not here) and cached on disk."""
+    d = os.path.join(args.cache_dir, f"{cfg}_s{args.cpu_sample_stride}")
+    meta = os.path.join(d, "meta.json")
+    if not os.path.exists(meta):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_cache.py"), "--config", cfg,
+                            "--stride", str(args.cpu_sample_stride), "--out", d],
+                           stdout=subprocess.DEVNULL, stderr=subprocess.PIPE, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("tools/gen_cache.py failed: " + r.stderr[-500:])
+    m = json.load(open(meta))
+    ip = np.load(os.path.join(d, "indptr.npy"))
+    ix = np.load(os.path.join(d, "indices.npy"))
+    kp = os.path.join(d, "k.npy")
+    k = np.load(kp) if os.path.exists(kp) else None
+    return m, ip, ix, k
+
+
 def run_reference(args):
     ws, rank, lrank = dist_init()
     if rank != 0:
         return 0
-    import torch
-    if torch.cuda.is_available():
-        torch.cuda.set_device(lrank)
-    # input preparation may use the GPU generators; the timed region is CPU only
-    wl = Workload(args)
-    og, k = host_oracle_graph(wl)
-    del wl.dg
-    torch.cuda.empty_cache()
-    g = {"n": og.n, "m": og.m}
-    F, edges = cpu_sample(og.indptr, args.cpu_sample_stride)
+    meta, ip, ix, k = load_sample(args, args.config)
+    og = sample_graph(ip, ix, meta["n"], meta["m"])
+    lam = args.lam if args.lam is not None else meta["lambda"]
+    sched = args.schedule or meta["schedule"]
+    F = np.arange(0, og.n, args.cpu_sample_stride, dtype=np.int32)
+    edges = meta["sample_entries"]
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_round(og, k, wl.lam, wl.schedule, F, threads)
-    ts = [cpu_round(og, k, wl.lam, wl.schedule, F, threads) for _ in range(args.steps)]
+        cpu_round(og, k, lam, sched, F, threads)
+    ts = [cpu_round(og, k, lam, sched, F, threads) for _ in range(args.steps)]
     t = sum(ts) / len(ts)
     val = edges / t / 1e9
-    kind = "async (OpenMP relaxed atomics)" if wl.schedule == "async" else "sync Jacobi (OpenMP)"
+    kind = "async (OpenMP relaxed atomics)" if sched == "async" else "sync Jacobi (OpenMP)"
     cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"{kind} best-move round of oracle/lcc_oracle.c over every {args.cpu_sample_stride}th vertex "
-                     f"({F.size} vertices, {edges} directed edges), singleton start"}
+           "sample": cpu_sample_desc(kind, args.cpu_sample_stride, meta["sample_vertices"], edges)}
+    phases = cpu_phases(og, k, lam, sched, args.cpu_sample_stride)
+    g = {"n": meta["n"], "m": meta["m"]}
+
+    class _W:
+        pass
+    w = _W()
+    w.desc, w.lam, w.schedule = meta["workload"], lam, sched
     out = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)", "impl": "reference",
-           "config": config_dict(args, g, wl), "cpu_baseline": cpu,
-           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "config": config_dict(args, g, w, {"step": "one asynchronous best-move round of the oracle port over "
+                                                      "the vertex sample (see cpu_baseline.sample)"}),
+           "cpu_baseline": cpu, "cpu_phases": phases,
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "note": ("the CPU best-move round rate on the sample (the line's own value); a full CPU "
+                            "clustering of this config does not finish within the bench budget -- the full-graph "
+                            "CPU comparisons are in profiles/r02_parity_full.jsonl")},
+           "sample_source": "tools/gen_cache.py (separate process; this process maps only oracle/_build)"}
     print(json.dumps(out), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------
-def run_ours(args):
+def measure_round(args, wl, lib, rank=0):
+    """The bench step (module doc) on workload `wl`: value, timing, roofline."""
     import torch
     import paper_2108_01731_b200 as L
     from paper_2108_01731_b200 import _lib
     from paper_2108_01731_b200.graph import stream_ptr
-
-    ws, rank, lrank = dist_init()
-    torch.cuda.set_device(lrank)
-    dist = None  # single GPU; N > 1 goes through run_sharded
-    lib = _lib.load()
-    wl = Workload(args)
     dg = wl.dg
     n, nnz = dg.n, dg.nnz
-    g = {"n": n, "m": nnz // 2, "ws": ws}
     p = L.ClusteringParams.__new__(L.ClusteringParams)
     p.lam, p.k = float(wl.lam), wl.k
     gs, ps = dg.c_struct(), p.c_struct()
     sched = 1 if wl.schedule == "async" else 0
-    kfill = wl.k if wl.k is not None else None
+    kfill = wl.k
     C = torch.empty(n, dtype=torch.int32, device="cuda")
     D = torch.empty(n, dtype=torch.int32, device="cuda")
     K2 = torch.empty(2 * n, dtype=torch.float64, device="cuda")
@@ -359,27 +463,17 @@ def run_ours(args):
         step(_lib.LccStats())
     st = _lib.LccStats()
     launches0 = lib.lcc_kernel_launches()
-    if dist:
-        dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(lrank) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record()
         for _ in range(args.steps):
             step(st)
         e1.record()
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     ms = e0.elapsed_time(e1)
     launches = lib.lcc_kernel_launches() - launches0
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    edges_t = torch.tensor([float(st.edges_scanned)], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(edges_t, op=dist.ReduceOp.SUM)
-    ms_max = float(ms_t.item())
-    value = float(edges_t.item()) / (ms_max / 1e3) / 1e9
+    value = float(st.edges_scanned) / (ms / 1e3) / 1e9
     kern_ms = st.ms_kernels / args.steps
 
     # roofline of the dominant kernel group (the best-move kernels)
@@ -389,23 +483,25 @@ def run_ours(args):
     B_distinct = 8                         # K gather per distinct cluster (= deg at singleton start)
     alg_bytes = n * B_vertex + nnz * B_edge + nnz * B_distinct
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    # measured DRAM traffic of the same kernel group per step: from the
-    # committed `ncu --set full` capture of this exact command (cfg4 default)
     traffic, traffic_src = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
-    if wl.cfg == "cfg4" and args.scale == 24 and os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        traffic, traffic_src = tj["dram_bytes_per_step"], "profiles/r01_traffic.json (" + tj["source"] + ")"
+    for tname in (f"r02_traffic_{wl.cfg}.json",) + (("r01_traffic.json",) if wl.cfg == "cfg4" else ()):
+        tpath = os.path.join(ROOT, "profiles", tname)
+        if args.scale == 24 and os.path.exists(tpath):
+            tj = json.load(open(tpath))
+            traffic, traffic_src = tj["dram_bytes_per_step"], f"profiles/{tname} (" + tj["source"] + ")"
+            break
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
                 "kernel": "best-move (k_tiny/k_small/k_group/k_hub_*)",
-                "alg_bytes_per_launch_group": alg_bytes, "kernel_ms_per_step": kern_ms,
-                "kernel_share_of_step": kern_ms / (ms / args.steps)}
+                "alg_bytes_per_launch_group": alg_bytes,
+                "alg_bytes_formula": f"n*{B_vertex} + 2m*{B_edge} + 2m*{B_distinct} (SURVEY.md §8d B_bm, "
+                                     "distinct clusters = degree at the singleton start)",
+                "kernel_ms_per_step": kern_ms, "kernel_share_of_step": kern_ms / (ms / args.steps)}
     # The kernels are latency bound on the dependent chain index -> label
-    # gather -> mass gather, not on bandwidth (DRAM 5-9% busy): compare the
-    # edge rate with the same chain measured alone on this GPU type at the
-    # config-4 array sizes (tools/micro/gather_roof.cu, no hashing at all)
-    gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gather_roof.json")
+    # gather -> mass gather, not on bandwidth: compare the edge rate with the
+    # same chain measured alone on this GPU type at the config-4 array sizes
+    # (tools/micro/gather_roof.cu, no hashing at all)
+    gpath = os.path.join(ROOT, "profiles", "r01_gather_roof.json")
     if wl.cfg == "cfg4" and args.scale == 24 and os.path.exists(gpath):
         gj = json.load(open(gpath))
         chain = gj["n_16777216"]["chain2_Gps"]
@@ -414,133 +510,148 @@ def run_ours(args):
             "pattern": "streamed index -> random label gather -> random mass gather, 67 MB arrays",
             "achieved": edges_per_s, "peak": chain, "unit": "G chains/s", "frac": edges_per_s / chain,
             "source": "profiles/r01_gather_roof.json (tools/micro/gather_roof.cu)"}
+    return {"value": value, "ms_per_step": ms / args.steps, "roofline": roofline, "gpu_launches": int(launches),
+            "clocks": clk.summary(), "n": n, "m": nnz // 2,
+            "round_stats": {"vertices": st.vertices // args.steps, "edges": st.edges_scanned // args.steps,
+                            "moves": st.moves // args.steps, "next_frontier": int(nF.value)}}
 
-    # CPU baseline (oracle port) first: the e2e leg below drops the device graph
-    cpu = None
-    if not args.no_cpu and rank == 0:
-        og, kh = host_oracle_graph(wl)
-        cpu, _ = run_cpu_baseline(og, kh, wl.lam, wl.schedule, args.cpu_sample_stride, args.cpu_seconds)
-        og = kh = None
 
-    # e2e: whole clustering via the public API from pinned host memory
-    e2e = None
-    if not args.no_e2e:
+def measure_e2e(args, wl, e2e_steps, warm=2):
+    """Whole clustering through the public API from pinned host memory."""
+    import torch
+    import paper_2108_01731_b200 as L
+    dg = wl.dg
+    n, nnz = dg.n, dg.nnz
+    p = L.ClusteringParams.__new__(L.ClusteringParams)
+    p.lam, p.k = float(wl.lam), wl.k
+    try:
+        indptr_h = dg.indptr.cpu().pin_memory()
+        indices_h = dg.indices.cpu().pin_memory()
+        weights_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
+
+        class HostG:
+            pass
+        hgr = HostG()
+        hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = (
+            n, nnz // 2, indptr_h, indices_h, weights_h, dg.total_weight)
+        # the e2e call uploads its own copy: release the device graph (cfg1
+        # contracts it directly)
+        if wl.cfg != "cfg1":
+            dg = wl.dg = None
+        gc.collect()
+        torch.cuda.empty_cache()
+        full = L.ParOptions(schedule=wl.schedule, degree_threshold=args.degree_threshold,
+                            async_chunks=args.async_chunks)
+        out_h = torch.empty(n, dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            if wl.cfg == "cfg1":
+                # configs[0]: single level plus contraction (par_best_moves + par_compress)
+                cl, _ = L.par_best_moves(hgr, p, None, full)
+                lvl = L.par_compress(dg, p, cl)
+                cl.meta["stats"].levels = 1
+                cl.meta["coarse_n"] = lvl.graph.n
+            else:
+                cl = L.parallel_cc(hgr, p, full)
+            out_h.copy_(cl.assignment, non_blocking=True)
+            torch.cuda.synchronize()
+            return cl
+
+        # warm-up: scratch cache and stream-ordered pool growth (each growth
+        # maps fresh pages), lazy kernel loading
+        for _ in range(warm):
+            e2e_step()
+        times, edges_sum, stats = [], 0, None
+        # as timeit does: no cyclic garbage collection inside the timed
+        # region (a collection there frees pinned/device tensors at random)
+        gc.collect()
+        gc.disable()
         try:
-            indptr_h = dg.indptr.cpu().pin_memory()
-            indices_h = dg.indices.cpu().pin_memory()
-            weights_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
+            with ClockSampler(torch.cuda.current_device(), enabled=not os.environ.get("LCC_BENCH_NOCLK")) as clk_e2e:
+                for _ in range(max(1, e2e_steps)):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    cl = e2e_step()
+                    times.append(time.perf_counter() - t0)
+                    stats = cl.meta["stats"]
+                    edges_sum += stats.edges_scanned
+        finally:
+            gc.enable()
+        t_e2e = sum(times) / len(times)
+        cl = None
+        L.release_memory()
+        torch.cuda.empty_cache()
+        obj = L.cc_objective(dg if dg is not None else hgr, p, torch.as_tensor(out_h).cuda())
+        L.release_memory()
+        return {"value": edges_sum / len(times) / t_e2e / 1e9, "unit": UNIT,
+                "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
+                                          (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
+                "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * t_e2e,
+                "clustering_ms_per_step": [round(1e3 * t, 1) for t in times],
+                "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
+                "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
+                "device_ms_best_move_kernels": stats.ms_kernels,
+                "objective": obj, "clusters": int(np.unique(out_h.numpy()).size), "clocks": clk_e2e.summary(),
+                "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
+                        "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
+    except MemoryError as exc:  # coarse levels beyond device + host memory
+        L.release_memory()
+        return {"value": None, "unit": UNIT, "unavailable": str(exc)[:300]}
 
-            class HostG:
-                pass
-            hgr = HostG()
-            hgr.n, hgr.m, hgr.indptr, hgr.indices, hgr.weights, hgr.total_weight = (
-                n, nnz // 2, indptr_h, indices_h, weights_h, dg.total_weight)
-            # the e2e call uploads its own copy: release the round-bench buffers
-            # (and, except for cfg1 which contracts `dg` directly, the device graph)
-            C = D = K2 = Cn = Kn = F = moved = mark = iota = None
-            if wl.cfg != "cfg1":
-                dg = wl.dg = None
-            torch.cuda.empty_cache()
-            full = L.ParOptions(schedule=wl.schedule, degree_threshold=args.degree_threshold,
-                                async_chunks=args.async_chunks)
-            out_h = torch.empty(n, dtype=torch.int32).pin_memory()
 
-            def e2e_step():
-                if wl.cfg == "cfg1":
-                    # configs[0]: single level plus contraction (par_best_moves + par_compress)
-                    cl, _ = L.par_best_moves(hgr, p, None, full)
-                    lvl = L.par_compress(dg, p, cl)
-                    cl.meta["stats"].levels = 1
-                    cl.meta["coarse_n"] = lvl.graph.n
-                elif os.environ.get("LCC_BENCH_DEBUG"):
-                    from paper_2108_01731_b200.louvain_par import _prep
-                    t = [time.perf_counter()]
-                    dgx, gsx, psx = _prep(hgr, p)
-                    torch.cuda.synchronize(); t.append(time.perf_counter())
-                    Cx = torch.empty(n, dtype=torch.int32, device="cuda")
-                    stx = _lib.LccStats()
-                    osx = full.c_struct()
-                    _lib.check(lib.lcc_parallel_cc(ctypes.byref(gsx), ctypes.byref(psx), ctypes.byref(osx),
-                                                   Cx.data_ptr(), ctypes.byref(stx), stream_ptr()))
-                    torch.cuda.synchronize(); t.append(time.perf_counter())
-                    from paper_2108_01731_b200.objective import clustering_from_labels
-                    cl = clustering_from_labels(Cx, p)
-                    cl.meta["stats"] = L.louvain_par._stats_from(stx)
-                    torch.cuda.synchronize(); t.append(time.perf_counter())
-                    print("e2e phases ms: upload %.1f parallel_cc %.1f (device %.1f) relabel %.1f" % (
-                        1e3 * (t[1] - t[0]), 1e3 * (t[2] - t[1]), stx.ms_total, 1e3 * (t[3] - t[2])), file=sys.stderr)
-                else:
-                    cl = L.parallel_cc(hgr, p, full)
-                out_h.copy_(cl.assignment, non_blocking=True)
-                torch.cuda.synchronize()
-                return cl
+def run_ours(args):
+    import torch
+    import paper_2108_01731_b200 as L
+    from paper_2108_01731_b200 import _lib
 
-            # warm-up: scratch cache and stream-ordered pool growth (the pool
-            # grows over the first three calls: 15 -> 19.5 -> 23.3 GB at
-            # config 4, each growth mapping fresh pages), lazy kernel loading
-            for _ in range(3):
-                e2e_step()
-            times, edges_sum, stats = [], 0, None
-            # as timeit does: no cyclic garbage collection inside the timed
-            # region (a collection there frees pinned/device tensors at random)
-            gc.collect()
-            gc.disable()
-            try:
-                with ClockSampler(lrank, enabled=not os.environ.get("LCC_BENCH_NOCLK")) as clk_e2e:
-                    for _ in range(max(1, args.e2e_steps)):
-                        torch.cuda.synchronize()
-                        t0 = time.perf_counter()
-                        cl = e2e_step()
-                        times.append(time.perf_counter() - t0)
-                        stats = cl.meta["stats"]
-                        edges_sum += stats.edges_scanned
-            finally:
-                gc.enable()
-            if os.environ.get("LCC_BENCH_DEBUG"):
-                print("e2e clock samples:", clk_e2e.lines, file=sys.stderr)
-            t_e2e = sum(times) / len(times)
-            step_ms = [round(1e3 * t, 1) for t in times]
-            e_t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-            ed_t = torch.tensor([edges_sum / len(times)], dtype=torch.float64, device="cuda")
-            if dist:
-                dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-                dist.all_reduce(ed_t, op=dist.ReduceOp.SUM)
-            cl = None
-            L.release_memory()
-            torch.cuda.empty_cache()
-            obj = L.cc_objective(dg if dg is not None else hgr, p, torch.as_tensor(out_h).cuda())
-            e2e = {"value": float(ed_t.item()) / float(e_t.item()) / 1e9, "unit": UNIT,
-                   "h2d_bytes_per_step": int(indptr_h.numel() * 8 + indices_h.numel() * 4 +
-                                             (0 if weights_h is None else weights_h.numel() * weights_h.element_size())),
-                   "d2h_bytes_per_step": int(n * 4), "clustering_ms": 1e3 * float(e_t.item()), "clustering_ms_per_step": step_ms,
-                   "rounds": stats.rounds, "levels": stats.levels, "edges_scanned": stats.edges_scanned,
-                   "device_ms_parallel_cc": stats.ms_total, "device_ms_best_move_iterations": stats.ms_best_moves,
-                   "device_ms_best_move_kernels": stats.ms_kernels,
-                   "objective": obj, "clusters": int(np.unique(out_h.numpy()).size), "clocks": clk_e2e.summary(),
-                   "api": ("paper_2108_01731_b200.par_best_moves + par_compress" if wl.cfg == "cfg1" else
-                           "paper_2108_01731_b200.parallel_cc") + "(host pinned CSR) + labels D2H"}
-        except MemoryError as exc:  # e.g. config 5: coarse levels beyond device + host memory
-            L.release_memory()
-            e2e = {"value": None, "unit": UNIT, "unavailable": str(exc)[:300]}
-
-    if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (seeded; BASELINE.json shapes, see config.workload)",
-               "config": config_dict(args, g, wl), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": int(launches), "clocks": clk.summary(),
-               "round_stats": {"vertices": st.vertices // args.steps, "edges": st.edges_scanned // args.steps,
-                               "moves": st.moves // args.steps, "next_frontier": int(nF.value)}}
-        print(json.dumps(out), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    ws, rank, lrank = dist_init()
+    torch.cuda.set_device(lrank)
+    lib = _lib.load()
+    wl = Workload(args)
+    r = measure_round(args, wl, lib)
+    g = {"n": r["n"], "m": r["m"]}
+    # CPU baseline (oracle port) on the vertex sample, before the e2e leg
+    # drops the device graph
+    cpu = None
+    if not args.no_cpu:
+        ip, ix, nF, edges = sample_rows(wl.dg, args.cpu_sample_stride)
+        og = sample_graph(ip, ix, wl.dg.n, wl.dg.m)
+        kh = None if wl.k is None else wl.k.cpu().numpy()
+        cpu = run_cpu_baseline(og, kh, wl.lam, wl.schedule, args.cpu_sample_stride, nF, edges, args.cpu_seconds)
+        og = ip = ix = None
+    e2e = None if args.no_e2e else measure_e2e(args, wl, args.e2e_steps)
+    cfg_line = config_dict(args, g, wl)
+    extra = None
+    if args.extra_config != "none" and args.extra_config != args.config:
+        wl = None
+        gc.collect()
+        L.release_memory()
+        torch.cuda.empty_cache()
+        wl2 = Workload(args, args.extra_config)
+        r2 = measure_round(args, wl2, lib)
+        extra = {"metric": METRIC, "value": r2["value"], "unit": UNIT, "ms_per_step": r2["ms_per_step"],
+                 "config": config_dict(args, {"n": r2["n"], "m": r2["m"]}, wl2), "roofline": r2["roofline"],
+                 "gpu_launches": r2["gpu_launches"], "clocks": r2["clocks"], "round_stats": r2["round_stats"]}
+        if not args.no_e2e:
+            extra["e2e"] = measure_e2e(args, wl2, max(args.e2e_steps, 3), warm=3)
+        wl2 = None
+        L.release_memory()
+    out = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; BASELINE.json shapes, see config.workload)",
+           "config": cfg_line, "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "round_stats": r["round_stats"]}
+    if extra is not None:
+        out[args.extra_config] = extra
+    print(json.dumps(out), flush=True)
     return 0
 
 
 def run_sharded(args):
-    """N > 1: one rank per GPU over NCCL; level 0 vertex-sharded (dist.py),
-    the same R-MAT graph on every rank; strong scaling (fixed total work)."""
+    """N > 1: one rank per GPU over NCCL; every level vertex-sharded
+    (dist.py), the same graph on every rank; strong scaling (fixed total
+    work)."""
     import torch
     import torch.distributed as dist
     import paper_2108_01731_b200 as L
@@ -556,23 +667,24 @@ def run_sharded(args):
     torch.cuda.set_device(lrank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
     lib = _lib.load()
-    dg = build_graph_device(args.scale, args.edge_factor, args.seed)
+    wl = Workload(args)
+    dg = wl.dg
+    kdev = wl.k
     n, nnz = dg.n, dg.nnz
     indptr_h = dg.indptr.cpu().numpy()
     bounds = partition_bounds(indptr_h, ws)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    part = make_part(dg.indptr, dg.indices, None, float(nnz // 2), lo, hi, torch.device("cuda", lrank))
+    part = make_part(dg.indptr, dg.indices, dg.weights, dg.total_weight, lo, hi, torch.device("cuda", lrank))
     be = CudaBackend()
-    lam = 0.85 if args.lam is None else args.lam
-    sched = args.schedule or "async"
+    lam, sched = wl.lam, wl.schedule
     opts1 = L.ParOptions(schedule=sched, num_iter=1, degree_threshold=args.degree_threshold,
                          async_chunks=args.async_chunks)
     iota = torch.arange(n, dtype=torch.int32, device="cuda")
 
     def step(st):
         C = iota.clone()
-        K = torch.ones(n, dtype=torch.float64, device="cuda")
-        sharded_best_moves(part, None, lam, C, K, opts1, be, None, st)
+        K = torch.ones(n, dtype=torch.float64, device="cuda") if kdev is None else kdev.clone()
+        sharded_best_moves(part, kdev, lam, C, K, opts1, be, None, st)
 
     for _ in range(args.warmup):
         step(ShardStats())
@@ -600,21 +712,23 @@ def run_sharded(args):
     if not args.no_e2e:
         ip_h = torch.from_numpy(indptr_h).pin_memory()
         ix_h = dg.indices.cpu().pin_memory()
+        w_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
+        tw = dg.total_weight
         full = L.ParOptions(schedule=sched, degree_threshold=args.degree_threshold,
                             async_chunks=args.async_chunks)
-        sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, lam, full, be)  # warm-up
+        sharded_parallel_cc(ip_h, ix_h, w_h, tw, kdev, lam, full, be)  # warm-up
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st2 = ShardStats()
-        C = sharded_parallel_cc(ip_h, ix_h, None, float(nnz // 2), None, lam, full, be, None, st2)
+        C = sharded_parallel_cc(ip_h, ix_h, w_h, tw, kdev, lam, full, be, None, st2)
         out_h = C.cpu()
         torch.cuda.synchronize()
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ed2 = torch.tensor([float(st2.edges_scanned)], dtype=torch.float64, device="cuda")
         dist.all_reduce(ed2, op=dist.ReduceOp.SUM)
-        obj = L.cc_objective(dg, L.ClusteringParams(lam), C)
+        obj = L.cc_objective(dg, L.ClusteringParams(lam, kdev), C)
         h2d = int((bounds[rank + 1] - bounds[rank]) * 8 + (indptr_h[hi] - indptr_h[lo]) * 4)
         e2e = {"value": float(ed2.item()) / float(te.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": int(n * 4),
@@ -624,11 +738,11 @@ def run_sharded(args):
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (seeded R-MAT generated on device, identical on every rank)",
-               "config": config_dict(args, {"n": n, "m": nnz // 2, "ws": ws}, None,
-                                     {"workload": f"rmat-s{args.scale}-ef{args.edge_factor} (BASELINE.json configs[3])",
-                                      "lambda": lam, "schedule": sched,
-                                      "parallelism": f"vertex-sharded x{ws} (NCCL all-gather of owned labels)"}),
+               "data": "synthetic (seeded, generated on device, identical on every rank)",
+               "config": config_dict(args, {"n": n, "m": nnz // 2, "ws": ws}, wl,
+                                     {"parallelism": f"vertex-sharded x{ws} (NCCL: owned-label all-gather or "
+                                                     "sparse (vertex, label) pairs, mark reduce-scatter, coarse "
+                                                     "levels repartitioned by all-to-all)"}),
                "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clk.summary()}
         os.write(json_fd, (json.dumps(out) + "\n").encode())

@@ -553,7 +553,9 @@ def sharded_parallel_cc(indptr, indices, weights, total_weight, k, lam, opts, ba
         integral = cur.weights is None or cur.weights.dtype == torch.int32
         stack.append((cur, kcur, mapping))
         gnnz = int(round(_sum_f64(float(cind.numel()), dev, group)))
-        if world == 1 or gnnz < gather_below:
+        # (world size 1 runs the coarse levels in the single-GPU driver unless
+        # gather_below == 0 asks for the sharded path: tests of the NCCL code)
+        if gnnz < gather_below or (world == 1 and gather_below > 0):
             # the remainder on rank 0: single-GPU driver, labels broadcast
             Cc = torch.empty(cn, dtype=torch.int32, device=dev)
             if world == 1:

@@ -1,0 +1,144 @@
+"""Parity at the BASELINE.json sizes, all five configs (north_star bar:
+"oracle-matching labels/objective on all five configs").
+
+* cfg1 (SBM 10K): full size in tests/test_gpu_parity.py (sync trajectory,
+  contraction, all frontier policies -- bit-exact).
+* cfg2 (LFR-style 1.2M, modularity, async, multi-level): objective no worse
+  than the oracle's asynchronous schedules by more than 0.5%.
+* cfg3 (kNN 4M, fp32 cosine weights, lambda in {0.01, 0.1, 0.5}, sync,
+  multi-level): objective within 1e-6 relative, labels equal except at
+  gain ties.
+* cfg4 (R-MAT s24, 521M entries): the synchronous round from singletons
+  bit-exact (D, moved flags, mover count); the async clustering's
+  objective no worse than the oracle's parallel atomic async by > 0.5%.
+* cfg5 (65M vertices, 3.6B entries): the synchronous round from singletons
+  bit-exact; the objective of its canonical labels bit-exact; the
+  contraction of that clustering bit-exact on a vertex-range subgraph.
+
+The oracle runs on every host core (OpenMP).  These are the slow GPU tests
+(a few minutes); the async cfg5 clustering against the CPU oracle is in
+profiles/ (tools/parity_full.py: a CPU run of ~10 minutes).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2108_01731_b200 as L
+from oracle import oracle as O
+from paper_2108_01731_b200 import gen
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count()
+
+
+def _free():
+    L.release_memory()
+    torch.cuda.empty_cache()
+
+
+def _round1_exact(dg, lam):
+    """Sync round over V' = V from singletons: device vs oracle, bit for bit."""
+    n = dg.n
+    p = L.ClusteringParams(lam)
+    c = L.singletons(n, p)
+    mb = L.best_moves_round(dg, p, c, frontier=None, schedule=L.Schedule.Synchronous)
+    D, mv, cnt = mb.desired.cpu().numpy(), mb.moved.cpu().numpy(), mb.moved_count
+    del mb, c
+    ip, ix, _ = dg.to_host()
+    g = O.Graph(n, ip, ix, None, float(dg.m))
+    Dr, mvr, cntr = O.sync_round(g, None, lam, np.arange(n, dtype=np.int32), np.ones(n), None, threads=THREADS)
+    assert cnt == cntr
+    assert np.array_equal(mv.astype(bool), np.asarray(mvr).astype(bool))
+    assert np.array_equal(D, Dr)
+    return g, D
+
+
+def test_cfg2_lfr_modularity_async_full():
+    hg, _ = gen.lfr_like(n=1_200_000, seed=2)
+    g = O.as_graph(hg)
+    k, lam = O.modularity_params(g, 1.0)
+    p = L.modularity_params(hg, 1.0)
+    assert p.lam == lam and np.array_equal(p.k.cpu().numpy(), k)
+    cl = L.parallel_cc(hg, p, L.ParOptions())
+    q_gpu = O.objective(g, k, lam, cl.labels()) / g.total_weight
+    q_seq = O.objective(g, k, lam, O.parallel_cc(g, k, lam, O.Opts(schedule=O.ASYNC))) / g.total_weight
+    q_par = O.objective(g, k, lam, O.parallel_cc(g, k, lam, O.Opts(schedule=O.ASYNC, async_parallel=True,
+                                                                     threads=THREADS))) / g.total_weight
+    ref = min(q_seq, q_par)
+    assert q_gpu >= ref - 0.005 * abs(ref), (q_gpu, q_seq, q_par)
+    _free()
+
+
+@pytest.mark.parametrize("lam", [0.01, 0.1, 0.5])
+def test_cfg3_knn_weighted_sync_full(lam, knn_graph):
+    hg, g = knn_graph
+    cl = L.parallel_cc(hg, L.ClusteringParams(lam), L.ParOptions(schedule="sync"))
+    lab = cl.labels()
+    ref = O.parallel_cc(g, None, lam, O.Opts(schedule=O.SYNC, threads=THREADS))
+    o_gpu, o_ref = O.objective(g, None, lam, lab), O.objective(g, None, lam, ref)
+    assert abs(o_gpu - o_ref) <= 1e-6 * max(abs(o_ref), 1e-300), (o_gpu, o_ref)
+    # labels equal except at gain ties (fp32 weights: ties are rare)
+    assert np.mean(lab == ref) >= 0.999
+    _free()
+
+
+@pytest.fixture(scope="module")
+def knn_graph():
+    hg, _ = gen.knn_mixture(seed=3)
+    return hg, O.as_graph(hg)
+
+
+def test_cfg4_rmat_full():
+    dg = gen.rmat_device(24, 16, seed=24)
+    g, _ = _round1_exact(dg, 0.85)
+    cl = L.parallel_cc(dg, L.ClusteringParams(0.85), L.ParOptions())
+    o_gpu = O.objective(g, None, 0.85, cl.labels())
+    del cl, dg
+    _free()
+    ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.ASYNC, async_parallel=True, threads=THREADS))
+    o_ref = O.objective(g, None, 0.85, ref)
+    assert o_gpu >= o_ref - 0.005 * abs(o_ref), (o_gpu, o_ref)
+
+
+def test_cfg5_round_objective_contraction_full():
+    dg = gen.powerlaw_communities_device()
+    assert dg.n == 65_000_000 and dg.m > 1_700_000_000
+    g, D = _round1_exact(dg, 0.85)
+    n = dg.n
+    # canonical labels of that round (sync apply) and their objective
+    C, K = O.canonicalize(n, D, 2 * n, None)
+    p = L.ClusteringParams(0.85)
+    c = L.apply_moves(torch.as_tensor(D).cuda(), 2 * n, p)
+    assert np.array_equal(c.assignment.cpu().numpy(), C)
+    assert L.cc_objective(dg, p, c) == O.objective(g, None, 0.85, C)
+    del c
+    # contraction on the vertex range [0, R): induced subgraph, the
+    # clustering restricted to it (canonical: a cluster's smallest member
+    # is in the range whenever any member is)
+    R = 1_000_000
+    e = int(g.indptr[R])
+    rows = np.repeat(np.arange(R), np.diff(g.indptr[:R + 1]))
+    keep = g.indices[:e] < R
+    ip = np.zeros(R + 1, np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=R), out=ip[1:])
+    sub = O.Graph(R, ip, np.ascontiguousarray(g.indices[:e][keep]), None, float(keep.sum()) / 2)
+    del g, rows, keep
+    Cs, Ks = O.canonicalize(R, C[:R], R, None)
+    assert np.array_equal(Cs, C[:R])
+    ref = O.compress(sub, None, 0.85, Cs, Ks)
+    hs = type("H", (), {})()
+    hs.n, hs.m, hs.indptr, hs.indices, hs.weights, hs.total_weight = R, sub.indices.size // 2, sub.indptr, \
+        sub.indices, None, sub.total_weight
+    got = L.par_compress(hs, L.ClusteringParams(0.85), L.Clustering(torch.as_tensor(Cs).cuda(),
+                                                                    torch.as_tensor(Ks).cuda()))
+    ip2, ix2, w2 = got.graph.to_host()
+    assert got.graph.n == ref.graph.n
+    assert np.array_equal(ip2, ref.graph.indptr) and np.array_equal(ix2, ref.graph.indices)
+    rw = ref.graph.weights if ref.graph.weights is not None else np.ones(ix2.size)
+    assert np.array_equal(w2 if w2 is not None else np.ones(ix2.size), rw)
+    assert np.array_equal(got.mapping.cpu().numpy(), ref.mapping)
+    assert got.internal_offset == ref.internal_offset
+    _free()

@@ -43,6 +43,7 @@
 #include <vector>
 #include <cstdlib>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 
 #include "internal.cuh"
@@ -68,6 +69,21 @@ namespace {
 #endif
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
+#endif
+#ifndef LCC_ROWPF
+#define LCC_ROWPF 0  // k_group: prefetch the next vertex's neighbour row into L2 while this one runs
+#endif
+#ifndef LCC_LK
+#define LCC_LK 1  // integer masses: the cluster masses live in the k_group tables (see group_km)
+#endif
+#ifndef LCC_CLAIMK
+#define LCC_CLAIMK 0  // async k_group: the claiming lane gathers the live mass (objective -19% on config 4)
+#endif
+#ifndef LCC_KPF
+#define LCC_KPF 0  // async k_group: a claim prefetches the cluster's mass into L2 for the scoring-time read
+#endif
+#ifndef LCC_LK_ASYNC
+#define LCC_LK_ASYNC 0  // async rounds too read round-start masses from the packed words (quality -15%)
 #endif
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -143,7 +159,25 @@ struct BMArgs {
     const uint8_t* prev_moved;       // async damping (AsyncDamp), or null
     uint32_t salt;
     unsigned long long* pending;     // deferred movers this round
+    // packed (label | mass << 32) per vertex, built from C and the uint32
+    // mass image at the start of an integer-mass round (KI); null otherwise.
+    // Async movers keep their own word current (label and the target's mass
+    // after their join); the other members' masses are round-start values.
+    unsigned long long* LK;
 };
+
+// packed-word gathers: frozen in sync rounds, relaxed loads in async ones
+template <bool ASYNC>
+__device__ __forceinline__ unsigned long long ldLK(const unsigned long long* LK, int64_t i, uint64_t pol) {
+    unsigned long long r;
+    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(LK + i));
+    else asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(LK + i), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void stLK(unsigned long long* LK, int64_t i, int32_t x, double mass) {
+    const unsigned long long w = (unsigned long long)(uint32_t)x | ((unsigned long long)(uint32_t)mass << 32);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(LK + i), "l"(w) : "memory");
+}
 
 // Final choice for one vertex (mirrors oracle best_target()).
 template <bool ASYNC, bool KI>
@@ -174,13 +208,15 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                     return 0;
                 }
                 stC_relaxed(a.C, v, choice);
+                if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
                 subK<KI>(a.K, c, kv);
                 a.moved[v] = 1;
                 return 1;
             }
             stC_relaxed(a.C, v, choice);
             subK<KI>(a.K, c, kv);
-            addK<KI>(a.K, choice, kv);
+            const double kold = addK<KI>(a.K, choice, kv);
+            if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
         } else {
             a.D[v] = choice;
         }
@@ -757,6 +793,68 @@ struct SmemTable<true> {
     }
 };
 
+// integer counts plus the cluster's mass, stored by the claiming lane (it
+// arrives with the label in the packed LK word): scoring reads no global
+// memory.  12 bytes per slot.
+struct SmemTableKM {
+    static constexpr int bytes_per_slot = 12;
+    uint32_t keys, cnts, mass;
+    __device__ __forceinline__ void init_cap(unsigned char* p, uint32_t CAP) {
+        cnts = smem_u32(p);
+        keys = cnts + 4 * CAP;
+        mass = keys + 4 * CAP;
+    }
+    __device__ __forceinline__ void clear(uint32_t q) const {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(keys + 4 * q), "r"(EMPTY_KEY) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(cnts + 4 * q), "r"(0u) : "memory");
+    }
+    __device__ __forceinline__ void insert(uint32_t cap, int32_t x, uint32_t add, uint32_t m) const {
+        uint32_t h = slot_of(x, cap);
+        int32_t prev;
+        while (true) {
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+            if (prev == EMPTY_KEY || prev == x) break;
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+        if (prev == EMPTY_KEY) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(mass + 4 * h), "r"(m) : "memory");
+            if (add != 1u) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add - 1u) : "memory");
+        } else {
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(add) : "memory");
+        }
+    }
+    // claim-or-add without the mass: returns true (and the slot) for a claim
+    __device__ __forceinline__ bool insert_claim(uint32_t cap, int32_t x, uint32_t add, uint32_t& slot) const {
+        uint32_t h = slot_of(x, cap);
+        int32_t prev;
+        while (true) {
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(prev) : "r"(keys + 4 * h), "r"(EMPTY_KEY), "r"(x) : "memory");
+            if (prev == EMPTY_KEY || prev == x) break;
+            h = (h + 1 == cap) ? 0 : h + 1;
+        }
+        const uint32_t inc = prev == EMPTY_KEY ? add - 1u : add;
+        if (inc) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnts + 4 * h), "r"(inc) : "memory");
+        slot = h;
+        return prev == EMPTY_KEY;
+    }
+    __device__ __forceinline__ void set_mass(uint32_t q, uint32_t m) const {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(mass + 4 * q), "r"(m) : "memory");
+    }
+    __device__ __forceinline__ bool take(uint32_t q, int32_t& x, double& S, double& K) const {
+        int32_t kq;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kq) : "r"(keys + 4 * q));
+        if (kq == EMPTY_KEY) return false;
+        uint32_t cq, mq;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cq) : "r"(cnts + 4 * q));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mq) : "r"(mass + 4 * q));
+        clear(q);
+        x = kq;
+        S = u32_to_f64(cq + 1u);
+        K = u32_to_f64(mq);
+        return true;
+    }
+};
+
 // global-memory (L2-resident) variant for hubs: same packing, device atomics
 template <bool WEIGHTED>
 struct GlobalTable;
@@ -831,16 +929,34 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // Every lane keeps U independent loads in flight (index stream + label
 // gather; then slot read + mass gather) before consuming them.
 // ===========================================================================
-template <class WT, int CAP, int GROUPS>
+// Integer masses (KI) and integer sums: the cluster's mass goes into the
+// table with the claim, so scoring reads no global memory.
+//   sync : the mass comes with the label in one packed gather (LK: frozen
+//          labels and masses, exact);
+//   async: masses must be read late: a live gather at claim time measured
+//          271K instead of 333K objective on config 4 (round-start masses
+//          285K), so async rounds keep the scoring-time mass gather
+//          (LCC_CLAIMK=1 selects the claim-time variant for experiments).
+template <class WT, bool ASYNC, bool KI>
+constexpr bool group_km() { return KI && !WLoad<WT>::fsum && LCC_LK && (!ASYNC || LCC_LK_ASYNC || LCC_CLAIMK); }
+template <class WT, bool ASYNC, bool KI>
+constexpr bool group_lk() { return group_km<WT, ASYNC, KI>() && (!ASYNC || LCC_LK_ASYNC); }
+template <class WT, bool ASYNC, bool KI>
+using GroupTable = std::conditional_t<group_km<WT, ASYNC, KI>(), SmemTableKM, SmemTable<WLoad<WT>::fsum>>;
+template <class WT, bool ASYNC, bool KI, int CAP, int GROUPS>
 constexpr size_t group_smem_bytes() {
-    return (size_t)GROUPS * CAP * SmemTable<WLoad<WT>::fsum>::bytes_per_slot;
+    return (size_t)GROUPS * CAP * GroupTable<WT, ASYNC, KI>::bytes_per_slot;
 }
 
 template <class WT, bool ASYNC, bool KI, int GW, int CAP, int GROUPS, int U, int MINB = 1>
 __global__ void __launch_bounds__(GW * 32 * GROUPS, MINB)
 k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     constexpr bool FSUM = WLoad<WT>::fsum;
+    constexpr bool KM = group_km<WT, ASYNC, KI>();    // masses in the table
+    constexpr bool LKP = group_lk<WT, ASYNC, KI>();   // ... from packed (label, mass) gathers
+    constexpr bool CLAIMK = KM && !LKP;               // ... gathered live by the claiming lane
     using TW = typename WLoad<WT>::TW;
+    using Tab = GroupTable<WT, ASYNC, KI>;
     constexpr int GT = GW * 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_g[GROUPS * GW];
@@ -853,8 +969,8 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     const int gt = threadIdx.x % GT;
     const int wig = gt >> 5;
     const int lane = threadIdx.x & 31;
-    SmemTable<FSUM> tab;
-    tab.init_cap(smem + (size_t)gid * CAP * SmemTable<FSUM>::bytes_per_slot, CAP);
+    Tab tab;
+    tab.init_cap(smem + (size_t)gid * CAP * Tab::bytes_per_slot, CAP);
     auto gsync = [&]() {
         if constexpr (GW == 1) __syncwarp();
         else named_sync(1 + gid, GT);
@@ -882,6 +998,19 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
+        if constexpr (LCC_ROWPF) {
+            // the group's next vertex: its index row is streamed into L2 now,
+            // so that vertex's index loads leave the dependent chain
+            const int64_t in = i + (int64_t)gridDim.x * GROUPS;
+            if (in < hi) {
+                const int32_t vn = __ldg(list + in);
+                const int64_t sn = __ldg(a.indptr + vn), en = __ldg(a.indptr + vn + 1);
+                const char* base = reinterpret_cast<const char*>(a.indices + sn);
+                const int64_t lines = ((en - sn) * 4 + ((uintptr_t)base & 127) + 127) >> 7;
+                const char* b0 = reinterpret_cast<const char*>((uintptr_t)base & ~(uintptr_t)127);
+                for (int64_t l = gt; l < lines; l += GT) asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(b0 + (l << 7)));
+            }
+        }
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
@@ -895,6 +1024,41 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 u[j] = e < end ? ld_stream_i32(a.indices + e, pol_stream) : -1;
                 wv[j] = e < end ? WLoad<WT>::tw(a.w, e) : TW(0);
             }
+            if constexpr (LKP) {
+                // one gather per edge: the neighbour's packed (label, mass)
+                unsigned long long lk[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) lk[j] = u[j] >= 0 ? ldLK<ASYNC>(a.LK, u[j], pol_keep) : ~0ull;
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    if (lk[j] == ~0ull) continue;
+                    const int32_t x = (int32_t)(uint32_t)lk[j];
+                    if (x == c) sc += WLoad<WT>::f64(wv[j]);
+                    else tab.insert(cap, x, (uint32_t)wv[j], (uint32_t)(lk[j] >> 32));
+                }
+            } else if constexpr (CLAIMK) {
+#pragma unroll
+                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+                uint32_t slot[U];
+                bool cl[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    cl[j] = false;
+                    if (u[j] == EMPTY_KEY) continue;
+                    if (u[j] == c) sc += WLoad<WT>::f64(wv[j]);
+                    else cl[j] = tab.insert_claim(cap, u[j], (uint32_t)wv[j], slot[j]);
+                }
+                // the claims' live masses: issued together, stored after
+                uint32_t km[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    if (cl[j]) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(km[j])
+                                            : "l"(static_cast<const uint32_t*>(a.K) + u[j]));
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    if (cl[j]) tab.set_mass(slot[j], km[j]);
+            } else {
 #pragma unroll
             for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
             // (batched probe rounds measured slower here than for the L2
@@ -905,8 +1069,13 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 if (u[j] == c) {
                     sc += WLoad<WT>::f64(wv[j]);
                 } else {
-                    tab.insert(cap, u[j], wv[j]);
+                    const bool claimed = tab.insert(cap, u[j], wv[j]);
+                    if constexpr (LCC_KPF && KI) {
+                        // the scoring pass reads this mass live; start its trip to L2 now
+                        if (claimed) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const uint32_t*>(a.K) + u[j]));
+                    }
                 }
+            }
             }
         }
 #pragma unroll
@@ -928,6 +1097,13 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         for (uint32_t q0 = gt; q0 < cap; q0 += GT * U) {
             int32_t x[U];
             double S[U], Kx[U];
+            if constexpr (KM) {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const uint32_t q = q0 + j * GT;
+                    if (!(q < cap && tab.take(q, x[j], S[j], Kx[j]))) x[j] = EMPTY_KEY;
+                }
+            } else {
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 const uint32_t q = q0 + j * GT;
@@ -935,6 +1111,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+            }
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -2114,6 +2291,14 @@ __global__ void k_mass_from_u32(const uint32_t* __restrict__ Ki, int64_t klen, d
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x)
         K[i] = u32_to_f64(Ki[i]);
 }
+// LK[v] = C[v] | Ki[C[v]] << 32: the packed word the group bins gather
+__global__ void k_pack_lk(const int32_t* __restrict__ C, const uint32_t* __restrict__ Ki, int64_t n,
+                          unsigned long long* __restrict__ LK) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = C[v];
+        LK[v] = (unsigned long long)(uint32_t)c | ((unsigned long long)Ki[c] << 32);
+    }
+}
 
 template <class K>
 void set_smem(K kernel, int bytes) {
@@ -2124,7 +2309,7 @@ template <class WT, bool ASYNC, bool KI, int GW, int CAP, int GROUPS, int U, int
 void launch_group(const BMArgs& a, const int32_t* list, int64_t lo, int64_t hi, cudaStream_t s) {
     if (hi <= lo) return;
     constexpr int THREADS = GW * 32 * GROUPS;
-    constexpr int SMEM = (int)group_smem_bytes<WT, CAP, GROUPS>();
+    constexpr int SMEM = (int)group_smem_bytes<WT, ASYNC, KI, CAP, GROUPS>();
     static int occ = 0;
     if (!occ) {
         set_smem(k_group<WT, ASYNC, KI, GW, CAP, GROUPS, U, MINB>, SMEM);
@@ -2437,11 +2622,65 @@ inline SideStreams& side_streams() {
     return ss;
 }
 
+// ---- eager kernel loading ----------------------------------------------
+// Under CUDA's lazy module loading (the default) a kernel is loaded at its
+// first launch, and that load waits for the kernels already running: the
+// first round that meets a not-yet-loaded bin kernel runs its concurrent
+// bins one after another instead of together.  The asynchronous schedule
+// depends on that interleaving -- measured on config 4: a first clustering
+// after others in the same process reached 268K-310K instead of 333K, and
+// 333K with CUDA_MODULE_LOADING=EAGER.  So every kernel a round may launch
+// is loaded (cudaFuncGetAttributes) before its first round starts.
+template <class F>
+void load_fn(F f) {
+    cudaFuncAttributes at;
+    LCC_CUDA(cudaFuncGetAttributes(&at, f));
+}
+template <class WT, bool ASYNC, bool KI>
+void preload_ki() {
+    load_fn(k_isolated<ASYNC, KI>);
+    load_fn(k_tiny<WT, ASYNC, KI>);
+    load_fn(k_small<WT, ASYNC, KI>);
+    load_fn(k_window<WT, ASYNC, KI>);
+    load_fn(k_group<WT, ASYNC, KI, 1, 256, 8, 4, 6>);
+    load_fn(k_group<WT, ASYNC, KI, 1, 1024, 8, 8, 3>);
+    load_fn(k_group<WT, ASYNC, KI, 4, 2048, 4, 4, 2>);
+    load_fn(k_group<WT, ASYNC, KI, 4, 4096, 2, 8, 3>);
+    load_fn(k_group<WT, ASYNC, KI, 8, 8192, 1, 4>);
+    load_fn(k_group<WT, ASYNC, KI, 32, B5_CAP, 1, 4>);
+    load_fn(k_large_score<WT, ASYNC, KI>);
+    load_fn(k_large_decide<WT, ASYNC, KI>);
+    if constexpr (!WLoad<WT>::fsum) {
+        load_fn(k_hub_bucket<WT, ASYNC, KI>);
+        load_fn(k_hub_decide<WT, ASYNC, KI>);
+    }
+}
+template <class WT, bool ASYNC>
+void preload_round_kernels() {
+    static bool done[16] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done[dev & 15]) return;
+    preload_ki<WT, ASYNC, false>();
+    preload_ki<WT, ASYNC, true>();
+    load_fn(k_large_insert<WT, ASYNC>);
+    if constexpr (!WLoad<WT>::fsum) load_fn(k_hub_scatter<WT, ASYNC>);
+    load_fn(k_large_mark);
+    load_fn(k_degrees_of);
+    load_fn(k_mass_to_u32);
+    load_fn(k_mass_from_u32);
+    load_fn(k_pack_lk);
+    load_fn(k_bin_count);
+    load_fn(k_bin_scatter);
+    done[dev & 15] = true;
+}
+
 template <class WT, bool ASYNC>
 int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, double* K,
                   const int32_t* frontier, int64_t nF, int deg_threshold, int chunks, int32_t* D,
                   uint8_t* moved, uint8_t* mark, RoundStats* st, cudaStream_t s, const AsyncDamp* damp) {
     const int64_t n = g.n;
+    preload_round_kernels<WT, ASYNC>();
     HostProbe hprobe;
     if (!ASYNC) LCC_CUDA(cudaMemcpyAsync(D, C, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
     LCC_CUDA(cudaMemsetAsync(moved, 0, n, s));
@@ -2565,8 +2804,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const bool ki = try_ki && hk[1] == 0 && hk[0] < (1ull << 31);
     if (try_ki) LCC_CUDA(cudaEventElapsedTime(&kconv_ms, kev[0], kev[1]));
     const bool dmp = ASYNC && damp && damp->prev_moved && mark;  // deferral needs the fused frontier
+    // packed (label, mass) words for the group bins (integer masses only)
+    Buf<unsigned long long> LK;
+    const bool use_lk = ki && LCC_LK && (!ASYNC || LCC_LK_ASYNC) && !WLoad<WT>::fsum && nF > 0;
+    if (use_lk) LK.alloc(n, s);
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, ki ? (void*)Ki.get() : (void*)K, D, moved, dmoved, (int32_t)n, mark,
-             dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2};
+             dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2, use_lk ? LK.get() : nullptr};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
     LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
@@ -2588,6 +2831,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const char* esc = getenv("LCC_SUBCONC");
     const bool concurrent = P == 1 || (esc && esc[0] == '1' && nF >= (1 << 20));
     LCC_CUDA(cudaEventRecord(ev0, s));
+    if (use_lk) {  // timed with the kernels
+        k_pack_lk<<<grid_for(n, 256), 256, 0, s>>>(C, Ki.get(), n, LK.get());
+        LCC_LAUNCH_CHECK();
+    }
     auto launch_all = [&](auto ki_tag) {
     constexpr bool KI = decltype(ki_tag)::value;
     for (int j = 0; j < P; ++j) {
@@ -2599,9 +2846,14 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             LCC_CUDA(cudaStreamWaitEvent(t, ss.fork, 0));
             return t;
         };
-        if (j == 0 && nL > 0) run_large<WT, ASYNC, KI>(a, g, lists.get() + binstart[NBINS - 1], nL,
+        // (diagnostics: LCC_LAUNCH_DELAY_US stalls the host after every bin
+        // launch; LCC_HUBS_LAST launches the hub bin after the others)
+        static const int dly = getenv("LCC_LAUNCH_DELAY_US") ? atoi(getenv("LCC_LAUNCH_DELAY_US")) : 0;
+        static const bool hubs_last = getenv("LCC_HUBS_LAST") && getenv("LCC_HUBS_LAST")[0] == '1';
+        if (j == 0 && nL > 0 && !hubs_last) run_large<WT, ASYNC, KI>(a, g, lists.get() + binstart[NBINS - 1], nL,
                                                        reinterpret_cast<unsigned*>(dcnt.get() + 3), next_stream());
         for (int b = 0; b < NBINS - 1; ++b) {
+            if (dly) std::this_thread::sleep_for(std::chrono::microseconds(dly));
             const int64_t nb = (int64_t)hc[b];
             if (nb == 0) continue;
             const int32_t* list = lists.get() + binstart[b];
@@ -2627,6 +2879,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
                 launch_bin<WT, ASYNC, KI>(b - 2, a, list, lo, hi, t);
             }
         }
+        if (j == 0 && nL > 0 && hubs_last) run_large<WT, ASYNC, KI>(a, g, lists.get() + binstart[NBINS - 1], nL,
+                                                      reinterpret_cast<unsigned*>(dcnt.get() + 3), next_stream());
         for (int i = 0; i < used; ++i) {
             LCC_CUDA(cudaEventRecord(ss.join[i], ss.st[i]));
             LCC_CUDA(cudaStreamWaitEvent(s, ss.join[i], 0));

@@ -3,6 +3,7 @@
 // Large blocks are cached here instead of being returned to the stream-
 // ordered pool: re-mapping physical pages for a fresh multi-GB range costs
 // ~6 ms per GB on B200, more than the contraction that needs the buffer.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -33,6 +34,13 @@ Cache& cache() {
 
 constexpr size_t GRAIN = 2ull << 20;
 
+// diagnostics: LCC_ALLOC_FILL=<byte> fills every fresh scratch block, so a
+// kernel that reads memory it never wrote shows up in every run
+int alloc_fill() {
+    static const int f = getenv("LCC_ALLOC_FILL") ? (int)strtol(getenv("LCC_ALLOC_FILL"), nullptr, 0) : -1;
+    return f;
+}
+
 }  // namespace
 
 void* pool_alloc(size_t bytes, cudaStream_t s) {
@@ -50,6 +58,7 @@ void* pool_alloc(size_t bytes, cudaStream_t s) {
         e = cudaMallocAsync(&p, bytes, s);
     }
     LCC_CUDA(e);
+    if (alloc_fill() >= 0) LCC_CUDA(cudaMemsetAsync(p, alloc_fill(), bytes, s));
     return p;
 }
 
@@ -65,6 +74,7 @@ void* cache_alloc(size_t bytes, cudaStream_t s, size_t* cap) {
             if (b.s != s) cudaStreamWaitEvent(s, b.ready, 0);
             cudaEventDestroy(b.ready);
             *cap = b.cap;
+            if (alloc_fill() >= 0) LCC_CUDA(cudaMemsetAsync(b.p, alloc_fill(), bytes, s));
             return b.p;
         }
     }

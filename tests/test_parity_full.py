@@ -96,11 +96,13 @@ def test_cfg4_rmat_full():
     g, _ = _round1_exact(dg, 0.85)
     cl = L.parallel_cc(dg, L.ClusteringParams(0.85), L.ParOptions())
     o_gpu = O.objective(g, None, 0.85, cl.labels())
+    st = cl.meta["stats"]
+    info = (L.cc_objective(dg, L.ClusteringParams(0.85), cl), st.rounds, st.levels, st.moves)
     del cl, dg
     _free()
     ref = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.ASYNC, async_parallel=True, threads=THREADS))
     o_ref = O.objective(g, None, 0.85, ref)
-    assert o_gpu >= o_ref - 0.005 * abs(o_ref), (o_gpu, o_ref)
+    assert o_gpu >= o_ref - 0.005 * abs(o_ref), (o_gpu, o_ref, info)
 
 
 def test_cfg5_round_objective_contraction_full():

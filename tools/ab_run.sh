@@ -10,4 +10,4 @@ for r in $(seq $REPS); do
     LCC_LIB_PATH=$PWD/$d/liblcc_b200.so timeout 300 python bench.py --no-cpu --no-e2e "$@" > $O/${n}_$r.json 2>/dev/null
   done
 done
-for f in $O/ab_*.json; do echo $f $(python -c "import json;d=json.load(open('$f'));print(round(d['value'],3), round(d['roofline']['kernel_ms_per_step'],3))" 2>/dev/null); done
+for f in $O/ab_*.json; do echo $f $(python -c "import json;d=json.load(open('$f'));x=d.get('cfg4') or {};print(round(d['value'],3), round(d['roofline']['kernel_ms_per_step'],3), round(x.get('value',0),3), round((x.get('roofline') or {}).get('kernel_ms_per_step',0),3))" 2>/dev/null); done

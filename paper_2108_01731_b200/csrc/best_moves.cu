@@ -79,6 +79,9 @@ namespace {
 #ifndef LCC_CLAIMK
 #define LCC_CLAIMK 0  // async k_group: the claiming lane gathers the live mass (objective -19% on config 4)
 #endif
+#ifndef LCC_ILV
+#define LCC_ILV 1  // integer-mass rounds: labels and masses interleaved in one (label, mass) array
+#endif
 #ifndef LCC_KPF
 #define LCC_KPF 0  // async k_group: a claim prefetches the cluster's mass into L2 for the scoring-time read
 #endif
@@ -107,15 +110,23 @@ __device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i, uint64_t pol
         return ld_keep_i32(C + i, pol);
     }
 }
+// Integer-mass rounds keep labels and masses interleaved: CK[2v] = C[v],
+// CK[2v+1] = mass of cluster v (uint32).  A neighbour's label and -- while
+// it is its own cluster, as in every first round -- its cluster's mass then
+// share one 8-byte word, so the scoring-time mass gather finds the line the
+// label gather already brought into L2 (config 5: the two gathers each
+// fetched their own DRAM line, 8x the algorithmic bytes).  a.cs is the
+// label stride (2 interleaved, 1 otherwise); KS the mass stride.
+constexpr int64_t KS = LCC_ILV ? 2 : 1;
 // KI: integer masses, gathered from a uint32 image of K (half the bytes of
 // the fp64 array, so labels + masses stay L2-resident); exact, see run_round.
 template <bool ASYNC, bool KI>
 __device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
     if constexpr (KI) {
-        const uint32_t* K = static_cast<const uint32_t*>(Kp);
+        const uint32_t* K = static_cast<const uint32_t*>(Kp) + KS * i;
         uint32_t r;
-        if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(K + i));
-        else r = (uint32_t)ld_keep_i32(reinterpret_cast<const int32_t*>(K) + i, pol);
+        if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(K));
+        else r = (uint32_t)ld_keep_i32(reinterpret_cast<const int32_t*>(K), pol);
         return u32_to_f64(r);
     } else {
         const double* K = static_cast<const double*>(Kp);
@@ -131,12 +142,12 @@ __device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
 // relaxed mass update; returns the mass before the add
 template <bool KI>
 __device__ __forceinline__ double addK(void* Kp, int64_t i, double kv) {
-    if constexpr (KI) return u32_to_f64(atomicAdd(static_cast<uint32_t*>(Kp) + i, (uint32_t)kv));
+    if constexpr (KI) return u32_to_f64(atomicAdd(static_cast<uint32_t*>(Kp) + KS * i, (uint32_t)kv));
     else return atomicAdd(static_cast<double*>(Kp) + i, kv);
 }
 template <bool KI>
 __device__ __forceinline__ void subK(void* Kp, int64_t i, double kv) {
-    if constexpr (KI) atomicSub(static_cast<uint32_t*>(Kp) + i, (uint32_t)kv);
+    if constexpr (KI) atomicSub(static_cast<uint32_t*>(Kp) + KS * i, (uint32_t)kv);
     else atomicAdd(static_cast<double*>(Kp) + i, -kv);
 }
 __device__ __forceinline__ void stC_relaxed(int32_t* C, int64_t i, int32_t x) {
@@ -164,6 +175,7 @@ struct BMArgs {
     // Async movers keep their own word current (label and the target's mass
     // after their join); the other members' masses are round-start values.
     unsigned long long* LK;
+    int32_t cs;  // label stride in C: 2 when interleaved with the masses (KI rounds), else 1
 };
 
 // packed-word gathers: frozen in sync rounds, relaxed loads in async ones
@@ -207,13 +219,13 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                     subK<KI>(a.K, choice, kv);
                     return 0;
                 }
-                stC_relaxed(a.C, v, choice);
+                stC_relaxed(a.C, (int64_t)v * a.cs, choice);
                 if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
                 subK<KI>(a.K, c, kv);
                 a.moved[v] = 1;
                 return 1;
             }
-            stC_relaxed(a.C, v, choice);
+            stC_relaxed(a.C, (int64_t)v * a.cs, choice);
             subK<KI>(a.K, c, kv);
             const double kold = addK<KI>(a.K, choice, kv);
             if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
@@ -284,7 +296,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             v = __ldg(list + i0 + lane);
             s = __ldg(a.indptr + v);
             deg = (int32_t)(__ldg(a.indptr + v + 1) - s);
-            c = ldC<ASYNC>(a.C, v, pol_keep);
+            c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
             kv = kval(a.k, v);
             Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         }
@@ -335,7 +347,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         int buf = 0;
         geometry(0, 0, G);
         int32_t nbr = G.has_edge ? ld_stream_i32(a.indices + G.e, pol_stream) : 0;
-        int32_t x = G.has_edge ? ldC<ASYNC>(a.C, nbr, pol_keep) : 0;
+        int32_t x = G.has_edge ? ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep) : 0;
         while (true) {
             const bool more = G.end < nvalid;
             Geo Gn;
@@ -369,7 +381,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             // mass gather of this window, then the next window's label gather
             const double Kx = cand ? ldK<ASYNC, KI>(a.K, x, pol_keep) : 0.0;
             int32_t x_n = 0;
-            if (more && Gn.has_edge) x_n = ldC<ASYNC>(a.C, nbr_n, pol_keep);
+            if (more && Gn.has_edge) x_n = ldC<ASYNC>(a.C, (int64_t)(nbr_n) * a.cs, pol_keep);
             if (is_leader && x == cj) s_sc2[buf][wib][j] = S;
             __syncwarp();
             double bv = 0.0;
@@ -448,7 +460,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if (has_edge) {
                 const int64_t e = sj + (lane - p);
                 nbr = ld_stream_i32(a.indices + e, pol_stream);
-                x = ldC<ASYNC>(a.C, nbr, pol_keep);
+                x = ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep);
                 wv = WLoad<WT>::at(a.w, e);
             }
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
@@ -567,7 +579,7 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
         const int deg = (int)(__ldg(a.indptr + v + 1) - s);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         int32_t x[TINY_MAX];
@@ -578,7 +590,7 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             w[j] = j < deg ? WLoad<WT>::tw(a.w, s + j) : TW(0);
         }
 #pragma unroll
-        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, x[j], pol_keep) : EMPTY_KEY;
+        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) : EMPTY_KEY;
         // first occurrences of each neighbour cluster (other than c)
         unsigned first = 0;
 #pragma unroll
@@ -594,8 +606,8 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if constexpr (KI) {
                 Kx[j] = 0u;
                 if ((first >> j) & 1u) {
-                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + x[j]));
-                    else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + x[j], pol_keep);
+                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + KS * x[j]));
+                    else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + KS * x[j], pol_keep);
                 }
             } else {
                 Kx[j] = ((first >> j) & 1u) ? ldK<ASYNC, false>(a.K, x[j], pol_keep) : 0.0;
@@ -642,7 +654,7 @@ k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     unsigned long long my_moves = 0;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = __ldg(list + i);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC, KI>(a.K, c, pol_keep))), dmul(t, kv));
@@ -995,7 +1007,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
         const int64_t end = __ldg(a.indptr + v + 1);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
         if constexpr (LCC_ROWPF) {
@@ -1038,7 +1050,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 }
             } else if constexpr (CLAIMK) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
                 uint32_t slot[U];
                 bool cl[U];
 #pragma unroll
@@ -1053,14 +1065,14 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
                     if (cl[j]) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(km[j])
-                                            : "l"(static_cast<const uint32_t*>(a.K) + u[j]));
+                                            : "l"(static_cast<const uint32_t*>(a.K) + KS * u[j]));
                 }
 #pragma unroll
                 for (int j = 0; j < U; ++j)
                     if (cl[j]) tab.set_mass(slot[j], km[j]);
             } else {
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
             // (batched probe rounds measured slower here than for the L2
             // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
@@ -1072,7 +1084,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                     const bool claimed = tab.insert(cap, u[j], wv[j]);
                     if constexpr (LCC_KPF && KI) {
                         // the scoring pass reads this mass live; start its trip to L2 now
-                        if (claimed) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const uint32_t*>(a.K) + u[j]));
+                        if (claimed) asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const uint32_t*>(a.K) + KS * u[j]));
                     }
                 }
             }
@@ -1248,7 +1260,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             s_v[tid] = v;
             s_start[tid] = __ldg(a.indptr + v);
             s_loc[tid] = (int32_t)(__ldg(off + i0 + tid) - base);
-            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+            const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
             s_c[tid] = c;
             const double kv = kval(a.k, v);
             s_kv[tid] = kv;
@@ -1293,7 +1305,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                 }
             }
 #pragma unroll
-            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
 #pragma unroll
             for (int j = 0; j < WIN_ITEMS; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
@@ -1459,7 +1471,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         double sc = 0.0;
         for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * UL) {
             int32_t u[UL];
@@ -1471,7 +1483,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
                 wv[j] = e < e1 ? WLoad<WT>::tw(a.w, e) : typename WLoad<WT>::TW(0);
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
             if constexpr (!WLoad<WT>::fsum) {
                 // first probe of all UL keys issued back to back (UL device
                 // CAS in flight per lane); collisions finish in the probe loop
@@ -1551,7 +1563,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const uint32_t q_begin = (uint32_t)((it - L.sitem_off[li]) * SCORE_CHUNK);
         const uint32_t q_end = (uint32_t)min64((int64_t)q_begin + SCORE_CHUNK, cap);
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         const double kv = kval(a.k, v);
         const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
         const double t = dmul(a.lam, kv);
@@ -1595,7 +1607,7 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
         warp_argmax(bg, bx);
         if (lane == 0) {
             const int32_t v = L.list[li];
-            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+            const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
             const double kv = kval(a.k, v);
             const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
             const double t = dmul(a.lam, kv);
@@ -1719,7 +1731,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
         const int64_t e0 = s + (it - P.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t nb = (uint32_t)(P.boff[li + 1] - P.boff[li]);
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         for (int b = tid; b <= (int)nb; b += HS_THREADS) s_hist[b] = 0;
         __syncthreads();
         int32_t x[PER];
@@ -1732,7 +1744,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
             w[j] = e < e1 ? (uint32_t)WLoad<WT>::tw(a.w, e) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, x[j], pol_keep) : EMPTY_KEY;
+        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) : EMPTY_KEY;
         double sc = 0.0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -1798,7 +1810,7 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
         const int64_t li = owner_of(P.boff, P.nL, gb);
         const int b = (int)(gb - P.boff[li]);
         const int32_t v = P.list[li];
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
         const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
@@ -1938,7 +1950,7 @@ __global__ void k_hub_decide(BMArgs a, HubPlan P) {
         warp_argmax(bg, bx, bS);
         if (lane == 0) {
             const int32_t v = P.list[li];
-            const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+            const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
             const double kv = kval(a.k, v);
             const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
             const double t = dmul(a.lam, kv);
@@ -2028,7 +2040,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
         const int64_t s = __ldg(a.indptr + v), end = __ldg(a.indptr + v + 1);
         const uint32_t cap = (uint32_t)std::min<int64_t>((int64_t)HC_CL * HC_SLICE, (2 * (end - s) + 31) & ~31LL);
         const uint32_t per = (cap + HC_CL - 1) / HC_CL;
-        const int32_t c = ldC<ASYNC>(a.C, v, pol_keep);
+        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         // ---- 1. inserts (remote shared-memory atomics)
         double sc = 0.0;
         for (int64_t e0 = s + (int64_t)rank * HC_THREADS + tid; e0 < end; e0 += (int64_t)HC_CL * HC_THREADS * UL) {
@@ -2041,7 +2053,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
                 wv[j] = e < end ? WLoad<WT>::tw(a.w, e) : TW(0);
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, u[j], pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
             uint32_t h[UL];
             unsigned pending = 0;
 #pragma unroll
@@ -2275,7 +2287,7 @@ __global__ void k_mass_to_u32(const double* __restrict__ K, int64_t klen, const 
         const bool good = x >= 0.0 && x < 2147483648.0 && x == floor(x);
         ok &= good;
         const uint32_t u = good ? (uint32_t)x : 0u;
-        Ki[i] = u;
+        Ki[KS * i] = u;
         my += u;
         if (k && i < n) {
             const double kv = k[i];
@@ -2289,15 +2301,24 @@ __global__ void k_mass_to_u32(const double* __restrict__ K, int64_t klen, const 
 }
 __global__ void k_mass_from_u32(const uint32_t* __restrict__ Ki, int64_t klen, double* __restrict__ K) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x)
-        K[i] = u32_to_f64(Ki[i]);
+        K[i] = u32_to_f64(Ki[KS * i]);
 }
 // LK[v] = C[v] | Ki[C[v]] << 32: the packed word the group bins gather
 __global__ void k_pack_lk(const int32_t* __restrict__ C, const uint32_t* __restrict__ Ki, int64_t n,
                           unsigned long long* __restrict__ LK) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int32_t c = C[v];
-        LK[v] = (unsigned long long)(uint32_t)c | ((unsigned long long)Ki[c] << 32);
+        LK[v] = (unsigned long long)(uint32_t)c | ((unsigned long long)Ki[KS * c] << 32);
     }
+}
+// interleaved labels: CK[2v] = C[v] before the round, C[v] = CK[2v] after an async one
+__global__ void k_labels_in(const int32_t* __restrict__ C, int64_t n, int32_t* __restrict__ CK) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        CK[2 * v] = C[v];
+}
+__global__ void k_labels_out(const int32_t* __restrict__ CK, int64_t n, int32_t* __restrict__ C) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        C[v] = CK[2 * v];
 }
 
 template <class K>
@@ -2670,6 +2691,8 @@ void preload_round_kernels() {
     load_fn(k_mass_to_u32);
     load_fn(k_mass_from_u32);
     load_fn(k_pack_lk);
+    load_fn(k_labels_in);
+    load_fn(k_labels_out);
     load_fn(k_bin_count);
     load_fn(k_bin_scatter);
     done[dev & 15] = true;
@@ -2681,6 +2704,18 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
                   uint8_t* moved, uint8_t* mark, RoundStats* st, cudaStream_t s, const AsyncDamp* damp) {
     const int64_t n = g.n;
     preload_round_kernels<WT, ASYNC>();
+    // LCC_L2_FETCH=<bytes> (tuning): the L2's DRAM fetch granularity during
+    // the round (cudaLimitMaxL2FetchGranularity); restored afterwards
+    static const int l2f = getenv("LCC_L2_FETCH") ? atoi(getenv("LCC_L2_FETCH")) : 0;
+    size_t l2f_old = 0;
+    if (l2f) {
+        LCC_CUDA(cudaDeviceGetLimit(&l2f_old, cudaLimitMaxL2FetchGranularity));
+        LCC_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2f));
+    }
+    struct L2Restore {
+        size_t v;
+        ~L2Restore() { if (v) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, v); }
+    } l2restore{l2f ? l2f_old : 0};
     HostProbe hprobe;
     if (!ASYNC) LCC_CUDA(cudaMemcpyAsync(D, C, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
     LCC_CUDA(cudaMemsetAsync(moved, 0, n, s));
@@ -2768,11 +2803,11 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     cudaEvent_t kev[2] = {nullptr, nullptr};
     if (try_ki) {
         for (auto& e : kev) LCC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
-        Ki.alloc(klen, s);
+        Ki.alloc(KS * klen, s);  // interleaved: (label, mass) pairs -- masses at odd words, labels below
         kchk.alloc(2, s);
         LCC_CUDA(cudaMemsetAsync(kchk.get(), 0, sizeof(unsigned long long) * 2, s));
         LCC_CUDA(cudaEventRecord(kev[0], s));
-        k_mass_to_u32<<<grid_for(klen, 256), 256, 0, s>>>(K, klen, k, n, Ki.get(), kchk.get(),
+        k_mass_to_u32<<<grid_for(klen, 256), 256, 0, s>>>(K, klen, k, n, Ki.get() + (KS - 1), kchk.get(),
                                                            reinterpret_cast<unsigned*>(kchk.get() + 1));
         LCC_LAUNCH_CHECK();
         LCC_CUDA(cudaEventRecord(kev[1], s));
@@ -2808,8 +2843,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     Buf<unsigned long long> LK;
     const bool use_lk = ki && LCC_LK && (!ASYNC || LCC_LK_ASYNC) && !WLoad<WT>::fsum && nF > 0;
     if (use_lk) LK.alloc(n, s);
-    BMArgs a{g.indptr, g.indices, g.weights, k, lam, C, ki ? (void*)Ki.get() : (void*)K, D, moved, dmoved, (int32_t)n, mark,
-             dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2, use_lk ? LK.get() : nullptr};
+    const bool ilv = ki && LCC_ILV;
+    int32_t* CK = ilv ? reinterpret_cast<int32_t*>(Ki.get()) : nullptr;  // labels at even, masses at odd
+    BMArgs a{g.indptr, g.indices, g.weights, k, lam, ilv ? CK : C,
+             ki ? (void*)(Ki.get() + (KS - 1)) : (void*)K, D, moved, dmoved, (int32_t)n, mark,
+             dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2, use_lk ? LK.get() : nullptr,
+             ilv ? 2 : 1};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
     LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
@@ -2831,8 +2870,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const char* esc = getenv("LCC_SUBCONC");
     const bool concurrent = P == 1 || (esc && esc[0] == '1' && nF >= (1 << 20));
     LCC_CUDA(cudaEventRecord(ev0, s));
-    if (use_lk) {  // timed with the kernels
-        k_pack_lk<<<grid_for(n, 256), 256, 0, s>>>(C, Ki.get(), n, LK.get());
+    if (ilv) {  // timed with the kernels
+        k_labels_in<<<grid_for(n, 256), 256, 0, s>>>(C, n, CK);
+        LCC_LAUNCH_CHECK();
+    }
+    if (use_lk) {
+        k_pack_lk<<<grid_for(n, 256), 256, 0, s>>>(C, Ki.get() + (KS - 1), n, LK.get());
         LCC_LAUNCH_CHECK();
     }
     auto launch_all = [&](auto ki_tag) {
@@ -2889,9 +2932,13 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     };
     if (ki) launch_all(std::true_type{});
     else launch_all(std::false_type{});
-    if (ki && ASYNC) {  // async moves updated the image: back to fp64 K
-        k_mass_from_u32<<<grid_for(klen, 256), 256, 0, s>>>(Ki.get(), klen, K);
+    if (ki && ASYNC) {  // async moves updated the image: back to fp64 K (and the labels to C)
+        k_mass_from_u32<<<grid_for(klen, 256), 256, 0, s>>>(Ki.get() + (KS - 1), klen, K);
         LCC_LAUNCH_CHECK();
+        if (ilv) {
+            k_labels_out<<<grid_for(n, 256), 256, 0, s>>>(CK, n, C);
+            LCC_LAUNCH_CHECK();
+        }
     }
     hprobe.mark("launches");
     LCC_CUDA(cudaEventRecord(ev1, s));

@@ -49,6 +49,12 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# A clustering service keeps its scratch mapped between calls: fresh device
+# memory costs ~6 ms per GB to map and the config-5 contraction peaks near
+# 160 GB, so trimming to the library default (64 GB) after every call and
+# growing back cost ~1.5 s per config-5 clustering (measured 6.5 -> 4.5 s).
+# lcc_release_memory() / paper_2108_01731_b200.release_memory() hands it back.
+os.environ.setdefault("LCC_POOL_KEEP_GB", "150")
 
 METRIC = "best-move edge throughput (Gedges/s)"
 UNIT = "Gedges/s"
@@ -347,7 +353,7 @@ def config_dict(args, g, wl=None, extra=None):
                  "next active set)",
          "l2": "inputs larger than L2 (CSR indices %.2f GB vs 126 MB L2); no flush" % (4 * 2 * g["m"] / 1e9)
                if 8 * g["m"] > 126e6 else "inputs smaller than L2 (launch/L2 bound config)",
-         "parallelism": "single-gpu"}
+         "parallelism": "single-gpu", "pool_keep_gb": float(os.environ.get("LCC_POOL_KEEP_GB", "64"))}
     if extra:
         d.update(extra)
     return d

@@ -491,6 +491,8 @@ def measure_round(args, wl, lib, rank=0):
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic, traffic_src = None, None
     for tname in (f"r02_traffic_{wl.cfg}.json",) + (("r01_traffic.json",) if wl.cfg == "cfg4" else ()):
+        if wl.cfg not in ("cfg4", "cfg5"):
+            break
         tpath = os.path.join(ROOT, "profiles", tname)
         if args.scale == 24 and os.path.exists(tpath):
             tj = json.load(open(tpath))
@@ -498,6 +500,9 @@ def measure_round(args, wl, lib, rank=0):
             break
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
+                # measured DRAM bytes over this run's kernel time: how close the
+                # random-gather traffic itself runs to the HBM peak
+                "traffic_frac": (traffic / (kern_ms / 1e3) / 1e9 / peak) if traffic else None,
                 "kernel": "best-move (k_tiny/k_small/k_group/k_hub_*)",
                 "alg_bytes_per_launch_group": alg_bytes,
                 "alg_bytes_formula": f"n*{B_vertex} + 2m*{B_edge} + 2m*{B_distinct} (SURVEY.md §8d B_bm, "

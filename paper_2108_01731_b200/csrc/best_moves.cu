@@ -70,6 +70,12 @@ namespace {
 #ifndef LCC_VALIDATE
 #define LCC_VALIDATE 1  // async: re-check the gain with the target's mass at commit time
 #endif
+#ifndef LCC_TMAPF
+#define LCC_TMAPF 0  // k_group: the TMA unit bulk-prefetches the next vertex's row into L2
+#endif
+#ifndef LCC_HDRPF
+#define LCC_HDRPF 0  // k_group: vertex headers (list entry, row bounds) loaded ahead
+#endif
 #ifndef LCC_ROWPF
 #define LCC_ROWPF 0  // k_group: prefetch the next vertex's neighbour row into L2 while this one runs
 #endif
@@ -1003,13 +1009,56 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             for (int64_t e = prev_s + gt; e < prev_e; e += GT) a.mark[__ldg(a.indices + e)] = 1;
         }
     };
-    for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += (int64_t)gridDim.x * GROUPS) {
-        const int32_t v = __ldg(list + i);
-        const int64_t s = __ldg(a.indptr + v);
-        const int64_t end = __ldg(a.indptr + v + 1);
+    // vertex headers one vertex ahead (LCC_HDRPF): the next vertex's list
+    // entry two steps ahead, its row bounds one step ahead, so a vertex's
+    // first index loads do not wait on the list -> indptr chain
+    const int64_t vstep = (int64_t)gridDim.x * GROUPS;
+    int32_t v_nx = 0, v_nn = 0;
+    int64_t s_nx = 0, e_nx = 0;
+    if constexpr (LCC_HDRPF) {
+        const int64_t i0 = lo + (int64_t)blockIdx.x * GROUPS + gid;
+        if (i0 < hi) {
+            v_nx = __ldg(list + i0);
+            s_nx = __ldg(a.indptr + v_nx);
+            e_nx = __ldg(a.indptr + v_nx + 1);
+        }
+        if (i0 + vstep < hi) v_nn = __ldg(list + i0 + vstep);
+    }
+    for (int64_t i = lo + (int64_t)blockIdx.x * GROUPS + gid; i < hi; i += vstep) {
+        int32_t v;
+        int64_t s, end;
+        if constexpr (LCC_HDRPF) {
+            v = v_nx;
+            s = s_nx;
+            end = e_nx;
+            if (i + vstep < hi) {
+                v_nx = v_nn;
+                s_nx = __ldg(a.indptr + v_nx);
+                e_nx = __ldg(a.indptr + v_nx + 1);
+                if (i + 2 * vstep < hi) v_nn = __ldg(list + i + 2 * vstep);
+            }
+        } else {
+            v = __ldg(list + i);
+            s = __ldg(a.indptr + v);
+            end = __ldg(a.indptr + v + 1);
+        }
         const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
+        if constexpr (LCC_TMAPF) {
+            // one cp.async.bulk.prefetch.L2 per row, issued by the group's
+            // first lane: the next vertex's index row is on its way to L2
+            // while this vertex runs (16-byte aligned, size a multiple of 16)
+            const int64_t in = i + (int64_t)gridDim.x * GROUPS;
+            if (gt == 0 && in < hi) {
+                const int32_t vn = __ldg(list + in);
+                const int64_t sn = __ldg(a.indptr + vn), en = __ldg(a.indptr + vn + 1);
+                const uintptr_t b0 = (uintptr_t)(a.indices + sn) & ~(uintptr_t)15;
+                const uintptr_t b1 = ((uintptr_t)(a.indices + en) + 15) & ~(uintptr_t)15;
+                if (b1 > b0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((uint32_t)(b1 - b0)) : "memory");
+            }
+        }
         if constexpr (LCC_ROWPF) {
             // the group's next vertex: its index row is streamed into L2 now,
             // so that vertex's index loads leave the dependent chain
@@ -2748,6 +2797,15 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
                        // chunks < 0: at least -chunks (driver: rounds after the first)
         const int64_t f = std::max<int64_t>(nF, 1);
         P = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((1LL << 22) + f - 1) / f));
+        // and no sub-round larger than a wave of LCC_WAVE vertices (default
+        // 4M; 0 = off).  One 65M-vertex wave (config 5) let millions of
+        // vertices decide on the same stale state: objective 6.90M against
+        // the CPU parallel-async oracle's 7.45M (-7.4%); 4M-vertex waves
+        // with the bins concurrent inside each: 7.43-7.44M (-0.1%), and the
+        // clustering got faster (fewer rounds and levels).  Config 4 (one
+        // 16.8M wave was 333K): 305-306K, CPU 303.4K.
+        static const int64_t wave = getenv("LCC_WAVE") ? atoll(getenv("LCC_WAVE")) : (1LL << 22);
+        if (wave > 0) P = std::max<int>(P, (int)std::min<int64_t>(64, (f + wave - 1) / wave));
         if (chunks < 0) P = std::max(P, -chunks);
     }
     BinEdges be;
@@ -2866,9 +2924,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     // order on the caller's stream: the interleaving is what breaks symmetry
     // on small graphs (measured on the config-1 SBM).
     SideStreams& ss = side_streams();
-    // (large frontiers: bins may also overlap inside each ordered sub-round)
+    // (frontiers of a wave or more: the bins also overlap inside each ordered
+    // sub-round -- measured better objectives than bin-ordered sub-rounds
+    // there, 7.44M vs 7.40M on config 5; LCC_SUBCONC=0/1 forces it off/on)
     const char* esc = getenv("LCC_SUBCONC");
-    const bool concurrent = P == 1 || (esc && esc[0] == '1' && nF >= (1 << 20));
+    const bool concurrent = P == 1 || (esc ? (esc[0] == '1' && nF >= (1 << 20))
+                                           : nF >= (1 << 22));
     LCC_CUDA(cudaEventRecord(ev0, s));
     if (ilv) {  // timed with the kernels
         k_labels_in<<<grid_for(n, 256), 256, 0, s>>>(C, n, CK);

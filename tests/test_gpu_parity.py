@@ -605,3 +605,51 @@ def test_hub_buckets_multipass_exact(nclus):
     D0, m0, c0 = O.sync_round(g, None, 0.3, C, K)
     D1, m1, c1 = gpu_sync_round(hg, None, 0.3, C, K)
     assert np.array_equal(D0, D1) and c0 == c1
+
+
+@pytest.mark.parametrize("wkind", ["none", "u32"])
+def test_compress_segmented_identical(wkind, monkeypatch):
+    """The segmented contraction (per-row window sorts and the device sort
+    for rows over 2048 entries; the default on graphs of 2^30+ entries)
+    equals the global-sort path and the oracle bit for bit -- hubs of 6K and
+    12K neighbours take the long-row path, every other row the windows."""
+    rng = np.random.default_rng(72)
+    hg = hub_graph(rng, 30_000, [5, 77, 901], [6000, 12000, 2500], base_p=0.0004)
+    if wkind == "u32":
+        src = np.repeat(np.arange(hg.n), np.diff(hg.indptr))
+        lo_, hi_ = np.minimum(src, hg.indices), np.maximum(src, hg.indices)
+        hg.weights = ((lo_ * 7 + hi_ * 13) % 5 + 1).astype(np.float64)
+        hg.total_weight = float(hg.weights.sum() / 2)
+    g = og(hg)
+    n = g.n
+    for merges in (0, 3, 500, n // 3):
+        lab = np.arange(n, dtype=np.int32)
+        a = rng.choice(n, size=merges, replace=False)
+        b = rng.choice(n, size=merges, replace=False)
+        lab[a] = np.minimum(lab[a], b).astype(np.int32)
+        C, K = O.canonicalize(n, lab, n, None)
+        outs = []
+        for seg in ("1", "0"):
+            monkeypatch.setenv("LCC_CONTRACT_SEG", seg)
+            c = L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda())
+            lvl = L.par_compress(dg(hg), L.ClusteringParams(0.4), c)
+            outs.append((lvl.mapping.cpu().numpy(), lvl.graph.indptr.cpu().numpy(), lvl.graph.indices.cpu().numpy(),
+                         lvl.graph.weights.cpu().numpy(), lvl.internal_offset, lvl.graph.total_weight))
+        sg, st = outs
+        for x, y in zip(sg[:4], st[:4]):
+            assert np.array_equal(x, y)
+        assert sg[4] == st[4] and sg[5] == st[5]
+        lvl0 = O.compress(g, None, 0.4, C, K)
+        assert np.array_equal(sg[1], lvl0.graph.indptr) and np.array_equal(sg[2], lvl0.graph.indices)
+        assert np.array_equal(sg[3], lvl0.graph.weights)
+
+
+def test_parallel_cc_sync_segmented_exact(monkeypatch):
+    """Full sync clustering with every contraction on the segmented path."""
+    monkeypatch.setenv("LCC_CONTRACT_SEG", "1")
+    u, v = rmat_pairs_host(14, 16 << 14, 0.57, 0.19, 0.19, 3)
+    hg = csr_from_pairs(1 << 14, u, v)
+    g = og(hg)
+    C0 = O.parallel_cc(g, None, 0.85, O.Opts(schedule=O.SYNC))
+    cl = L.parallel_cc(hg, L.ClusteringParams(0.85), L.ParOptions(schedule="sync"))
+    assert np.array_equal(cl.labels(), C0)

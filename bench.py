@@ -80,7 +80,7 @@ def parse(argv=None):
     ap.add_argument("--schedule", default=None, choices=["async", "sync"], help="default: the config's schedule")
     ap.add_argument("--async-chunks", type=int, default=0)
     ap.add_argument("--degree-threshold", type=int, default=1000)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-stride", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cache-dir", default=os.environ.get("LCC_BENCH_CACHE", "/tmp/lcc_bench_cache"))
@@ -670,6 +670,10 @@ def run_sharded(args):
     from paper_2108_01731_b200.dist import CudaBackend, ShardStats, make_part, partition_bounds, sharded_best_moves, sharded_parallel_cc
 
     ws, rank, lrank = dist_init()
+    # the sharded driver interleaves torch allocations (partial coarse CSRs,
+    # exchange buffers) with library calls: keep less library scratch mapped
+    # between calls than a single-process clustering service would
+    os.environ["LCC_POOL_KEEP_GB"] = os.environ.get("LCC_SHARDED_POOL_KEEP_GB", "32")
     # NCCL may print its version banner on fd 1 at communicator creation:
     # route fd 1 to stderr for the run and write the JSON line to the saved fd
     json_fd = os.dup(1)
@@ -686,6 +690,13 @@ def run_sharded(args):
     bounds = partition_bounds(indptr_h, ws)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     part = make_part(dg.indptr, dg.indices, dg.weights, dg.total_weight, lo, hi, torch.device("cuda", lrank))
+    # host copies for the e2e leg and the objective; the device graph itself
+    # is not needed once the owned part is built
+    ix_host = dg.indices.cpu()
+    w_host = None if dg.weights is None else dg.weights.cpu()
+    tw = dg.total_weight
+    wl.dg = dg = None
+    torch.cuda.empty_cache()
     be = CudaBackend()
     lam, sched = wl.lam, wl.schedule
     opts1 = L.ParOptions(schedule=sched, num_iter=1, degree_threshold=args.degree_threshold,
@@ -722,9 +733,8 @@ def run_sharded(args):
     e2e = None
     if not args.no_e2e:
         ip_h = torch.from_numpy(indptr_h).pin_memory()
-        ix_h = dg.indices.cpu().pin_memory()
-        w_h = None if dg.weights is None else dg.weights.cpu().pin_memory()
-        tw = dg.total_weight
+        ix_h = ix_host.pin_memory()
+        w_h = None if w_host is None else w_host.pin_memory()
         full = L.ParOptions(schedule=sched, degree_threshold=args.degree_threshold,
                             async_chunks=args.async_chunks)
         sharded_parallel_cc(ip_h, ix_h, w_h, tw, kdev, lam, full, be)  # warm-up
@@ -739,7 +749,12 @@ def run_sharded(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ed2 = torch.tensor([float(st2.edges_scanned)], dtype=torch.float64, device="cuda")
         dist.all_reduce(ed2, op=dist.ReduceOp.SUM)
-        obj = L.cc_objective(dg, L.ClusteringParams(lam, kdev), C)
+        hgo = type("H", (), {})()
+        hgo.n, hgo.m, hgo.indptr, hgo.indices, hgo.weights, hgo.total_weight = n, nnz // 2, ip_h, ix_h, w_h, tw
+        part = None
+        torch.cuda.empty_cache()
+        L.release_memory()
+        obj = L.cc_objective(hgo, L.ClusteringParams(lam, kdev), C)
         h2d = int((bounds[rank + 1] - bounds[rank]) * 8 + (indptr_h[hi] - indptr_h[lo]) * 4)
         e2e = {"value": float(ed2.item()) / float(te.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": int(n * 4),

@@ -199,14 +199,20 @@ class CudaBackend:
                                              cw.data_ptr(), ctypes.byref(cn), ctypes.byref(cnnz), ctypes.byref(off),
                                              ctypes.byref(tot), stream_ptr()))
         cn, cnnz = cn.value, cnnz.value
-        return cn, cptr[:cn + 1], cind[:cnnz], cw[:cnnz], ck[:cn], mapping[:n]
+        cw = cw[:cnnz]
+        if part.weights is None or part.weights.dtype == torch.int32:
+            # integer sums: keep them as int32 (the uint32 tables of the next
+            # level) and drop the fp64 buffer (8 -> 4 bytes per entry)
+            cw = cw.to(torch.int32)
+        return cn, cptr[:cn + 1], cind[:cnnz], cw, ck[:cn], mapping[:n]
 
     def parallel_cc(self, indptr, indices, weights, total_weight, k, lam, opts):
         from .louvain_par import parallel_cc
         from .objective import ClusteringParams
         n = indptr.numel() - 1
-        if weights is not None and weights.dtype != torch.int32:
+        if weights is not None and weights.dtype not in (torch.int32, torch.float64):
             weights = weights.to(self.device, torch.float64)
+        if weights is not None and weights.dtype == torch.float64:
             # integral coarse weights (multi-edge counts of an unweighted or
             # integer-weighted level 0) run on the exact uint32 tables, as in
             # the single-process driver

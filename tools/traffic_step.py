@@ -8,6 +8,7 @@ import json
 import sys
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "second": 1e3}
 BEST = ("k_group", "k_small", "k_tiny", "k_isolated", "k_hub_", "k_large_", "k_window")
 

@@ -623,27 +623,8 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     int64_t R = 0;
     double intra_w = 0.0;
     bool fast_done = false;
-    // integer sums on graphs of >= 2^30 entries: the segmented path, which
-    // needs 8 instead of ~24-32 bytes of scratch per entry.  Measured over 6
-    // config-5 clusterings (3.6B entries): 3.1-3.7 s steady state against
-    // 3.6-10.4 s with the global sort, whose 60-90 GB of double-buffered keys
-    // and values kept the pool re-mapping pages; config 4 (521M entries)
-    // keeps the global sort and its mostly-singleton fast path (352 vs 427 ms).
-    // LCC_CONTRACT_SEG=0/1 forces either.
-    const char* esg = getenv("LCC_CONTRACT_SEG");
-    const bool use_seg = esg ? esg[0] == '1' : nnz >= (1LL << 30);
-    if (nnz > 0 && int_out && use_seg) {
-        unsigned long long* di = dintra.get();
-        R = compress_seg<WT>(g, mapping, cn, out, di, s);
-        unsigned long long hintra = 0;
-        LCC_CUDA(cudaMemcpyAsync(&hintra, di, sizeof(hintra), cudaMemcpyDeviceToHost, s));
-        LCC_CUDA(cudaStreamSynchronize(s));
-        intra_w = (double)hintra;
-        fast_done = true;
-        tr.mark("segmented");
-    }
     const char* ef = getenv("LCC_CONTRACT_FAST");
-    if (!fast_done && nnz > 0 && !(ef && ef[0] == '0')) {
+    if (nnz > 0 && !(ef && ef[0] == '0')) {
         // complex rows: members of non-singleton clusters and their neighbours
         Buf<int32_t> csize(cn, s);
         LCC_CUDA(cudaMemsetAsync(csize.get(), 0, sizeof(int32_t) * cn, s));
@@ -783,6 +764,26 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
             }
             tr.mark("emit(fast)");
         }
+    }
+    // (when the mostly-singleton fast path did not apply) integer sums on
+    // graphs of >= 2^30 entries: the segmented path, which
+    // needs 8 instead of ~24-32 bytes of scratch per entry.  Measured over 6
+    // config-5 clusterings (3.6B entries): 3.1-3.7 s steady state against
+    // 3.6-10.4 s with the global sort, whose 60-90 GB of double-buffered keys
+    // and values kept the pool re-mapping pages; config 4 (521M entries)
+    // keeps the global sort and its mostly-singleton fast path (352 vs 427 ms).
+    // LCC_CONTRACT_SEG=0/1 forces either.
+    const char* esg = getenv("LCC_CONTRACT_SEG");
+    const bool use_seg = esg ? esg[0] == '1' : nnz >= (1LL << 30);
+    if (!fast_done && nnz > 0 && int_out && use_seg) {
+        unsigned long long* di = dintra.get();
+        R = compress_seg<WT>(g, mapping, cn, out, di, s);
+        unsigned long long hintra = 0;
+        LCC_CUDA(cudaMemcpyAsync(&hintra, di, sizeof(hintra), cudaMemcpyDeviceToHost, s));
+        LCC_CUDA(cudaStreamSynchronize(s));
+        intra_w = (double)hintra;
+        fast_done = true;
+        tr.mark("segmented");
     }
     if (!fast_done && nnz > 0) {
         Buf<uint64_t> ka(nnz, s), kb(nnz, s);

@@ -629,6 +629,7 @@ def test_compress_segmented_identical(wkind, monkeypatch):
         lab[a] = np.minimum(lab[a], b).astype(np.int32)
         C, K = O.canonicalize(n, lab, n, None)
         outs = []
+        monkeypatch.setenv("LCC_CONTRACT_FAST", "0")  # (it would take the few-merge cases first)
         for seg in ("1", "0"):
             monkeypatch.setenv("LCC_CONTRACT_SEG", seg)
             c = L.Clustering(torch.as_tensor(C).cuda(), torch.as_tensor(K).cuda())

@@ -47,15 +47,24 @@ void* pool_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, bytes, s);
     if (e == cudaErrorMemoryAllocation) {
-        // give cached blocks and unused pool memory back, then try once more
+        // First hand the library's cached blocks back to the pool: the pool
+        // keeps that memory mapped and can serve the request from it (no page
+        // mapping).  Only if that fails, release the pool's unused memory to
+        // the driver -- everything mapped again afterwards costs ~6 ms per GB
+        // (measured: a config-5 contraction step 0.1 s -> 1.6 s after a full
+        // trim).
         cudaGetLastError();
         trim_cache(0, s);
-        cudaStreamSynchronize(s);
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-            cudaMemPoolTrimTo(pool, 0);
+        cudaDeviceSynchronize();  // (the frees ran on the legacy stream)
         e = cudaMallocAsync(&p, bytes, s);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+                cudaMemPoolTrimTo(pool, 0);
+            e = cudaMallocAsync(&p, bytes, s);
+        }
     }
     LCC_CUDA(e);
     if (alloc_fill() >= 0) LCC_CUDA(cudaMemsetAsync(p, alloc_fill(), bytes, s));

@@ -85,6 +85,9 @@ namespace {
 #ifndef LCC_CLAIMK
 #define LCC_CLAIMK 0  // async k_group: the claiming lane gathers the live mass (objective -19% on config 4)
 #endif
+#ifndef LCC_ASYNC_HINT
+#define LCC_ASYNC_HINT 0  // async label / mass loads carry the evict-last L2 policy too
+#endif
 #ifndef LCC_ILV
 #define LCC_ILV 1  // integer-mass rounds: labels and masses interleaved in one (label, mass) array
 #endif
@@ -110,7 +113,10 @@ template <bool ASYNC>
 __device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i, uint64_t pol) {
     if constexpr (ASYNC) {
         int32_t r;
-        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(C + i));
+        if constexpr (LCC_ASYNC_HINT)  // relaxed, with the evict-last L2 policy of the sync path
+            asm volatile("ld.relaxed.gpu.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(C + i), "l"(pol));
+        else
+            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(C + i));
         return r;
     } else {
         return ld_keep_i32(C + i, pol);
@@ -131,7 +137,9 @@ __device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
     if constexpr (KI) {
         const uint32_t* K = static_cast<const uint32_t*>(Kp) + KS * i;
         uint32_t r;
-        if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(K));
+        if constexpr (ASYNC && LCC_ASYNC_HINT)
+            asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(K), "l"(pol));
+        else if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(K));
         else r = (uint32_t)ld_keep_i32(reinterpret_cast<const int32_t*>(K), pol);
         return u32_to_f64(r);
     } else {

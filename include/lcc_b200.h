@@ -38,6 +38,10 @@ typedef enum {
 /* LCC_W_U32: non-negative integer weights (multi-edge counts, e.g. every
  * coarse level of an unweighted graph), summed exactly in 32-bit integers;
  * requires 2 * total_weight < 2^32.                                          */
+/* lcc_graph.flags: LCC_GRAPH_PARTIAL_ROWS -- only some vertices carry their
+ * rows (a rank's shard in the vertex-partitioned driver), so the CSR is not
+ * symmetric as stored.  Whole graphs pass 0.                                 */
+enum { LCC_GRAPH_PARTIAL_ROWS = 1 };
 typedef enum { LCC_W_NONE = 0, LCC_W_F32 = 1, LCC_W_F64 = 2, LCC_W_U32 = 3 } lcc_wtype;
 /* ParOptions.schedule */
 typedef enum { LCC_SYNC = 0, LCC_ASYNC = 1 } lcc_schedule;
@@ -58,7 +62,7 @@ typedef struct {
     const int32_t* indices; /* [nnz], sorted within each row, no self loops */
     const void* weights;    /* [nnz] float, double or uint32, or NULL      */
     int32_t wtype;          /* lcc_wtype                                    */
-    int32_t _pad;
+    int32_t flags;          /* LCC_GRAPH_* bits (0 for a whole graph)       */
     double total_weight;    /* sum of w over undirected edges               */
 } lcc_graph;
 

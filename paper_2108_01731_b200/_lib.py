@@ -15,6 +15,7 @@ SO_PATH = os.environ.get("LCC_LIB_PATH") or os.path.join(_HERE, "_lib", "liblcc_
 
 LCC_OK, LCC_ERR_INVALID, LCC_ERR_CUDA, LCC_ERR_OOM = 0, 1, 2, 3
 W_NONE, W_F32, W_F64, W_U32 = 0, 1, 2, 3
+GRAPH_PARTIAL_ROWS = 1  # lcc_graph.flags: a rank's shard (only owned vertices carry rows)
 SYNC, ASYNC = 0, 1
 FRONTIER_ALL, FRONTIER_VERTEX_NBRS, FRONTIER_CLUSTER_NBRS = 0, 1, 2
 
@@ -37,7 +38,7 @@ class NativeLibraryError(RuntimeError):
 class LccGraph(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("indptr", ctypes.c_void_p),
                 ("indices", ctypes.c_void_p), ("weights", ctypes.c_void_p), ("wtype", ctypes.c_int32),
-                ("_pad", ctypes.c_int32), ("total_weight", ctypes.c_double)]
+                ("flags", ctypes.c_int32), ("total_weight", ctypes.c_double)]
 
 
 class LccParams(ctypes.Structure):

@@ -190,6 +190,11 @@ struct BMArgs {
     // after their join); the other members' masses are round-start values.
     unsigned long long* LK;
     int32_t cs;  // label stride in C: 2 when interleaved with the masses (KI rounds), else 1
+    // the round's n-byte frontier mask: deferred async movers set their own
+    // entry here; `mark` (above) is the same array when movers push their
+    // neighbours inside the kernels, null when the marks are pulled after
+    // the round (k_pull_head / k_pull_rest)
+    uint8_t* dmark;
 };
 
 // packed-word gathers: frozen in sync rounds, relaxed loads in async ones
@@ -218,7 +223,7 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
         if constexpr (ASYNC) {
             if (a.prev_moved && a.prev_moved[v] && (hash32((uint32_t)v * 0x9E3779B9u + a.salt) & 1u)) {
                 // deferred: v moved last iteration too; it stays in the frontier
-                a.mark[v] = 1;
+                a.dmark[v] = 1;
                 atomicAdd(a.pending, 1ull);
                 return 0;
             }
@@ -2677,6 +2682,83 @@ struct HostProbe {
     }
 };
 
+// ---- pulled VertexNeighbors marks (direction-optimising frontier) -------
+// A round whose movers are a large part of the graph flags the next frontier
+// from the receiving side instead: mark[v] |= OR over u in N(v) of moved[u].
+// On a symmetric CSR this is exactly the set the movers' pushes produce
+// (every neighbour of a mover), but it costs one short scan per vertex --
+// with most vertices moving, the first entries of a row already hold a
+// mover -- instead of one random byte store per entry of every mover's row.
+// At config 5 those stores fell out of the 126 MB L2 next to the 520 MB
+// (label, mass) image and came back as read-modify-write DRAM traffic.
+// Head: thread per vertex, the row's first PULL_HEAD entries (independent
+// loads); rows not settled there go to a queue that k_pull_rest scans a warp
+// per row with early exit.  The moved flags (n bytes) are kept in L2.
+constexpr int PULL_HEAD = 4;
+__global__ void __launch_bounds__(256) k_pull_head(const int64_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices,
+                                                   const uint8_t* __restrict__ moved, uint8_t* __restrict__ mark,
+                                                   int64_t n, int32_t* __restrict__ rest,
+                                                   unsigned long long* __restrict__ nrest) {
+    const uint64_t pol_s = policy_evict_first(), pol_k = policy_evict_last();
+    const unsigned lane = lane_id();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const int64_t v = base + lane;
+        bool queue = false;
+        if (v < n && !mark[v]) {  // deferred movers are in already
+            const int64_t s = indptr[v], d = indptr[v + 1] - s;
+            int32_t u[PULL_HEAD];
+#pragma unroll
+            for (int j = 0; j < PULL_HEAD; ++j) u[j] = j < d ? ld_stream_i32(indices + s + j, pol_s) : -1;
+            uint32_t hit = 0;
+#pragma unroll
+            for (int j = 0; j < PULL_HEAD; ++j) {
+                if (u[j] >= 0) {
+                    uint16_t m;
+                    asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(m) : "l"(moved + u[j]), "l"(pol_k));
+                    hit |= m;
+                }
+            }
+            if (hit) mark[v] = 1;
+            else queue = d > PULL_HEAD;
+        }
+        const unsigned q = __ballot_sync(FULL, queue);
+        if (q) {
+            unsigned long long at = 0;
+            if (lane == (unsigned)(__ffs(q) - 1)) at = atomicAdd(nrest, (unsigned long long)__popc(q));
+            at = __shfl_sync(FULL, at, __ffs(q) - 1);
+            if (queue) rest[at + __popc(q & ((1u << lane) - 1u))] = (int32_t)v;
+        }
+    }
+}
+__global__ void __launch_bounds__(256) k_pull_rest(const int64_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices,
+                                                   const uint8_t* __restrict__ moved, uint8_t* __restrict__ mark,
+                                                   const int32_t* __restrict__ rest,
+                                                   const unsigned long long* __restrict__ nrest) {
+    const uint64_t pol_s = policy_evict_first(), pol_k = policy_evict_last();
+    const unsigned lane = lane_id();
+    const int64_t nq = (int64_t)*nrest;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); i < nq; i += warps) {
+        const int32_t v = rest[i];
+        const int64_t end = indptr[v + 1];
+        for (int64_t e0 = indptr[v] + PULL_HEAD; e0 < end; e0 += 32) {
+            const int64_t e = e0 + lane;
+            uint16_t m = 0;
+            if (e < end) {
+                const int32_t u = ld_stream_i32(indices + e, pol_s);
+                asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(m) : "l"(moved + u), "l"(pol_k));
+            }
+            if (__ballot_sync(FULL, m != 0)) {
+                if (lane == 0) mark[v] = 1;
+                break;
+            }
+        }
+    }
+}
+
 // side streams for concurrent bin kernels (one set per device, created once)
 struct SideStreams {
     cudaStream_t st[NBINS];
@@ -2744,6 +2826,8 @@ void preload_round_kernels() {
     load_fn(k_large_insert<WT, ASYNC>);
     if constexpr (!WLoad<WT>::fsum) load_fn(k_hub_scatter<WT, ASYNC>);
     load_fn(k_large_mark);
+    load_fn(k_pull_head);
+    load_fn(k_pull_rest);
     load_fn(k_degrees_of);
     load_fn(k_mass_to_u32);
     load_fn(k_mass_from_u32);
@@ -2905,6 +2989,16 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const bool ki = try_ki && hk[1] == 0 && hk[0] < (1ull << 31);
     if (try_ki) LCC_CUDA(cudaEventElapsedTime(&kconv_ms, kev[0], kev[1]));
     const bool dmp = ASYNC && damp && damp->prev_moved && mark;  // deferral needs the fused frontier
+    // neighbour marks: pushed by the movers inside the kernels (default), or
+    // pulled after them (k_pull_*, LCC_PULL=1; whole graphs only -- a shard's
+    // CSR holds only its own rows).  Measured on B200, round 1 from
+    // singletons: pull 120.4 vs push 115.3 ms (config 5), 12.0 vs 10.7 ms
+    // (config 4), config-5 clustering 4.2-4.8 vs 3.0 s -- the asynchronous
+    // kernels run slower without the mark stores between vertices (the same
+    // interleaving effect as round 1's unfused-mark test), more than the
+    // stores cost.
+    const char* epl = getenv("LCC_PULL");
+    const bool pull = mark && nF > 0 && !(g.flags & LCC_GRAPH_PARTIAL_ROWS) && epl && epl[0] == '1';
     // packed (label, mass) words for the group bins (integer masses only)
     Buf<unsigned long long> LK;
     const bool use_lk = ki && LCC_LK && (!ASYNC || LCC_LK_ASYNC) && !WLoad<WT>::fsum && nF > 0;
@@ -2914,7 +3008,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, ilv ? CK : C,
              ki ? (void*)(Ki.get() + (KS - 1)) : (void*)K, D, moved, dmoved, (int32_t)n, mark,
              dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2, use_lk ? LK.get() : nullptr,
-             ilv ? 2 : 1};
+             ilv ? 2 : 1, mark};
+    if (pull) a.mark = nullptr;  // neighbour marks pulled after the kernels
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
     LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
@@ -3001,6 +3096,15 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     };
     if (ki) launch_all(std::true_type{});
     else launch_all(std::false_type{});
+    if (pull) {
+        Buf<int32_t> rest(n, s);
+        Buf<unsigned long long> nrest(1, s);
+        LCC_CUDA(cudaMemsetAsync(nrest.get(), 0, sizeof(unsigned long long), s));
+        k_pull_head<<<grid_for(n, 256, 16), 256, 0, s>>>(g.indptr, g.indices, moved, mark, n, rest.get(), nrest.get());
+        LCC_LAUNCH_CHECK();
+        k_pull_rest<<<num_sms() * 8, 256, 0, s>>>(g.indptr, g.indices, moved, mark, rest.get(), nrest.get());
+        LCC_LAUNCH_CHECK();
+    }
     if (ki && ASYNC) {  // async moves updated the image: back to fp64 K (and the labels to C)
         k_mass_from_u32<<<grid_for(klen, 256), 256, 0, s>>>(Ki.get() + (KS - 1), klen, K);
         LCC_LAUNCH_CHECK();

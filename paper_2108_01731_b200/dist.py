@@ -130,7 +130,7 @@ class CudaBackend:
             wp = part.weights.data_ptr()
         nnz = int(part.indices.numel())
         return _lib.LccGraph(part.n, nnz, part.indptr.data_ptr(), part.indices.data_ptr() if nnz else None, wp,
-                             wtype, 0, part.total_weight)
+                             wtype, _lib.GRAPH_PARTIAL_ROWS, part.total_weight)
 
     @staticmethod
     def _p(k, lam) -> _lib.LccParams:

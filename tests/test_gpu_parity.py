@@ -283,7 +283,12 @@ def test_parallel_cc_sync_exact(refine, policy):
     assert L.cc_objective(hg, L.ClusteringParams(0.85), cl) == O.objective(g, None, 0.85, C0)
 
 
-def test_parallel_cc_sync_rmat_exact():
+@pytest.mark.parametrize("pull", [None, "0", "1"])
+def test_parallel_cc_sync_rmat_exact(pull, monkeypatch):
+    """R-MAT s14, sync, VertexNeighbors + refine: bit-exact labels with the
+    default mark direction, always-push and always-pull."""
+    if pull is not None:
+        monkeypatch.setenv("LCC_PULL", pull)
     u, v = rmat_pairs_host(14, 16 << 14, 0.57, 0.19, 0.19, 3)
     hg = csr_from_pairs(1 << 14, u, v)
     g = og(hg)
@@ -440,9 +445,13 @@ def test_cfg3_knn_weighted_sync(lam):
 @pytest.mark.parametrize("window", ["1", "0"])
 @pytest.mark.parametrize("large_min", ["2048", "10240"])
 @pytest.mark.parametrize("schedule", [L.Schedule.Synchronous, L.Schedule.Asynchronous])
-def test_fused_frontier_mask_exact(window, large_min, schedule, monkeypatch):
+@pytest.mark.parametrize("pull", ["0", "1"])
+def test_fused_frontier_mask_exact(window, large_min, schedule, pull, monkeypatch):
     """The VertexNeighbors frontier fused into the round (nbr_mark) equals the
-    oracle's compute_frontier of the round's movers, in every kernel shape."""
+    oracle's compute_frontier of the round's movers, in every kernel shape,
+    whether the movers push the marks (LCC_PULL=0) or the round pulls them
+    after its kernels (LCC_PULL=1)."""
+    monkeypatch.setenv("LCC_PULL", pull)
     monkeypatch.setenv("LCC_WINDOW", window)
     monkeypatch.setenv("LCC_LARGE_MIN", large_min)
     rng = np.random.default_rng(23)

@@ -86,6 +86,7 @@ def parse(argv=None):
     ap.add_argument("--cache-dir", default=os.environ.get("LCC_BENCH_CACHE", "/tmp/lcc_bench_cache"))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-contraction", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="run the vertex-sharded NCCL driver even at world size 1 (exercises the N>1 path on one GPU)")
     return ap.parse_args(argv)
@@ -521,10 +522,78 @@ def measure_round(args, wl, lib, rank=0):
             "pattern": "streamed index -> random label gather -> random mass gather, 67 MB arrays",
             "achieved": edges_per_s, "peak": chain, "unit": "G chains/s", "frac": edges_per_s / chain,
             "source": "profiles/r01_gather_roof.json (tools/micro/gather_roof.cu)"}
+    # Config 5: the (label, mass) array (520 MB) is far beyond L2, so the
+    # round is bound by how many random DRAM accesses per second the GPU
+    # sustains, not by bytes: tools/micro/fetch_gran.cu measures that rate
+    # alone (random 8-byte gathers from a 2 GB array, every load a miss)
+    fpath = os.path.join(ROOT, "profiles", "r02_fetch_gran.json")
+    if wl.cfg == "cfg5" and os.path.exists(fpath):
+        fj = json.load(open(fpath))
+        edges_per_s = nnz / (kern_ms / 1e3) / 1e9
+        roofline["access_roofline"] = {
+            "pattern": "one random 8-byte (label, mass) gather per scanned entry, 520 MB array (L2 hit rate 12-28%)",
+            "achieved": edges_per_s, "peak": fj["random_gather_ceiling_G_per_s"], "unit": "G gathers/s",
+            "frac": edges_per_s / fj["random_gather_ceiling_G_per_s"],
+            "source": "profiles/r02_fetch_gran.json (tools/micro/fetch_gran.cu: the rate is the same for 64- and "
+                      "128-byte fetches, i.e. access-count bound, not byte bound)"}
+    contraction = None
+    if not args.no_contraction and wl.cfg in ("cfg4", "cfg5"):
+        contraction = measure_contraction(args, wl, lib, gs, ps, Cn, Kn, peak, peak_kind)
     return {"value": value, "ms_per_step": ms / args.steps, "roofline": roofline, "gpu_launches": int(launches),
+            "contraction": contraction,
             "clocks": clk.summary(), "n": n, "m": nnz // 2,
             "round_stats": {"vertices": st.vertices // args.steps, "edges": st.edges_scanned // args.steps,
                             "moves": st.moves // args.steps, "next_frontier": int(nF.value)}}
+
+
+def measure_contraction(args, wl, lib, gs, ps, Cn, Kn, peak, peak_kind, reps=3):
+    """par_compress (lcc_par_compress) of the state one best-move iteration
+    from singletons leaves: device time per call and its HBM roofline.
+    Algorithmic bytes: every fine entry read once with its neighbour's coarse
+    id (4 + 4), the per-vertex renumbering (n * 12), and the coarse CSR
+    written once (8 per coarse entry + 8 per coarse row)."""
+    import torch
+    from paper_2108_01731_b200 import _lib
+    from paper_2108_01731_b200.graph import stream_ptr
+    n, nnz = wl.dg.n, wl.dg.nnz
+    try:
+        mapping = torch.empty(n, dtype=torch.int32, device="cuda")
+        ck = torch.empty(n, dtype=torch.float64, device="cuda")
+        cptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        cind = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        cw = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        cn, cnnz = ctypes.c_int64(), ctypes.c_int64()
+        off, tot = ctypes.c_double(), ctypes.c_double()
+
+        def call():
+            _lib.check(lib.lcc_par_compress(ctypes.byref(gs), ctypes.byref(ps), Cn.data_ptr(), Kn.data_ptr(),
+                                            mapping.data_ptr(), ck.data_ptr(), cptr.data_ptr(), cind.data_ptr(),
+                                            cw.data_ptr(), ctypes.byref(cn), ctypes.byref(cnnz), ctypes.byref(off),
+                                            ctypes.byref(tot), stream_ptr()))
+        call()  # warm-up: scratch mapped
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            call()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = sorted(times)[len(times) // 2]
+        alg = nnz * 8 + n * 12 + cnnz.value * 8 + cn.value * 8
+        ach = alg / (ms / 1e3) / 1e9
+        return {"api": "lcc_par_compress (C ABI; the double-precision weight output of the ABI included)",
+                "ms": ms, "ms_all": times, "fine_entries": nnz, "coarse_vertices": cn.value,
+                "coarse_entries": cnnz.value, "Gentries_per_s": nnz / (ms / 1e3) / 1e9,
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                             "peak_kind": peak_kind, "alg_bytes": alg,
+                             "alg_bytes_formula": "2m*8 + n*12 + coarse_entries*8 + coarse_vertices*8"}}
+    except Exception as exc:  # memory-tight boxes: the round numbers stand without it
+        return {"unavailable": str(exc)[:200]}
+    finally:
+        mapping = ck = cptr = cind = cw = None
+        torch.cuda.empty_cache()  # 43 GB of outputs at config 5: back to the driver before the e2e leg
 
 
 def measure_e2e(args, wl, e2e_steps, warm=2):
@@ -642,7 +711,8 @@ def run_ours(args):
         r2 = measure_round(args, wl2, lib)
         extra = {"metric": METRIC, "value": r2["value"], "unit": UNIT, "ms_per_step": r2["ms_per_step"],
                  "config": config_dict(args, {"n": r2["n"], "m": r2["m"]}, wl2), "roofline": r2["roofline"],
-                 "gpu_launches": r2["gpu_launches"], "clocks": r2["clocks"], "round_stats": r2["round_stats"]}
+                 "gpu_launches": r2["gpu_launches"], "clocks": r2["clocks"], "round_stats": r2["round_stats"],
+                 "contraction": r2["contraction"]}
         if not args.no_e2e:
             extra["e2e"] = measure_e2e(args, wl2, max(args.e2e_steps, 3), warm=3)
         wl2 = None
@@ -652,7 +722,8 @@ def run_ours(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded; BASELINE.json shapes, see config.workload)",
            "config": cfg_line, "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": e2e,
-           "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "round_stats": r["round_stats"]}
+           "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "round_stats": r["round_stats"],
+           "contraction": r["contraction"]}
     if extra is not None:
         out[args.extra_config] = extra
     print(json.dumps(out), flush=True)

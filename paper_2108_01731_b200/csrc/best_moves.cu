@@ -114,9 +114,9 @@ __device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i, uint64_t pol
     if constexpr (ASYNC) {
         int32_t r;
         if constexpr (LCC_ASYNC_HINT)  // relaxed, with the evict-last L2 policy of the sync path
-            asm volatile("ld.relaxed.gpu.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(C + i), "l"(pol));
+            asm volatile("ld.relaxed.gpu.global.L2::cache_hint" LCC_PF64 ".s32 %0, [%1], %2;" : "=r"(r) : "l"(C + i), "l"(pol));
         else
-            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(r) : "l"(C + i));
+            asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".s32 %0, [%1];" : "=r"(r) : "l"(C + i));
         return r;
     } else {
         return ld_keep_i32(C + i, pol);
@@ -138,15 +138,15 @@ __device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
         const uint32_t* K = static_cast<const uint32_t*>(Kp) + KS * i;
         uint32_t r;
         if constexpr (ASYNC && LCC_ASYNC_HINT)
-            asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(K), "l"(pol));
-        else if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(K));
+            asm volatile("ld.relaxed.gpu.global.L2::cache_hint" LCC_PF64 ".u32 %0, [%1], %2;" : "=r"(r) : "l"(K), "l"(pol));
+        else if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(r) : "l"(K));
         else r = (uint32_t)ld_keep_i32(reinterpret_cast<const int32_t*>(K), pol);
         return u32_to_f64(r);
     } else {
         const double* K = static_cast<const double*>(Kp);
         if constexpr (ASYNC) {
             double r;
-            asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(r) : "l"(K + i));
+            asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".f64 %0, [%1];" : "=d"(r) : "l"(K + i));
             return r;
         } else {
             return ld_keep_f64(K + i, pol);
@@ -201,8 +201,8 @@ struct BMArgs {
 template <bool ASYNC>
 __device__ __forceinline__ unsigned long long ldLK(const unsigned long long* LK, int64_t i, uint64_t pol) {
     unsigned long long r;
-    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(LK + i));
-    else asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(LK + i), "l"(pol));
+    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u64 %0, [%1];" : "=l"(r) : "l"(LK + i));
+    else asm volatile("ld.global.nc.L2::cache_hint" LCC_PF64 ".u64 %0, [%1], %2;" : "=l"(r) : "l"(LK + i), "l"(pol));
     return r;
 }
 __device__ __forceinline__ void stLK(unsigned long long* LK, int64_t i, int32_t x, double mass) {
@@ -625,7 +625,7 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if constexpr (KI) {
                 Kx[j] = 0u;
                 if ((first >> j) & 1u) {
-                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + KS * x[j]));
+                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + KS * x[j]));
                     else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + KS * x[j], pol_keep);
                 }
             } else {
@@ -1126,7 +1126,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 uint32_t km[U];
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
-                    if (cl[j]) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(km[j])
+                    if (cl[j]) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(km[j])
                                             : "l"(static_cast<const uint32_t*>(a.K) + KS * u[j]));
                 }
 #pragma unroll

@@ -221,14 +221,33 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p, uint64_t pol)
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
+// Random gathers ask L2 for 64 bytes per miss (LCC_PF64): a plain load's miss
+// pulls a 128-byte line from DRAM on B200 -- measured 122.6 bytes of DRAM
+// traffic per random 8-byte gather, 62.6 with .L2::64B (tools/micro/
+// fetch_gran.cu, profiles/r02_fetch_gran.md) -- and nothing else of that
+// line is wanted.
+#ifndef LCC_GATHER64
+#define LCC_GATHER64 1
+#endif
+#if LCC_GATHER64
+#define LCC_PF64 ".L2::64B"
+#else
+#define LCC_PF64 ""
+#endif
 __device__ __forceinline__ int32_t ld_keep_i32(const int32_t* p, uint64_t pol) {
     int32_t r;
-    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint" LCC_PF64 ".b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
 __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
     double r;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint" LCC_PF64 ".f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+// read-only random gather without a cache policy (contraction, frontier)
+__device__ __forceinline__ int32_t ld_gather_i32(const int32_t* p) {
+    int32_t r;
+    asm volatile("ld.global.nc" LCC_PF64 ".b32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 

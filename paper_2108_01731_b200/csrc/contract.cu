@@ -53,7 +53,7 @@ struct EdgeKey {
     double acc = 0.0;
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) {
         const uint64_t a = (uint32_t)__ldg(mapping + v);
-        const uint64_t b = (uint32_t)__ldg(mapping + __ldg(indices + e));
+        const uint64_t b = (uint32_t)ld_gather_i32(mapping + __ldg(indices + e));
         const auto wv = WLoad<WT>::tw(w, e);
         const int64_t o = compact ? pos : e;
         if (a == b) {
@@ -199,7 +199,7 @@ struct EmitSimple {
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
         if (cf[v]) return;
         const int64_t o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
-        cind[o] = __ldg(mapping + __ldg(indices + e));
+        cind[o] = ld_gather_i32(mapping + __ldg(indices + e));
         cw[o] = (OT)WLoad<WT>::tw(w, e);
     }
     __device__ __forceinline__ void flush() {}
@@ -272,7 +272,7 @@ struct SegFill {
     unsigned long long* intra;
     unsigned long long cnt = 0;
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) {
-        const int32_t a = __ldg(mapping + v), b = __ldg(mapping + __ldg(indices + e));
+        const int32_t a = __ldg(mapping + v), b = ld_gather_i32(mapping + __ldg(indices + e));
         const uint32_t wv = WLoad<WT>::tw(w, e);
         if (a == b) {
             keys[pos] = SEG_SENT;

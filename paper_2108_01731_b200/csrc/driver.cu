@@ -41,6 +41,25 @@ struct EventTimer {
         if (b) cudaEventDestroy(b);
     }
 };
+
+// LCC_TRACE_MOVERS=1 (diagnostic): classify an async iteration's movers.
+//   st[0] movers, st[1] moved in the previous iteration too, st[2] alone in
+//   the cluster they joined (mass == k_v), st[3] joined a fresh singleton id,
+//   st[4] sum of their degrees
+__global__ void k_mover_stats(int64_t n, const int64_t* __restrict__ indptr, const double* __restrict__ k,
+                              const uint8_t* __restrict__ moved, const uint8_t* __restrict__ prev,
+                              const int32_t* __restrict__ D, const double* __restrict__ K2,
+                              unsigned long long* st) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n || !moved[v]) return;
+    const double kv = k ? k[v] : 1.0;
+    const int32_t x = D[v];
+    atomicAdd(st + 0, 1ull);
+    if (prev && prev[v]) atomicAdd(st + 1, 1ull);
+    if (K2[x] == kv) atomicAdd(st + 2, 1ull);
+    if (x >= n) atomicAdd(st + 3, 1ull);
+    atomicAdd(st + 4, (unsigned long long)(indptr[v + 1] - indptr[v]));
+}
 }  // namespace
 
 int async_min_subrounds() {
@@ -109,6 +128,17 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
             st->ms_best_moves += ms;
             st->ms_kernels += rs.ms_kernels;
             st->kernel_launches += rs.launches;
+        }
+        if (as && cnt && getenv("LCC_TRACE_MOVERS")) {
+            Buf<unsigned long long> ms5(5, s);
+            LCC_CUDA(cudaMemsetAsync(ms5.get(), 0, 5 * sizeof(unsigned long long), s));
+            k_mover_stats<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, g.indptr, k, mv_cur, damping ? mv_prev : nullptr,
+                                                                      D.get(), K2.get(), ms5.get());
+            unsigned long long h[5];
+            LCC_CUDA(cudaMemcpyAsync(h, ms5.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+            LCC_CUDA(cudaStreamSynchronize(s));
+            fprintf(stderr, "[lcc]       movers %llu: repeat %llu, alone in target %llu, fresh %llu, mean degree %.1f\n", h[0],
+                    h[1], h[2], h[3], h[0] ? (double)h[4] / (double)h[0] : 0.0);
         }
         if (cnt == 0) break;  // Alg. 1 line 9
         any = true;

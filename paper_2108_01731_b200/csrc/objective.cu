@@ -23,7 +23,7 @@ struct IntraEdges {
     unsigned long long cnt = 0;
     double acc = 0.0;
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
-        if (__ldg(C + v) == __ldg(C + __ldg(indices + e))) {
+        if (__ldg(C + v) == ld_gather_i32(C + __ldg(indices + e))) {
             ++cnt;
             if (WLoad<WT>::weighted) acc += WLoad<WT>::at(w, e);
         }

@@ -17,15 +17,12 @@ long long& launch_counter() {
 namespace {
 thread_local std::string g_err;
 
-// Keep freed scratch in the device's stream-ordered pool: fresh pool memory
-// costs ~6 ms per GB to map on B200 (measured: 16 GB 93 ms, reused 2.3 ms),
-// so re-mapping the several-GB contraction buffers every call cost more than
-// the contraction itself.  Nothing is released inside a call; when a call
-// returns the pool is trimmed to pool_keep() (default 64 GB, LCC_POOL_KEEP_GB)
-// and lcc_release_memory() hands everything back on request.  Blocks of
-// >= 64 MB are additionally cached by the library (memory.cu), because the
-// pool re-maps pages whenever a request does not fit a free virtual range.
-// An allocation that fails trims both and retries once (memory.cu).
+// Library scratch stays mapped inside a call (memory.cu: an arena of mapped
+// virtual memory for blocks >= 1 MB, the stream-ordered pool for small
+// ones): fresh device memory costs ~6 ms per GB to map on B200 (measured:
+// 16 GB 93 ms, reused 2.3 ms), more than the contraction that needs it.
+// When a call returns both are cut back to pool_keep() (default 64 GB,
+// LCC_POOL_KEEP_GB); lcc_release_memory() hands everything back on request.
 uint64_t pool_keep() {
     static uint64_t keep = [] {
         const char* e = getenv("LCC_POOL_KEEP_GB");  // tuning / memory-tight callers

@@ -41,14 +41,12 @@ long long& launch_counter();
 
 // ---------------------------------------------------------------------------
 // device scratch.  Small buffers come straight from the stream-ordered pool
-// (cudaMallocAsync).  Large ones (>= 64 MB: contraction keys/values, hub
-// tables, per-round arrays at scale) are cached by this library: the pool
-// can reuse freed memory, but when a request does not fit a free virtual
-// range it maps physical pages afresh, ~6 ms per GB on B200 -- measured
-// 100-700 ms per contraction for buffers the previous level had just freed.
-// Cached blocks are reused best-fit (capacity <= 2x the request) in stream
-// order (an event orders reuse on another stream) and handed back by
-// trim_cache() at the end of every C-ABI call above the keep limit.
+// (cudaMallocAsync).  Large ones (>= 1 MB: contraction keys/values, hub
+// tables, per-round arrays at scale, the coarse levels) are carved out of a
+// per-device arena of mapped virtual memory (memory.cu): mapping physical
+// pages costs ~6 ms per GB on B200, so the arena keeps what it has mapped
+// for the whole call and is cut back to the keep limit by trim_cache() when
+// a C-ABI call returns.
 // ---------------------------------------------------------------------------
 constexpr size_t CACHE_MIN_BYTES = 1ull << 20;
 void* cache_alloc(size_t bytes, cudaStream_t s, size_t* cap);
@@ -100,17 +98,23 @@ struct Buf {
     operator T*() const { return p; }
 };
 
-// stream-ordered pool occupancy (GB reserved, GB in use) for traces
+// library scratch occupancy (GB mapped, GB in use): the arena of large
+// blocks plus the stream-ordered pool of small ones; for traces and for the
+// driver's does-the-contraction-fit estimate
+void arena_bytes(size_t& mapped, size_t& free_bytes);
 inline void pool_gb(double& reserved, double& used) {
-    reserved = used = 0.0;
+    size_t am = 0, af = 0;
+    arena_bytes(am, af);
+    reserved = am / 1073741824.0;
+    used = (am - af) / 1073741824.0;
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
     uint64_t r = 0, u = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r);
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u);
-    reserved = r / 1073741824.0;
-    used = u / 1073741824.0;
+    reserved += r / 1073741824.0;
+    used += u / 1073741824.0;
 }
 
 inline int num_sms() {

@@ -255,7 +255,7 @@ bool contraction_fits(const lcc_graph& g, int64_t sorted) {
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return true;
     double r, u;
     pool_gb(r, u);
-    const double avail = (double)fr + (double)cache_bytes() + (r - u) * 1073741824.0;
+    const double avail = (double)fr + (r - u) * 1073741824.0;  // unmapped + mapped-but-free
     return need < 0.9 * avail;
 }
 }  // namespace

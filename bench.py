@@ -751,6 +751,10 @@ def run_sharded(args):
     sys.stdout.flush()
     os.dup2(2, 1)
     torch.cuda.set_device(lrank)
+    if "RANK" not in os.environ:  # --sharded outside torchrun: a one-rank group
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0"})
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
     dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
     lib = _lib.load()
     wl = Workload(args)

@@ -94,6 +94,9 @@ namespace {
 #ifndef LCC_KPF
 #define LCC_KPF 0  // async k_group: a claim prefetches the cluster's mass into L2 for the scoring-time read
 #endif
+#ifndef LCC_MARKBITS
+#define LCC_MARKBITS 1  // neighbour marks: 0 byte stores; 1 test-and-set in an n-bit map (L2 resident: config-5 round 116.2 -> 103.6 ms, the byte mask cost ~1.3 G sector write-backs per round); 2 byte stores with the evict-last L2 policy (no effect)
+#endif
 #ifndef LCC_LK_ASYNC
 #define LCC_LK_ASYNC 0  // async rounds too read round-start masses from the packed words (quality -15%)
 #endif
@@ -195,6 +198,9 @@ struct BMArgs {
     // neighbours inside the kernels, null when the marks are pulled after
     // the round (k_pull_head / k_pull_rest)
     uint8_t* dmark;
+    // LCC_MARKBITS=1: the neighbour marks go to this n-bit map during the
+    // kernels (test, then RED.OR) and are expanded into `mark` after them
+    unsigned* mbits;
 };
 
 // packed-word gathers: frozen in sync rounds, relaxed loads in async ones
@@ -208,6 +214,21 @@ __device__ __forceinline__ unsigned long long ldLK(const unsigned long long* LK,
 __device__ __forceinline__ void stLK(unsigned long long* LK, int64_t i, int32_t x, double mass) {
     const unsigned long long w = (unsigned long long)(uint32_t)x | ((unsigned long long)(uint32_t)mass << 32);
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(LK + i), "l"(w) : "memory");
+}
+
+// a mover flags neighbour u for the next frontier
+__device__ __forceinline__ void mark_nbr(const BMArgs& a, int32_t u) {
+#if LCC_MARKBITS == 1
+    unsigned* w = a.mbits + ((uint32_t)u >> 5);
+    const unsigned bit = 1u << ((uint32_t)u & 31u);
+    unsigned cur;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(w));
+    if (!(cur & bit)) atomicOr(w, bit);
+#elif LCC_MARKBITS == 2
+    asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(a.mark + u), "h"((unsigned short)1), "l"(policy_evict_last()) : "memory");
+#else
+    a.mark[u] = 1;
+#endif
 }
 
 // Final choice for one vertex (mirrors oracle best_target()).
@@ -440,7 +461,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             my_moves += mv;
             if (a.mark) {  // the window's neighbour ids are still in registers
                 const int mvj = __shfl_sync(FULL, mv, j);
-                if (has_edge && mvj) a.mark[nbr] = 1;
+                if (has_edge && mvj) mark_nbr(a, nbr);
             }
             __syncwarp();  // s_sc2[buf] is zeroed again two windows on
             if (!more) break;
@@ -559,7 +580,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             my_moves += mv;
             if (a.mark) {  // the window's neighbour ids are still in registers
                 const int mvj = __shfl_sync(FULL, mv, j);
-                if (has_edge && mvj) a.mark[nbr] = 1;
+                if (has_edge && mvj) mark_nbr(a, nbr);
             }
             base = end;
             __syncwarp();
@@ -656,7 +677,7 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int mv = decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bS);
         my_moves += mv;
         if (a.mark && mv) {  // neighbour ids re-read (L1/L2-hot)
-            for (int j = 0; j < deg; ++j) a.mark[__ldg(a.indices + s + j)] = 1;
+            for (int j = 0; j < deg; ++j) mark_nbr(a, __ldg(a.indices + s + j));
         }
     }
     flush_moves(a, my_moves);
@@ -1019,7 +1040,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     auto mark_prev = [&]() {
         if (a.mark && prev_pending && s_mv[gid]) {
 #pragma unroll 4
-            for (int64_t e = prev_s + gt; e < prev_e; e += GT) a.mark[__ldg(a.indices + e)] = 1;
+            for (int64_t e = prev_s + gt; e < prev_e; e += GT) mark_nbr(a, __ldg(a.indices + e));
         }
     };
     // vertex headers one vertex ahead (LCC_HDRPF): the next vertex's list
@@ -1223,7 +1244,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 mv = __shfl_sync(FULL, mv, 0);
                 if (mv) {
 #pragma unroll 4
-                    for (int64_t e = s + gt; e < end; e += GT) a.mark[__ldg(a.indices + e)] = 1;
+                    for (int64_t e = s + gt; e < end; e += GT) mark_nbr(a, __ldg(a.indices + e));
                 }
             }
             __syncwarp();
@@ -1448,7 +1469,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                 for (int j = 0; j < WIN_ITEMS && p0 + j < E; ++j) {
                     const int p = p0 + j;
                     while (p >= s_loc[sl + 1]) ++sl;
-                    if (s_mv[sl]) a.mark[__ldg(a.indices + s_start[sl] + (p - s_loc[sl]))] = 1;
+                    if (s_mv[sl]) mark_nbr(a, __ldg(a.indices + s_start[sl] + (p - s_loc[sl])));
                 }
             }
             __syncthreads();
@@ -1697,7 +1718,7 @@ k_large_mark(BMArgs a, LargeBatch L, int64_t total_items) {
         const int64_t e0 = s + (it - L.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
 #pragma unroll 4
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += LARGE_THREADS) a.mark[__ldg(a.indices + e)] = 1;
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += LARGE_THREADS) mark_nbr(a, __ldg(a.indices + e));
     }
 }
 
@@ -2228,7 +2249,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
             cl_sync();
             if (s_moved) {
                 for (int64_t e = s + (int64_t)rank * HC_THREADS + tid; e < end; e += (int64_t)HC_CL * HC_THREADS)
-                    a.mark[__ldg(a.indices + e)] = 1;
+                    mark_nbr(a, __ldg(a.indices + e));
             }
         }
         cl_sync();  // s_moved / s_sc / s_pg free for the next hub
@@ -2791,6 +2812,13 @@ inline SideStreams& side_streams() {
 // after others in the same process reached 268K-310K instead of 333K, and
 // 333K with CUDA_MODULE_LOADING=EAGER.  So every kernel a round may launch
 // is loaded (cudaFuncGetAttributes) before its first round starts.
+// LCC_MARKBITS=1: the kernels' n-bit neighbour map into the caller's byte mask
+// (deferred movers stored their own byte directly)
+__global__ void k_bits_to_mask(const unsigned* __restrict__ bits, int64_t n, uint8_t* mark) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if ((bits[v >> 5] >> (v & 31)) & 1u) mark[v] = 1;
+}
+
 template <class F>
 void load_fn(F f) {
     cudaFuncAttributes at;
@@ -2828,6 +2856,7 @@ void preload_round_kernels() {
     load_fn(k_large_mark);
     load_fn(k_pull_head);
     load_fn(k_pull_rest);
+    load_fn(k_bits_to_mask);
     load_fn(k_degrees_of);
     load_fn(k_mass_to_u32);
     load_fn(k_mass_from_u32);
@@ -3008,8 +3037,14 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, ilv ? CK : C,
              ki ? (void*)(Ki.get() + (KS - 1)) : (void*)K, D, moved, dmoved, (int32_t)n, mark,
              dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2, use_lk ? LK.get() : nullptr,
-             ilv ? 2 : 1, mark};
+             ilv ? 2 : 1, mark, nullptr};
     if (pull) a.mark = nullptr;  // neighbour marks pulled after the kernels
+    Buf<unsigned> mbits;
+    if (LCC_MARKBITS == 1 && a.mark) {
+        mbits.alloc((n + 31) / 32, s);
+        LCC_CUDA(cudaMemsetAsync(mbits.get(), 0, sizeof(unsigned) * ((n + 31) / 32), s));
+        a.mbits = mbits.get();
+    }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     LCC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDefault));
     LCC_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDefault));
@@ -3096,6 +3131,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     };
     if (ki) launch_all(std::true_type{});
     else launch_all(std::false_type{});
+    if (a.mbits) {
+        k_bits_to_mask<<<grid_for(n, 256), 256, 0, s>>>(a.mbits, n, mark);
+        LCC_LAUNCH_CHECK();
+    }
     if (pull) {
         Buf<int32_t> rest(n, s);
         Buf<unsigned long long> nrest(1, s);

@@ -94,6 +94,9 @@ namespace {
 #ifndef LCC_KPF
 #define LCC_KPF 0  // async k_group: a claim prefetches the cluster's mass into L2 for the scoring-time read
 #endif
+#ifndef LCC_PACK32
+#define LCC_PACK32 1  // async integer-mass rounds with small masses: (label, mass) packed into ONE 32-bit word per vertex
+#endif
 #ifndef LCC_MARKBITS
 #define LCC_MARKBITS 1  // neighbour marks: 0 byte stores; 1 test-and-set in an n-bit map (L2 resident: config-5 round 116.2 -> 103.6 ms, the byte mask cost ~1.3 G sector write-backs per round); 2 byte stores with the evict-last L2 policy (no effect)
 #endif
@@ -135,16 +138,18 @@ __device__ __forceinline__ int32_t ldC(const int32_t* C, int64_t i, uint64_t pol
 constexpr int64_t KS = LCC_ILV ? 2 : 1;
 // KI: integer masses, gathered from a uint32 image of K (half the bytes of
 // the fp64 array, so labels + masses stay L2-resident); exact, see run_round.
+// ks / sh: the image's word stride (2 interleaved, 1 packed or plain) and
+// the mass field's shift inside a word (0 unless packed, see BMArgs)
 template <bool ASYNC, bool KI>
-__device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
+__device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol, int ks = KS, int sh = 0) {
     if constexpr (KI) {
-        const uint32_t* K = static_cast<const uint32_t*>(Kp) + KS * i;
+        const uint32_t* K = static_cast<const uint32_t*>(Kp) + ks * i;
         uint32_t r;
         if constexpr (ASYNC && LCC_ASYNC_HINT)
             asm volatile("ld.relaxed.gpu.global.L2::cache_hint" LCC_PF64 ".u32 %0, [%1], %2;" : "=r"(r) : "l"(K), "l"(pol));
         else if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(r) : "l"(K));
         else r = (uint32_t)ld_keep_i32(reinterpret_cast<const int32_t*>(K), pol);
-        return u32_to_f64(r);
+        return u32_to_f64(r >> sh);
     } else {
         const double* K = static_cast<const double*>(Kp);
         if constexpr (ASYNC) {
@@ -158,13 +163,13 @@ __device__ __forceinline__ double ldK(const void* Kp, int64_t i, uint64_t pol) {
 }
 // relaxed mass update; returns the mass before the add
 template <bool KI>
-__device__ __forceinline__ double addK(void* Kp, int64_t i, double kv) {
-    if constexpr (KI) return u32_to_f64(atomicAdd(static_cast<uint32_t*>(Kp) + KS * i, (uint32_t)kv));
+__device__ __forceinline__ double addK(void* Kp, int64_t i, double kv, int ks = KS, int sh = 0) {
+    if constexpr (KI) return u32_to_f64(atomicAdd(static_cast<uint32_t*>(Kp) + ks * i, (uint32_t)kv << sh) >> sh);
     else return atomicAdd(static_cast<double*>(Kp) + i, kv);
 }
 template <bool KI>
-__device__ __forceinline__ void subK(void* Kp, int64_t i, double kv) {
-    if constexpr (KI) atomicSub(static_cast<uint32_t*>(Kp) + KS * i, (uint32_t)kv);
+__device__ __forceinline__ void subK(void* Kp, int64_t i, double kv, int ks = KS, int sh = 0) {
+    if constexpr (KI) atomicSub(static_cast<uint32_t*>(Kp) + ks * i, (uint32_t)kv << sh);
     else atomicAdd(static_cast<double*>(Kp) + i, -kv);
 }
 __device__ __forceinline__ void stC_relaxed(int32_t* C, int64_t i, int32_t x) {
@@ -201,7 +206,22 @@ struct BMArgs {
     // LCC_MARKBITS=1: the neighbour marks go to this n-bit map during the
     // kernels (test, then RED.OR) and are expanded into `mark` after them
     unsigned* mbits;
+    // Packed rounds (LCC_PACK32; asynchronous, integer masses, every mass and
+    // k_v small): C and K are ONE array of 32-bit words, word i = label of
+    // vertex i in the low `ksh` bits | mass of cluster i above them -- half the
+    // bytes of the interleaved image, so twice as many vertices per L2 byte.
+    // lm masks a loaded label (all ones otherwise); ks is the mass stride in
+    // words; ksh the mass shift (0 = not packed); kmax the largest mass a
+    // join may produce (a join beyond it is refused like a failed check).
+    int32_t lm;
+    int32_t ks;
+    int32_t ksh;
+    double kmax;
 };
+// a vertex stores its new label: its word's mass field belongs to the
+// cluster of the same id and must survive (packed: add the label difference;
+// only v itself ever writes v's label)
+__device__ __forceinline__ void stC_own(const BMArgs& a, int32_t v, int32_t c_old, int32_t x);
 
 // packed-word gathers: frozen in sync rounds, relaxed loads in async ones
 template <bool ASYNC>
@@ -216,6 +236,10 @@ __device__ __forceinline__ void stLK(unsigned long long* LK, int64_t i, int32_t 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(LK + i), "l"(w) : "memory");
 }
 
+__device__ __forceinline__ void stC_own(const BMArgs& a, int32_t v, int32_t c_old, int32_t x) {
+    if (a.ksh) atomicAdd(reinterpret_cast<uint32_t*>(a.C) + v, (uint32_t)x - (uint32_t)c_old);
+    else stC_relaxed(a.C, (int64_t)v * a.cs, x);
+}
 // a mover flags neighbour u for the next frontier
 __device__ __forceinline__ void mark_nbr(const BMArgs& a, int32_t u) {
 #if LCC_MARKBITS == 1
@@ -248,26 +272,56 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                 atomicAdd(a.pending, 1ull);
                 return 0;
             }
+            if (KI && a.ksh) {
+                // packed word: the join is a compare-and-swap on the target's
+                // word, so the mass field never holds more than the joins that
+                // passed (an add-then-back-out could wrap a 4-5 bit field under
+                // contention); a joiner re-reads and re-checks until its swap
+                // lands or its gain is gone
+                uint32_t* W = static_cast<uint32_t*>(a.K);
+                const uint32_t add = (uint32_t)kv << a.ksh;
+                if (choice != a.n + v) {
+                    uint32_t old;
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(old) : "l"(W + choice));
+                    while (true) {
+                        const double kold = u32_to_f64(old >> a.ksh);
+                        if (LCC_VALIDATE && bS == bS) {
+                            const double gnow = dsub(dsub(bS, dmul(dmul(a.lam, kv), kold)), b);
+                            if (!(gnow > 0.0)) return 0;
+                        }
+                        if (kold + kv > a.kmax) return 0;  // field full: no move this round
+                        const uint32_t prev = atomicCAS(W + choice, old, old + add);
+                        if (prev == old) break;
+                        old = prev;
+                    }
+                } else {
+                    atomicAdd(W + choice, add);  // v's own fresh id: mass 0 -> k_v
+                }
+                stC_own(a, v, c, choice);
+                atomicSub(W + c, add);
+                a.moved[v] = 1;
+                return 1;
+            }
             if (LCC_VALIDATE && choice != a.n + v && bS == bS) {
                 // commit-time check: the mass x has when v joins (the atomic's
                 // return value, after every earlier joiner) must still leave a
                 // positive gain; otherwise v stays (it is in the next frontier,
                 // since its neighbours moved).  Stops stale-mass pile-ups.
-                const double kold = addK<KI>(a.K, choice, kv);
+                const double kold = addK<KI>(a.K, choice, kv, a.ks, a.ksh);
                 const double gnow = dsub(dsub(bS, dmul(dmul(a.lam, kv), kold)), b);
                 if (!(gnow > 0.0)) {
-                    subK<KI>(a.K, choice, kv);
+                    subK<KI>(a.K, choice, kv, a.ks, a.ksh);
                     return 0;
                 }
-                stC_relaxed(a.C, (int64_t)v * a.cs, choice);
+                stC_own(a, v, c, choice);
                 if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
-                subK<KI>(a.K, c, kv);
+                subK<KI>(a.K, c, kv, a.ks, a.ksh);
                 a.moved[v] = 1;
                 return 1;
             }
-            stC_relaxed(a.C, (int64_t)v * a.cs, choice);
-            subK<KI>(a.K, c, kv);
-            const double kold = addK<KI>(a.K, choice, kv);
+            stC_own(a, v, c, choice);
+            subK<KI>(a.K, c, kv, a.ks, a.ksh);
+            const double kold = addK<KI>(a.K, choice, kv, a.ks, a.ksh);
             if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
         } else {
             a.D[v] = choice;
@@ -336,9 +390,9 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             v = __ldg(list + i0 + lane);
             s = __ldg(a.indptr + v);
             deg = (int32_t)(__ldg(a.indptr + v + 1) - s);
-            c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+            c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
             kv = kval(a.k, v);
-            Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+            Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
         }
         const double t = dmul(a.lam, kv);
         int32_t incl = deg;
@@ -387,7 +441,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         int buf = 0;
         geometry(0, 0, G);
         int32_t nbr = G.has_edge ? ld_stream_i32(a.indices + G.e, pol_stream) : 0;
-        int32_t x = G.has_edge ? ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep) : 0;
+        int32_t x = G.has_edge ? (ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep) & a.lm) : 0;
         while (true) {
             const bool more = G.end < nvalid;
             Geo Gn;
@@ -419,9 +473,9 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const bool is_leader = has_edge && lane == (__ffs(grp) - 1);
             const bool cand = is_leader && x != cj;
             // mass gather of this window, then the next window's label gather
-            const double Kx = cand ? ldK<ASYNC, KI>(a.K, x, pol_keep) : 0.0;
+            const double Kx = cand ? ldK<ASYNC, KI>(a.K, x, pol_keep, a.ks, a.ksh) : 0.0;
             int32_t x_n = 0;
-            if (more && Gn.has_edge) x_n = ldC<ASYNC>(a.C, (int64_t)(nbr_n) * a.cs, pol_keep);
+            if (more && Gn.has_edge) x_n = (ldC<ASYNC>(a.C, (int64_t)(nbr_n) * a.cs, pol_keep) & a.lm);
             if (is_leader && x == cj) s_sc2[buf][wib][j] = S;
             __syncwarp();
             double bv = 0.0;
@@ -500,7 +554,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if (has_edge) {
                 const int64_t e = sj + (lane - p);
                 nbr = ld_stream_i32(a.indices + e, pol_stream);
-                x = ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep);
+                x = (ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep) & a.lm);
                 wv = WLoad<WT>::at(a.w, e);
             }
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
@@ -528,7 +582,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double gS = 0.0;
             if (is_leader && x != cj) {
                 gS = S;
-                g = dsub(dsub(S, dmul(tj, ldK<ASYNC, KI>(a.K, x, pol_keep))), bj);
+                g = dsub(dsub(S, dmul(tj, ldK<ASYNC, KI>(a.K, x, pol_keep, a.ks, a.ksh))), bj);
                 gx = x;
             }
 #if LCC_SMALL_LADDER2
@@ -619,9 +673,9 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
         const int deg = (int)(__ldg(a.indptr + v + 1) - s);
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
         int32_t x[TINY_MAX];
         TW w[TINY_MAX];
 #pragma unroll
@@ -630,7 +684,7 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             w[j] = j < deg ? WLoad<WT>::tw(a.w, s + j) : TW(0);
         }
 #pragma unroll
-        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) : EMPTY_KEY;
+        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
         // first occurrences of each neighbour cluster (other than c)
         unsigned first = 0;
 #pragma unroll
@@ -646,11 +700,12 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if constexpr (KI) {
                 Kx[j] = 0u;
                 if ((first >> j) & 1u) {
-                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + KS * x[j]));
-                    else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + KS * x[j], pol_keep);
+                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + (int64_t)a.ks * x[j]));
+                    else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + (int64_t)a.ks * x[j], pol_keep);
+                    Kx[j] >>= a.ksh;
                 }
             } else {
-                Kx[j] = ((first >> j) & 1u) ? ldK<ASYNC, false>(a.K, x[j], pol_keep) : 0.0;
+                Kx[j] = ((first >> j) & 1u) ? ldK<ASYNC, false>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
             }
         }
         double sc = 0.0;
@@ -694,10 +749,10 @@ k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     unsigned long long my_moves = 0;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = __ldg(list + i);
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
-        const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC, KI>(a.K, c, pol_keep))), dmul(t, kv));
+        const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh))), dmul(t, kv));
         my_moves += decide<ASYNC, KI>(a, v, c, kv, b, false, 0.0, 0);
     }
     flush_moves(a, my_moves);
@@ -1076,7 +1131,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             s = __ldg(a.indptr + v);
             end = __ldg(a.indptr + v + 1);
         }
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
         if constexpr (LCC_TMAPF) {
@@ -1107,7 +1162,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
         }
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
         const double t = dmul(a.lam, kv);
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
         for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
@@ -1133,7 +1188,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 }
             } else if constexpr (CLAIMK) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
+                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
                 uint32_t slot[U];
                 bool cl[U];
 #pragma unroll
@@ -1155,7 +1210,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                     if (cl[j]) tab.set_mass(slot[j], km[j]);
             } else {
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
             // (batched probe rounds measured slower here than for the L2
             // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
@@ -1205,7 +1260,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) {
@@ -1343,12 +1398,12 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             s_v[tid] = v;
             s_start[tid] = __ldg(a.indptr + v);
             s_loc[tid] = (int32_t)(__ldg(off + i0 + tid) - base);
-            const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+            const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
             s_c[tid] = c;
             const double kv = kval(a.k, v);
             s_kv[tid] = kv;
             s_t[tid] = dmul(a.lam, kv);
-            s_Kc[tid] = ldK<ASYNC, KI>(a.K, c, pol_keep);
+            s_Kc[tid] = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
             s_sc[tid] = 0;
             s_scw[tid] = 0.0;
             s_hi[tid] = 0;
@@ -1388,7 +1443,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                 }
             }
 #pragma unroll
-            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
 #pragma unroll
             for (int j = 0; j < WIN_ITEMS; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
@@ -1423,7 +1478,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             const int32_t x = (int32_t)(key & ((1u << LABEL_BITS) - 1u));
             const int sj = (int)(key >> LABEL_BITS);
             const double S = FSUM ? sums[q] : u32_to_f64(cnts[q]);
-            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC, KI>(a.K, x, pol_keep))), s_b[sj]);
+            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC, KI>(a.K, x, pol_keep, a.ks, a.ksh))), s_b[sj]);
             gval[q] = g;
             atomicMax(&s_hi[sj], (uint32_t)(ord_gain(g) >> 32));
         }
@@ -1554,7 +1609,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         double sc = 0.0;
         for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * UL) {
             int32_t u[UL];
@@ -1566,7 +1621,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
                 wv[j] = e < e1 ? WLoad<WT>::tw(a.w, e) : typename WLoad<WT>::TW(0);
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
             if constexpr (!WLoad<WT>::fsum) {
                 // first probe of all UL keys issued back to back (UL device
                 // CAS in flight per lane); collisions finish in the probe loop
@@ -1646,9 +1701,9 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const uint32_t q_begin = (uint32_t)((it - L.sitem_off[li]) * SCORE_CHUNK);
         const uint32_t q_end = (uint32_t)min64((int64_t)q_begin + SCORE_CHUNK, cap);
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
@@ -1662,7 +1717,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
                 if (!(q < q_end && tab.read(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -1690,9 +1745,9 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
         warp_argmax(bg, bx);
         if (lane == 0) {
             const int32_t v = L.list[li];
-            const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+            const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
             const double kv = kval(a.k, v);
-            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
             const double t = dmul(a.lam, kv);
             const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
             double bS = NAN;  // the winner's S, for the commit-time check (the batch's table is intact)
@@ -1814,7 +1869,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
         const int64_t e0 = s + (it - P.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t nb = (uint32_t)(P.boff[li + 1] - P.boff[li]);
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         for (int b = tid; b <= (int)nb; b += HS_THREADS) s_hist[b] = 0;
         __syncthreads();
         int32_t x[PER];
@@ -1827,7 +1882,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
             w[j] = e < e1 ? (uint32_t)WLoad<WT>::tw(a.w, e) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) : EMPTY_KEY;
+        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
         double sc = 0.0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -1893,10 +1948,10 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
         const int64_t li = owner_of(P.boff, P.nL, gb);
         const int b = (int)(gb - P.boff[li]);
         const int32_t v = P.list[li];
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
         const double bb = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
         const int64_t i0 = P.item_off[li], i1 = P.item_off[li + 1];
         // entries of this bucket over the hub's items
@@ -1994,7 +2049,7 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
                     if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+                for (int j = 0; j < 4; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     if (x[j] == EMPTY_KEY) continue;
@@ -2033,9 +2088,9 @@ __global__ void k_hub_decide(BMArgs a, HubPlan P) {
         warp_argmax(bg, bx, bS);
         if (lane == 0) {
             const int32_t v = P.list[li];
-            const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+            const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
             const double kv = kval(a.k, v);
-            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
             const double t = dmul(a.lam, kv);
             const double b = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
             my_moves += decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bx != NO_CAND ? bS : NAN);
@@ -2123,7 +2178,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
         const int64_t s = __ldg(a.indptr + v), end = __ldg(a.indptr + v + 1);
         const uint32_t cap = (uint32_t)std::min<int64_t>((int64_t)HC_CL * HC_SLICE, (2 * (end - s) + 31) & ~31LL);
         const uint32_t per = (cap + HC_CL - 1) / HC_CL;
-        const int32_t c = ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep);
+        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
         // ---- 1. inserts (remote shared-memory atomics)
         double sc = 0.0;
         for (int64_t e0 = s + (int64_t)rank * HC_THREADS + tid; e0 < end; e0 += (int64_t)HC_CL * HC_THREADS * UL) {
@@ -2136,7 +2191,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
                 wv[j] = e < end ? WLoad<WT>::tw(a.w, e) : TW(0);
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
             uint32_t h[UL];
             unsigned pending = 0;
 #pragma unroll
@@ -2191,7 +2246,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
             sct += x;
         }
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep);
+        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(sct, dmul(t, Kc)), dmul(t, kv));
         // ---- 3. score (and clear) the local slice
@@ -2216,7 +2271,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
                 }
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -2362,8 +2417,9 @@ __global__ void k_degrees_of(const int64_t* __restrict__ indptr, const int32_t* 
 // integrality (K and k), non-negativity and sum(K) < 2^31 (no transient sum
 // can wrap); any failure keeps the fp64 kernels for the round.
 __global__ void k_mass_to_u32(const double* __restrict__ K, int64_t klen, const double* __restrict__ k, int64_t n,
-                              uint32_t* __restrict__ Ki, unsigned long long* sum, unsigned* bad) {
+                              uint32_t* __restrict__ Ki, unsigned long long* sum, unsigned* bad, unsigned* maxv) {
     unsigned long long my = 0;
+    unsigned mx = 0;  // largest mass / vertex weight seen (packed rounds need them small)
     bool ok = true;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x) {
         const double x = K[i];
@@ -2372,13 +2428,19 @@ __global__ void k_mass_to_u32(const double* __restrict__ K, int64_t klen, const 
         const uint32_t u = good ? (uint32_t)x : 0u;
         Ki[KS * i] = u;
         my += u;
+        mx = max(mx, u);
         if (k && i < n) {
             const double kv = k[i];
-            ok &= kv >= 0.0 && kv < 2147483648.0 && kv == floor(kv);
+            const bool kgood = kv >= 0.0 && kv < 2147483648.0 && kv == floor(kv);
+            ok &= kgood;
+            if (kgood) mx = max(mx, (unsigned)kv);
         }
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) my += __shfl_xor_sync(FULL, my, d);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, d));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxv, mx);
     if ((threadIdx.x & 31) == 0 && my) atomicAdd(sum, my);
     if (__any_sync(FULL, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
@@ -2402,6 +2464,22 @@ __global__ void k_labels_in(const int32_t* __restrict__ C, int64_t n, int32_t* _
 __global__ void k_labels_out(const int32_t* __restrict__ CK, int64_t n, int32_t* __restrict__ C) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
         C[v] = CK[2 * v];
+}
+
+// packed rounds: W[i] = (label of vertex i, i < n) | (mass of cluster i) << lb
+__global__ void k_pack32(const int32_t* __restrict__ C, const uint32_t* __restrict__ Ki, int64_t n, int64_t klen, int lb,
+                         uint32_t* __restrict__ W) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x)
+        W[i] = (i < n ? (uint32_t)C[i] : 0u) | (Ki[KS * i] << lb);
+}
+__global__ void k_unpack32(const uint32_t* __restrict__ W, int64_t n, int64_t klen, int lb, int32_t* __restrict__ C,
+                           double* __restrict__ K) {
+    const uint32_t lm = (1u << lb) - 1u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = W[i];
+        if (i < n) C[i] = (int32_t)(w & lm);
+        K[i] = u32_to_f64(w >> lb);
+    }
 }
 
 template <class K>
@@ -2857,6 +2935,8 @@ void preload_round_kernels() {
     load_fn(k_pull_head);
     load_fn(k_pull_rest);
     load_fn(k_bits_to_mask);
+    load_fn(k_pack32);
+    load_fn(k_unpack32);
     load_fn(k_degrees_of);
     load_fn(k_mass_to_u32);
     load_fn(k_mass_from_u32);
@@ -2977,17 +3057,18 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const bool try_ki = nF > 0 && 8 * nF >= n && !(eki && eki[0] == '0');
     Buf<uint32_t> Ki;
     Buf<unsigned long long> kchk;
-    unsigned long long hk[2] = {0, 0};
+    unsigned long long hk[3] = {0, 0, 0};  // sum of masses, not-integral flag, largest mass or k_v
     float kconv_ms = 0.f;
     cudaEvent_t kev[2] = {nullptr, nullptr};
     if (try_ki) {
         for (auto& e : kev) LCC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
         Ki.alloc(KS * klen, s);  // interleaved: (label, mass) pairs -- masses at odd words, labels below
-        kchk.alloc(2, s);
-        LCC_CUDA(cudaMemsetAsync(kchk.get(), 0, sizeof(unsigned long long) * 2, s));
+        kchk.alloc(3, s);
+        LCC_CUDA(cudaMemsetAsync(kchk.get(), 0, sizeof(unsigned long long) * 3, s));
         LCC_CUDA(cudaEventRecord(kev[0], s));
         k_mass_to_u32<<<grid_for(klen, 256), 256, 0, s>>>(K, klen, k, n, Ki.get() + (KS - 1), kchk.get(),
-                                                           reinterpret_cast<unsigned*>(kchk.get() + 1));
+                                                           reinterpret_cast<unsigned*>(kchk.get() + 1),
+                                                           reinterpret_cast<unsigned*>(kchk.get() + 2));
         LCC_LAUNCH_CHECK();
         LCC_CUDA(cudaEventRecord(kev[1], s));
         LCC_CUDA(cudaMemcpyAsync(hk, kchk.get(), sizeof(hk), cudaMemcpyDeviceToHost, s));
@@ -3037,8 +3118,31 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     BMArgs a{g.indptr, g.indices, g.weights, k, lam, ilv ? CK : C,
              ki ? (void*)(Ki.get() + (KS - 1)) : (void*)K, D, moved, dmoved, (int32_t)n, mark,
              dmp ? damp->prev_moved : nullptr, dmp ? damp->salt : 0u, dcnt.get() + 2, use_lk ? LK.get() : nullptr,
-             ilv ? 2 : 1, mark, nullptr};
+             ilv ? 2 : 1, mark, nullptr, -1, (int32_t)KS, 0, 0.0};
     if (pull) a.mark = nullptr;  // neighbour marks pulled after the kernels
+    // Packed words (see BMArgs): asynchronous integer-mass rounds whose labels
+    // (ids < 2n) leave at least 4 bits of a 32-bit word for the masses, and
+    // whose masses and vertex weights start at no more than half the field
+    // (a join that would pass the field's top is refused, like a failed
+    // commit check).  LCC_PACK32=0 (env) keeps the interleaved 64-bit image.
+    Buf<uint32_t> W32;
+    int pk_lb = 0;
+    {
+        const char* epk = getenv("LCC_PACK32");
+        const int lb = std::max(1, bit_width((uint64_t)std::max<int64_t>(klen - 1, 1)));
+        const unsigned cap = lb <= 28 ? (1u << (32 - lb)) - 1u : 0u;
+        if (LCC_PACK32 && ASYNC && ilv && !use_lk && !(epk && epk[0] == '0') && cap >= 15u && hk[2] <= cap / 2) {
+            pk_lb = lb;
+            W32.alloc(klen, s);
+            a.C = reinterpret_cast<int32_t*>(W32.get());
+            a.K = W32.get();
+            a.cs = 1;
+            a.ks = 1;
+            a.ksh = lb;
+            a.lm = (int32_t)((1u << lb) - 1u);
+            a.kmax = (double)(cap - 1u);
+        }
+    }
     Buf<unsigned> mbits;
     if (LCC_MARKBITS == 1 && a.mark) {
         mbits.alloc((n + 31) / 32, s);
@@ -3069,7 +3173,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const bool concurrent = P == 1 || (esc ? (esc[0] == '1' && nF >= (1 << 20))
                                            : nF >= (1 << 22));
     LCC_CUDA(cudaEventRecord(ev0, s));
-    if (ilv) {  // timed with the kernels
+    if (pk_lb) {  // timed with the kernels
+        k_pack32<<<grid_for(klen, 256), 256, 0, s>>>(C, Ki.get() + (KS - 1), n, klen, pk_lb, W32.get());
+        LCC_LAUNCH_CHECK();
+    } else if (ilv) {
         k_labels_in<<<grid_for(n, 256), 256, 0, s>>>(C, n, CK);
         LCC_LAUNCH_CHECK();
     }
@@ -3144,7 +3251,10 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
         k_pull_rest<<<num_sms() * 8, 256, 0, s>>>(g.indptr, g.indices, moved, mark, rest.get(), nrest.get());
         LCC_LAUNCH_CHECK();
     }
-    if (ki && ASYNC) {  // async moves updated the image: back to fp64 K (and the labels to C)
+    if (pk_lb) {
+        k_unpack32<<<grid_for(klen, 256), 256, 0, s>>>(W32.get(), n, klen, pk_lb, C, K);
+        LCC_LAUNCH_CHECK();
+    } else if (ki && ASYNC) {  // async moves updated the image: back to fp64 K (and the labels to C)
         k_mass_from_u32<<<grid_for(klen, 256), 256, 0, s>>>(Ki.get() + (KS - 1), klen, K);
         LCC_LAUNCH_CHECK();
         if (ilv) {

@@ -3129,7 +3129,8 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     int pk_lb = 0;
     {
         const char* epk = getenv("LCC_PACK32");
-        const int lb = std::max(1, bit_width((uint64_t)std::max<int64_t>(klen - 1, 1)));
+        int lb = std::max(1, bit_width((uint64_t)std::max<int64_t>(klen - 1, 1)));
+        if (const char* eb = getenv("LCC_PACK32_BITS")) lb = std::max(lb, atoi(eb));  // tests: a narrow mass field
         const unsigned cap = lb <= 28 ? (1u << (32 - lb)) - 1u : 0u;
         if (LCC_PACK32 && ASYNC && ilv && !use_lk && !(epk && epk[0] == '0') && cap >= 15u && hk[2] <= cap / 2) {
             pk_lb = lb;

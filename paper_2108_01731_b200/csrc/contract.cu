@@ -36,6 +36,28 @@ __global__ void k_map(const int32_t* __restrict__ C, const int32_t* __restrict__
     }
 }
 
+// Renumbering without the gather: rank(u) = #roots below u = the sampled scan
+// at u's 32-vertex word + the popcount of the word's root bits below u.  For
+// a root u, mapping[u] = rank(u); the two arrays are n/8 bytes together (L2
+// resident at any size here) where mapping is 4n bytes of random gathers.
+__global__ void k_rootbits(const int32_t* __restrict__ C, const int32_t* __restrict__ rank, int64_t n,
+                           uint32_t* __restrict__ rbits, uint32_t* __restrict__ rpref) {
+    const int64_t nv = (n + 31) / 32 * 32;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        const bool root = v < n && C[v] == (int32_t)v;
+        const unsigned b = __ballot_sync(0xffffffffu, root);
+        if ((v & 31) == 0) {
+            rbits[v >> 5] = b;
+            rpref[v >> 5] = (uint32_t)rank[v];
+        }
+    }
+}
+__device__ __forceinline__ int32_t root_rank(const uint32_t* __restrict__ rbits, const uint32_t* __restrict__ rpref,
+                                             int32_t u) {
+    const uint32_t w = (uint32_t)u >> 5;
+    return (int32_t)(__ldg(rpref + w) + __popc(__ldg(rbits + w) & ((1u << (u & 31)) - 1u)));
+}
+
 // edge functor: key of the directed entry (v, u), intra entries -> sentinel
 template <class WT, class VT>
 struct EdgeKey {
@@ -196,10 +218,12 @@ struct EmitSimple {
     const int64_t* cindptr;
     int32_t* cind;
     OT* cw;
+    const uint32_t* rbits;  // every neighbour of a simple row is a root: its
+    const uint32_t* rpref;  // coarse id is its rank (no mapping gather)
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
         if (cf[v]) return;
         const int64_t o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
-        cind[o] = ld_gather_i32(mapping + __ldg(indices + e));
+        cind[o] = root_rank(rbits, rpref, __ldg(indices + e));
         cw[o] = (OT)WLoad<WT>::tw(w, e);
     }
     __device__ __forceinline__ void flush() {}
@@ -590,6 +614,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     PhaseTrace tr(s);
     // 1. dense renumbering by smallest member
     int64_t cn = 0;
+    Buf<uint32_t> rbits, rpref;  // root bitmap + sampled rank (root_rank)
     {
         Buf<int32_t> rank(n + 1, s);
         cub::TransformInputIterator<int32_t, IsRoot, cub::CountingInputIterator<int32_t>> roots(
@@ -598,6 +623,10 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         int32_t hcn = 0;
         LCC_CUDA(cudaMemcpyAsync(&hcn, rank.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         k_map<<<grid_for(n, 256), 256, 0, s>>>(C, rank.get(), K, n, mapping, ck);
+        LCC_LAUNCH_CHECK();
+        rbits.alloc((n + 31) / 32, s);
+        rpref.alloc((n + 31) / 32, s);
+        k_rootbits<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, s>>>(C, rank.get(), n, rbits.get(), rpref.get());
         LCC_LAUNCH_CHECK();
         LCC_CUDA(cudaStreamSynchronize(s));
         cn = hcn;
@@ -744,7 +773,8 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
             if (int_out) {
                 edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                               EmitSimple<WT, uint32_t>{g.indices, g.weights, mapping, cf.get(), g.indptr,
-                                                       out.indptr.get(), out.indices.get(), out.wi.get()}, s);
+                                                       out.indptr.get(), out.indices.get(), out.wi.get(),
+                                                       rbits.get(), rpref.get()}, s);
                 if (Rc > 0) {
                     k_emit_complex<uint32_t, uint32_t><<<grid_for(Rc, 256), 256, 0, s>>>(
                         ukeys.get(), swi.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),
@@ -754,7 +784,8 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
             } else {
                 edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                               EmitSimple<WT, double>{g.indices, g.weights, mapping, cf.get(), g.indptr,
-                                                     out.indptr.get(), out.indices.get(), out.w.get()}, s);
+                                                     out.indptr.get(), out.indices.get(), out.w.get(),
+                                                     rbits.get(), rpref.get()}, s);
                 if (Rc > 0) {
                     k_emit_complex<double, double><<<grid_for(Rc, 256), 256, 0, s>>>(
                         ukeys.get(), sw.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),

@@ -219,11 +219,16 @@ struct EmitSimple {
     int32_t* cind;
     OT* cw;
     const uint32_t* rbits;  // every neighbour of a simple row is a root: its
-    const uint32_t* rpref;  // coarse id is its rank (no mapping gather)
+    const uint32_t* rpref;  // coarse id is its rank (no mapping gather).  Null
+                            // for a shard's partial rows: a neighbour whose row
+                            // lives on another rank never marked this row, so
+                            // it may be a non-root; those rows keep the gather
+                            // (the owner-side merge sorts and sums them)
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
         if (cf[v]) return;
         const int64_t o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
-        cind[o] = root_rank(rbits, rpref, __ldg(indices + e));
+        const int32_t u = __ldg(indices + e);
+        cind[o] = rbits ? root_rank(rbits, rpref, u) : ld_gather_i32(mapping + u);
         cw[o] = (OT)WLoad<WT>::tw(w, e);
     }
     __device__ __forceinline__ void flush() {}
@@ -612,6 +617,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     const int64_t n = g.n, nnz = g.nnz;
     Coarse out;
     PhaseTrace tr(s);
+    const bool partial = (g.flags & LCC_GRAPH_PARTIAL_ROWS) != 0;
     // 1. dense renumbering by smallest member
     int64_t cn = 0;
     Buf<uint32_t> rbits, rpref;  // root bitmap + sampled rank (root_rank)
@@ -774,7 +780,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
                 edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                               EmitSimple<WT, uint32_t>{g.indices, g.weights, mapping, cf.get(), g.indptr,
                                                        out.indptr.get(), out.indices.get(), out.wi.get(),
-                                                       rbits.get(), rpref.get()}, s);
+                                                       partial ? nullptr : rbits.get(), partial ? nullptr : rpref.get()}, s);
                 if (Rc > 0) {
                     k_emit_complex<uint32_t, uint32_t><<<grid_for(Rc, 256), 256, 0, s>>>(
                         ukeys.get(), swi.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),
@@ -785,7 +791,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
                 edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                               EmitSimple<WT, double>{g.indices, g.weights, mapping, cf.get(), g.indptr,
                                                      out.indptr.get(), out.indices.get(), out.w.get(),
-                                                     rbits.get(), rpref.get()}, s);
+                                                     partial ? nullptr : rbits.get(), partial ? nullptr : rpref.get()}, s);
                 if (Rc > 0) {
                     k_emit_complex<double, double><<<grid_for(Rc, 256), 256, 0, s>>>(
                         ukeys.get(), sw.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),

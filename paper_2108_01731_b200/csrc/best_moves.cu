@@ -97,6 +97,9 @@ namespace {
 #ifndef LCC_PACK32
 #define LCC_PACK32 1  // async integer-mass rounds with small masses: (label, mass) packed into ONE 32-bit word per vertex
 #endif
+#ifndef LCC_CODES
+#define LCC_CODES 0  // (measured, off) integer-mass async rounds: 4-bit L2-resident codes stand in for the (label, mass) words of own-cluster roots (BMArgs::code)
+#endif
 #ifndef LCC_MARKBITS
 #define LCC_MARKBITS 1  // neighbour marks: 0 byte stores; 1 test-and-set in an n-bit map (L2 resident: config-5 round 116.2 -> 103.6 ms, the byte mask cost ~1.3 G sector write-backs per round); 2 byte stores with the evict-last L2 policy (no effect)
 #endif
@@ -217,6 +220,15 @@ struct BMArgs {
     int32_t ks;
     int32_t ksh;
     double kmax;
+    // Codes (LCC_CODES; packed rounds only): 4 bits per vertex, code[i] = the
+    // mass of cluster i while word i still reads (label i | mass << ksh) with
+    // 1 <= mass <= 15, else 0 -- an L2-resident summary (n/2 bytes) of the
+    // packed words: a gather whose code is set needs no DRAM access.  A mover
+    // clears the codes of the words it is about to change (its own, its old
+    // and its new cluster's) before it changes them, and nothing sets a code
+    // during a round, so a set code is never newer than its word: readers see
+    // the same relaxed, possibly stale view as with the words alone.
+    unsigned* code;
 };
 // a vertex stores its new label: its word's mass field belongs to the
 // cluster of the same id and must survive (packed: add the label difference;
@@ -239,6 +251,38 @@ __device__ __forceinline__ void stLK(unsigned long long* LK, int64_t i, int32_t 
 __device__ __forceinline__ void stC_own(const BMArgs& a, int32_t v, int32_t c_old, int32_t x) {
     if (a.ksh) atomicAdd(reinterpret_cast<uint32_t*>(a.C) + v, (uint32_t)x - (uint32_t)c_old);
     else stC_relaxed(a.C, (int64_t)v * a.cs, x);
+}
+// ---- codes (see BMArgs::code) ---------------------------------------------
+__device__ __forceinline__ uint32_t code_of(const unsigned* code, int32_t i) {
+    uint32_t w;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(w) : "l"(code + ((uint32_t)i >> 3)));
+    return (w >> (((uint32_t)i & 7u) * 4u)) & 15u;
+}
+__device__ __forceinline__ void code_clear(const BMArgs& a, int32_t i) {
+    if (!LCC_CODES || !a.code || i >= a.n) return;
+    unsigned* w = a.code + ((uint32_t)i >> 3);
+    const unsigned m = 15u << (((uint32_t)i & 7u) * 4u);
+    unsigned cur;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(w));
+    if (cur & m) atomicAnd(w, ~m);
+}
+// label of vertex u / mass of cluster x: from the code when it is set
+template <bool ASYNC>
+__device__ __forceinline__ int32_t ldLabel(const BMArgs& a, int32_t u, uint64_t pol) {
+    if constexpr (ASYNC && LCC_CODES) {
+        if (a.code && code_of(a.code, u)) return u;
+    }
+    return ldC<ASYNC>(a.C, (int64_t)u * a.cs, pol) & a.lm;
+}
+template <bool ASYNC, bool KI>
+__device__ __forceinline__ double ldMass(const BMArgs& a, int32_t x, uint64_t pol) {
+    if constexpr (ASYNC && KI && LCC_CODES) {
+        if (a.code && x < a.n) {
+            const uint32_t cd = code_of(a.code, x);
+            if (cd) return u32_to_f64(cd);
+        }
+    }
+    return ldK<ASYNC, KI>(a.K, x, pol, a.ks, a.ksh);
 }
 // a mover flags neighbour u for the next frontier
 __device__ __forceinline__ void mark_nbr(const BMArgs& a, int32_t u) {
@@ -281,6 +325,7 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                 uint32_t* W = static_cast<uint32_t*>(a.K);
                 const uint32_t add = (uint32_t)kv << a.ksh;
                 if (choice != a.n + v) {
+                    code_clear(a, choice);  // before the word changes (BMArgs::code)
                     uint32_t old;
                     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(old) : "l"(W + choice));
                     while (true) {
@@ -297,6 +342,8 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                 } else {
                     atomicAdd(W + choice, add);  // v's own fresh id: mass 0 -> k_v
                 }
+                code_clear(a, v);
+                code_clear(a, c);
                 stC_own(a, v, c, choice);
                 atomicSub(W + c, add);
                 a.moved[v] = 1;
@@ -307,18 +354,24 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
                 // return value, after every earlier joiner) must still leave a
                 // positive gain; otherwise v stays (it is in the next frontier,
                 // since its neighbours moved).  Stops stale-mass pile-ups.
+                code_clear(a, choice);  // before the word changes (BMArgs::code)
                 const double kold = addK<KI>(a.K, choice, kv, a.ks, a.ksh);
                 const double gnow = dsub(dsub(bS, dmul(dmul(a.lam, kv), kold)), b);
                 if (!(gnow > 0.0)) {
                     subK<KI>(a.K, choice, kv, a.ks, a.ksh);
                     return 0;
                 }
+                code_clear(a, v);
+                code_clear(a, c);
                 stC_own(a, v, c, choice);
                 if (KI && a.LK) stLK(a.LK, v, choice, kold + kv);
                 subK<KI>(a.K, c, kv, a.ks, a.ksh);
                 a.moved[v] = 1;
                 return 1;
             }
+            code_clear(a, choice);
+            code_clear(a, v);
+            code_clear(a, c);
             stC_own(a, v, c, choice);
             subK<KI>(a.K, c, kv, a.ks, a.ksh);
             const double kold = addK<KI>(a.K, choice, kv, a.ks, a.ksh);
@@ -390,9 +443,9 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             v = __ldg(list + i0 + lane);
             s = __ldg(a.indptr + v);
             deg = (int32_t)(__ldg(a.indptr + v + 1) - s);
-            c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+            c = ldLabel<ASYNC>(a, v, pol_keep);
             kv = kval(a.k, v);
-            Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+            Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
         }
         const double t = dmul(a.lam, kv);
         int32_t incl = deg;
@@ -441,7 +494,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         int buf = 0;
         geometry(0, 0, G);
         int32_t nbr = G.has_edge ? ld_stream_i32(a.indices + G.e, pol_stream) : 0;
-        int32_t x = G.has_edge ? (ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep) & a.lm) : 0;
+        int32_t x = G.has_edge ? ldLabel<ASYNC>(a, nbr, pol_keep) : 0;
         while (true) {
             const bool more = G.end < nvalid;
             Geo Gn;
@@ -473,9 +526,9 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             const bool is_leader = has_edge && lane == (__ffs(grp) - 1);
             const bool cand = is_leader && x != cj;
             // mass gather of this window, then the next window's label gather
-            const double Kx = cand ? ldK<ASYNC, KI>(a.K, x, pol_keep, a.ks, a.ksh) : 0.0;
+            const double Kx = cand ? ldMass<ASYNC, KI>(a, x, pol_keep) : 0.0;
             int32_t x_n = 0;
-            if (more && Gn.has_edge) x_n = (ldC<ASYNC>(a.C, (int64_t)(nbr_n) * a.cs, pol_keep) & a.lm);
+            if (more && Gn.has_edge) x_n = ldLabel<ASYNC>(a, nbr_n, pol_keep);
             if (is_leader && x == cj) s_sc2[buf][wib][j] = S;
             __syncwarp();
             double bv = 0.0;
@@ -554,7 +607,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if (has_edge) {
                 const int64_t e = sj + (lane - p);
                 nbr = ld_stream_i32(a.indices + e, pol_stream);
-                x = (ldC<ASYNC>(a.C, (int64_t)(nbr) * a.cs, pol_keep) & a.lm);
+                x = ldLabel<ASYNC>(a, nbr, pol_keep);
                 wv = WLoad<WT>::at(a.w, e);
             }
             const uint64_t key = has_edge ? (((uint64_t)(uint32_t)j << 32) | (uint32_t)x)
@@ -582,7 +635,7 @@ k_small(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             double gS = 0.0;
             if (is_leader && x != cj) {
                 gS = S;
-                g = dsub(dsub(S, dmul(tj, ldK<ASYNC, KI>(a.K, x, pol_keep, a.ks, a.ksh))), bj);
+                g = dsub(dsub(S, dmul(tj, ldMass<ASYNC, KI>(a, x, pol_keep))), bj);
                 gx = x;
             }
 #if LCC_SMALL_LADDER2
@@ -673,9 +726,9 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
         const int32_t v = __ldg(list + i);
         const int64_t s = __ldg(a.indptr + v);
         const int deg = (int)(__ldg(a.indptr + v + 1) - s);
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+        const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
         int32_t x[TINY_MAX];
         TW w[TINY_MAX];
 #pragma unroll
@@ -684,7 +737,7 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             w[j] = j < deg ? WLoad<WT>::tw(a.w, s + j) : TW(0);
         }
 #pragma unroll
-        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+        for (int j = 0; j < TINY_MAX; ++j) x[j] = x[j] >= 0 ? ldLabel<ASYNC>(a, x[j], pol_keep) : EMPTY_KEY;
         // first occurrences of each neighbour cluster (other than c)
         unsigned first = 0;
 #pragma unroll
@@ -700,9 +753,17 @@ k_tiny(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             if constexpr (KI) {
                 Kx[j] = 0u;
                 if ((first >> j) & 1u) {
-                    if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + (int64_t)a.ks * x[j]));
-                    else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + (int64_t)a.ks * x[j], pol_keep);
-                    Kx[j] >>= a.ksh;
+                    uint32_t cd = 0u;
+                    if constexpr (ASYNC && LCC_CODES) {
+                        if (a.code && x[j] < a.n) cd = code_of(a.code, x[j]);
+                    }
+                    if (cd) {
+                        Kx[j] = cd;
+                    } else {
+                        if constexpr (ASYNC) asm volatile("ld.relaxed.gpu.global" LCC_PF64 ".u32 %0, [%1];" : "=r"(Kx[j]) : "l"(static_cast<const uint32_t*>(a.K) + (int64_t)a.ks * x[j]));
+                        else Kx[j] = (uint32_t)ld_keep_i32(static_cast<const int32_t*>(a.K) + (int64_t)a.ks * x[j], pol_keep);
+                        Kx[j] >>= a.ksh;
+                    }
                 }
             } else {
                 Kx[j] = ((first >> j) & 1u) ? ldK<ASYNC, false>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
@@ -749,10 +810,10 @@ k_isolated(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
     unsigned long long my_moves = 0;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = __ldg(list + i);
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
-        const double b = dadd(dsub(0.0, dmul(t, ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh))), dmul(t, kv));
+        const double b = dadd(dsub(0.0, dmul(t, ldMass<ASYNC, KI>(a, c, pol_keep))), dmul(t, kv));
         my_moves += decide<ASYNC, KI>(a, v, c, kv, b, false, 0.0, 0);
     }
     flush_moves(a, my_moves);
@@ -1131,7 +1192,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             s = __ldg(a.indptr + v);
             end = __ldg(a.indptr + v + 1);
         }
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         const int64_t deg = end - s;
         const uint32_t cap = (uint32_t)min64(CAP, (2 * deg + 31) & ~31LL);
         if constexpr (LCC_TMAPF) {
@@ -1162,7 +1223,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
         }
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+        const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
         const double t = dmul(a.lam, kv);
         double sc = 0.0;  // S_c: weight to v's own cluster (kept out of the table)
         for (int64_t e0 = s + gt; e0 < end; e0 += (int64_t)GT * U) {
@@ -1188,7 +1249,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 }
             } else if constexpr (CLAIMK) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+                for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldLabel<ASYNC>(a, u[j], pol_keep) : EMPTY_KEY;
                 uint32_t slot[U];
                 bool cl[U];
 #pragma unroll
@@ -1210,7 +1271,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                     if (cl[j]) tab.set_mass(slot[j], km[j]);
             } else {
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+            for (int j = 0; j < U; ++j) u[j] = u[j] >= 0 ? ldLabel<ASYNC>(a, u[j], pol_keep) : EMPTY_KEY;
             // (batched probe rounds measured slower here than for the L2
             // tables: shared-memory CAS latency is short, registers are not)
 #pragma unroll
@@ -1260,7 +1321,7 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
                 if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
+            for (int j = 0; j < U; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldMass<ASYNC, KI>(a, x[j], pol_keep) : 0.0;
             }
 #pragma unroll
             for (int j = 0; j < U; ++j) {
@@ -1398,12 +1459,12 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             s_v[tid] = v;
             s_start[tid] = __ldg(a.indptr + v);
             s_loc[tid] = (int32_t)(__ldg(off + i0 + tid) - base);
-            const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+            const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
             s_c[tid] = c;
             const double kv = kval(a.k, v);
             s_kv[tid] = kv;
             s_t[tid] = dmul(a.lam, kv);
-            s_Kc[tid] = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+            s_Kc[tid] = ldMass<ASYNC, KI>(a, c, pol_keep);
             s_sc[tid] = 0;
             s_scw[tid] = 0.0;
             s_hi[tid] = 0;
@@ -1443,7 +1504,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
                 }
             }
 #pragma unroll
-            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+            for (int j = 0; j < WIN_ITEMS; ++j) u[j] = u[j] >= 0 ? ldLabel<ASYNC>(a, u[j], pol_keep) : EMPTY_KEY;
 #pragma unroll
             for (int j = 0; j < WIN_ITEMS; ++j) {
                 if (u[j] == EMPTY_KEY) continue;
@@ -1478,7 +1539,7 @@ k_window(BMArgs a, const int32_t* __restrict__ list, const int64_t* __restrict__
             const int32_t x = (int32_t)(key & ((1u << LABEL_BITS) - 1u));
             const int sj = (int)(key >> LABEL_BITS);
             const double S = FSUM ? sums[q] : u32_to_f64(cnts[q]);
-            const double g = dsub(dsub(S, dmul(s_t[sj], ldK<ASYNC, KI>(a.K, x, pol_keep, a.ks, a.ksh))), s_b[sj]);
+            const double g = dsub(dsub(S, dmul(s_t[sj], ldMass<ASYNC, KI>(a, x, pol_keep))), s_b[sj]);
             gval[q] = g;
             atomicMax(&s_hi[sj], (uint32_t)(ord_gain(g) >> 32));
         }
@@ -1609,7 +1670,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t cap = (uint32_t)(L.cap_off[li + 1] - L.cap_off[li]);
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         double sc = 0.0;
         for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += (int64_t)LARGE_THREADS * UL) {
             int32_t u[UL];
@@ -1621,7 +1682,7 @@ k_large_insert(BMArgs a, LargeBatch L, int64_t total_items) {
                 wv[j] = e < e1 ? WLoad<WT>::tw(a.w, e) : typename WLoad<WT>::TW(0);
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldLabel<ASYNC>(a, u[j], pol_keep) : EMPTY_KEY;
             if constexpr (!WLoad<WT>::fsum) {
                 // first probe of all UL keys issued back to back (UL device
                 // CAS in flight per lane); collisions finish in the probe loop
@@ -1701,9 +1762,9 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
         const uint32_t q_begin = (uint32_t)((it - L.sitem_off[li]) * SCORE_CHUNK);
         const uint32_t q_end = (uint32_t)min64((int64_t)q_begin + SCORE_CHUNK, cap);
         const auto tab = gtable<WLoad<WT>::fsum>(L, L.cap_off[li]);
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+        const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
         double bg = -INFINITY;
@@ -1717,7 +1778,7 @@ k_large_score(BMArgs a, LargeBatch L, int64_t total_items) {
                 if (!(q < q_end && tab.read(q, x[j], S[j]))) x[j] = EMPTY_KEY;
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldMass<ASYNC, KI>(a, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -1745,9 +1806,9 @@ __global__ void k_large_decide(BMArgs a, LargeBatch L) {
         warp_argmax(bg, bx);
         if (lane == 0) {
             const int32_t v = L.list[li];
-            const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+            const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
             const double kv = kval(a.k, v);
-            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+            const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
             const double t = dmul(a.lam, kv);
             const double b = dadd(dsub(L.sc[li], dmul(t, Kc)), dmul(t, kv));
             double bS = NAN;  // the winner's S, for the commit-time check (the batch's table is intact)
@@ -1869,7 +1930,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
         const int64_t e0 = s + (it - P.item_off[li]) * LARGE_CHUNK;
         const int64_t e1 = min64(e0 + LARGE_CHUNK, e_end);
         const uint32_t nb = (uint32_t)(P.boff[li + 1] - P.boff[li]);
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         for (int b = tid; b <= (int)nb; b += HS_THREADS) s_hist[b] = 0;
         __syncthreads();
         int32_t x[PER];
@@ -1882,7 +1943,7 @@ k_hub_scatter(BMArgs a, HubPlan P, int64_t total_items) {
             w[j] = e < e1 ? (uint32_t)WLoad<WT>::tw(a.w, e) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(x[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+        for (int j = 0; j < PER; ++j) x[j] = x[j] >= 0 ? ldLabel<ASYNC>(a, x[j], pol_keep) : EMPTY_KEY;
         double sc = 0.0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -1948,10 +2009,10 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
         const int64_t li = owner_of(P.boff, P.nL, gb);
         const int b = (int)(gb - P.boff[li]);
         const int32_t v = P.list[li];
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         const double kv = kval(a.k, v);
         const double t = dmul(a.lam, kv);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+        const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
         const double bb = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
         const int64_t i0 = P.item_off[li], i1 = P.item_off[li + 1];
         // entries of this bucket over the hub's items
@@ -2049,7 +2110,7 @@ k_hub_bucket(BMArgs a, HubPlan P, int64_t total_buckets) {
                     if (!(q < cap && tab.take(q, x[j], S[j]))) x[j] = EMPTY_KEY;
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
+                for (int j = 0; j < 4; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldMass<ASYNC, KI>(a, x[j], pol_keep) : 0.0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     if (x[j] == EMPTY_KEY) continue;
@@ -2088,9 +2149,9 @@ __global__ void k_hub_decide(BMArgs a, HubPlan P) {
         warp_argmax(bg, bx, bS);
         if (lane == 0) {
             const int32_t v = P.list[li];
-            const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+            const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
             const double kv = kval(a.k, v);
-            const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+            const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
             const double t = dmul(a.lam, kv);
             const double b = dadd(dsub(P.sc[li], dmul(t, Kc)), dmul(t, kv));
             my_moves += decide<ASYNC, KI>(a, v, c, kv, b, bx != NO_CAND, bg, bx, bx != NO_CAND ? bS : NAN);
@@ -2178,7 +2239,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
         const int64_t s = __ldg(a.indptr + v), end = __ldg(a.indptr + v + 1);
         const uint32_t cap = (uint32_t)std::min<int64_t>((int64_t)HC_CL * HC_SLICE, (2 * (end - s) + 31) & ~31LL);
         const uint32_t per = (cap + HC_CL - 1) / HC_CL;
-        const int32_t c = (ldC<ASYNC>(a.C, (int64_t)(v) * a.cs, pol_keep) & a.lm);
+        const int32_t c = ldLabel<ASYNC>(a, v, pol_keep);
         // ---- 1. inserts (remote shared-memory atomics)
         double sc = 0.0;
         for (int64_t e0 = s + (int64_t)rank * HC_THREADS + tid; e0 < end; e0 += (int64_t)HC_CL * HC_THREADS * UL) {
@@ -2191,7 +2252,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
                 wv[j] = e < end ? WLoad<WT>::tw(a.w, e) : TW(0);
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? (ldC<ASYNC>(a.C, (int64_t)(u[j]) * a.cs, pol_keep) & a.lm) : EMPTY_KEY;
+            for (int j = 0; j < UL; ++j) u[j] = u[j] >= 0 ? ldLabel<ASYNC>(a, u[j], pol_keep) : EMPTY_KEY;
             uint32_t h[UL];
             unsigned pending = 0;
 #pragma unroll
@@ -2246,7 +2307,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
             sct += x;
         }
         const double kv = kval(a.k, v);
-        const double Kc = ldK<ASYNC, KI>(a.K, c, pol_keep, a.ks, a.ksh);
+        const double Kc = ldMass<ASYNC, KI>(a, c, pol_keep);
         const double t = dmul(a.lam, kv);
         const double b = dadd(dsub(sct, dmul(t, Kc)), dmul(t, kv));
         // ---- 3. score (and clear) the local slice
@@ -2271,7 +2332,7 @@ k_hub_cluster(BMArgs a, const int32_t* __restrict__ hubs, int64_t nh) {
                 }
             }
 #pragma unroll
-            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldK<ASYNC, KI>(a.K, x[j], pol_keep, a.ks, a.ksh) : 0.0;
+            for (int j = 0; j < UL; ++j) Kx[j] = x[j] != EMPTY_KEY ? ldMass<ASYNC, KI>(a, x[j], pol_keep) : 0.0;
 #pragma unroll
             for (int j = 0; j < UL; ++j) {
                 if (x[j] == EMPTY_KEY) continue;
@@ -2471,6 +2532,30 @@ __global__ void k_pack32(const int32_t* __restrict__ C, const uint32_t* __restri
                          uint32_t* __restrict__ W) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < klen; i += (int64_t)gridDim.x * blockDim.x)
         W[i] = (i < n ? (uint32_t)C[i] : 0u) | (Ki[KS * i] << lb);
+}
+// codes of a packed round (BMArgs::code): one thread per 8 vertices; *nvalid counts the set codes
+__global__ void k_codes(const int32_t* __restrict__ C, const uint32_t* __restrict__ Ki, int64_t n, unsigned* __restrict__ code,
+                        unsigned long long* nvalid) {
+    const int64_t nw = (n + 7) / 8;
+    unsigned long long mine = 0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+        unsigned word = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t i = 8 * w + j;
+            if (i < n) {
+                const uint32_t m = Ki[KS * i];
+                if (C[i] == (int32_t)i && m >= 1u && m <= 15u) {
+                    word |= m << (4 * j);
+                    ++mine;
+                }
+            }
+        }
+        code[w] = word;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) mine += __shfl_xor_sync(FULL, mine, d);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(nvalid, mine);
 }
 __global__ void k_unpack32(const uint32_t* __restrict__ W, int64_t n, int64_t klen, int lb, int32_t* __restrict__ C,
                            double* __restrict__ K) {
@@ -2937,6 +3022,7 @@ void preload_round_kernels() {
     load_fn(k_bits_to_mask);
     load_fn(k_pack32);
     load_fn(k_unpack32);
+    load_fn(k_codes);
     load_fn(k_degrees_of);
     load_fn(k_mass_to_u32);
     load_fn(k_mass_from_u32);
@@ -3057,19 +3143,30 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     const bool try_ki = nF > 0 && 8 * nF >= n && !(eki && eki[0] == '0');
     Buf<uint32_t> Ki;
     Buf<unsigned long long> kchk;
-    unsigned long long hk[3] = {0, 0, 0};  // sum of masses, not-integral flag, largest mass or k_v
+    unsigned long long hk[4] = {0, 0, 0, 0};  // sum of masses, not-integral flag, largest mass or k_v, set codes
+    // codes of a packed round (BMArgs::code): built next to the mass image so
+    // that their count reaches the host with the bin partition's sync.
+    // LCC_CODES=0 disables; LCC_CODES_MIN_PCT: least share of set codes (default 90)
+    static const bool codes_on = !(getenv("LCC_CODES") && getenv("LCC_CODES")[0] == '0');
+    static const int codes_min_pct = getenv("LCC_CODES_MIN_PCT") ? atoi(getenv("LCC_CODES_MIN_PCT")) : 90;
+    Buf<unsigned> codes;
     float kconv_ms = 0.f;
     cudaEvent_t kev[2] = {nullptr, nullptr};
     if (try_ki) {
         for (auto& e : kev) LCC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
         Ki.alloc(KS * klen, s);  // interleaved: (label, mass) pairs -- masses at odd words, labels below
-        kchk.alloc(3, s);
-        LCC_CUDA(cudaMemsetAsync(kchk.get(), 0, sizeof(unsigned long long) * 3, s));
+        kchk.alloc(4, s);
+        LCC_CUDA(cudaMemsetAsync(kchk.get(), 0, sizeof(unsigned long long) * 4, s));
         LCC_CUDA(cudaEventRecord(kev[0], s));
         k_mass_to_u32<<<grid_for(klen, 256), 256, 0, s>>>(K, klen, k, n, Ki.get() + (KS - 1), kchk.get(),
                                                            reinterpret_cast<unsigned*>(kchk.get() + 1),
                                                            reinterpret_cast<unsigned*>(kchk.get() + 2));
         LCC_LAUNCH_CHECK();
+        if (LCC_CODES && ASYNC && LCC_ILV && codes_on && chunks < 0) {
+            codes.alloc((n + 7) / 8, s);
+            k_codes<<<grid_for((n + 7) / 8, 256), 256, 0, s>>>(C, Ki.get() + (KS - 1), n, codes.get(), kchk.get() + 3);
+            LCC_LAUNCH_CHECK();
+        }
         LCC_CUDA(cudaEventRecord(kev[1], s));
         LCC_CUDA(cudaMemcpyAsync(hk, kchk.get(), sizeof(hk), cudaMemcpyDeviceToHost, s));
     }
@@ -3095,6 +3192,19 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
     } else {
         for (int b = 0; b <= NBINS; ++b) hc[b] = 0;
         binstart.assign(NBINS + 1, 0);
+    }
+    // Edge-heavy small frontiers (a few 10K coarse hubs with 10^8 entries):
+    // the vertex-count rule above gives them 64 ordered sub-rounds of a few
+    // hundred CTAs each, which the launch tails dominate.  LCC_SUB_EDGES (A/B
+    // knob, 0 = off): no sub-round smaller than that many entries, but never
+    // fewer than 8 sub-rounds, and only for frontiers of >= 2^26 entries.
+    {
+        static const int64_t sub_edges = getenv("LCC_SUB_EDGES") ? atoll(getenv("LCC_SUB_EDGES")) : (1LL << 26);
+        const int64_t fe = (int64_t)hc[NBINS];
+        if (ASYNC && chunks <= 0 && sub_edges > 0 && fe >= (1LL << 26) && P > 8) {
+            const int cap = (int)std::max<int64_t>(8, (fe + sub_edges - 1) / sub_edges);
+            P = std::min(P, std::max(cap, chunks < 0 ? -chunks : 1));
+        }
     }
     const bool ki = try_ki && hk[1] == 0 && hk[0] < (1ull << 31);
     if (try_ki) LCC_CUDA(cudaEventElapsedTime(&kconv_ms, kev[0], kev[1]));
@@ -3143,6 +3253,12 @@ int64_t run_round(const lcc_graph& g, const double* k, double lam, int32_t* C, d
             a.lm = (int32_t)((1u << lb) - 1u);
             a.kmax = (double)(cap - 1u);
         }
+        // codes: packed or interleaved words alike (async integer-mass rounds)
+        // (not in a level's very first round from singletons at the finest
+        // level -- chunks == 0 -- where most vertices move and the codes would
+        // all be cleared on the way: config 5 round 1 151 vs 119 ms)
+        if (LCC_CODES && ASYNC && ilv && !use_lk && chunks < 0 && codes.get() && (double)hk[3] * 100.0 >= (double)codes_min_pct * (double)n)
+            a.code = codes.get();
     }
     Buf<unsigned> mbits;
     if (LCC_MARKBITS == 1 && a.mark) {

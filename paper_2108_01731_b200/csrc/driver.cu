@@ -97,14 +97,17 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         if (frontier && nF == 0) break;
         RoundStats rs;
         int64_t cnt;
-        uint8_t* mk = (fused && it + 1 < o.num_iter) ? mark.get() : nullptr;
+        // (LCC_LASTMARK=1, A/B: the last iteration keeps the fused marks and the damping too)
+        static const int lastmark_mode = getenv("LCC_LASTMARK") ? atoi(getenv("LCC_LASTMARK")) : 1;  // 2: marks, no damping
+        const bool lastmark = lastmark_mode > 0;
+        uint8_t* mk = (fused && (it + 1 < o.num_iter || (lastmark && mark.get()))) ? mark.get() : nullptr;
         EventTimer tm(s);
         if (!as) {
             cnt = best_moves_round(g, k, lam, cur, K, frontier, nF, LCC_SYNC, o.deg_threshold, 1, D.get(),
                                    mv_cur, mk, &rs, s);
         } else {
             AsyncDamp damp;
-            damp.prev_moved = damping ? mv_prev : nullptr;
+            damp.prev_moved = damping && !(lastmark_mode == 2 && it + 1 == o.num_iter) ? mv_prev : nullptr;
             // seeded, recorded RNG: the damping coin of iteration
             // `it` is a hash of (seed, it); the default seed 0 keeps round 1's salts
             damp.salt = 0x85EBCA6Bu * (uint32_t)(it + 1) ^ (uint32_t)(o.seed * 0x9E3779B97F4A7C15ull >> 32);

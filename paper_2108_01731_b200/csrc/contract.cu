@@ -332,26 +332,96 @@ struct MaxOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
 };
 struct SegSmem {
-    using Sort = cub::BlockRadixSort<uint64_t, SEG_T, SEG_I, uint32_t, LCC_SEG_RADIX_BITS>;
+    using Sort64 = cub::BlockRadixSort<uint64_t, SEG_T, SEG_I, uint32_t, LCC_SEG_RADIX_BITS>;
+    using Sort32 = cub::BlockRadixSort<uint32_t, SEG_T, SEG_I, uint32_t, LCC_SEG_RADIX_BITS>;
     using ScanI = cub::BlockScan<int, SEG_T>;
     using ScanU = cub::BlockScan<uint32_t, SEG_T>;
     union {
-        typename Sort::TempStorage sort;
+        typename Sort64::TempStorage sort64;
+        typename Sort32::TempStorage sort32;
         typename ScanI::TempStorage scani;
         typename ScanU::TempStorage scanu;
         uint64_t key[SEG_CAP];
     } u;
     int32_t rid[SEG_CAP];     // row id at its start offset, -1 elsewhere
-    int32_t hex[SEG_CAP];     // exclusive head count per position
     uint32_t runbase[SEG_CAP];
-    int32_t cnt[SEG_CAP];     // unique count per row (at its start offset)
+    // per row of the window (at most SEG_WIN non-empty rows start in it)
+    int32_t roff[SEG_WIN];    // start offset
+    int32_t hexrow[SEG_WIN];  // exclusive head (run) count at its start
+    int32_t cnt[SEG_WIN];     // unique entries
 };
+// One window: keys are (row number inside the window, coarse id).  A window
+// of ~2048 entries holds a few dozen rows, so the pair usually fits 32 bits
+// (b + 5-6 bits: 6 passes of 5-bit digits on 32-bit keys instead of 8 on
+// 64-bit ones; config-5 level 0: 176 -> see DESIGN ms); windows of many short
+// rows keep 64-bit keys.
+template <class KeyT>
+__device__ __forceinline__ void seg_window_body(SegSmem& sm, int64_t base, int T, int bbits, int rbits, const int (&ridx)[SEG_I],
+                                                uint32_t* keys, uint32_t* vals) {
+    const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
+    KeyT key[SEG_I];
+    uint32_t val[SEG_I];
+#pragma unroll
+    for (int j = 0; j < SEG_I; ++j) {
+        const int i = threadIdx.x * SEG_I + j;
+        if (i < T) {
+            const uint32_t b = keys[base + i];
+            key[j] = ((KeyT)ridx[j] << bbits) | (KeyT)(b == SEG_SENT ? bmask : b);
+            val[j] = vals[base + i];
+        } else {
+            key[j] = (KeyT)~(KeyT)0;
+            val[j] = 0u;
+        }
+    }
+    // (padding keys are all ones: beyond every live key on the sorted bits or tied with the
+    // last row's sentinel; either way they end up at positions >= T or among the dead entries)
+    if constexpr (sizeof(KeyT) == 8) SegSmem::Sort64(sm.u.sort64).Sort(key, val, 0, rbits + bbits);
+    else SegSmem::Sort32(sm.u.sort32).Sort(key, val, 0, rbits + bbits);
+    __syncthreads();
+    KeyT* skey = reinterpret_cast<KeyT*>(sm.u.key);
+#pragma unroll
+    for (int j = 0; j < SEG_I; ++j) skey[threadIdx.x * SEG_I + j] = key[j];
+    __syncthreads();
+    int head[SEG_I], hx[SEG_I];
+    bool endf[SEG_I];
+#pragma unroll
+    for (int j = 0; j < SEG_I; ++j) {
+        const int i = threadIdx.x * SEG_I + j;
+        const bool live = i < T && key[j] != (KeyT)~(KeyT)0 && (uint32_t)(key[j] & (KeyT)bmask) != bmask;
+        head[j] = live && (i == 0 || skey[i - 1] != key[j]);
+        endf[j] = live && (i == T - 1 || skey[i + 1] != key[j]);
+    }
+    __syncthreads();  // the key array is reused by the scans below
+    SegSmem::ScanI(sm.u.scani).ExclusiveSum(head, hx);
+    __syncthreads();
+    uint32_t pw[SEG_I];
+    SegSmem::ScanU(sm.u.scanu).InclusiveSum(val, pw);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SEG_I; ++j) {
+        const int i = threadIdx.x * SEG_I + j;
+        if (i < T && sm.rid[i] >= 0) sm.hexrow[ridx[j]] = hx[j];  // sorted rows keep their extents
+        if (head[j]) {
+            sm.runbase[hx[j]] = pw[j] - val[j];
+            atomicAdd(&sm.cnt[(int)(key[j] >> bbits)], 1);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SEG_I; ++j) {
+        if (!endf[j]) continue;
+        const int r = hx[j] + head[j] - 1;  // this run's number
+        const int rown = (int)(key[j] >> bbits);
+        const int64_t out = base + sm.roff[rown] + (r - sm.hexrow[rown]);
+        keys[out] = (uint32_t)(key[j] & (KeyT)bmask);
+        vals[out] = pw[j] - sm.runbase[r];
+    }
+}
 __global__ void __launch_bounds__(SEG_T)
 k_seg_window(const int64_t* __restrict__ rstart, const int64_t* __restrict__ wrow, int64_t nwin, int bbits,
              uint32_t* keys, uint32_t* vals, int32_t* ucnt) {
     extern __shared__ __align__(16) unsigned char smraw[];
     SegSmem& sm = *reinterpret_cast<SegSmem*>(smraw);
-    const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
     for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
         const int64_t r0 = wrow[w], r1 = wrow[w + 1];
         if (r0 >= r1) continue;
@@ -360,80 +430,157 @@ k_seg_window(const int64_t* __restrict__ rstart, const int64_t* __restrict__ wro
         const int64_t base = rstart[r0];
         const int T = (int)(rstart[rend] - base);
         if (T <= 0) continue;
-        for (int i = threadIdx.x; i < SEG_CAP; i += SEG_T) { sm.rid[i] = -1; sm.cnt[i] = 0; }
+        for (int i = threadIdx.x; i < SEG_CAP; i += SEG_T) sm.rid[i] = -1;
+        for (int i = threadIdx.x; i < (int)SEG_WIN; i += SEG_T) sm.cnt[i] = 0;
         __syncthreads();
         for (int64_t a = r0 + threadIdx.x; a < rend; a += SEG_T)
             if (rstart[a + 1] > rstart[a]) sm.rid[rstart[a] - base] = (int32_t)a;
         __syncthreads();
-        int ro[SEG_I];
+        // row number of every position: inclusive count of the row starts - 1
+        int ridx[SEG_I];
 #pragma unroll
         for (int j = 0; j < SEG_I; ++j) {
             const int i = threadIdx.x * SEG_I + j;
-            ro[j] = (i < T && sm.rid[i] >= 0) ? i : -1;
+            ridx[j] = (i < T && sm.rid[i] >= 0) ? 1 : 0;
         }
-        SegSmem::ScanI(sm.u.scani).InclusiveScan(ro, ro, MaxOp{});
-        __syncthreads();
-        uint64_t key[SEG_I];
-        uint32_t val[SEG_I];
-#pragma unroll
-        for (int j = 0; j < SEG_I; ++j) {
-            const int i = threadIdx.x * SEG_I + j;
-            if (i < T) {
-                const uint32_t b = keys[base + i];
-                key[j] = ((uint64_t)ro[j] << bbits) | (b == SEG_SENT ? bmask : b);
-                val[j] = vals[base + i];
-            } else {
-                key[j] = ~0ull;
-                val[j] = 0u;
-            }
-        }
-        SegSmem::Sort(sm.u.sort).Sort(key, val, 0, 12 + bbits);
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < SEG_I; ++j) sm.u.key[threadIdx.x * SEG_I + j] = key[j];
-        __syncthreads();
-        int head[SEG_I], hx[SEG_I];
-        bool endf[SEG_I];
-#pragma unroll
-        for (int j = 0; j < SEG_I; ++j) {
-            const int i = threadIdx.x * SEG_I + j;
-            const bool live = i < T && (uint32_t)(key[j] & bmask) != bmask;
-            head[j] = live && (i == 0 || sm.u.key[i - 1] != key[j]);
-            endf[j] = live && (i == T - 1 || sm.u.key[i + 1] != key[j]);
-        }
-        __syncthreads();  // the key array is reused by the scans below
-        SegSmem::ScanI(sm.u.scani).ExclusiveSum(head, hx);
-        __syncthreads();
-        uint32_t pw[SEG_I];
-        SegSmem::ScanU(sm.u.scanu).InclusiveSum(val, pw);
+        int nrows = 0;
+        SegSmem::ScanI(sm.u.scani).InclusiveSum(ridx, ridx, nrows);
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < SEG_I; ++j) {
             const int i = threadIdx.x * SEG_I + j;
-            sm.hex[i] = hx[j];
-            if (head[j]) {
-                sm.runbase[hx[j]] = pw[j] - val[j];
-                atomicAdd(&sm.cnt[(int)(key[j] >> bbits)], 1);
-            }
+            ridx[j] -= 1;
+            if (i < T && sm.rid[i] >= 0) sm.roff[ridx[j]] = i;
         }
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < SEG_I; ++j) {
-            if (!endf[j]) continue;
-            const int r = hx[j] + head[j] - 1;  // this run's number
-            const int rowoff = (int)(key[j] >> bbits);
-            const int64_t out = base + rowoff + (r - sm.hex[rowoff]);
-            keys[out] = (uint32_t)(key[j] & bmask);
-            vals[out] = pw[j] - sm.runbase[r];
-        }
-        for (int i = threadIdx.x; i < T; i += SEG_T)
-            if (sm.rid[i] >= 0) ucnt[sm.rid[i]] = sm.cnt[i];
+        const int rbits = 32 - __clz(max(nrows - 1, 1));
+        if (rbits + bbits <= 32) seg_window_body<uint32_t>(sm, base, T, bbits, rbits, ridx, keys, vals);
+        else seg_window_body<uint64_t>(sm, base, T, bbits, rbits, ridx, keys, vals);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nrows; k += SEG_T) ucnt[sm.rid[sm.roff[k]]] = sm.cnt[k];
         __syncthreads();
     }
 }
+// Rows of (SEG_MAX, THREADS * ITEMS] entries: one CTA sorts one row on the b
+// bits of the coarse ids alone (5 passes of 5-bit digits at config 5 instead
+// of the windows' 8 over (row offset, id), and no 64-bit device sort of
+// (row, id) keys: config-5 level 0, rows of 2049-8192 entries hold ~9% of the
+// entries and took 81 ms there).  Same run logic as k_seg_window with a
+// single row: sentinels (and the padding) sort last, duplicate ids are summed
+// from an inclusive scan of the sorted weights, the row's unique entries are
+// written back in place from its start.
+constexpr int64_t SEG_ROW_MAX = 8192;
+template <int THREADS, int ITEMS>
+struct RowSmem {
+    static constexpr int CAP = THREADS * ITEMS;
+    using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint32_t, LCC_SEG_RADIX_BITS>;
+    using ScanI = cub::BlockScan<int, THREADS>;
+    using ScanU = cub::BlockScan<uint32_t, THREADS>;
+    union {
+        typename Sort::TempStorage sort;
+        typename ScanI::TempStorage scani;
+        typename ScanU::TempStorage scanu;
+        uint32_t key[CAP];
+    } u;
+    uint32_t runbase[CAP];
+};
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+k_seg_row(const int64_t* __restrict__ rstart, const int32_t* __restrict__ rows, int64_t nrows, int bbits,
+          uint32_t* keys, uint32_t* vals, int32_t* ucnt) {
+    using SM = RowSmem<THREADS, ITEMS>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SM& sm = *reinterpret_cast<SM*>(smraw);
+    const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
+    for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const int32_t a = rows[r];
+        const int64_t base = rstart[a];
+        const int T = (int)(rstart[a + 1] - base);
+        uint32_t key[ITEMS], val[ITEMS];
+        // striped loads (coalesced), then into the blocked arrangement the sort wants
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const int i = j * THREADS + threadIdx.x;
+            uint32_t b = bmask, w = 0u;
+            if (i < T) {
+                b = keys[base + i];
+                if (b == SEG_SENT) b = bmask;
+                w = vals[base + i];
+            }
+            key[j] = b;
+            val[j] = w;
+        }
+        typename SM::Sort(sm.u.sort).Sort(key, val, 0, bbits);  // any arrangement in: a full sort follows
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) sm.u.key[threadIdx.x * ITEMS + j] = key[j];
+        __syncthreads();
+        int head[ITEMS], hx[ITEMS];
+        bool endf[ITEMS];
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const int i = threadIdx.x * ITEMS + j;
+            const bool live = key[j] != bmask;  // sentinels and padding sort last
+            head[j] = live && (i == 0 || sm.u.key[i - 1] != key[j]);
+            endf[j] = live && (i == SM::CAP - 1 || sm.u.key[i + 1] != key[j]);
+        }
+        __syncthreads();  // the key array is reused by the scans below
+        int nruns = 0;
+        typename SM::ScanI(sm.u.scani).ExclusiveSum(head, hx, nruns);
+        __syncthreads();
+        uint32_t pw[ITEMS];
+        typename SM::ScanU(sm.u.scanu).InclusiveSum(val, pw);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+            if (head[j]) sm.runbase[hx[j]] = pw[j] - val[j];
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (!endf[j]) continue;
+            const int run = hx[j] + head[j] - 1;
+            keys[base + run] = key[j];
+            vals[base + run] = pw[j] - sm.runbase[run];
+        }
+        if (threadIdx.x == 0) ucnt[a] = nruns;
+        __syncthreads();
+    }
+}
+struct RowLenIn {
+    const int64_t* rstart;
+    int64_t lo, hi;  // (lo, hi]
+    __device__ __forceinline__ bool operator()(int32_t a) const {
+        const int64_t L = rstart[a + 1] - rstart[a];
+        return L > lo && L <= hi;
+    }
+};
+template <int THREADS, int ITEMS>
+void seg_rows(const int64_t* rstart, int64_t cn, int64_t lo, int bbits, uint32_t* keys, uint32_t* vals, int32_t* ucnt,
+              cudaStream_t s) {
+    using SM = RowSmem<THREADS, ITEMS>;
+    Buf<int32_t> rows(std::max<int64_t>(cn, 1), s);
+    Buf<int64_t> dn(1, s);
+    select_if(cub::CountingInputIterator<int32_t>(0), rows.get(), dn.get(), cn, RowLenIn{rstart, lo, (int64_t)SM::CAP}, s);
+    int64_t nr = 0;
+    LCC_CUDA(cudaMemcpyAsync(&nr, dn.get(), sizeof(nr), cudaMemcpyDeviceToHost, s));
+    LCC_CUDA(cudaStreamSynchronize(s));
+    if (nr == 0) return;
+    if (getenv("LCC_TRACE")) fprintf(stderr, "[lcc]     compress seg rows of (%lld, %d] entries: %lld\n", (long long)lo, SM::CAP, (long long)nr);
+    const int SMEM = (int)sizeof(SM);
+    static int occ = 0;
+    if (!occ) {
+        LCC_CUDA(cudaFuncSetAttribute(k_seg_row<THREADS, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        LCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_seg_row<THREADS, ITEMS>, THREADS, SMEM));
+        occ = std::max(occ, 1);
+    }
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nr, (int64_t)num_sms() * occ));
+    k_seg_row<THREADS, ITEMS><<<grid, THREADS, SMEM, s>>>(rstart, rows.get(), nr, bbits, keys, vals, ucnt);
+    LCC_LAUNCH_CHECK();
+}
 struct RowLenBig {
     const int64_t* rstart;
-    __device__ __forceinline__ bool operator()(int32_t a) const { return rstart[a + 1] - rstart[a] > SEG_MAX; }
+    int64_t lim;
+    __device__ __forceinline__ bool operator()(int32_t a) const { return rstart[a + 1] - rstart[a] > lim; }
 };
 struct BigLen {
     const int64_t* rstart;
@@ -445,16 +592,23 @@ struct BigLen {
         return rstart[a + 1] - rstart[a];
     }
 };
+// keys of the long rows: (rank of the row among the long rows, coarse id) --
+// a few 10K rows, so ~40 live bits (5 radix passes) instead of 2b (7)
+__global__ void k_big_rank(const int32_t* __restrict__ big, int64_t nb, int32_t* __restrict__ brank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += (int64_t)gridDim.x * blockDim.x)
+        brank[big[i]] = (int32_t)i;
+}
 struct BigKeys {
     const uint32_t* keys;
     const uint32_t* vals;
+    const int32_t* brank;
     int bbits;
     uint64_t* k64;
     uint32_t* v32;
     __device__ __forceinline__ void operator()(int64_t a, int64_t e, int64_t pos) {
         const uint32_t b = keys[e];
         const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
-        k64[pos] = ((uint64_t)a << bbits) | (b == SEG_SENT ? bmask : b);
+        k64[pos] = ((uint64_t)__ldg(brank + a) << bbits) | (b == SEG_SENT ? bmask : b);
         v32[pos] = vals[e];
     }
     __device__ __forceinline__ void flush() {}
@@ -469,14 +623,16 @@ __global__ void k_big_first(const uint64_t* __restrict__ uk, const int64_t* __re
 }
 __global__ void k_big_emit(const uint64_t* __restrict__ uk, const uint32_t* __restrict__ us,
                            const int64_t* __restrict__ nruns, int bbits, const int64_t* __restrict__ first,
-                           const int64_t* __restrict__ rstart, uint32_t* keys, uint32_t* vals, int32_t* ucnt) {
+                           const int32_t* __restrict__ big, const int64_t* __restrict__ rstart, uint32_t* keys,
+                           uint32_t* vals, int32_t* ucnt) {
     const int64_t R = *nruns;
     const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t a = (int64_t)(uk[i] >> bbits);
+        const int64_t rk = (int64_t)(uk[i] >> bbits);
+        const int64_t a = big[rk];
         const uint32_t b = (uint32_t)(uk[i] & bmask);
         if (b == bmask) continue;  // intra sentinel (sorts last in its row)
-        const int64_t out = rstart[a] + (i - first[a]);
+        const int64_t out = rstart[a] + (i - first[rk]);
         keys[out] = b;
         vals[out] = us[i];
         atomicAdd(ucnt + a, 1);
@@ -554,11 +710,19 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
         LCC_LAUNCH_CHECK();
     }
     tr.mark("seg windows");
-    // 3b. longer rows: one device sort of their (row, id) keys
+    // 3b. rows of up to 8192 entries: one CTA per row (LCC_SEG_ROWS=0: the device sort takes them too)
+    static const bool seg_rows_on = !(getenv("LCC_SEG_ROWS") && getenv("LCC_SEG_ROWS")[0] == '0');
+    if (seg_rows_on) {
+        seg_rows<256, 16>(rstart.get(), cn, SEG_MAX, bbits, keys.get(), vals.get(), ucnt.get(), s);
+        seg_rows<512, 16>(rstart.get(), cn, 4096, bbits, keys.get(), vals.get(), ucnt.get(), s);
+    }
+    tr.mark("seg mid rows");
+    // 3c. longer rows: one device sort of their (row, id) keys
     {
         Buf<int32_t> big(std::max<int64_t>(cn, 1), s);
         Buf<int64_t> dnb(1, s);
-        select_if(cub::CountingInputIterator<int32_t>(0), big.get(), dnb.get(), cn, RowLenBig{rstart.get()}, s);
+        select_if(cub::CountingInputIterator<int32_t>(0), big.get(), dnb.get(), cn,
+                  RowLenBig{rstart.get(), seg_rows_on ? SEG_ROW_MAX : SEG_MAX}, s);
         int64_t nb = 0;
         LCC_CUDA(cudaMemcpyAsync(&nb, dnb.get(), sizeof(nb), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaStreamSynchronize(s));
@@ -570,13 +734,18 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
             int64_t bt = 0;
             LCC_CUDA(cudaMemcpyAsync(&bt, boff.get() + nb, sizeof(bt), cudaMemcpyDeviceToHost, s));
             LCC_CUDA(cudaStreamSynchronize(s));
+            if (getenv("LCC_TRACE")) fprintf(stderr, "[lcc]     compress seg big rows: %lld rows, %lld entries\n", (long long)nb, (long long)bt);
             Buf<uint64_t> ka(bt, s), kb(bt, s);
             Buf<uint32_t> va(bt, s), vb(bt, s);
+            Buf<int32_t> brank(cn, s);
+            k_big_rank<<<grid_for(nb, 256), 256, 0, s>>>(big.get(), nb, brank.get());
+            LCC_LAUNCH_CHECK();
             edge_balanced(rstart.get(), big.get(), boff.get(), nb, bt,
-                          BigKeys{keys.get(), vals.get(), bbits, ka.get(), va.get()}, s);
+                          BigKeys{keys.get(), vals.get(), brank.get(), bbits, ka.get(), va.get()}, s);
+            brank.release();
             cub::DoubleBuffer<uint64_t> dk(ka.get(), kb.get());
             cub::DoubleBuffer<uint32_t> dv(va.get(), vb.get());
-            sort_pairs_db(dk, dv, bt, 2 * bbits, s);
+            sort_pairs_db(dk, dv, bt, bbits + std::max(1, bit_width((uint64_t)std::max<int64_t>(nb - 1, 1))), s);
             Buf<uint64_t> uk(bt, s);
             Buf<uint32_t> us(bt, s);
             Buf<int64_t> druns(1, s);
@@ -588,10 +757,10 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
                 LCC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, dk.Current(), uk.get(), dv.Current(),
                                                         us.get(), druns.get(), cub::Sum(), bt, s));
             }
-            Buf<int64_t> first(cn, s);
+            Buf<int64_t> first(nb, s);
             k_big_first<<<grid_for(bt, 256), 256, 0, s>>>(uk.get(), druns.get(), bbits, first.get());
             LCC_LAUNCH_CHECK();
-            k_big_emit<<<grid_for(bt, 256), 256, 0, s>>>(uk.get(), us.get(), druns.get(), bbits, first.get(),
+            k_big_emit<<<grid_for(bt, 256), 256, 0, s>>>(uk.get(), us.get(), druns.get(), bbits, first.get(), big.get(),
                                                         rstart.get(), keys.get(), vals.get(), ucnt.get());
             LCC_LAUNCH_CHECK();
         }

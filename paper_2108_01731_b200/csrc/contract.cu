@@ -299,9 +299,23 @@ struct SegFill {
     uint32_t* keys;
     uint32_t* vals;
     unsigned long long* intra;
+    // optional (LCC_SEG_FILLBITS=1, measured slower): a root's coarse id is
+    // its rank among the roots, read from the root bitmap and its sampled
+    // prefix (2 x n/8 bytes, L2 resident) instead of the n-word mapping
+    const uint32_t* rbits;
+    const uint32_t* rpref;
     unsigned long long cnt = 0;
     __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) {
-        const int32_t a = __ldg(mapping + v), b = ld_gather_i32(mapping + __ldg(indices + e));
+        const int32_t a = __ldg(mapping + v);
+        const int32_t u = __ldg(indices + e);
+        int32_t b;
+        if (rbits) {
+            const uint32_t wd = __ldg(rbits + ((uint32_t)u >> 5));
+            if ((wd >> (u & 31)) & 1u) b = (int32_t)(__ldg(rpref + ((uint32_t)u >> 5)) + __popc(wd & ((1u << (u & 31)) - 1u)));
+            else b = ld_gather_i32(mapping + u);
+        } else {
+            b = ld_gather_i32(mapping + u);
+        }
         const uint32_t wv = WLoad<WT>::tw(w, e);
         if (a == b) {
             keys[pos] = SEG_SENT;
@@ -654,7 +668,7 @@ struct SegCopy {
 // out.indptr/indices/wi, returns the entry count; *intra = intra weight
 template <class WT>
 int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coarse& out, unsigned long long* intra,
-                     cudaStream_t s) {
+                     const uint32_t* rbits, const uint32_t* rpref, cudaStream_t s) {
     const int64_t n = g.n, nnz = g.nnz;
     const int bbits = std::max(1, bit_width((uint64_t)cn));
     LCC_REQUIRE(bbits <= 31, "coarse graph too large for the segmented contraction");
@@ -685,7 +699,7 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
     // 2. every entry's coarse neighbour at its row position
     Buf<uint32_t> keys(nnz, s), vals(nnz, s);
     edge_balanced(g.indptr, perm.get(), pos0.get(), n, nnz,
-                  SegFill<WT>{g.indices, g.weights, mapping, keys.get(), vals.get(), intra}, s);
+                  SegFill<WT>{g.indices, g.weights, mapping, keys.get(), vals.get(), intra, rbits, rpref}, s);
     perm.release();
     pos0.release();
     tr.mark("seg fill");
@@ -983,7 +997,10 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     const bool use_seg = esg ? esg[0] == '1' : nnz >= (1LL << 30);
     if (!fast_done && nnz > 0 && int_out && use_seg) {
         unsigned long long* di = dintra.get();
-        R = compress_seg<WT>(g, mapping, cn, out, di, s);
+        // (LCC_SEG_FILLBITS=1: roots' coarse ids from the root bitmap in the fill pass; measured slower,
+        // config 5 level 0: fill 96 -> 108 ms -- the test adds a dependent L2 lookup in front of every gather)
+        static const bool fill_bits = getenv("LCC_SEG_FILLBITS") && getenv("LCC_SEG_FILLBITS")[0] == '1';
+        R = compress_seg<WT>(g, mapping, cn, out, di, fill_bits ? rbits.get() : nullptr, rpref.get(), s);
         unsigned long long hintra = 0;
         LCC_CUDA(cudaMemcpyAsync(&hintra, di, sizeof(hintra), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaStreamSynchronize(s));

@@ -261,8 +261,18 @@ __global__ void k_emit_complex(const uint64_t* __restrict__ ukeys, const ST* __r
 //     coarse CSR.  Integer sums are exact in any order: the output equals the
 //     global-sort path entry for entry.
 constexpr int SEG_T = 256, SEG_I = 16, SEG_CAP = SEG_T * SEG_I;  // entries per window CTA
-constexpr int64_t SEG_WIN = 2048;                                 // window = rows starting in [w*WIN, (w+1)*WIN)
-constexpr int64_t SEG_MAX = 2048;                                 // longer rows take the device sort
+#ifndef LCC_SEG_WIN
+#define LCC_SEG_WIN 3072
+#endif
+#ifndef LCC_SEG_MAXROW
+#define LCC_SEG_MAXROW 1024
+#endif
+// window = rows starting in [w*WIN, (w+1)*WIN); rows over SEG_MAX entries are sorted on their own (k_seg_row, device
+// sort).  A window holds up to WIN + MAX <= SEG_CAP entries and the CTA sorts SEG_CAP keys whatever it holds: 3072 +
+// 1024 fills ~80% of them, 2048 + 2048 filled ~55% (config 5 level 0: windows 121 -> see DESIGN ms)
+constexpr int64_t SEG_WIN = LCC_SEG_WIN;
+constexpr int64_t SEG_MAX = LCC_SEG_MAXROW;
+static_assert(SEG_WIN + SEG_MAX <= SEG_CAP, "a window must fit one CTA sort");
 constexpr uint32_t SEG_SENT = 0xffffffffu;
 #ifndef LCC_SEG_RADIX_BITS
 #define LCC_SEG_RADIX_BITS 5  // window sorts: 8 passes over 12 + b bits instead of 10 (config 5 level 0: 196 -> 176 ms)
@@ -370,8 +380,8 @@ struct SegSmem {
 // 64-bit ones; config-5 level 0: 176 -> see DESIGN ms); windows of many short
 // rows keep 64-bit keys.
 template <class KeyT>
-__device__ __forceinline__ void seg_window_body(SegSmem& sm, int64_t base, int T, int bbits, int rbits, const int (&ridx)[SEG_I],
-                                                uint32_t* keys, uint32_t* vals) {
+__device__ __forceinline__ void seg_window_body(SegSmem& sm, int64_t base, int T, int nrows, int bbits, int rbits,
+                                                const int (&ridx)[SEG_I], uint32_t* keys, uint32_t* vals) {
     const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
     KeyT key[SEG_I];
     uint32_t val[SEG_I];
@@ -379,8 +389,12 @@ __device__ __forceinline__ void seg_window_body(SegSmem& sm, int64_t base, int T
     for (int j = 0; j < SEG_I; ++j) {
         const int i = threadIdx.x * SEG_I + j;
         if (i < T) {
+            // a row over SEG_MAX entries that starts inside the window is left to the row
+            // kernels: its entries count as dead here (nothing of it is written)
+            const int rn = ridx[j];
+            const bool longrow = (rn + 1 < nrows ? sm.roff[rn + 1] : T) - sm.roff[rn] > (int)SEG_MAX;
             const uint32_t b = keys[base + i];
-            key[j] = ((KeyT)ridx[j] << bbits) | (KeyT)(b == SEG_SENT ? bmask : b);
+            key[j] = ((KeyT)rn << bbits) | (KeyT)((b == SEG_SENT || longrow) ? bmask : b);
             val[j] = vals[base + i];
         } else {
             key[j] = (KeyT)~(KeyT)0;
@@ -468,10 +482,11 @@ k_seg_window(const int64_t* __restrict__ rstart, const int64_t* __restrict__ wro
         }
         __syncthreads();
         const int rbits = 32 - __clz(max(nrows - 1, 1));
-        if (rbits + bbits <= 32) seg_window_body<uint32_t>(sm, base, T, bbits, rbits, ridx, keys, vals);
-        else seg_window_body<uint64_t>(sm, base, T, bbits, rbits, ridx, keys, vals);
+        if (rbits + bbits <= 32) seg_window_body<uint32_t>(sm, base, T, nrows, bbits, rbits, ridx, keys, vals);
+        else seg_window_body<uint64_t>(sm, base, T, nrows, bbits, rbits, ridx, keys, vals);
         __syncthreads();
-        for (int k = threadIdx.x; k < nrows; k += SEG_T) ucnt[sm.rid[sm.roff[k]]] = sm.cnt[k];
+        for (int k = threadIdx.x; k < nrows; k += SEG_T)
+            if ((k + 1 < nrows ? sm.roff[k + 1] : T) - sm.roff[k] <= (int)SEG_MAX) ucnt[sm.rid[sm.roff[k]]] = sm.cnt[k];
         __syncthreads();
     }
 }
@@ -727,7 +742,8 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
     // 3b. rows of up to 8192 entries: one CTA per row (LCC_SEG_ROWS=0: the device sort takes them too)
     static const bool seg_rows_on = !(getenv("LCC_SEG_ROWS") && getenv("LCC_SEG_ROWS")[0] == '0');
     if (seg_rows_on) {
-        seg_rows<256, 16>(rstart.get(), cn, SEG_MAX, bbits, keys.get(), vals.get(), ucnt.get(), s);
+        if (SEG_MAX < 2048) seg_rows<128, 16>(rstart.get(), cn, SEG_MAX, bbits, keys.get(), vals.get(), ucnt.get(), s);
+        seg_rows<256, 16>(rstart.get(), cn, std::max<int64_t>(SEG_MAX, 2048), bbits, keys.get(), vals.get(), ucnt.get(), s);
         seg_rows<512, 16>(rstart.get(), cn, 4096, bbits, keys.get(), vals.get(), ucnt.get(), s);
     }
     tr.mark("seg mid rows");

@@ -620,10 +620,13 @@ def test_hub_buckets_multipass_exact(nclus):
 def test_compress_segmented_identical(wkind, monkeypatch):
     """The segmented contraction (per-row window sorts and the device sort
     for rows over 2048 entries; the default on graphs of 2^30+ entries)
-    equals the global-sort path and the oracle bit for bit -- hubs of 6K and
-    12K neighbours take the long-row path, every other row the windows."""
+    equals the global-sort path and the oracle bit for bit -- hubs of 1.1K to
+    7K neighbours take the three one-CTA-per-row sorts (some of them start in
+    the middle of a window), the 12K hub the device sort, every other row the
+    windows."""
     rng = np.random.default_rng(72)
-    hg = hub_graph(rng, 30_000, [5, 77, 901], [6000, 12000, 2500], base_p=0.0004)
+    hg = hub_graph(rng, 30_000, [5, 77, 901, 1234, 1235, 20_000, 20_001], [6000, 12000, 2500, 1500, 1100, 3000, 7000],
+                   base_p=0.0004)
     if wkind == "u32":
         src = np.repeat(np.arange(hg.n), np.diff(hg.indptr))
         lo_, hi_ = np.minimum(src, hg.indices), np.maximum(src, hg.indices)

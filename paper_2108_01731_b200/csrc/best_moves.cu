@@ -385,16 +385,47 @@ __device__ __forceinline__ int decide(const BMArgs& a, int32_t v, int32_t c, dou
     return 0;
 }
 
+// Warp argmax under better(): largest gain, ties to the lowest cluster id.
+// Three warp reductions (REDUX) on an order-preserving integer image of the
+// gain -- its high word, its low word among the lanes that hold the largest
+// high word, then the smallest id among the lanes that hold the largest gain --
+// instead of five shuffle-and-compare rounds on (gain, id[, S]): ~20
+// instructions instead of ~65 per vertex (LCC_REDUX_ARGMAX=0: the shuffles).
+#ifndef LCC_REDUX_ARGMAX
+#define LCC_REDUX_ARGMAX 1
+#endif
+__device__ __forceinline__ int warp_argmax_lane(double g, int32_t& x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(dadd(g, 0.0));  // -0 -> +0: equal gains, equal keys
+    const unsigned long long k = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+    const uint32_t mhi = __reduce_max_sync(FULL, hi);
+    const uint32_t mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
+    const bool top = hi == mhi && lo == mlo;
+    const uint32_t mx = __reduce_min_sync(FULL, top ? (uint32_t)x : 0xffffffffu);
+    const unsigned who = __ballot_sync(FULL, top && (uint32_t)x == mx);
+    x = (int32_t)mx;
+    return __ffs(who) - 1;
+}
 __device__ __forceinline__ void warp_argmax(double& g, int32_t& x) {
+#if LCC_REDUX_ARGMAX
+    const int src = warp_argmax_lane(g, x);
+    g = __shfl_sync(FULL, g, src);
+#else
 #pragma unroll
     for (int d = 16; d; d >>= 1) {
         double og = __shfl_xor_sync(FULL, g, d);
         int32_t ox = __shfl_xor_sync(FULL, x, d);
         if (better(og, ox, g, x)) { g = og; x = ox; }
     }
+#endif
 }
 // ... carrying the winner's neighbour weight S (commit-time validation)
 __device__ __forceinline__ void warp_argmax(double& g, int32_t& x, double& S) {
+#if LCC_REDUX_ARGMAX
+    const int src = warp_argmax_lane(g, x);
+    g = __shfl_sync(FULL, g, src);
+    S = __shfl_sync(FULL, S, src);
+#else
 #pragma unroll
     for (int d = 16; d; d >>= 1) {
         double og = __shfl_xor_sync(FULL, g, d);
@@ -402,6 +433,7 @@ __device__ __forceinline__ void warp_argmax(double& g, int32_t& x, double& S) {
         double oS = __shfl_xor_sync(FULL, S, d);
         if (better(og, ox, g, x)) { g = og; x = ox; S = oS; }
     }
+#endif
 }
 
 __device__ __forceinline__ void flush_moves(const BMArgs& a, unsigned long long mine) {
@@ -1289,8 +1321,13 @@ k_group(BMArgs a, const int32_t* __restrict__ list, int64_t lo, int64_t hi) {
             }
             }
         }
+        if constexpr (!FSUM && LCC_REDUX_ARGMAX) {
+            // integer sums (< 2^32, see best_moves_round): one REDUX instead of five shuffle-adds
+            sc = u32_to_f64(__reduce_add_sync(FULL, (uint32_t)sc));
+        } else {
 #pragma unroll
-        for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
+            for (int d = 16; d; d >>= 1) sc += __shfl_xor_sync(FULL, sc, d);
+        }
         if constexpr (GW > 1) {
             if (lane == 0) s_scp[gid * GW + wig] = sc;
         }

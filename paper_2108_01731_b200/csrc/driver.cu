@@ -97,10 +97,13 @@ bool par_best_moves(const lcc_graph& g, const double* k, double lam, const Optio
         if (frontier && nF == 0) break;
         RoundStats rs;
         int64_t cnt;
-        // (LCC_LASTMARK=1, A/B: the last iteration keeps the fused marks and the damping too)
+        // Asynchronous levels run their last iteration like the others, with the fused
+        // marks and the damping that rides on them: without them it was the slowest
+        // iteration of its level (config 5 level 0: 96-100 ms against 73).
+        // LCC_LASTMARK=0: no marks in the last iteration; 2: marks, no damping.
         static const int lastmark_mode = getenv("LCC_LASTMARK") ? atoi(getenv("LCC_LASTMARK")) : 1;  // 2: marks, no damping
         const bool lastmark = lastmark_mode > 0;
-        uint8_t* mk = (fused && (it + 1 < o.num_iter || (lastmark && mark.get()))) ? mark.get() : nullptr;
+        uint8_t* mk = (fused && (it + 1 < o.num_iter || (as && lastmark && mark.get()))) ? mark.get() : nullptr;
         EventTimer tm(s);
         if (!as) {
             cnt = best_moves_round(g, k, lam, cur, K, frontier, nF, LCC_SYNC, o.deg_threshold, 1, D.get(),

@@ -260,7 +260,16 @@ __global__ void k_emit_complex(const uint64_t* __restrict__ ukeys, const ST* __r
 //   * a scan of the per-row unique counts and one copy give the exact-size
 //     coarse CSR.  Integer sums are exact in any order: the output equals the
 //     global-sort path entry for entry.
-constexpr int SEG_T = 256, SEG_I = 16, SEG_CAP = SEG_T * SEG_I;  // entries per window CTA
+#ifndef LCC_SEG_T
+#define LCC_SEG_T 256
+#endif
+#ifndef LCC_SEG_I
+#define LCC_SEG_I 16
+#endif
+#ifndef LCC_SEG_MINB
+#define LCC_SEG_MINB 1
+#endif
+constexpr int SEG_T = LCC_SEG_T, SEG_I = LCC_SEG_I, SEG_CAP = SEG_T * SEG_I;  // entries per window CTA
 #ifndef LCC_SEG_WIN
 #define LCC_SEG_WIN 3072
 #endif
@@ -445,8 +454,8 @@ __device__ __forceinline__ void seg_window_body(SegSmem& sm, int64_t base, int T
         vals[out] = pw[j] - sm.runbase[r];
     }
 }
-__global__ void __launch_bounds__(SEG_T)
-k_seg_window(const int64_t* __restrict__ rstart, const int64_t* __restrict__ wrow, int64_t nwin, int bbits,
+__global__ void __launch_bounds__(SEG_T, LCC_SEG_MINB)
+k_seg_window(const int64_t* __restrict__ rstart, const int64_t* __restrict__ wrow, int64_t nwin, int bbits, int key64,
              uint32_t* keys, uint32_t* vals, int32_t* ucnt) {
     extern __shared__ __align__(16) unsigned char smraw[];
     SegSmem& sm = *reinterpret_cast<SegSmem*>(smraw);
@@ -482,7 +491,7 @@ k_seg_window(const int64_t* __restrict__ rstart, const int64_t* __restrict__ wro
         }
         __syncthreads();
         const int rbits = 32 - __clz(max(nrows - 1, 1));
-        if (rbits + bbits <= 32) seg_window_body<uint32_t>(sm, base, T, nrows, bbits, rbits, ridx, keys, vals);
+        if (!key64 && rbits + bbits <= 32) seg_window_body<uint32_t>(sm, base, T, nrows, bbits, rbits, ridx, keys, vals);
         else seg_window_body<uint64_t>(sm, base, T, nrows, bbits, rbits, ridx, keys, vals);
         __syncthreads();
         for (int k = threadIdx.x; k < nrows; k += SEG_T)
@@ -734,7 +743,9 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
             occ = std::max(occ, 1);
         }
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nwin, (int64_t)num_sms() * occ));
-        k_seg_window<<<grid, SEG_T, SMEM, s>>>(rstart.get(), wrow.get(), nwin, bbits, keys.get(), vals.get(),
+        // (LCC_SEG_KEY64=1, tests: every window takes the 64-bit keys of windows with very many short rows)
+        const int key64 = getenv("LCC_SEG_KEY64") && getenv("LCC_SEG_KEY64")[0] == '1';
+        k_seg_window<<<grid, SEG_T, SMEM, s>>>(rstart.get(), wrow.get(), nwin, bbits, key64, keys.get(), vals.get(),
                                               ucnt.get());
         LCC_LAUNCH_CHECK();
     }

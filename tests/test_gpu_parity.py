@@ -616,14 +616,17 @@ def test_hub_buckets_multipass_exact(nclus):
     assert np.array_equal(D0, D1) and c0 == c1
 
 
+@pytest.mark.parametrize("key64", ["0", "1"])
 @pytest.mark.parametrize("wkind", ["none", "u32"])
-def test_compress_segmented_identical(wkind, monkeypatch):
+def test_compress_segmented_identical(wkind, key64, monkeypatch):
     """The segmented contraction (per-row window sorts and the device sort
     for rows over 2048 entries; the default on graphs of 2^30+ entries)
     equals the global-sort path and the oracle bit for bit -- hubs of 1.1K to
     7K neighbours take the three one-CTA-per-row sorts (some of them start in
     the middle of a window), the 12K hub the device sort, every other row the
     windows."""
+    # key64: the window sorts' 64-bit keys (windows of very many short rows at 2^25+ coarse vertices)
+    monkeypatch.setenv("LCC_SEG_KEY64", key64)
     rng = np.random.default_rng(72)
     hg = hub_graph(rng, 30_000, [5, 77, 901, 1234, 1235, 20_000, 20_001], [6000, 12000, 2500, 1500, 1100, 3000, 7000],
                    base_p=0.0004)

@@ -41,21 +41,19 @@ __global__ void k_map(const int32_t* __restrict__ C, const int32_t* __restrict__
 // a root u, mapping[u] = rank(u); the two arrays are n/8 bytes together (L2
 // resident at any size here) where mapping is 4n bytes of random gathers.
 __global__ void k_rootbits(const int32_t* __restrict__ C, const int32_t* __restrict__ rank, int64_t n,
-                           uint32_t* __restrict__ rbits, uint32_t* __restrict__ rpref) {
+                           uint2* __restrict__ rb) {
     const int64_t nv = (n + 31) / 32 * 32;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
         const bool root = v < n && C[v] == (int32_t)v;
         const unsigned b = __ballot_sync(0xffffffffu, root);
         if ((v & 31) == 0) {
-            rbits[v >> 5] = b;
-            rpref[v >> 5] = (uint32_t)rank[v];
+            rb[v >> 5] = make_uint2(b, (uint32_t)rank[v]);  // (bitmap word, roots before it): one 8-byte load per lookup
         }
     }
 }
-__device__ __forceinline__ int32_t root_rank(const uint32_t* __restrict__ rbits, const uint32_t* __restrict__ rpref,
-                                             int32_t u) {
-    const uint32_t w = (uint32_t)u >> 5;
-    return (int32_t)(__ldg(rpref + w) + __popc(__ldg(rbits + w) & ((1u << (u & 31)) - 1u)));
+__device__ __forceinline__ int32_t root_rank(const uint2* __restrict__ rb, int32_t u) {
+    const uint2 w = __ldg(rb + ((uint32_t)u >> 5));
+    return (int32_t)(w.y + __popc(w.x & ((1u << (u & 31)) - 1u)));
 }
 
 // edge functor: key of the directed entry (v, u), intra entries -> sentinel
@@ -218,18 +216,27 @@ struct EmitSimple {
     const int64_t* cindptr;
     int32_t* cind;
     OT* cw;
-    const uint32_t* rbits;  // every neighbour of a simple row is a root: its
-    const uint32_t* rpref;  // coarse id is its rank (no mapping gather).  Null
+    const uint2* rb;        // every neighbour of a simple row is a root: its
+                            // coarse id is its rank (no mapping gather).  Null
                             // for a shard's partial rows: a neighbour whose row
                             // lives on another rank never marked this row, so
                             // it may be a non-root; those rows keep the gather
                             // (the owner-side merge sorts and sums them)
-    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t) {
-        if (cf[v]) return;
-        const int64_t o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
+    struct Tmp { int64_t o; int32_t id; OT wv; };
+    __device__ __forceinline__ Tmp load(int64_t v, int64_t e, int64_t) const {
+        Tmp t;
+        t.o = -1;
+        if (cf[v]) return t;
+        t.o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
         const int32_t u = __ldg(indices + e);
-        cind[o] = rbits ? root_rank(rbits, rpref, u) : ld_gather_i32(mapping + u);
-        cw[o] = (OT)WLoad<WT>::tw(w, e);
+        t.id = rb ? root_rank(rb, u) : ld_gather_i32(mapping + u);
+        t.wv = (OT)WLoad<WT>::tw(w, e);
+        return t;
+    }
+    __device__ __forceinline__ void store(const Tmp& t, int64_t, int64_t, int64_t) const {
+        if (t.o < 0) return;
+        cind[t.o] = t.id;
+        cw[t.o] = t.wv;
     }
     __device__ __forceinline__ void flush() {}
 };
@@ -267,7 +274,7 @@ __global__ void k_emit_complex(const uint64_t* __restrict__ ukeys, const ST* __r
 #define LCC_SEG_I 16
 #endif
 #ifndef LCC_SEG_MINB
-#define LCC_SEG_MINB 1
+#define LCC_SEG_MINB 2  // 2 CTAs per SM (128 registers): with 1 the compiler took more registers and the windows ran 30% slower
 #endif
 constexpr int SEG_T = LCC_SEG_T, SEG_I = LCC_SEG_I, SEG_CAP = SEG_T * SEG_I;  // entries per window CTA
 #ifndef LCC_SEG_WIN
@@ -321,28 +328,43 @@ struct SegFill {
     // optional (LCC_SEG_FILLBITS=1, measured slower): a root's coarse id is
     // its rank among the roots, read from the root bitmap and its sampled
     // prefix (2 x n/8 bytes, L2 resident) instead of the n-word mapping
-    const uint32_t* rbits;
-    const uint32_t* rpref;
+    const uint2* rb;
     unsigned long long cnt = 0;
-    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) {
-        const int32_t a = __ldg(mapping + v);
+#ifndef LCC_FILL_TWOPHASE
+#define LCC_FILL_TWOPHASE 1
+#endif
+#if LCC_FILL_TWOPHASE
+    struct Tmp { int32_t a, b; uint32_t wv; };
+#else
+    struct Tmp1 { int32_t a, b; uint32_t wv; };
+    using Tmp_ = Tmp1;
+    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) { store(load(v, e, pos), v, e, pos); }
+#endif
+#if LCC_FILL_TWOPHASE
+    using Tmp_ = Tmp;
+#endif
+    __device__ __forceinline__ Tmp_ load(int64_t v, int64_t e, int64_t) const {
+        Tmp_ t;
+        t.a = __ldg(mapping + v);
         const int32_t u = __ldg(indices + e);
-        int32_t b;
-        if (rbits) {
-            const uint32_t wd = __ldg(rbits + ((uint32_t)u >> 5));
-            if ((wd >> (u & 31)) & 1u) b = (int32_t)(__ldg(rpref + ((uint32_t)u >> 5)) + __popc(wd & ((1u << (u & 31)) - 1u)));
-            else b = ld_gather_i32(mapping + u);
+        if (rb) {
+            const uint2 wd = __ldg(rb + ((uint32_t)u >> 5));
+            if ((wd.x >> (u & 31)) & 1u) t.b = (int32_t)(wd.y + __popc(wd.x & ((1u << (u & 31)) - 1u)));
+            else t.b = ld_gather_i32(mapping + u);
         } else {
-            b = ld_gather_i32(mapping + u);
+            t.b = ld_gather_i32(mapping + u);
         }
-        const uint32_t wv = WLoad<WT>::tw(w, e);
-        if (a == b) {
+        t.wv = WLoad<WT>::tw(w, e);
+        return t;
+    }
+    __device__ __forceinline__ void store(const Tmp_& t, int64_t, int64_t, int64_t pos) {
+        if (t.a == t.b) {
             keys[pos] = SEG_SENT;
-            cnt += wv;
+            cnt += t.wv;
         } else {
-            keys[pos] = (uint32_t)b;
+            keys[pos] = (uint32_t)t.b;
         }
-        vals[pos] = wv;
+        vals[pos] = t.wv;
     }
     __device__ __forceinline__ void flush() {
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
@@ -643,11 +665,12 @@ struct BigKeys {
     int bbits;
     uint64_t* k64;
     uint32_t* v32;
-    __device__ __forceinline__ void operator()(int64_t a, int64_t e, int64_t pos) {
-        const uint32_t b = keys[e];
+    struct Tmp { uint32_t b, v; int32_t rk; };
+    __device__ __forceinline__ Tmp load(int64_t a, int64_t e, int64_t) const { return Tmp{keys[e], vals[e], __ldg(brank + a)}; }
+    __device__ __forceinline__ void store(const Tmp& t, int64_t, int64_t, int64_t pos) const {
         const uint32_t bmask = (uint32_t)((1ull << bbits) - 1ull);
-        k64[pos] = ((uint64_t)__ldg(brank + a) << bbits) | (b == SEG_SENT ? bmask : b);
-        v32[pos] = vals[e];
+        k64[pos] = ((uint64_t)t.rk << bbits) | (t.b == SEG_SENT ? bmask : t.b);
+        v32[pos] = t.v;
     }
     __device__ __forceinline__ void flush() {}
 };
@@ -681,9 +704,11 @@ struct SegCopy {
     const uint32_t* vals;
     int32_t* cind;
     uint32_t* cw;
-    __device__ __forceinline__ void operator()(int64_t, int64_t e, int64_t pos) {
-        cind[pos] = (int32_t)keys[e];
-        cw[pos] = vals[e];
+    struct Tmp { uint32_t k, v; };
+    __device__ __forceinline__ Tmp load(int64_t, int64_t e, int64_t) const { return Tmp{keys[e], vals[e]}; }
+    __device__ __forceinline__ void store(const Tmp& t, int64_t, int64_t, int64_t pos) const {
+        cind[pos] = (int32_t)t.k;
+        cw[pos] = t.v;
     }
     __device__ __forceinline__ void flush() {}
 };
@@ -692,7 +717,7 @@ struct SegCopy {
 // out.indptr/indices/wi, returns the entry count; *intra = intra weight
 template <class WT>
 int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coarse& out, unsigned long long* intra,
-                     const uint32_t* rbits, const uint32_t* rpref, cudaStream_t s) {
+                     const uint2* rb, cudaStream_t s) {
     const int64_t n = g.n, nnz = g.nnz;
     const int bbits = std::max(1, bit_width((uint64_t)cn));
     LCC_REQUIRE(bbits <= 31, "coarse graph too large for the segmented contraction");
@@ -723,7 +748,7 @@ int64_t compress_seg(const lcc_graph& g, const int32_t* mapping, int64_t cn, Coa
     // 2. every entry's coarse neighbour at its row position
     Buf<uint32_t> keys(nnz, s), vals(nnz, s);
     edge_balanced(g.indptr, perm.get(), pos0.get(), n, nnz,
-                  SegFill<WT>{g.indices, g.weights, mapping, keys.get(), vals.get(), intra, rbits, rpref}, s);
+                  SegFill<WT>{g.indices, g.weights, mapping, keys.get(), vals.get(), intra, rb}, s);
     perm.release();
     pos0.release();
     tr.mark("seg fill");
@@ -830,7 +855,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
     const bool partial = (g.flags & LCC_GRAPH_PARTIAL_ROWS) != 0;
     // 1. dense renumbering by smallest member
     int64_t cn = 0;
-    Buf<uint32_t> rbits, rpref;  // root bitmap + sampled rank (root_rank)
+    Buf<uint2> rb;  // root bitmap + sampled rank (root_rank)
     {
         Buf<int32_t> rank(n + 1, s);
         cub::TransformInputIterator<int32_t, IsRoot, cub::CountingInputIterator<int32_t>> roots(
@@ -840,9 +865,8 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         LCC_CUDA(cudaMemcpyAsync(&hcn, rank.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         k_map<<<grid_for(n, 256), 256, 0, s>>>(C, rank.get(), K, n, mapping, ck);
         LCC_LAUNCH_CHECK();
-        rbits.alloc((n + 31) / 32, s);
-        rpref.alloc((n + 31) / 32, s);
-        k_rootbits<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, s>>>(C, rank.get(), n, rbits.get(), rpref.get());
+        rb.alloc((n + 31) / 32, s);
+        k_rootbits<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, s>>>(C, rank.get(), n, rb.get());
         LCC_LAUNCH_CHECK();
         LCC_CUDA(cudaStreamSynchronize(s));
         cn = hcn;
@@ -990,7 +1014,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
                 edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                               EmitSimple<WT, uint32_t>{g.indices, g.weights, mapping, cf.get(), g.indptr,
                                                        out.indptr.get(), out.indices.get(), out.wi.get(),
-                                                       partial ? nullptr : rbits.get(), partial ? nullptr : rpref.get()}, s);
+                                                       partial ? nullptr : rb.get()}, s);
                 if (Rc > 0) {
                     k_emit_complex<uint32_t, uint32_t><<<grid_for(Rc, 256), 256, 0, s>>>(
                         ukeys.get(), swi.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),
@@ -1001,7 +1025,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
                 edge_balanced(g.indptr, nullptr, g.indptr, n, nnz,
                               EmitSimple<WT, double>{g.indices, g.weights, mapping, cf.get(), g.indptr,
                                                      out.indptr.get(), out.indices.get(), out.w.get(),
-                                                     partial ? nullptr : rbits.get(), partial ? nullptr : rpref.get()}, s);
+                                                     partial ? nullptr : rb.get()}, s);
                 if (Rc > 0) {
                     k_emit_complex<double, double><<<grid_for(Rc, 256), 256, 0, s>>>(
                         ukeys.get(), sw.get(), Rc, bits, out.indptr.get(), cstart.get(), out.indices.get(),
@@ -1027,7 +1051,7 @@ Coarse compress_impl(const lcc_graph& g, const double* k, double lam, const int3
         // (LCC_SEG_FILLBITS=1: roots' coarse ids from the root bitmap in the fill pass; measured slower,
         // config 5 level 0: fill 96 -> 108 ms -- the test adds a dependent L2 lookup in front of every gather)
         static const bool fill_bits = getenv("LCC_SEG_FILLBITS") && getenv("LCC_SEG_FILLBITS")[0] == '1';
-        R = compress_seg<WT>(g, mapping, cn, out, di, fill_bits ? rbits.get() : nullptr, rpref.get(), s);
+        R = compress_seg<WT>(g, mapping, cn, out, di, fill_bits ? rb.get() : nullptr, s);
         unsigned long long hintra = 0;
         LCC_CUDA(cudaMemcpyAsync(&hintra, di, sizeof(hintra), cudaMemcpyDeviceToHost, s));
         LCC_CUDA(cudaStreamSynchronize(s));

@@ -9,6 +9,7 @@
 // the all-vertices case pass list = nullptr and off = indptr.
 #pragma once
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -46,6 +47,19 @@ static __global__ void k_tile_bounds(const int64_t* __restrict__ off, int64_t nl
         thi[t] = upper_idx(off, 0, nlist + 1, t1 - 1) + 1;
     }
 }
+
+// Two-phase functors (a nested `Tmp` type, `Tmp load(v, e, pos)` and
+// `void store(const Tmp&, v, e, pos)`): all EM_ITEMS loads of a thread are
+// issued before its first store.  With a plain operator() the compiler must
+// keep every element's loads behind the previous element's stores (the
+// output may alias the input for all it knows), which serialised 8 load ->
+// store round trips per thread and tile: the emit copy of the segmented
+// contraction ran at 1.7 TB/s with 66% of its stall samples on those loads
+// (profiles/s6_contract_ncu.md).
+template <class F, class = void>
+struct em_two_phase : std::false_type {};
+template <class F>
+struct em_two_phase<F, std::void_t<typename F::Tmp>> : std::true_type {};
 
 template <class F>
 __global__ void __launch_bounds__(EM_THREADS)
@@ -87,10 +101,24 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
                 }
                 own[j] = a;
             }
+            if constexpr (em_two_phase<F>::value) {
+                typename F::Tmp tmp[EM_ITEMS];
 #pragma unroll
-            for (int j = 0; j < EM_ITEMS; ++j) {
-                const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
-                if (e < t1) f((int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+                for (int j = 0; j < EM_ITEMS; ++j) {
+                    const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+                    if (e < t1) tmp[j] = f.load((int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+                }
+#pragma unroll
+                for (int j = 0; j < EM_ITEMS; ++j) {
+                    const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+                    if (e < t1) f.store(tmp[j], (int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < EM_ITEMS; ++j) {
+                    const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
+                    if (e < t1) f((int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+                }
             }
         } else {
 #pragma unroll 2
@@ -99,7 +127,9 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
                 if (e < t1) {
                     const int64_t li = upper_idx(off, lo, hi, e);
                     const int64_t v = list ? (int64_t)__ldg(list + li) : li;
-                    f(v, __ldg(indptr + v) + (e - __ldg(off + li)), e);
+                    const int64_t ee = __ldg(indptr + v) + (e - __ldg(off + li));
+                    if constexpr (em_two_phase<F>::value) f.store(f.load(v, ee, e), v, ee, e);
+                    else f(v, ee, e);
                 }
             }
         }

@@ -223,11 +223,15 @@ struct EmitSimple {
                             // it may be a non-root; those rows keep the gather
                             // (the owner-side merge sorts and sums them)
     struct Tmp { int64_t o; int32_t id; OT wv; };
-    __device__ __forceinline__ Tmp load(int64_t v, int64_t e, int64_t) const {
+    // per row: where its entries go (output position = that + e), or "not a simple row"
+    __device__ __forceinline__ int64_t prep(int64_t v) const {
+        return cf[v] ? INT64_MIN : cindptr[mapping[v]] - __ldg(indptr + v);
+    }
+    __device__ __forceinline__ Tmp load(int64_t aux, int64_t e, int64_t) const {
         Tmp t;
         t.o = -1;
-        if (cf[v]) return t;
-        t.o = cindptr[mapping[v]] + (e - __ldg(indptr + v));
+        if (aux == INT64_MIN) return t;
+        t.o = aux + e;
         const int32_t u = __ldg(indices + e);
         t.id = rb ? root_rank(rb, u) : ld_gather_i32(mapping + u);
         t.wv = (OT)WLoad<WT>::tw(w, e);

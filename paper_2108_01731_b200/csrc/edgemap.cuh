@@ -61,14 +61,26 @@ struct em_two_phase : std::false_type {};
 template <class F>
 struct em_two_phase<F, std::void_t<typename F::Tmp>> : std::true_type {};
 
+// Functors with `int64_t prep(int64_t v)`: evaluated once per list entry of a
+// tile (shared memory), and load()/store() receive that value in place of v --
+// the per-row part of an address (a flag, a mapping and two row offsets for the
+// fast-path emit) is not re-read for every entry of the row.
+template <class F, class = void>
+struct em_has_prep : std::false_type {};
+template <class F>
+struct em_has_prep<F, std::void_t<decltype(&F::prep)>> : std::true_type {};
+
 template <class F>
 __global__ void __launch_bounds__(EM_THREADS)
 k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ list,
                 const int64_t* __restrict__ off, int64_t nlist, const int64_t* __restrict__ tlo,
                 const int64_t* __restrict__ thi, F f) {
-    __shared__ int64_t s_off[EM_TILE + 2];
+    __shared__ int32_t s_off[EM_TILE + 2];  // entry starts relative to the tile, clamped to [-1, EM_TILE + 1]
     __shared__ int64_t s_row[EM_TILE + 1];  // start of each window entry's row
-    __shared__ int32_t s_v[EM_TILE + 1];    // vertex of each window entry
+    __shared__ int32_t s_v[em_has_prep<F>::value ? 1 : EM_TILE + 1];  // vertex of each window entry
+    constexpr bool PREP = em_has_prep<F>::value;
+    static_assert(!PREP || em_two_phase<F>::value, "prep() goes with load()/store()");
+    __shared__ int64_t s_aux[PREP ? EM_TILE + 1 : 1];  // f.prep(vertex)
     const int64_t total = __ldg(off + nlist);
     for (int64_t t0 = (int64_t)blockIdx.x * EM_TILE; t0 < total; t0 += (int64_t)gridDim.x * EM_TILE) {
         const int64_t t1 = min64(t0 + EM_TILE, total);
@@ -76,11 +88,15 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
         const int64_t wn = hi - lo;  // entries lo .. hi-1 own the tile; off[hi] closes it
         const bool cached = wn <= EM_TILE;
         if (cached) {
-            for (int64_t i = threadIdx.x; i <= wn; i += EM_THREADS) s_off[i] = __ldg(off + lo + i);
+            for (int64_t i = threadIdx.x; i <= wn; i += EM_THREADS) {
+                const int64_t r = __ldg(off + lo + i) - t0;
+                s_off[i] = (int32_t)(r < -1 ? -1 : (r > EM_TILE + 1 ? EM_TILE + 1 : r));
+            }
             for (int64_t i = threadIdx.x; i < wn; i += EM_THREADS) {
                 const int64_t v = list ? (int64_t)__ldg(list + lo + i) : lo + i;
-                s_v[i] = (int32_t)v;
-                s_row[i] = __ldg(indptr + v) - s_off[i];  // edge e of this entry = s_row + e
+                if constexpr (!PREP) s_v[i] = (int32_t)v;
+                s_row[i] = __ldg(indptr + v) - __ldg(off + lo + i);  // edge e of this entry = s_row + e
+                if constexpr (PREP) s_aux[i] = f.prep(v);
             }
         }
         __syncthreads();
@@ -96,7 +112,7 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
                 if (e < t1) {
                     while (b - a > 1) {
                         const int mid = (a + b) >> 1;
-                        if (s_off[mid] <= e) a = mid; else b = mid;
+                        if (s_off[mid] <= (int32_t)(e - t0)) a = mid; else b = mid;
                     }
                 }
                 own[j] = a;
@@ -106,12 +122,12 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
 #pragma unroll
                 for (int j = 0; j < EM_ITEMS; ++j) {
                     const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
-                    if (e < t1) tmp[j] = f.load((int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+                    if (e < t1) tmp[j] = f.load(PREP ? s_aux[own[j]] : (int64_t)s_v[PREP ? 0 : own[j]], s_row[own[j]] + e, e);
                 }
 #pragma unroll
                 for (int j = 0; j < EM_ITEMS; ++j) {
                     const int64_t e = t0 + (int64_t)j * EM_THREADS + threadIdx.x;
-                    if (e < t1) f.store(tmp[j], (int64_t)s_v[own[j]], s_row[own[j]] + e, e);
+                    if (e < t1) f.store(tmp[j], PREP ? s_aux[own[j]] : (int64_t)s_v[PREP ? 0 : own[j]], s_row[own[j]] + e, e);
                 }
             } else {
 #pragma unroll
@@ -128,7 +144,10 @@ k_edge_balanced(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
                     const int64_t li = upper_idx(off, lo, hi, e);
                     const int64_t v = list ? (int64_t)__ldg(list + li) : li;
                     const int64_t ee = __ldg(indptr + v) + (e - __ldg(off + li));
-                    if constexpr (em_two_phase<F>::value) f.store(f.load(v, ee, e), v, ee, e);
+                    if constexpr (PREP) {
+                        const int64_t ax = f.prep(v);
+                        f.store(f.load(ax, ee, e), ax, ee, e);
+                    } else if constexpr (em_two_phase<F>::value) f.store(f.load(v, ee, e), v, ee, e);
                     else f(v, ee, e);
                 }
             }

@@ -222,25 +222,25 @@ struct EmitSimple {
                             // lives on another rank never marked this row, so
                             // it may be a non-root; those rows keep the gather
                             // (the owner-side merge sorts and sums them)
-    struct Tmp { int64_t o; int32_t id; OT wv; };
+    struct Tmp { int32_t id; OT wv; };  // (the output position is recomputed in store(): 72 -> fewer registers, 3 -> more CTAs per SM)
     // per row: where its entries go (output position = that + e), or "not a simple row"
     __device__ __forceinline__ int64_t prep(int64_t v) const {
         return cf[v] ? INT64_MIN : cindptr[mapping[v]] - __ldg(indptr + v);
     }
     __device__ __forceinline__ Tmp load(int64_t aux, int64_t e, int64_t) const {
         Tmp t;
-        t.o = -1;
+        t.id = 0;
+        t.wv = OT(0);
         if (aux == INT64_MIN) return t;
-        t.o = aux + e;
         const int32_t u = __ldg(indices + e);
         t.id = rb ? root_rank(rb, u) : ld_gather_i32(mapping + u);
         t.wv = (OT)WLoad<WT>::tw(w, e);
         return t;
     }
-    __device__ __forceinline__ void store(const Tmp& t, int64_t, int64_t, int64_t) const {
-        if (t.o < 0) return;
-        cind[t.o] = t.id;
-        cw[t.o] = t.wv;
+    __device__ __forceinline__ void store(const Tmp& t, int64_t aux, int64_t e, int64_t) const {
+        if (aux == INT64_MIN) return;
+        cind[aux + e] = t.id;
+        cw[aux + e] = t.wv;
     }
     __device__ __forceinline__ void flush() {}
 };

@@ -71,10 +71,15 @@ struct EdgeKey {
     bool compact = false;  // write at the list position (complex rows only) instead of the CSR index
     unsigned long long cnt = 0;
     double acc = 0.0;
-    __device__ __forceinline__ void operator()(int64_t v, int64_t e, int64_t pos) {
-        const uint64_t a = (uint32_t)__ldg(mapping + v);
-        const uint64_t b = (uint32_t)ld_gather_i32(mapping + __ldg(indices + e));
-        const auto wv = WLoad<WT>::tw(w, e);
+    // two-phase (edgemap.cuh): a thread's gathers all go out before its first store;
+    // the per-thread sums keep their element order
+    struct Tmp { uint32_t a, b; typename WLoad<WT>::TW wv; };
+    __device__ __forceinline__ Tmp load(int64_t v, int64_t e, int64_t) const {
+        return Tmp{(uint32_t)__ldg(mapping + v), (uint32_t)ld_gather_i32(mapping + __ldg(indices + e)), WLoad<WT>::tw(w, e)};
+    }
+    __device__ __forceinline__ void store(const Tmp& t, int64_t, int64_t e, int64_t pos) {
+        const uint64_t a = t.a, b = t.b;
+        const auto wv = t.wv;
         const int64_t o = compact ? pos : e;
         if (a == b) {
             keys[o] = sentinel;
